@@ -1,0 +1,272 @@
+"""ctypes front-end of the CPU oracle (oracle/sg_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference leg may use it; the product package
+(paper_2512_11473_b200/) never imports it.  Arrays are numpy; the oracle is
+fp64 on a dense fine grid (M = 4N points per axis), tables follow SURVEY.md
+8(c.1) O3-O5, fields O6-O10.  Every function cites the paper passage it
+follows in sg_oracle.c.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "sg_oracle.c")
+LIB = os.path.join(HERE, "liboracle.so")
+
+CFLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+          "-std=c11", "-Wall", "-Wno-unknown-pragmas"]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (gcc, no FMA contraction, IEEE double)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        tmp = LIB + ".tmp"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, SRC, "-lm"])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+class _Prim(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("p", C.c_double * 12)]
+
+
+class _Grid(C.Structure):
+    _fields_ = [("lower", C.c_double * 3), ("cell", C.c_double), ("n", C.c_int32 * 3),
+                ("pad", C.c_int32), ("far", C.c_double), ("init_scale", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(LIB)
+        P = C.c_void_p
+        L.or_sdf.restype = C.c_double
+        L.or_sdf.argtypes = [P, C.c_int32, P]
+        L.or_sdf_batch.argtypes = [P, C.c_int32, C.c_int64, P, P]
+        L.or_far.restype = C.c_double
+        L.or_far.argtypes = [P]
+        L.or_tag.argtypes = [P, P, C.c_int32, P, P]
+        L.or_compact.restype = C.c_int64
+        L.or_compact.argtypes = [P, P, P, P, P, P]
+        L.or_neighbours.argtypes = [P, P, C.c_int32, P, P, C.c_int64, P]
+        L.or_phi_dense.argtypes = [P, P, C.c_int32, P, P]
+        L.or_phi_point.restype = C.c_double
+        L.or_phi_point.argtypes = [P, P, C.c_int32, P, C.c_int64, C.c_int64, C.c_int64]
+        L.or_reinit_dense.argtypes = [P, P, C.c_int32, P, P, P, C.c_double]
+        L.or_reinit_point_from_init.restype = C.c_double
+        L.or_reinit_point_from_init.argtypes = [P, P, C.c_int32, P, C.c_int64, C.c_int64,
+                                                C.c_int64, C.c_double]
+        L.or_gradient_dense.argtypes = [P, P, C.c_int32, P, P, P, P]
+        L.or_kernel_taps.restype = C.c_int32
+        L.or_kernel_taps.argtypes = [C.c_double, C.c_double, P, P, P]
+        L.or_heaviside.restype = C.c_double
+        L.or_heaviside.argtypes = [C.c_double, C.c_double]
+        L.or_kernel_dense.argtypes = [P, P, C.c_int32, P, P, C.c_double, P, P]
+        L.or_probe.restype = C.c_int64
+        L.or_probe.argtypes = [P, P, C.c_int32, P, P, P, C.c_int64, P, P, P]
+        L.or_gather_packages.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_double, P]
+        L.or_set_threads.argtypes = [C.c_int32]
+        L.or_get_threads.restype = C.c_int32
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def set_threads(n: int) -> None:
+    lib().or_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().or_get_threads())
+
+
+@dataclass
+class Tables:
+    cat: np.ndarray        # u8[Nz,Ny,Nx] flattened: 0/1 inactive by sign, 2 inner, 3 core
+    bg: np.ndarray         # u32[N^3]
+    meta_cell: np.ndarray  # u32[n_pkg]
+    meta_cat: np.ndarray   # u8[n_pkg]
+    nb: np.ndarray         # u32[n_pkg, 27]
+    plane_count: np.ndarray  # i64[Nz]
+    n_pkg: int
+    near_ties: int
+
+
+class Oracle:
+    """Dense fp64 oracle bound to one workload (geometry + grid)."""
+
+    def __init__(self, w):
+        self.w = w
+        self._g = _Grid()
+        for k in range(3):
+            self._g.lower[k] = w.lower[k]
+            self._g.n[k] = w.n[k]
+        self._g.cell = w.cell
+        self._g.far = w.far
+        self._g.init_scale = w.init_scale
+        self._prims = (_Prim * max(1, len(w.prims)))()
+        for i, pr in enumerate(w.prims):
+            self._prims[i].kind = pr.kind
+            for j, v in enumerate(pr.p):
+                self._prims[i].p[j] = v
+        self.n_prims = len(w.prims)
+        self.tables: Tables | None = None
+
+    # handles
+    @property
+    def g(self):
+        return C.byref(self._g)
+
+    @property
+    def prims(self):
+        return C.cast(self._prims, C.c_void_p)
+
+    @property
+    def far(self) -> float:
+        return float(lib().or_far(self.g))
+
+    @property
+    def dx(self) -> float:
+        return self.w.cell / 4.0
+
+    @property
+    def m(self):
+        return tuple(4 * n for n in self.w.n)  # (Mx, My, Mz)
+
+    # O1
+    def sdf(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1, 3))
+        out = np.empty(x.shape[0])
+        lib().or_sdf_batch(self.prims, self.n_prims, x.shape[0], _ptr(x), _ptr(out))
+        return out
+
+    # O3-O5
+    def build_tables(self) -> Tables:
+        nx, ny, nz = self.w.n
+        ncell = nx * ny * nz
+        cat = np.empty(ncell, np.uint8)
+        ties = C.c_int64(0)
+        lib().or_tag(self.g, self.prims, self.n_prims, _ptr(cat), C.byref(ties))
+        bg = np.empty(ncell, np.uint32)
+        n_active = int(np.count_nonzero(cat >= 2))
+        meta_cell = np.empty(n_active + 2, np.uint32)
+        meta_cat = np.empty(n_active + 2, np.uint8)
+        plane = np.zeros(nz, np.int64)
+        n_pkg = int(lib().or_compact(self.g, _ptr(cat), _ptr(bg), _ptr(meta_cell),
+                                     _ptr(meta_cat), _ptr(plane)))
+        assert n_pkg == n_active + 2
+        nb = np.empty((n_pkg, 27), np.uint32)
+        lib().or_neighbours(self.g, self.prims, self.n_prims, _ptr(bg), _ptr(meta_cell),
+                            n_pkg, _ptr(nb))
+        self.tables = Tables(cat, bg, meta_cell, meta_cat, nb, plane, n_pkg, int(ties.value))
+        return self.tables
+
+    def _bg(self):
+        if self.tables is None:
+            self.build_tables()
+        return self.tables.bg
+
+    # O6
+    def phi_dense(self) -> np.ndarray:
+        """Dense initial phi, shape (Mz, My, Mx) (x fastest)."""
+        mx, my, mz = self.m
+        phi = np.empty((mz, my, mx))
+        lib().or_phi_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi))
+        return phi
+
+    def phi_point(self, ix: int, iy: int, iz: int) -> float:
+        return float(lib().or_phi_point(self.g, self.prims, self.n_prims, _ptr(self._bg()),
+                                        ix, iy, iz))
+
+    # O7
+    def reinit_step(self, phi: np.ndarray, cfl: float | None = None) -> np.ndarray:
+        cfl = self.w.cfl if cfl is None else cfl
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        out = np.empty_like(phi)
+        lib().or_reinit_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
+                              _ptr(out), cfl)
+        return out
+
+    def reinit(self, phi: np.ndarray, iters: int, cfl: float | None = None) -> np.ndarray:
+        for _ in range(iters):
+            phi = self.reinit_step(phi, cfl)
+        return phi
+
+    def reinit_point_from_init(self, ix: int, iy: int, iz: int, cfl: float | None = None) -> float:
+        cfl = self.w.cfl if cfl is None else cfl
+        return float(lib().or_reinit_point_from_init(self.g, self.prims, self.n_prims,
+                                                     _ptr(self._bg()), ix, iy, iz, cfl))
+
+    # O8
+    def gradient(self, phi: np.ndarray):
+        """Returns (grad, normal), each shape (3, Mz, My, Mx)."""
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        grad = np.empty((3,) + phi.shape)
+        normal = np.empty((3,) + phi.shape)
+        lib().or_gradient_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
+                                _ptr(grad), _ptr(normal))
+        return grad, normal
+
+    # O9
+    def taps(self, h_ratio: float | None = None):
+        h_ratio = self.w.h_ratio if h_ratio is None else h_ratio
+        return kernel_taps(h_ratio, self.dx)
+
+    def kernel_integrals(self, phi: np.ndarray, h_ratio: float | None = None):
+        """Returns (K shape (Mz,My,Mx), G shape (3,Mz,My,Mx))."""
+        h_ratio = self.w.h_ratio if h_ratio is None else h_ratio
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        K = np.empty_like(phi)
+        G = np.empty((3,) + phi.shape)
+        lib().or_kernel_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
+                              h_ratio, _ptr(K), _ptr(G))
+        return K, G
+
+    # O10
+    def probe(self, phi: np.ndarray, grad: np.ndarray | None, pos: np.ndarray):
+        """pos (n,3) any float dtype (promoted to double). Returns (phi, grad, oob)."""
+        pos = np.ascontiguousarray(np.asarray(pos).astype(np.float64).reshape(-1, 3))
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        g3 = None if grad is None else np.ascontiguousarray(grad, dtype=np.float64)
+        n = pos.shape[0]
+        out_phi = np.empty(n)
+        out_grad = np.empty((n, 3))
+        oob = lib().or_probe(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
+                             _ptr(g3), n, _ptr(pos), _ptr(out_phi), _ptr(out_grad))
+        return out_phi, out_grad, int(oob)
+
+    # layout helper: dense plane -> package-major using the oracle's meta
+    def to_packages(self, dense: np.ndarray, far_neg: float, far_pos: float) -> np.ndarray:
+        t = self.tables if self.tables is not None else self.build_tables()
+        dense = np.ascontiguousarray(dense, dtype=np.float64)
+        out = np.empty((t.n_pkg, 64))
+        lib().or_gather_packages(self.g, _ptr(dense), _ptr(t.meta_cell), t.n_pkg, far_neg,
+                                 far_pos, _ptr(out))
+        return out
+
+
+def kernel_taps(h_ratio: float, dx: float):
+    """(o int[n,3], w[n], gw[n,3]) of the O9 stencil."""
+    o = np.empty((4096, 3), np.int32)
+    w = np.empty(4096)
+    gw = np.empty((4096, 3))
+    n = int(lib().or_kernel_taps(h_ratio, dx, _ptr(o), _ptr(w), _ptr(gw)))
+    return o[:n].copy(), w[:n].copy(), gw[:n].copy()
+
+
+def heaviside(u: float, eps: float) -> float:
+    return float(lib().or_heaviside(u, eps))

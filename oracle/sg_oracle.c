@@ -1,0 +1,704 @@
+/*
+ * sg_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of the contiguous
+ * sparse-grid hot path of Gu & Hu, "Contiguous Storage of Grid Data for
+ * Heterogeneous Computing" (arXiv 2512.11473; /root/reference/PAPER.md, cited
+ * below as P:<line>).  Everything is fp64 on a DENSE fine grid of M = 4N points
+ * per axis; the sparse package structure is produced only as the tables the
+ * paper defines (background table, meta, 27-neighbour table), so that the CUDA
+ * path's tables can be checked for identity and its fields scattered/gathered
+ * against dense arrays.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load this library.  It shares no code, header,
+ * helper or constant generator with the CUDA path (paper_2512_11473_b200/)
+ * and neither side includes or imports the other.
+ *
+ * Where PAPER.md is silent the reading taken is the one listed in DESIGN.md
+ * "Readings" (R-1 .. R-20, same numbering as SURVEY.md 8(c.3)).
+ *
+ * Build: gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared (no -ffast-math):
+ * every double operation is a separately rounded IEEE operation in the order
+ * written, which is what makes the tagging decision |f| < l_c reproducible.
+ *
+ * Parity status per function:
+ *   or_sdf            pinned: closed forms + brute-force surface sampling
+ *   or_tag/or_compact pinned: brute-force definition on tiny grids, invariants,
+ *                     independent counts
+ *   or_neighbours     pinned: definition by brute force, invariants
+ *   or_phi_dense      pinned: closed-form SDF values
+ *   or_reinit_dense   pinned: planar closed form, 2*SDF convergence, no sign
+ *                     flip; drift near kinks/medial axes: parity unpinned
+ *   or_gradient_dense pinned: affine exactness, sphere radial; band-edge values
+ *                     that use the far constant: parity unpinned
+ *   or_kernel_dense   pinned: S closed forms, S/2 at planar interface, sum gw=0
+ *   or_probe          pinned: affine reproduction, data-point identity, far/OOB
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* Primitive kinds: the numeric values are part of the C-ABI contract
+ * (include/sg.h documents the same numbers); they are restated here, not
+ * shared. */
+enum {
+    OR_SPHERE = 0,     /* p = cx cy cz r                         */
+    OR_SHELL = 1,      /* p = cx cy cz r_in r_out                */
+    OR_BOX = 2,        /* p = cx cy cz bx by bz (half extents)   */
+    OR_TORUS_X = 3,    /* p = cx cy cz R r, symmetry axis x      */
+    OR_TORUS_Y = 4,    /* p = cx cy cz R r, symmetry axis y      */
+    OR_TORUS_Z = 5,    /* p = cx cy cz R r, symmetry axis z      */
+    OR_TRIPRISM_Z = 6  /* p = ax ay bx by cx cy z0 z1 (ccw in xy) */
+};
+
+typedef struct {
+    int32_t kind;
+    int32_t pad;
+    double p[12];
+} or_prim;
+
+typedef struct {
+    double lower[3];
+    double cell;      /* l_c, Fig. 2 caption P:189-191 */
+    int32_t n[3];     /* background cells per axis                */
+    int32_t pad;
+    double far;       /* far-field magnitude, reading R-4          */
+    double init_scale;
+} or_grid;
+
+#define PKG 4 /* subdivision size, "default by 4"; fixed (R-9) */
+
+/* ------------------------------------------------------------------ O1 -- */
+/* Signed distance of the analytic primitives; negative inside.  The paper
+ * evaluates the level set from a signed-distance function; analytic
+ * SDFs stand in for the triangle-mesh SDF (out of scope). */
+
+static double sdf_prim(const or_prim* q, const double x[3]) {
+    const double* p = q->p;
+    switch (q->kind) {
+    case OR_SPHERE: {
+        double ex = x[0] - p[0], ey = x[1] - p[1], ez = x[2] - p[2];
+        return sqrt((ex * ex + ey * ey) + ez * ez) - p[3];
+    }
+    case OR_SHELL: {
+        double ex = x[0] - p[0], ey = x[1] - p[1], ez = x[2] - p[2];
+        double rm = 0.5 * (p[3] + p[4]);
+        double hw = 0.5 * (p[4] - p[3]);
+        return fabs(sqrt((ex * ex + ey * ey) + ez * ez) - rm) - hw;
+    }
+    case OR_BOX: {
+        double qx = fabs(x[0] - p[0]) - p[3];
+        double qy = fabs(x[1] - p[1]) - p[4];
+        double qz = fabs(x[2] - p[2]) - p[5];
+        double mx = fmax(qx, 0.0), my = fmax(qy, 0.0), mz = fmax(qz, 0.0);
+        return sqrt((mx * mx + my * my) + mz * mz) + fmin(fmax(qx, fmax(qy, qz)), 0.0);
+    }
+    case OR_TORUS_X: {
+        double ex = x[0] - p[0], ey = x[1] - p[1], ez = x[2] - p[2];
+        double t = sqrt(ey * ey + ez * ez) - p[3];
+        return sqrt(t * t + ex * ex) - p[4];
+    }
+    case OR_TORUS_Y: {
+        double ex = x[0] - p[0], ey = x[1] - p[1], ez = x[2] - p[2];
+        double t = sqrt(ex * ex + ez * ez) - p[3];
+        return sqrt(t * t + ey * ey) - p[4];
+    }
+    case OR_TORUS_Z: {
+        double ex = x[0] - p[0], ey = x[1] - p[1], ez = x[2] - p[2];
+        double t = sqrt(ex * ex + ey * ey) - p[3];
+        return sqrt(t * t + ez * ez) - p[4];
+    }
+    case OR_TRIPRISM_Z: {
+        /* exact 2-D triangle SDF: clamped point-segment distance to each
+         * edge, negative iff strictly left of all three (ccw) edges */
+        double dmin = 0.0;
+        int inside = 1;
+        for (int e = 0; e < 3; ++e) {
+            double ax = p[2 * e], ay = p[2 * e + 1];
+            double bx = p[2 * ((e + 1) % 3)], by = p[2 * ((e + 1) % 3) + 1];
+            double ux = bx - ax, uy = by - ay;
+            double wx = x[0] - ax, wy = x[1] - ay;
+            double t = (wx * ux + wy * uy) / (ux * ux + uy * uy);
+            t = fmin(fmax(t, 0.0), 1.0);
+            double dx = wx - ux * t, dy = wy - uy * t;
+            double d2 = dx * dx + dy * dy;
+            dmin = (e == 0) ? d2 : fmin(dmin, d2);
+            double cr = ux * wy - uy * wx;
+            if (!(cr > 0.0)) inside = 0;
+        }
+        double d2s = inside ? -sqrt(dmin) : sqrt(dmin);
+        double zc = 0.5 * (p[6] + p[7]);
+        double hl = 0.5 * (p[7] - p[6]);
+        double qz = fabs(x[2] - zc) - hl;
+        double mxy = fmax(d2s, 0.0), mz = fmax(qz, 0.0);
+        return fmin(fmax(d2s, qz), 0.0) + sqrt(mxy * mxy + mz * mz);
+    }
+    default:
+        return NAN;
+    }
+}
+
+/* union = min over primitives, in order */
+double or_sdf(const or_prim* prims, int32_t n_prims, const double x[3]) {
+    double f = INFINITY;
+    for (int i = 0; i < n_prims; ++i) {
+        double g = sdf_prim(&prims[i], x);
+        f = (i == 0) ? g : fmin(f, g);
+    }
+    return f;
+}
+
+void or_sdf_batch(const or_prim* prims, int32_t n_prims, int64_t n, const double* x,
+                  double* out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) out[i] = or_sdf(prims, n_prims, x + 3 * i);
+}
+
+/* ------------------------------------------------------------- helpers -- */
+
+static inline int64_t lin_cell(const or_grid* g, int64_t cx, int64_t cy, int64_t cz) {
+    /* R-1: x fastest, z slowest */
+    return cx + (int64_t)g->n[0] * (cy + (int64_t)g->n[1] * cz);
+}
+
+/* O2: centre of background cell c; multiply and add rounded separately */
+static inline void cell_centre(const or_grid* g, int64_t cx, int64_t cy, int64_t cz,
+                               double x[3]) {
+    x[0] = g->lower[0] + ((double)cx + 0.5) * g->cell;
+    x[1] = g->lower[1] + ((double)cy + 0.5) * g->cell;
+    x[2] = g->lower[2] + ((double)cz + 0.5) * g->cell;
+}
+
+static inline double data_spacing(const or_grid* g) { return g->cell / (double)PKG; }
+
+/* R-11: data point I sits at lower + (I + 0.5) dx */
+static inline void point_pos(const or_grid* g, int64_t ix, int64_t iy, int64_t iz,
+                             double x[3]) {
+    double dx = data_spacing(g);
+    x[0] = g->lower[0] + ((double)ix + 0.5) * dx;
+    x[1] = g->lower[1] + ((double)iy + 0.5) * dx;
+    x[2] = g->lower[2] + ((double)iz + 0.5) * dx;
+}
+
+double or_far(const or_grid* g) {
+    /* R-4: far = 4 l_c max(1, init_scale) unless given */
+    if (g->far > 0.0) return g->far;
+    double s = g->init_scale > 0.0 ? g->init_scale : 1.0;
+    return 4.0 * g->cell * (s > 1.0 ? s : 1.0);
+}
+
+static inline double init_scale(const or_grid* g) {
+    return g->init_scale > 0.0 ? g->init_scale : 1.0;
+}
+
+/* ------------------------------------------------------------ O3 / O4 -- */
+/* Category per background cell:
+ *   0 inactive, far-field negative (inside)     P:189-191, R-5
+ *   1 inactive, far-field positive (outside)
+ *   2 inner   (not core, some 26-neighbour core) P:507, R-3
+ *   3 core    (|f(centre)| < l_c)                P:499-502, R-2
+ * near_tie (optional) counts cells with ||f| - l_c| < 1e-12 l_c. */
+void or_tag(const or_grid* g, const or_prim* prims, int32_t n_prims, uint8_t* cat,
+            int64_t* near_tie) {
+    const int64_t nx = g->n[0], ny = g->n[1], nz = g->n[2];
+    const int64_t ncell = nx * ny * nz;
+    uint8_t* core = (uint8_t*)malloc((size_t)ncell);
+    uint8_t* neg = (uint8_t*)malloc((size_t)ncell);
+    int64_t ties = 0;
+#pragma omp parallel for collapse(2) schedule(static) reduction(+ : ties)
+    for (int64_t cz = 0; cz < nz; ++cz)
+        for (int64_t cy = 0; cy < ny; ++cy)
+            for (int64_t cx = 0; cx < nx; ++cx) {
+                double x[3];
+                cell_centre(g, cx, cy, cz, x);
+                double f = or_sdf(prims, n_prims, x);
+                int64_t L = lin_cell(g, cx, cy, cz);
+                core[L] = fabs(f) < g->cell;
+                neg[L] = f < 0.0;
+                if (fabs(fabs(f) - g->cell) < 1e-12 * g->cell) ties++;
+            }
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t cz = 0; cz < nz; ++cz)
+        for (int64_t cy = 0; cy < ny; ++cy)
+            for (int64_t cx = 0; cx < nx; ++cx) {
+                int64_t L = lin_cell(g, cx, cy, cz);
+                if (core[L]) {
+                    cat[L] = 3;
+                    continue;
+                }
+                int inner = 0;
+                for (int64_t oz = -1; oz <= 1 && !inner; ++oz)
+                    for (int64_t oy = -1; oy <= 1 && !inner; ++oy)
+                        for (int64_t ox = -1; ox <= 1 && !inner; ++ox) {
+                            int64_t qx = cx + ox, qy = cy + oy, qz = cz + oz;
+                            if (qx < 0 || qy < 0 || qz < 0 || qx >= nx || qy >= ny || qz >= nz)
+                                continue; /* R-3: clipped to the domain */
+                            if (core[lin_cell(g, qx, qy, qz)]) inner = 1;
+                        }
+                cat[L] = inner ? 2 : (neg[L] ? 0 : 1);
+            }
+    free(core);
+    free(neg);
+    if (near_tie) *near_tie = ties;
+}
+
+/* O4: ids 2.. in ascending linear cell order (R-1).
+ * bg[L] = id (active) or 0/1 (inactive, by sign).  meta_cell / meta_cat have
+ * room for ncell + 2 entries (caller sizes them); returns n_pkg incl. 0 and 1.
+ * plane_count[cz] (optional) = number of packages in background plane cz. */
+int64_t or_compact(const or_grid* g, const uint8_t* cat, uint32_t* bg, uint32_t* meta_cell,
+                   uint8_t* meta_cat, int64_t* plane_count) {
+    const int64_t nx = g->n[0], ny = g->n[1], nz = g->n[2];
+    const int64_t ncell = nx * ny * nz;
+    int64_t id = 2;
+    meta_cell[0] = 0xFFFFFFFFu;
+    meta_cat[0] = 0;
+    meta_cell[1] = 0xFFFFFFFFu;
+    meta_cat[1] = 1;
+    for (int64_t L = 0; L < ncell; ++L) {
+        uint8_t c = cat[L];
+        if (c >= 2) {
+            bg[L] = (uint32_t)id;
+            meta_cell[id] = (uint32_t)L;
+            meta_cat[id] = c;
+            if (plane_count) plane_count[L / (nx * ny)]++;
+            id++;
+        } else {
+            bg[L] = c; /* 0 negative far field, 1 positive far field */
+        }
+    }
+    return id;
+}
+
+/* Sign-based far package of a (possibly out-of-domain) background cell
+ * (R-6): 0 if f(centre) < 0 else 1.  In-domain cells read bg. */
+static inline uint32_t far_pkg_virtual(const or_grid* g, const or_prim* prims, int32_t n_prims,
+                                       int64_t cx, int64_t cy, int64_t cz) {
+    double x[3];
+    cell_centre(g, cx, cy, cz, x);
+    return or_sdf(prims, n_prims, x) < 0.0 ? 0u : 1u;
+}
+
+static inline int in_domain(const or_grid* g, int64_t cx, int64_t cy, int64_t cz) {
+    return cx >= 0 && cy >= 0 && cz >= 0 && cx < g->n[0] && cy < g->n[1] && cz < g->n[2];
+}
+
+/* O5: nb[id][ox + 3 oy + 9 oz] = package of cell c + o - 1 (P:303-313,
+ * R-8); singular rows point to themselves. */
+void or_neighbours(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
+                   const uint32_t* meta_cell, int64_t n_pkg, uint32_t* nb) {
+    const int64_t nx = g->n[0], ny = g->n[1];
+    for (int s = 0; s < 27; ++s) {
+        nb[s] = 0;
+        nb[27 + s] = 1;
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t id = 2; id < n_pkg; ++id) {
+        int64_t L = meta_cell[id];
+        int64_t cx = L % nx, cy = (L / nx) % ny, cz = L / (nx * ny);
+        for (int oz = 0; oz < 3; ++oz)
+            for (int oy = 0; oy < 3; ++oy)
+                for (int ox = 0; ox < 3; ++ox) {
+                    int64_t qx = cx + ox - 1, qy = cy + oy - 1, qz = cz + oz - 1;
+                    uint32_t v = in_domain(g, qx, qy, qz)
+                                     ? bg[lin_cell(g, qx, qy, qz)]
+                                     : far_pkg_virtual(g, prims, n_prims, qx, qy, qz);
+                    nb[id * 27 + ox + 3 * oy + 9 * oz] = v;
+                }
+    }
+}
+
+/* -------------------------------------------------------- dense access -- */
+/* Dense fine grid: I = ix + M0 (iy + M1 iz), M = 4 N.  A dense value of a
+ * point in an inactive cell is the far constant of its sign (the singular
+ * package value); a point outside the domain takes the sign of f
+ * at its virtual cell centre (R-6). */
+
+typedef struct {
+    const or_grid* g;
+    const or_prim* prims;
+    int32_t n_prims;
+    const uint32_t* bg;
+    int64_t m[3];
+    double far;
+} dense_ctx;
+
+static void dense_init(dense_ctx* d, const or_grid* g, const or_prim* prims, int32_t n_prims,
+                       const uint32_t* bg) {
+    d->g = g;
+    d->prims = prims;
+    d->n_prims = n_prims;
+    d->bg = bg;
+    for (int k = 0; k < 3; ++k) d->m[k] = (int64_t)PKG * g->n[k];
+    d->far = or_far(g);
+}
+
+static inline int64_t fdiv4(int64_t i) { return i >= 0 ? i / 4 : -((-i + 3) / 4); }
+
+/* value of a scalar dense field at fine index (ix,iy,iz), possibly outside */
+static inline double dense_get(const dense_ctx* d, const double* a, int64_t ix, int64_t iy,
+                               int64_t iz) {
+    if (ix >= 0 && iy >= 0 && iz >= 0 && ix < d->m[0] && iy < d->m[1] && iz < d->m[2])
+        return a[ix + d->m[0] * (iy + d->m[1] * iz)];
+    uint32_t s = far_pkg_virtual(d->g, d->prims, d->n_prims, fdiv4(ix), fdiv4(iy), fdiv4(iz));
+    return s == 0 ? -d->far : d->far;
+}
+
+/* is the cell owning fine index I active?  (in-domain only) */
+static inline int point_active(const dense_ctx* d, int64_t ix, int64_t iy, int64_t iz) {
+    return d->bg[lin_cell(d->g, ix / 4, iy / 4, iz / 4)] >= 2;
+}
+
+/* ----------------------------------------------------------------- O6 -- */
+/* Initial level set at every data point of every package:
+ * phi = init_scale * f(point) for points of active cells, far constant by
+ * sign elsewhere (Fig. 2 caption). */
+void or_phi_dense(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
+                  double* phi) {
+    dense_ctx d;
+    dense_init(&d, g, prims, n_prims, bg);
+    const double s = init_scale(g);
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t iz = 0; iz < d.m[2]; ++iz)
+        for (int64_t iy = 0; iy < d.m[1]; ++iy)
+            for (int64_t ix = 0; ix < d.m[0]; ++ix) {
+                uint32_t b = bg[lin_cell(g, ix / 4, iy / 4, iz / 4)];
+                double v;
+                if (b >= 2) {
+                    double x[3];
+                    point_pos(g, ix, iy, iz, x);
+                    v = s * or_sdf(prims, n_prims, x);
+                } else {
+                    v = b == 0 ? -d.far : d.far;
+                }
+                phi[ix + d.m[0] * (iy + d.m[1] * iz)] = v;
+            }
+}
+
+/* one point of O6 (for sampled checks at sizes where dense is too big) */
+double or_phi_point(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
+                    int64_t ix, int64_t iy, int64_t iz) {
+    dense_ctx d;
+    dense_init(&d, g, prims, n_prims, bg);
+    if (!(ix >= 0 && iy >= 0 && iz >= 0 && ix < d.m[0] && iy < d.m[1] && iz < d.m[2])) {
+        uint32_t sgn = far_pkg_virtual(g, prims, n_prims, fdiv4(ix), fdiv4(iy), fdiv4(iz));
+        return sgn == 0 ? -d.far : d.far;
+    }
+    uint32_t b = bg[lin_cell(g, ix / 4, iy / 4, iz / 4)];
+    if (b < 2) return b == 0 ? -d.far : d.far;
+    double x[3];
+    point_pos(g, ix, iy, iz, x);
+    return init_scale(g) * or_sdf(prims, n_prims, x);
+}
+
+/* ----------------------------------------------------------------- O7 -- */
+/* One Jacobi step of upwind Godunov reinitialisation (reading R-12: named by
+ * BASELINE.json north_star; the paper implies it):
+ *   s   = phi / sqrt(phi^2 + dx^2)
+ *   a_k = (phi_I - phi_{I-e_k}) / dx,  b_k = (phi_{I+e_k} - phi_I) / dx
+ *   phi > 0: g_k^2 = max(max(a,0)^2, min(b,0)^2)
+ *   phi < 0: g_k^2 = max(min(a,0)^2, max(b,0)^2)
+ *   phi' = phi - cfl dx s (sqrt(sum g_k^2) - 1);  phi == 0 stays 0.
+ * Active points only; inactive points are copied. */
+static inline double reinit_point(double c, const double nbm[3], const double nbp[3], double dx,
+                                  double cfl) {
+    if (c == 0.0) return c;
+    double s = c / sqrt(c * c + dx * dx);
+    double g2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        double a = (c - nbm[k]) / dx;
+        double b = (nbp[k] - c) / dx;
+        double u, v;
+        if (c > 0.0) {
+            u = fmax(a, 0.0);
+            v = fmin(b, 0.0);
+        } else {
+            u = fmin(a, 0.0);
+            v = fmax(b, 0.0);
+        }
+        g2 += fmax(u * u, v * v);
+    }
+    return c - cfl * dx * s * (sqrt(g2) - 1.0);
+}
+
+void or_reinit_dense(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
+                     const double* phi, double* out, double cfl) {
+    dense_ctx d;
+    dense_init(&d, g, prims, n_prims, bg);
+    const double dx = data_spacing(g);
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t iz = 0; iz < d.m[2]; ++iz)
+        for (int64_t iy = 0; iy < d.m[1]; ++iy)
+            for (int64_t ix = 0; ix < d.m[0]; ++ix) {
+                int64_t I = ix + d.m[0] * (iy + d.m[1] * iz);
+                if (!point_active(&d, ix, iy, iz)) {
+                    out[I] = phi[I];
+                    continue;
+                }
+                double nbm[3] = {dense_get(&d, phi, ix - 1, iy, iz), dense_get(&d, phi, ix, iy - 1, iz),
+                                 dense_get(&d, phi, ix, iy, iz - 1)};
+                double nbp[3] = {dense_get(&d, phi, ix + 1, iy, iz), dense_get(&d, phi, ix, iy + 1, iz),
+                                 dense_get(&d, phi, ix, iy, iz + 1)};
+                out[I] = reinit_point(phi[I], nbm, nbp, dx, cfl);
+            }
+}
+
+/* first reinit step at one point, inputs from O6 (sampled checks) */
+double or_reinit_point_from_init(const or_grid* g, const or_prim* prims, int32_t n_prims,
+                                 const uint32_t* bg, int64_t ix, int64_t iy, int64_t iz,
+                                 double cfl) {
+    double c = or_phi_point(g, prims, n_prims, bg, ix, iy, iz);
+    if (bg[lin_cell(g, ix / 4, iy / 4, iz / 4)] < 2) return c;
+    double nbm[3] = {or_phi_point(g, prims, n_prims, bg, ix - 1, iy, iz),
+                     or_phi_point(g, prims, n_prims, bg, ix, iy - 1, iz),
+                     or_phi_point(g, prims, n_prims, bg, ix, iy, iz - 1)};
+    double nbp[3] = {or_phi_point(g, prims, n_prims, bg, ix + 1, iy, iz),
+                     or_phi_point(g, prims, n_prims, bg, ix, iy + 1, iz),
+                     or_phi_point(g, prims, n_prims, bg, ix, iy, iz + 1)};
+    return reinit_point(c, nbm, nbp, data_spacing(g), cfl);
+}
+
+/* ----------------------------------------------------------------- O8 -- */
+/* Gradient by Lst. 5 with regularize(d+, d-) = (d+ + d-)/2 and
+ * division by dx (R-13):  grad_k = (phi_{I+e_k} - phi_{I-e_k}) / (2 dx);
+ * normal = grad/|grad| (0 if |grad| == 0).  Inactive points: 0 (R-16).
+ * grad, normal: three dense planes each (component-major), may be NULL. */
+void or_gradient_dense(const or_grid* g, const or_prim* prims, int32_t n_prims,
+                       const uint32_t* bg, const double* phi, double* grad, double* normal) {
+    dense_ctx d;
+    dense_init(&d, g, prims, n_prims, bg);
+    const double dx = data_spacing(g);
+    const int64_t plane = d.m[0] * d.m[1] * d.m[2];
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t iz = 0; iz < d.m[2]; ++iz)
+        for (int64_t iy = 0; iy < d.m[1]; ++iy)
+            for (int64_t ix = 0; ix < d.m[0]; ++ix) {
+                int64_t I = ix + d.m[0] * (iy + d.m[1] * iz);
+                double gv[3] = {0.0, 0.0, 0.0};
+                if (point_active(&d, ix, iy, iz)) {
+                    gv[0] = (dense_get(&d, phi, ix + 1, iy, iz) - dense_get(&d, phi, ix - 1, iy, iz)) / (2.0 * dx);
+                    gv[1] = (dense_get(&d, phi, ix, iy + 1, iz) - dense_get(&d, phi, ix, iy - 1, iz)) / (2.0 * dx);
+                    gv[2] = (dense_get(&d, phi, ix, iy, iz + 1) - dense_get(&d, phi, ix, iy, iz - 1)) / (2.0 * dx);
+                }
+                double mag = sqrt((gv[0] * gv[0] + gv[1] * gv[1]) + gv[2] * gv[2]);
+                for (int k = 0; k < 3; ++k) {
+                    if (grad) grad[k * plane + I] = gv[k];
+                    if (normal) normal[k * plane + I] = mag > 0.0 ? gv[k] / mag : 0.0;
+                }
+            }
+}
+
+/* ----------------------------------------------------------------- O9 -- */
+/* Kernel integrals with an SPH smoothing kernel on the sparse grid
+ * (kernel and Heaviside are reading R-14):
+ *   Wendland C2 (3-D), h = h_ratio dx, support 2h,
+ *   w[o]  = W(|o| dx) dx^3,  gw[o] = W'(|o| dx) (-o/|o|) dx^3,
+ *   H(u)  = smoothed Heaviside, eps = dx,
+ *   K_I = sum_o w[o] H(-phi_{I+o}),  G_I = sum_o gw[o] H(-phi_{I+o}).
+ * Inactive points: K = S (negative far field) or 0, G = 0 (R-16). */
+
+#define OR_MAX_TAPS 512
+
+typedef struct {
+    int n;
+    int o[OR_MAX_TAPS][3];
+    double w[OR_MAX_TAPS];
+    double gw[OR_MAX_TAPS][3];
+} taps_t;
+
+static void make_taps(double h_ratio, double dx, taps_t* t) {
+    const double PI = 3.14159265358979323846;
+    const double h = h_ratio * dx;
+    const double sigma = 21.0 / (16.0 * PI * h * h * h);
+    const int R = (int)ceil(2.0 * h_ratio);
+    t->n = 0;
+    for (int oz = -R; oz <= R; ++oz)
+        for (int oy = -R; oy <= R; ++oy)
+            for (int ox = -R; ox <= R; ++ox) {
+                double len = sqrt((double)(ox * ox + oy * oy + oz * oz));
+                double r = len * dx;
+                if (!(r < 2.0 * h)) continue;
+                double q = r / h;
+                double omq = 1.0 - 0.5 * q;
+                double W = sigma * omq * omq * omq * omq * (2.0 * q + 1.0);
+                double dW = -5.0 * sigma * q * omq * omq * omq / h;
+                int k = t->n++;
+                t->o[k][0] = ox;
+                t->o[k][1] = oy;
+                t->o[k][2] = oz;
+                t->w[k] = W * dx * dx * dx;
+                double o3[3] = {(double)ox, (double)oy, (double)oz};
+                for (int a = 0; a < 3; ++a)
+                    t->gw[k][a] = len > 0.0 ? dW * (-o3[a] / len) * dx * dx * dx : 0.0;
+            }
+}
+
+/* tap table export: returns count; o (n x 3 int), w (n), gw (n x 3) */
+int32_t or_kernel_taps(double h_ratio, double dx, int32_t* o, double* w, double* gw) {
+    taps_t t;
+    make_taps(h_ratio, dx, &t);
+    for (int k = 0; k < t.n; ++k) {
+        for (int a = 0; a < 3; ++a) {
+            if (o) o[3 * k + a] = t.o[k][a];
+            if (gw) gw[3 * k + a] = t.gw[k][a];
+        }
+        if (w) w[k] = t.w[k];
+    }
+    return t.n;
+}
+
+double or_heaviside(double u, double eps) {
+    const double PI = 3.14159265358979323846;
+    if (u < -eps) return 0.0;
+    if (u > eps) return 1.0;
+    return 0.5 * (1.0 + u / eps + sin(PI * u / eps) / PI);
+}
+
+void or_kernel_dense(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
+                     const double* phi, double h_ratio, double* K, double* G) {
+    dense_ctx d;
+    dense_init(&d, g, prims, n_prims, bg);
+    const double dx = data_spacing(g);
+    const int64_t plane = d.m[0] * d.m[1] * d.m[2];
+    taps_t* t = (taps_t*)malloc(sizeof(taps_t));
+    make_taps(h_ratio, dx, t);
+    double S = 0.0;
+    for (int k = 0; k < t->n; ++k) S += t->w[k];
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+    for (int64_t iz = 0; iz < d.m[2]; ++iz)
+        for (int64_t iy = 0; iy < d.m[1]; ++iy)
+            for (int64_t ix = 0; ix < d.m[0]; ++ix) {
+                int64_t I = ix + d.m[0] * (iy + d.m[1] * iz);
+                double k_acc = 0.0, gacc[3] = {0.0, 0.0, 0.0};
+                uint32_t b = bg[lin_cell(g, ix / 4, iy / 4, iz / 4)];
+                if (b >= 2) {
+                    for (int k = 0; k < t->n; ++k) {
+                        double v = dense_get(&d, phi, ix + t->o[k][0], iy + t->o[k][1], iz + t->o[k][2]);
+                        double H = or_heaviside(-v, dx);
+                        k_acc += t->w[k] * H;
+                        for (int a = 0; a < 3; ++a) gacc[a] += t->gw[k][a] * H;
+                    }
+                } else if (b == 0) {
+                    k_acc = S;
+                }
+                if (K) K[I] = k_acc;
+                if (G)
+                    for (int a = 0; a < 3; ++a) G[a * plane + I] = gacc[a];
+            }
+    free(t);
+}
+
+/* ---------------------------------------------------------------- O10 -- */
+/* Grid-particle coupling: containing-cell lookup through the
+ * background table, far constant for inactive cells, otherwise trilinear
+ * interpolation over the 8 data points around the position (R-15).  Index
+ * arithmetic in double: division and floor only.  Out-of-domain or NaN
+ * positions return (+far, 0) and are counted.
+ *   pos: n x 3 doubles; grad3: dense 3-plane gradient or NULL;
+ *   out_phi: n; out_grad: n x 3 or NULL.  Returns the OOB count. */
+int64_t or_probe(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
+                 const double* phi, const double* grad3, int64_t n, const double* pos,
+                 double* out_phi, double* out_grad) {
+    dense_ctx d;
+    dense_init(&d, g, prims, n_prims, bg);
+    const double dx = data_spacing(g);
+    const int64_t plane = d.m[0] * d.m[1] * d.m[2];
+    int64_t oob = 0;
+#pragma omp parallel for schedule(static) reduction(+ : oob)
+    for (int64_t p = 0; p < n; ++p) {
+        const double* x = pos + 3 * p;
+        double rphi = d.far, rg[3] = {0.0, 0.0, 0.0};
+        int ok = 1;
+        int64_t c[3];
+        for (int k = 0; k < 3; ++k) {
+            double upper = g->lower[k] + (double)g->n[k] * g->cell;
+            if (!(x[k] >= g->lower[k] && x[k] < upper)) {
+                ok = 0;
+                break;
+            }
+            c[k] = (int64_t)floor((x[k] - g->lower[k]) / g->cell);
+            if (c[k] > g->n[k] - 1) c[k] = g->n[k] - 1;
+        }
+        if (!ok) {
+            oob++;
+        } else {
+            uint32_t b = bg[lin_cell(g, c[0], c[1], c[2])];
+            if (b < 2) {
+                rphi = b == 0 ? -d.far : d.far;
+            } else {
+                int64_t a[3];
+                double t[3];
+                for (int k = 0; k < 3; ++k) {
+                    double u = (x[k] - g->lower[k]) / dx - 0.5;
+                    double fl = floor(u);
+                    a[k] = (int64_t)fl;
+                    t[k] = u - fl;
+                }
+                rphi = 0.0;
+                for (int bidx = 0; bidx < 8; ++bidx) {
+                    int b0 = bidx & 1, b1 = (bidx >> 1) & 1, b2 = (bidx >> 2) & 1;
+                    double w = ((b0 ? t[0] : 1.0 - t[0]) * (b1 ? t[1] : 1.0 - t[1])) *
+                               (b2 ? t[2] : 1.0 - t[2]);
+                    int64_t ix = a[0] + b0, iy = a[1] + b1, iz = a[2] + b2;
+                    rphi += w * dense_get(&d, phi, ix, iy, iz);
+                    if (grad3) {
+                        int in = ix >= 0 && iy >= 0 && iz >= 0 && ix < d.m[0] && iy < d.m[1] && iz < d.m[2];
+                        if (in) {
+                            int64_t I = ix + d.m[0] * (iy + d.m[1] * iz);
+                            for (int k = 0; k < 3; ++k) rg[k] += w * grad3[k * plane + I];
+                        }
+                    }
+                }
+            }
+        }
+        out_phi[p] = rphi;
+        if (out_grad)
+            for (int k = 0; k < 3; ++k) out_grad[3 * p + k] = rg[k];
+    }
+    return oob;
+}
+
+/* ------------------------------------------------------- layout helper -- */
+/* Gather a dense scalar plane into package-major order using the oracle's
+ * own meta table: out[id][i + 4 j + 16 k] = dense[4c + (i,j,k)] (R-9
+ * canonical order).  Singular packages take `far_neg` / `far_pos`. */
+void or_gather_packages(const or_grid* g, const double* dense, const uint32_t* meta_cell,
+                        int64_t n_pkg, double far_neg, double far_pos, double* out) {
+    const int64_t nx = g->n[0], ny = g->n[1];
+    const int64_t m0 = (int64_t)PKG * g->n[0], m1 = (int64_t)PKG * g->n[1];
+    for (int d = 0; d < 64; ++d) {
+        out[d] = far_neg;
+        out[64 + d] = far_pos;
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t id = 2; id < n_pkg; ++id) {
+        int64_t L = meta_cell[id];
+        int64_t cx = L % nx, cy = (L / nx) % ny, cz = L / (nx * ny);
+        for (int k = 0; k < 4; ++k)
+            for (int j = 0; j < 4; ++j)
+                for (int i = 0; i < 4; ++i)
+                    out[id * 64 + i + 4 * j + 16 * k] =
+                        dense[(4 * cx + i) + m0 * ((4 * cy + j) + m1 * (4 * cz + k))];
+    }
+}
+
+void or_set_threads(int32_t n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
+int32_t or_get_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -1,0 +1,585 @@
+"""Pins of the CPU oracle against things other than itself (CPU only).
+
+Each test names what fixes the expected value: a closed form, a brute-force
+enumeration of the definition on tiny inputs, a library routine, an
+invariant, or a number printed in SURVEY.md/SPEC.md (tests/golden, cited).
+Readings R-n refer to DESIGN.md "Readings" (= SURVEY.md 8(c.3)).
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+from scipy.spatial import cKDTree
+
+import workloads as W
+from conftest import golden
+
+# --------------------------------------------------------------- O1: SDFs --
+
+
+def _fib_sphere(c, r, n):
+    i = np.arange(n) + 0.5
+    phi = np.arccos(1 - 2 * i / n)
+    th = math.pi * (1 + 5 ** 0.5) * i
+    d = np.stack([np.cos(th) * np.sin(phi), np.sin(th) * np.sin(phi), np.cos(phi)], 1)
+    return np.asarray(c) + r * d
+
+
+def _grid2(n):
+    u = (np.arange(n) + 0.5) / n
+    a, b = np.meshgrid(u, u, indexing="ij")
+    return a.ravel(), b.ravel()
+
+
+def _box_surface(c, b, n):
+    pts = []
+    a, bb = _grid2(n)
+    for ax in range(3):
+        o1, o2 = [k for k in range(3) if k != ax]
+        for s in (-1, 1):
+            p = np.empty((a.size, 3))
+            p[:, ax] = c[ax] + s * b[ax]
+            p[:, o1] = c[o1] + (2 * a - 1) * b[o1]
+            p[:, o2] = c[o2] + (2 * bb - 1) * b[o2]
+            pts.append(p)
+    return np.concatenate(pts)
+
+
+def _torus_surface(c, R, r, axis, n):
+    th, ph = _grid2(n)
+    th = th * 2 * math.pi
+    ph = ph * 2 * math.pi
+    rad = R + r * np.cos(ph)
+    # local frame: symmetry axis -> 'axis'
+    u, v, w = rad * np.cos(th), r * np.sin(ph), rad * np.sin(th)
+    p = np.empty((u.size, 3))
+    others = [k for k in range(3) if k != axis]
+    p[:, others[0]] = u
+    p[:, axis] = v
+    p[:, others[1]] = w
+    return p + np.asarray(c)
+
+
+def _prism_surface(p, n):
+    A, B, Cc = np.array(p[0:2]), np.array(p[2:4]), np.array(p[4:6])
+    z0, z1 = p[6], p[7]
+    pts = []
+    s, t = _grid2(n)
+    m = s + t <= 1
+    tri = A + np.outer(s[m], B - A) + np.outer(t[m], Cc - A)
+    for z in (z0, z1):
+        pts.append(np.column_stack([tri, np.full(len(tri), z)]))
+    for P0, P1 in ((A, B), (B, Cc), (Cc, A)):
+        e = P0 + np.outer(s, P1 - P0)
+        pts.append(np.column_stack([e, z0 + t * (z1 - z0)]))
+    return np.concatenate(pts)
+
+
+def _surface(prim, n):
+    k, p = prim.kind, prim.p
+    if k == W.SPHERE:
+        return _fib_sphere(p[:3], p[3], n * n)
+    if k == W.SHELL:
+        return np.concatenate([_fib_sphere(p[:3], p[3], n * n), _fib_sphere(p[:3], p[4], n * n)])
+    if k == W.BOX:
+        return _box_surface(p[:3], p[3:6], n)
+    if k in (W.TORUS_X, W.TORUS_Y, W.TORUS_Z):
+        return _torus_surface(p[:3], p[3], p[4], k - W.TORUS_X, n)
+    if k == W.TRIPRISM_Z:
+        return _prism_surface(p, n)
+    raise ValueError(k)
+
+
+def _inside(prim, x):
+    """Plain containment predicates (sign check only)."""
+    k, p = prim.kind, prim.p
+    e = x - np.asarray(p[:3]) if k != W.TRIPRISM_Z else None
+    if k == W.SPHERE:
+        return np.linalg.norm(e, axis=1) < p[3]
+    if k == W.SHELL:
+        d = np.linalg.norm(e, axis=1)
+        return (d > p[3]) & (d < p[4])
+    if k == W.BOX:
+        return np.all(np.abs(e) < np.asarray(p[3:6]), axis=1)
+    if k in (W.TORUS_X, W.TORUS_Y, W.TORUS_Z):
+        ax = k - W.TORUS_X
+        o = [j for j in range(3) if j != ax]
+        ring = np.hypot(e[:, o[0]], e[:, o[1]])
+        return np.hypot(ring - p[3], e[:, ax]) < p[4]
+    raise ValueError(k)
+
+
+def _inside_prism(p, x):
+    ok = (x[:, 2] > p[6]) & (x[:, 2] < p[7])
+    for e in range(3):
+        ax, ay = p[2 * e], p[2 * e + 1]
+        bx, by = p[2 * ((e + 1) % 3)], p[2 * ((e + 1) % 3) + 1]
+        ok &= (bx - ax) * (x[:, 1] - ay) - (by - ay) * (x[:, 0] - ax) > 0
+    return ok
+
+
+PRIMS = [
+    W.Prim(W.SPHERE, (0.5, 0.5, 0.5, 0.3)),
+    W.Prim(W.SHELL, (0.5, 0.45, 0.55, 0.2, 0.26)),
+    W.Prim(W.BOX, (0.5, 0.5, 0.5, 0.1, 0.2, 0.3)),
+    W.Prim(W.TORUS_X, (0.5, 0.5, 0.5, 0.25, 0.07)),
+    W.Prim(W.TORUS_Y, (0.5, 0.5, 0.5, 0.3, 0.08)),
+    W.Prim(W.TORUS_Z, (0.5, 0.5, 0.5, 0.2, 0.1)),
+    W.prism_teaser(),
+]
+
+
+@pytest.mark.parametrize("prim", PRIMS, ids=lambda p: f"kind{p.kind}")
+def test_sdf_matches_brute_force_surface_distance(oracle_lib, prim):
+    """|f| equals the distance to a dense surface sampling (brute force,
+    scipy KD-tree) within the sampling gap; the sign is negative exactly for
+    points a plain containment predicate puts inside.  Pins O1."""
+    w = W.Workload("t", (16, 16, 16), 1 / 16, prims=(prim,))
+    o = oracle_lib.Oracle(w)
+    n = 700
+    surf = _surface(prim, n)
+    tree = cKDTree(surf)
+    # covering radius of the sampling: distance from an independent, offset
+    # sampling of the same surface to the nearest sample
+    gap = float(np.max(tree.query(_surface(prim, n + 37))[0]))
+    rng = np.random.default_rng(7)
+    x = rng.uniform(0.02, 0.98, size=(4000, 3))
+    f = o.sdf(x)
+    d_bf, _ = tree.query(x)
+    # sampling only over-estimates the distance, by at most ~ the gap
+    assert np.all(np.abs(f) <= d_bf + 1e-12)
+    assert np.all(d_bf - np.abs(f) <= 2.0 * gap), float(np.max(d_bf - np.abs(f)))
+    inside = _inside_prism(prim.p, x) if prim.kind == W.TRIPRISM_Z else _inside(prim, x)
+    clear = d_bf > 2 * gap
+    assert np.array_equal(f[clear] < 0, inside[clear])
+
+
+def test_sdf_closed_forms(oracle_lib):
+    """Closed forms at special points."""
+    def sdf(prim, pts):
+        return oracle_lib.Oracle(W.Workload("t", (8, 8, 8), 1 / 8, prims=(prim,))).sdf(pts)
+
+    assert sdf(PRIMS[0], [[0.5, 0.5, 0.5]])[0] == -0.3                  # sphere centre = -r
+    assert abs(sdf(PRIMS[0], [[0.9, 0.5, 0.5]])[0] - 0.1) < 1e-15       # on-axis outside
+    box = PRIMS[2]
+    assert abs(sdf(box, [[0.5, 0.5, 0.5]])[0] + 0.1) < 1e-15            # centre = -min(b)
+    assert abs(sdf(box, [[0.5, 0.5, 0.9]])[0] - 0.1) < 1e-15            # face distance
+    assert abs(sdf(box, [[0.7, 0.8, 0.9]])[0] - math.sqrt(0.1**2 + 0.1**2 + 0.1**2)) < 1e-15
+    assert abs(sdf(PRIMS[4], [[0.8, 0.5, 0.5]])[0] + 0.08) < 1e-15      # tube centre = -r
+    assert abs(sdf(PRIMS[4], [[0.5, 0.5, 0.5]])[0] - (math.hypot(0.3, 0) - 0.08)) < 1e-15
+    pr = PRIMS[6]
+    # prism centroid: max(-inradius, -half length) = -0.2 for circumradius 0.4
+    assert abs(sdf(pr, [[0.5, 0.5, 0.5]])[0] + 0.2) < 1e-12
+    assert abs(sdf(pr, [[0.5, 0.5, 0.95]])[0] - 0.1) < 1e-12            # above the top cap
+    shell = PRIMS[1]
+    assert abs(sdf(shell, [[0.5, 0.45, 0.55]])[0] - 0.2) < 1e-15        # centre of a shell
+    # union = min, in order
+    u = oracle_lib.Oracle(W.Workload("u", (8, 8, 8), 1 / 8, prims=(PRIMS[0], PRIMS[2])))
+    x = np.random.default_rng(1).uniform(0, 1, (100, 3))
+    assert np.array_equal(u.sdf(x), np.minimum(sdf(PRIMS[0], x), sdf(PRIMS[2], x)))
+
+
+# ------------------------------------------------------- O3-O5: tables ------
+
+
+def _brute_tables(o, w):
+    """The definition (R-1..R-6), enumerated with Python loops."""
+    nx, ny, nz = w.n
+    cells = list(itertools.product(range(nz), range(ny), range(nx)))  # z slowest
+    centres = np.array([[w.lower[0] + (cx + 0.5) * w.cell, w.lower[1] + (cy + 0.5) * w.cell,
+                         w.lower[2] + (cz + 0.5) * w.cell] for cz, cy, cx in cells])
+    f = o.sdf(centres)
+    core = {c: abs(v) < w.cell for c, v in zip(cells, f)}
+    neg = {c: v < 0 for c, v in zip(cells, f)}
+    active, cat = {}, {}
+    for (cz, cy, cx) in cells:
+        if core[(cz, cy, cx)]:
+            cat[(cz, cy, cx)] = 3
+            continue
+        inner = False
+        for oz, oy, ox in itertools.product((-1, 0, 1), repeat=3):
+            q = (cz + oz, cy + oy, cx + ox)
+            if q in core and core[q]:
+                inner = True
+        cat[(cz, cy, cx)] = 2 if inner else (0 if neg[(cz, cy, cx)] else 1)
+    bg = np.zeros(nx * ny * nz, np.uint32)
+    meta_cell = [0xFFFFFFFF, 0xFFFFFFFF]
+    meta_cat = [0, 1]
+    nid = 2
+    for L, c in enumerate(cells):
+        if cat[c] >= 2:
+            bg[L] = nid
+            active[c] = nid
+            meta_cell.append(L)
+            meta_cat.append(cat[c])
+            nid += 1
+        else:
+            bg[L] = cat[c]
+    nb = np.zeros((nid, 27), np.uint32)
+    nb[1, :] = 1
+    for (cz, cy, cx), pid in active.items():
+        for oz, oy, ox in itertools.product(range(3), repeat=3):
+            q = (cz + oz - 1, cy + oy - 1, cx + ox - 1)
+            if q in cat:
+                v = bg[q[2] + nx * (q[1] + ny * q[0])]
+            else:
+                xc = [w.lower[0] + (q[2] + 0.5) * w.cell, w.lower[1] + (q[1] + 0.5) * w.cell,
+                      w.lower[2] + (q[0] + 0.5) * w.cell]
+                v = 0 if o.sdf([xc])[0] < 0 else 1
+            nb[pid, ox + 3 * oy + 9 * oz] = v
+    return bg, np.array(meta_cell, np.uint32), np.array(meta_cat, np.uint8), nb
+
+
+@pytest.mark.parametrize("seed,n", [(0, 8), (1, 10), (2, 12), (3, 9), (4, 8), (5, 11)])
+def test_tables_equal_brute_force_definition(oracle_lib, seed, n):
+    w = W.random_scene(seed, n)
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    bg, mc, mk, nb = _brute_tables(o, w)
+    assert np.array_equal(t.bg, bg)
+    assert np.array_equal(t.meta_cell, mc)
+    assert np.array_equal(t.meta_cat, mk)
+    assert np.array_equal(t.nb, nb)
+
+
+def test_tables_c1_brute_force(oracle_lib):
+    w = W.config("C1")
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    bg, mc, mk, nb = _brute_tables(o, w)
+    assert np.array_equal(t.bg, bg) and np.array_equal(t.nb, nb)
+    assert np.array_equal(t.meta_cell, mc) and np.array_equal(t.meta_cat, mk)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "T1", "C3"])
+def test_tagging_counts_match_independent_numbers(oracle_lib, name):
+    """Counts from an independent numpy tagging."""
+    exp = golden("tagging_counts.json")[name]
+    o = oracle_lib.Oracle(W.config(name))
+    t = o.build_tables()
+    assert int(np.count_nonzero(t.cat == 3)) == exp["core"]
+    assert int(np.count_nonzero(t.cat == 2)) == exp["inner"]
+    assert t.n_pkg - 2 == exp["packages"]
+    assert t.near_ties == 0  # R-2: no near-ties on the configs
+
+
+def test_table_invariants(oracle_lib):
+    """Bijection bg<->meta, centre slot = self, singular rows
+    self, core rows never reach the far field (R-3), plane counts
+    partition the ids (R-1)."""
+    w = W.config("C2")
+    t = oracle_lib.Oracle(w).build_tables()
+    ids = np.arange(2, t.n_pkg)
+    assert np.array_equal(t.bg[t.meta_cell[2:]], ids.astype(np.uint32))
+    act = np.nonzero(t.bg >= 2)[0]
+    assert np.array_equal(t.meta_cell[t.bg[act]], act.astype(np.uint32))
+    assert np.all(np.diff(t.meta_cell[2:].astype(np.int64)) > 0)  # ascending L
+    assert np.array_equal(t.nb[ids, 13], ids.astype(np.uint32))
+    assert np.all(t.nb[0] == 0) and np.all(t.nb[1] == 1)
+    core = ids[t.meta_cat[2:] == 3]
+    assert np.all(t.nb[core] >= 2)
+    assert int(t.plane_count.sum()) == t.n_pkg - 2
+
+
+def test_memory_audit_topology_bytes(oracle_lib):
+    """Topology per package = 27 u32 neighbour words + meta (u32 cell + u8
+    category), independent of the number of fields."""
+    t = oracle_lib.Oracle(W.config("C1")).build_tables()
+    per_pkg = (t.nb.nbytes + t.meta_cell.nbytes + t.meta_cat.nbytes) / t.n_pkg
+    assert per_pkg == 27 * 4 + 4 + 1
+    # the eliminated per-datum address skin of the old design: 6x6x8 = 288 B
+    # per cell per variable in 2-D; in 3-D 6^3 x 8 = 1728 B.
+    assert 6 * 6 * 8 == 288 and per_pkg < 6 * 6 * 6 * 8
+
+
+# ------------------------------------------------------------- O6: init ----
+
+
+def test_phi_init_closed_form(oracle_lib):
+    """Data points at lower + (I + 1/2) dx (R-11); active cells hold
+    init_scale * (|x - c| - r) for the sphere; inactive the far constant."""
+    for scale in (1.0, 2.0):
+        w = W.config("C1").with_(init_scale=scale)
+        o = oracle_lib.Oracle(w)
+        t = o.build_tables()
+        phi = o.phi_dense()
+        m = 4 * w.n[0]
+        I = (np.arange(m) + 0.5) * w.dx
+        Z, Y, X = np.meshgrid(I, I, I, indexing="ij")
+        exact = scale * (np.sqrt((X - 0.5) ** 2 + (Y - 0.5) ** 2 + (Z - 0.5) ** 2) - 0.3)
+        cells = t.bg.reshape(w.n[2], w.n[1], w.n[0])
+        cb = np.repeat(np.repeat(np.repeat(cells, 4, 0), 4, 1), 4, 2)
+        act = cb >= 2
+        assert np.max(np.abs(phi[act] - exact[act])) < 1e-15
+        far = 4 * w.cell * max(1.0, scale)
+        assert np.all(phi[cb == 0] == -far) and np.all(phi[cb == 1] == far)
+        # reading R-4: every band value is strictly inside the far constant
+        assert np.max(np.abs(phi[act])) < far
+
+
+# ------------------------------------------------------------ O7: reinit ----
+
+
+def _box_face_world():
+    # big box; around the +x face centre the SDF is exactly x - 0.8 (planar)
+    return W.Workload("box", (16, 16, 16), 1 / 16, dtype="f64",
+                      prims=(W.Prim(W.BOX, (0.5, 0.5, 0.5, 0.3, 0.3, 0.3)),))
+
+
+def _planar_region(w, o):
+    m = 4 * w.n[0]
+    I = np.arange(m)
+    x = (I + 0.5) * w.dx
+    sel_x = (x > 0.8 - 6 * w.dx) & (x < 0.8 + 6 * w.dx)
+    sel_yz = (x > 0.4) & (x < 0.6)
+    return np.ix_(sel_yz, sel_yz, sel_x)
+
+
+def test_reinit_planar_fixed_point(oracle_lib):
+    """Exact SDF of a plane is a fixed point: per-step change is
+    rounding only (< 1e-10 dx)."""
+    w = _box_face_world()
+    o = oracle_lib.Oracle(w)
+    o.build_tables()
+    phi = o.phi_dense()
+    out = o.reinit_step(phi, 0.3)
+    reg = _planar_region(w, o)
+    assert np.max(np.abs(out[reg] - phi[reg])) < 1e-10 * w.dx
+
+
+def test_reinit_linear_slope2_closed_form(oracle_lib):
+    """phi = 2 (x - 0.8) (init_scale 2) on the planar region: every Godunov
+    upwind difference is 2 on both sides of the front and 0 across it, so one
+    step is phi - cfl dx * phi/sqrt(phi^2+dx^2) * (2 - 1) on both signs."""
+    w = _box_face_world().with_(init_scale=2.0)
+    o = oracle_lib.Oracle(w)
+    o.build_tables()
+    phi = o.phi_dense()
+    out = o.reinit_step(phi, 0.3)
+    reg = _planar_region(w, o)
+    p = phi[reg]
+    expect = p - 0.3 * w.dx * (p / np.sqrt(p * p + w.dx**2)) * 1.0
+    assert np.max(np.abs(out[reg] - expect)) < 1e-14
+    assert (p > 0).any() and (p < 0).any()
+
+
+def test_reinit_converges_to_distance(oracle_lib):
+    """From 2*SDF, 100 steps at cfl 0.3: band mean ||grad phi| - 1| < 0.05 in
+    core packages away from kinks, measured with numpy's own
+    gradient; no sign flip where |phi0| > 2 dx; zero level stays within
+    dx/4 of the exact sphere."""
+    w = W.Workload("sph", (24, 24, 24), 1 / 24, dtype="f64", init_scale=2.0,
+                   prims=(W.Prim(W.SPHERE, (0.5, 0.5, 0.5, 0.3)),))
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    phi0 = o.phi_dense()
+    phi = o.reinit(phi0, 100, 0.3)
+    cells = t.bg.reshape(w.n[::-1])
+    catd = t.cat.reshape(w.n[::-1])
+    cb = np.repeat(np.repeat(np.repeat(catd, 4, 0), 4, 1), 4, 2)
+    gz, gy, gx = np.gradient(phi, w.dx)
+    mag = np.sqrt(gx**2 + gy**2 + gz**2)
+    core = cb == 3
+    assert np.mean(np.abs(mag[core] - 1)) < 0.05
+    band = (cb >= 2) & (np.abs(phi0) > 2 * w.dx)
+    assert np.all(np.sign(phi[band]) == np.sign(phi0[band]))
+    # near-surface agreement with the exact distance
+    exact = phi0 / 2.0
+    near = (cb >= 2) & (np.abs(exact) < w.dx)
+    assert np.max(np.abs(phi[near] - exact[near])) < 0.25 * w.dx
+    assert cells.size == t.bg.size
+
+
+def test_reinit_point_from_init_matches_dense(oracle_lib):
+    w = W.config("C1")
+    o = oracle_lib.Oracle(w)
+    o.build_tables()
+    dense = o.reinit_step(o.phi_dense(), 0.3)
+    rng = np.random.default_rng(3)
+    for ix, iy, iz in rng.integers(0, 64, size=(200, 3)):
+        assert o.reinit_point_from_init(ix, iy, iz, 0.3) == dense[iz, iy, ix]
+
+
+# ---------------------------------------------------------- O8: gradient ----
+
+
+def test_gradient_exact_on_affine(oracle_lib):
+    w = W.config("C1")
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    m = 4 * w.n[0]
+    I = (np.arange(m) + 0.5) * w.dx
+    Z, Y, X = np.meshgrid(I, I, I, indexing="ij")
+    a = np.array([0.3, -0.7, 0.2])
+    phi = a[0] * X + a[1] * Y + a[2] * Z + 0.1
+    g, n = o.gradient(phi)
+    cb = np.repeat(np.repeat(np.repeat(t.bg.reshape(w.n[::-1]), 4, 0), 4, 1), 4, 2)
+    act = cb >= 2
+    for k in range(3):
+        assert np.max(np.abs(g[k][act] - a[k])) < 1e-12
+        assert np.max(np.abs(n[k][act] - a[k] / np.linalg.norm(a))) < 1e-12
+        assert np.all(g[k][~act] == 0) and np.all(n[k][~act] == 0)
+
+
+def test_gradient_sphere_radial(oracle_lib):
+    w = W.Workload("sph", (32, 32, 32), 1 / 32, dtype="f64",
+                   prims=(W.Prim(W.SPHERE, (0.5, 0.5, 0.5, 0.3)),))
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    phi = o.phi_dense()
+    g, n = o.gradient(phi)
+    m = 4 * w.n[0]
+    I = (np.arange(m) + 0.5) * w.dx
+    Z, Y, X = np.meshgrid(I, I, I, indexing="ij")
+    R = np.sqrt((X - .5) ** 2 + (Y - .5) ** 2 + (Z - .5) ** 2)
+    cat = np.repeat(np.repeat(np.repeat(t.cat.reshape(w.n[::-1]), 4, 0), 4, 1), 4, 2)
+    core = cat == 3
+    for k, C in enumerate((X, Y, Z)):
+        radial = (C - 0.5) / R
+        # central difference of |x| is second-order: error ~ (dx/r)^2
+        assert np.max(np.abs(n[k][core] - radial[core])) < 4 * (w.dx / 0.2) ** 2
+
+
+# ---------------------------------------------------- O9: kernel integral ----
+
+
+@pytest.mark.parametrize("hr,key", [(1.3, "1.3"), (1.0, "1.0")])
+def test_kernel_tap_sums(oracle_lib, hr, key):
+    gold = golden("kernel_sums.json")
+    for dx in (1 / 64, 1 / 512, 1 / 4096):
+        o, w, gw = oracle_lib.kernel_taps(hr, dx)
+        assert len(w) == gold["taps_" + key]
+        assert abs(w.sum() - gold["S_" + key]) < 1e-13
+        # antisymmetric gradient weights sum to zero; gw[0] = 0
+        assert np.max(np.abs(gw.sum(0))) < 1e-9 / dx
+        assert np.all(gw[(o == 0).all(1)] == 0)
+        # the continuum kernel integrates to 1: quadrature within 4 %
+        assert abs(w.sum() - 1) < 0.04
+
+
+def test_kernel_integral_closed_forms(oracle_lib):
+    """Deep interior K = S, G = 0; deep exterior K = 0; planar interface
+    through a data point K = S/2 (H(u) + H(-u) = 1 and symmetric taps), G along
+    -n."""
+    w = W.config("C1")
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    S = golden("kernel_sums.json")["S_1.3"]
+    m = 4 * w.n[0]
+    cb = np.repeat(np.repeat(np.repeat(t.bg.reshape(w.n[::-1]), 4, 0), 4, 1), 4, 2)
+    act = cb >= 2
+    K, G = o.kernel_integrals(np.full((m, m, m), -1.0), 1.3)
+    assert np.max(np.abs(K[act] - S)) < 1e-13 and np.max(np.abs(G[:, act])) < 1e-9
+    K, G = o.kernel_integrals(np.full((m, m, m), 1.0), 1.3)
+    assert np.max(np.abs(K[act])) == 0 and np.max(np.abs(G[:, act])) == 0
+    # inactive convention R-16
+    assert np.all(K[cb == 0] == pytest.approx(S)) and np.all(K[cb == 1] == 0)
+    # plane x = x_j through data points j: phi = x - x_j
+    I = (np.arange(m) + 0.5) * w.dx
+    Z, Y, X = np.meshgrid(I, I, I, indexing="ij")
+    xj = I[30]
+    K, G = o.kernel_integrals(X - xj, 1.3)
+    on = act & (np.abs(X - xj) < 1e-12)
+    assert on.sum() > 50
+    assert np.max(np.abs(K[on] - S / 2)) < 1e-14
+    assert np.all(G[0][on] < 0)
+    assert np.max(np.abs(G[1][on])) < 1e-9 and np.max(np.abs(G[2][on])) < 1e-9
+    # K is monotone across the plane and bounded by [0, S]
+    assert K[act].min() >= -1e-15 and K[act].max() <= S + 1e-14
+
+
+def test_heaviside(oracle_lib):
+    eps = 0.1
+    assert oracle_lib.heaviside(-0.2, eps) == 0 and oracle_lib.heaviside(0.2, eps) == 1
+    assert oracle_lib.heaviside(0.0, eps) == 0.5
+    for u in np.linspace(-eps, eps, 11):
+        assert abs(oracle_lib.heaviside(u, eps) + oracle_lib.heaviside(-u, eps) - 1) < 1e-15
+
+
+# -------------------------------------------------------------- O10: probe --
+
+
+def test_probe_affine_reproduction_and_far(oracle_lib):
+    """Trilinear interpolation reproduces affine fields exactly;
+    inactive cells give the far constants; outside/NaN are counted OOB
+    (S:187-189 batch form)."""
+    w = W.config("C1")
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    m = 4 * w.n[0]
+    I = (np.arange(m) + 0.5) * w.dx
+    Z, Y, X = np.meshgrid(I, I, I, indexing="ij")
+    a = np.array([0.3, -0.7, 0.2])
+    phi = a[0] * X + a[1] * Y + a[2] * Z + 0.1
+    grad = np.stack([np.full_like(phi, v) for v in (1.0, 2.0, 3.0)])
+    rng = np.random.default_rng(5)
+    pos = rng.uniform(0.1, 0.9, (20000, 3))
+    c = np.floor(pos / w.cell).astype(int)
+    active = t.bg[c[:, 0] + 16 * (c[:, 1] + 16 * c[:, 2])] >= 2
+    pphi, pg, oob = o.probe(phi, grad, pos)
+    assert oob == 0
+    exact = pos @ a + 0.1
+    assert np.max(np.abs(pphi[active] - exact[active])) < 1e-12
+    assert np.max(np.abs(pg[active] - [1.0, 2.0, 3.0])) < 1e-12
+    far = o.far
+    inact_bg = t.bg[c[:, 0] + 16 * (c[:, 1] + 16 * c[:, 2])][~active]
+    assert np.array_equal(pphi[~active], np.where(inact_bg == 0, -far, far))
+    assert np.all(pg[~active] == 0)
+    bad = np.array([[-0.1, 0.5, 0.5], [0.5, 1.0, 0.5], [np.nan, 0.5, 0.5], [0.5, 0.5, 1.5]])
+    pphi, pg, oob = o.probe(phi, grad, bad)
+    assert oob == 4 and np.all(pphi == far) and np.all(pg == 0)
+
+
+def test_probe_at_data_points_and_continuity(oracle_lib):
+    w = W.config("C1")
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    phi = o.phi_dense()
+    g, _ = o.gradient(phi)
+    cb = np.repeat(np.repeat(np.repeat(t.bg.reshape(w.n[::-1]), 4, 0), 4, 1), 4, 2)
+    idx = np.argwhere(cb == 3)[:500]  # (iz, iy, ix) of core points
+    pos = (idx[:, ::-1] + 0.5) * w.dx
+    pphi, pg, _ = o.probe(phi, g, pos)
+    assert np.array_equal(pphi, phi[idx[:, 0], idx[:, 1], idx[:, 2]])
+    # continuity across package faces x = k l_c inside the band
+    rng = np.random.default_rng(2)
+    eps = 1e-9 * w.dx
+    tested = 0
+    for _ in range(400):
+        p = rng.uniform(0.15, 0.85, 3)
+        p[0] = np.round(p[0] / w.cell) * w.cell
+        lo, hi = p.copy(), p.copy()
+        lo[0] -= eps
+        hi[0] += eps
+        c_lo, c_hi = np.floor(lo / w.cell).astype(int), np.floor(hi / w.cell).astype(int)
+        b_lo = t.bg[c_lo[0] + 16 * (c_lo[1] + 16 * c_lo[2])]
+        b_hi = t.bg[c_hi[0] + 16 * (c_hi[1] + 16 * c_hi[2])]
+        if b_lo < 2 or b_hi < 2:
+            continue
+        v, _, _ = o.probe(phi, None, np.stack([lo, hi]))
+        assert abs(v[0] - v[1]) < 1e-6 * w.cell
+        tested += 1
+    assert tested > 20
+
+
+# --------------------------------------------------------- inputs module ----
+
+
+def test_c4_particle_count_matches_survey():
+    """Lattice particle generator vs the count printed in SURVEY 8(d) C4."""
+    gold = golden("c4_particles.json")
+    pos = W.lattice_particles(W.config("C2"), jitter=0.0)
+    assert abs(pos.shape[0] - gold["n_particles"]) <= 1e-4 * gold["n_particles"]
+
+
+def test_splitmix64_reference_values():
+    # first three outputs of Vigna's splitmix64.c seeded with 0: next() adds
+    # the golden gamma to the state, then mixes; our counter form is
+    # splitmix64(k * gamma) for the k-th output.
+    g = np.uint64(0x9E3779B97F4A7C15)
+    with np.errstate(over="ignore"):
+        out = W.splitmix64(np.array([0, g, g * np.uint64(2)], dtype=np.uint64))
+    assert int(out[0]) == 0xE220A8397B1DCDAF
+    assert int(out[1]) == 0x6E789E6AA1B965F4
+    assert int(out[2]) == 0x06C45D188009454F

@@ -1,0 +1,208 @@
+"""Seeded synthetic inputs shared by the oracle side and the CUDA side.
+
+This module holds NO arithmetic of the method (no signed distance, tagging,
+stencil or interpolation): only the workload definitions (grid sizes,
+analytic geometry parameters, dtype, iteration counts) and the seeded particle
+generator, which uses its own plain point-in-prism predicate and a
+counter-based splitmix64 generator.  Both `oracle/` and
+`paper_2512_11473_b200/` are driven from here; neither imports the other.
+
+Workloads follow SURVEY.md 8(d) "Concrete synthetic inputs" (shapes of the
+paper's workloads: the sphere of BASELINE.json configs[0], the extruded prism
+of the teaser figure, the torus+box union, the shelled sphere of
+Table 1, and the multi-shell scene).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# Primitive kinds: numbers are part of the C-ABI (include/sg.h sg_prim_kind).
+SPHERE, SHELL, BOX, TORUS_X, TORUS_Y, TORUS_Z, TRIPRISM_Z = range(7)
+
+
+@dataclass(frozen=True)
+class Prim:
+    kind: int
+    p: tuple  # up to 12 doubles, meaning per kind documented in include/sg.h
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    n: tuple  # background cells per axis
+    cell: float  # l_c
+    lower: tuple = (0.0, 0.0, 0.0)
+    dtype: str = "f32"  # "f32" | "f64"
+    prims: tuple = ()
+    init_scale: float = 1.0
+    far: float = 0.0  # 0 -> 4 l_c max(1, init_scale)  (reading R-4)
+    iters: int = 20
+    cfl: float = 0.3
+    h_ratio: float = 1.3
+    particles: str = ""  # "" | "prism_lattice" | "sphere_lattice"
+    notes: str = ""
+
+    @property
+    def dx(self) -> float:
+        return self.cell / 4.0
+
+    @property
+    def far_value(self) -> float:
+        if self.far > 0:
+            return self.far
+        return 4.0 * self.cell * max(1.0, self.init_scale)
+
+    def with_(self, **kw) -> "Workload":
+        d = dict(self.__dict__)
+        d.update(kw)
+        return Workload(**d)
+
+
+def prism_teaser() -> Prim:
+    """Extruded equilateral triangle (teaser): circumcentre (0.5, 0.5),
+    circumradius 0.4, vertices at 90/210/330 degrees (ccw), z in [0.15, 0.85]."""
+    v = []
+    for deg in (90.0, 210.0, 330.0):
+        a = math.radians(deg)
+        v += [0.5 + 0.4 * math.cos(a), 0.5 + 0.4 * math.sin(a)]
+    return Prim(TRIPRISM_Z, tuple(v) + (0.15, 0.85))
+
+
+def _multi_shell() -> tuple:
+    prims = [Prim(SHELL, (0.5, 0.5, 0.5, 0.3, 0.31))]
+    for cz in (0.14, 0.86):
+        for cy in (0.14, 0.86):
+            for cx in (0.14, 0.86):
+                prims.append(Prim(SHELL, (cx, cy, cz, 0.05, 0.055)))
+    return tuple(prims)
+
+
+CONFIGS = {
+    # BASELINE.json configs[0]: sphere r=0.3, 16^3 cells x 4^3 packages, fp64
+    "C1": Workload("C1", (16, 16, 16), 1.0 / 16, dtype="f64",
+                   prims=(Prim(SPHERE, (0.5, 0.5, 0.5, 0.3)),), particles="sphere_lattice"),
+    # configs[1]: extruded prism at 512^3 effective, reinit 20 + normals, fp32
+    # configs[3] (C4) probes ~20M lattice particles against this grid.
+    "C2": Workload("C2", (128, 128, 128), 1.0 / 128, dtype="f32",
+                   prims=(prism_teaser(),), particles="prism_lattice"),
+    # configs[2]: torus (axis y) U box at 2048^3 effective
+    "C3": Workload("C3", (512, 512, 512), 1.0 / 512, dtype="f32",
+                   prims=(Prim(TORUS_Y, (0.5, 0.5, 0.5, 0.3, 0.08)),
+                          Prim(BOX, (0.5, 0.5, 0.5, 0.1, 0.1, 0.4)))),
+    # configs[4]: thin-shell multi-body scene at 4096^3 effective
+    "C5": Workload("C5", (1024, 1024, 1024), 1.0 / 1024, dtype="f32", prims=_multi_shell()),
+    # Table 1 shell under reading R-19 (dx = 1/1024)
+    "T1": Workload("T1", (256, 256, 256), 1.0 / 256, dtype="f32",
+                   prims=(Prim(SHELL, (0.5, 0.5, 0.5, 0.3, 0.31)),)),
+}
+
+
+def config(name: str) -> Workload:
+    return CONFIGS[name]
+
+
+# ------------------------------------------------------------ random scenes --
+
+def random_scene(seed: int, n: int, dtype: str = "f64") -> Workload:
+    """Small seeded scene (union of 1-3 spheres/boxes/tori) on an n^3 grid,
+    for table/field parity beyond the fixed configs.  Some scenes let the band
+    touch the domain boundary on purpose (reading R-6)."""
+    rng = np.random.default_rng(seed)
+    cell = 1.0 / n
+    prims = []
+    for _ in range(int(rng.integers(1, 4))):
+        kind = int(rng.choice([SPHERE, BOX, TORUS_X, TORUS_Y, TORUS_Z, SHELL]))
+        c = tuple(float(v) for v in rng.uniform(0.25, 0.75, 3))
+        if kind == SPHERE:
+            prims.append(Prim(kind, c + (float(rng.uniform(0.1, 0.35)),)))
+        elif kind == SHELL:
+            r = float(rng.uniform(0.15, 0.3))
+            prims.append(Prim(kind, c + (r, r + float(rng.uniform(0.01, 0.08)))))
+        elif kind == BOX:
+            prims.append(Prim(kind, c + tuple(float(v) for v in rng.uniform(0.05, 0.3, 3))))
+        else:
+            R = float(rng.uniform(0.12, 0.25))
+            prims.append(Prim(kind, c + (R, float(rng.uniform(0.04, 0.1)))))
+    return Workload(f"rand{seed}_{n}", (n, n, n), cell, dtype=dtype, prims=tuple(prims))
+
+
+# ------------------------------------------------------- particle generator --
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """Counter-based splitmix64 (Steele, Lea, Flood 2014) on uint64 arrays."""
+    with np.errstate(over="ignore"):
+        z = (x + np.uint64(0x9E3779B97F4A7C15)) & _M64
+        z = ((z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)) & _M64
+        z = ((z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)) & _M64
+        return z ^ (z >> np.uint64(31))
+
+
+def _inside_prism(prim: Prim, x, y, z):
+    """Closed point-in-prism predicate (edge-function signs; not an SDF)."""
+    p = prim.p
+    ok = (z >= p[6]) & (z <= p[7])
+    for e in range(3):
+        ax, ay = p[2 * e], p[2 * e + 1]
+        bx, by = p[2 * ((e + 1) % 3)], p[2 * ((e + 1) % 3) + 1]
+        ok &= (bx - ax) * (y - ay) - (by - ay) * (x - ax) >= 0.0
+    return ok
+
+
+def _inside_sphere(prim: Prim, x, y, z):
+    c = prim.p
+    return (x - c[0]) ** 2 + (y - c[1]) ** 2 + (z - c[2]) ** 2 <= c[3] ** 2
+
+
+def lattice_particles(w: Workload, dp: float | None = None, seed: int = 0,
+                      jitter: float = 0.25, order: str = "lattice",
+                      dtype=np.float32) -> np.ndarray:
+    """SPH-style particle set (C4): lattice points (i + 1/2) dp
+    inside the body, each coordinate jittered by U(-jitter dp, +jitter dp)
+    drawn from splitmix64(seed ^ (3 * index + axis)).  order "lattice" keeps
+    z-slowest lattice order (sorted by cell), "shuffled" applies a seeded
+    permutation.  Returns an (n, 3) array of `dtype`."""
+    dp = w.dx if dp is None else dp
+    prim = w.prims[0]
+    inside = {TRIPRISM_Z: _inside_prism, SPHERE: _inside_sphere}[prim.kind]
+    m = [int(round(w.n[k] * w.cell / dp)) for k in range(3)]
+    xs = w.lower[0] + (np.arange(m[0]) + 0.5) * dp
+    ys = w.lower[1] + (np.arange(m[1]) + 0.5) * dp
+    X, Y = np.meshgrid(xs, ys, indexing="xy")  # X varies fastest along axis 1
+    X = X.ravel()
+    Y = Y.ravel()
+    chunks = []
+    for iz in range(m[2]):
+        zc = w.lower[2] + (iz + 0.5) * dp
+        sel = inside(prim, X, Y, zc)
+        if sel.any():
+            pts = np.empty((int(sel.sum()), 3), dtype=np.float64)
+            pts[:, 0] = X[sel]
+            pts[:, 1] = Y[sel]
+            pts[:, 2] = zc
+            chunks.append(pts)
+    pos = np.concatenate(chunks) if chunks else np.zeros((0, 3))
+    n = pos.shape[0]
+    if jitter:
+        ctr = (np.arange(n, dtype=np.uint64) * np.uint64(3))[:, None] + np.arange(3, dtype=np.uint64)[None, :]
+        r = splitmix64(np.uint64(seed) ^ ctr)
+        u = (r >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+        pos = pos + (u - 0.5) * (2.0 * jitter * dp)
+    if order == "shuffled":
+        perm = np.random.default_rng(seed + 1).permutation(n)
+        pos = pos[perm]
+    return np.ascontiguousarray(pos.astype(dtype))
+
+
+def random_positions(w: Workload, n: int, seed: int = 0, margin: float = 0.0,
+                     dtype=np.float64) -> np.ndarray:
+    """Uniform positions in the domain (optionally shrunk by `margin`)."""
+    rng = np.random.default_rng(seed)
+    lo = np.array(w.lower) + margin
+    hi = np.array(w.lower) + np.array(w.n) * w.cell - margin
+    return np.ascontiguousarray(rng.uniform(lo, hi, size=(n, 3)).astype(dtype))
