@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark of the sparse-grid hot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C2] [--order lattice|shuffled] [--no-cpu-baseline]
+
+One STEP = one pass of the whole hot path over one synthetic batch
+ on the workload BASELINE.json's metric is quoted
+on (configs[1], "C2": extruded prism, 512^3 effective, fp32), with the
+configs[3] particle set ("C4": ~19.45 M jittered lattice particles inside the
+prism) as the probe batch:
+    sg_build (tag, compaction, neighbour table, initial phi)
+    sg_reinit (20 Godunov sweeps)
+    sg_gradient (grad + normal + kernel integrals)
+    sg_probe (phi and grad phi at every particle)
+value = active data points updated by the reinit + gradient sweeps per second
+of whole step (21 sweeps x 8.58 M active points), i.e. BASELINE's
+"active cells updated/s (reinit+gradient)"; probes/s and per-stage numbers are
+reported beside it.  Inputs are resident in HBM before timing; L2 is flushed
+(a 512 MiB write) between timed steps, outside the timed events.
+
+e2e: the same step through the C-ABI with HOST buffers: particle positions
+from pinned host memory, probe results back to pinned host memory (the
+library stages them in pipelined chunks) inside the timed region.
+
+--impl reference: the CPU oracle (oracle/, fp64, dense) as it stands, on
+this host's cores, each step a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "active cells updated/s (reinit+gradient) & particle probes/s; % of HBM peak, 1/2/4/8 GPU"
+UNIT = "cell-updates/s"
+REINIT_ITERS = 20
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="C2")
+    p.add_argument("--order", default="lattice", choices=["lattice", "shuffled"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def rank_info():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str, config: str):
+    """dram read+write bytes per launch from a committed ncu --set full
+    capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t.get(config, {}).get(kernel)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------- clocks ----
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ our arm ------
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    from paper_2512_11473_b200 import build as B
+    from paper_2512_11473_b200 import sg
+
+    B.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = W.config(args.config)
+    if world > 1:
+        from paper_2512_11473_b200 import slab as SL
+        return SL.bench_slab(args, w, rank, world, local)
+    stream = torch.cuda.current_stream()
+
+    pos_np = W.lattice_particles(w, seed=0, order=args.order, dtype=np.float32
+                                 if w.dtype == "f32" else np.float64)
+    n_part = pos_np.shape[0]
+    d_pos = torch.from_numpy(pos_np).to(dev)
+    d_phi = torch.empty(n_part, dtype=d_pos.dtype, device=dev)
+    d_grad = torch.empty((n_part, 3), dtype=d_pos.dtype, device=dev)
+    d_oob = torch.zeros(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    fields = sg.SG_GRAD | sg.SG_NORMAL | sg.SG_KINT
+
+    def step(ev, host=None):
+        ev[0].record(stream)
+        g = sg.Grid(w, stream=stream)
+        ev[1].record(stream)
+        g.reinit(REINIT_ITERS, w.cfl, stream=stream)
+        ev[2].record(stream)
+        g.gradient(fields, w.h_ratio, stream=stream)
+        ev[3].record(stream)
+        if host is None:
+            sg.sg_probe(g.handle, n_part, d_pos.data_ptr(), d_phi.data_ptr(), d_grad.data_ptr(),
+                        d_oob.data_ptr(), stream)
+        else:
+            hp, hphi, hgrad = host
+            sg.sg_probe(g.handle, n_part, hp.data_ptr(), hphi.data_ptr(), hgrad.data_ptr(),
+                        d_oob.data_ptr(), stream)
+        ev[4].record(stream)
+        info = g.info
+        g.close_async(stream)
+        return info
+
+    def mk():
+        return [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(mk())
+    torch.cuda.synchronize()
+
+    evs = [mk() for _ in range(args.steps)]
+    l0 = sg.sg_launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter()
+        for k in range(args.steps):
+            flush.zero_()
+            info = step(evs[k])
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    launches = sg.sg_launch_count() - l0
+    st = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(4)]
+                   for k in range(args.steps)])  # ms per stage
+    step_ms = st.sum(1)
+    ms = float(step_ms.mean())
+    n_pkg = info["n_pkg"]
+    n_act = (n_pkg - 2) * 64
+    updates = n_act * (REINIT_ITERS + 1)
+    value = updates / (ms * 1e-3)
+
+    # e2e: host buffers through the C-ABI
+    e2e = None
+    if not args.no_e2e:
+        hp = torch.from_numpy(pos_np).pin_memory()
+        hphi = torch.empty(n_part, dtype=hp.dtype).pin_memory()
+        hgrad = torch.empty((n_part, 3), dtype=hp.dtype).pin_memory()
+        for _ in range(max(1, args.warmup // 2)):
+            flush.zero_()
+            step(mk(), (hp, hphi, hgrad))
+        torch.cuda.synchronize()
+        e_ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ev = mk()
+            step(ev, (hp, hphi, hgrad))
+            torch.cuda.synchronize()
+            e_ms.append(ev[0].elapsed_time(ev[4]))
+        e_ms = float(np.mean(e_ms))
+        e2e = {"value": updates / (e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(hp.numel() * hp.element_size()),
+               "d2h_bytes_per_step": int((hphi.numel() + hgrad.numel()) * hphi.element_size()),
+               "ms_per_step": e_ms, "probes_per_s": n_part / (e_ms * 1e-3)}
+
+    # roofline of the dominant kernel (k_reinit: 20 launches per step)
+    esz = 4 if w.dtype == "f32" else 8
+    reinit_ms = float(st[:, 1].mean()) / REINIT_ITERS
+    bytes_per_cell = 2 * esz + 108 / 64  # read + write phi, neighbour row
+    alg_bytes = bytes_per_cell * n_act
+    hbm, peak_src = peaks()
+    achieved = alg_bytes / (reinit_ms * 1e-3) / 1e9
+    stage_names = ["build", "reinit", "gradient", "probe"]
+    stages = {n: {"ms": float(st[:, i].mean())} for i, n in enumerate(stage_names)}
+    stages["reinit"]["ms_per_sweep"] = reinit_ms
+    stages["reinit"]["cells_per_s"] = n_act / (reinit_ms * 1e-3)
+    stages["probe"]["probes_per_s"] = n_part / (stages["probe"]["ms"] * 1e-3)
+    grad_bytes = (esz + 6 * esz + 108 / 64) * n_act  # phi in, grad + normal out
+    stages["gradient"]["note"] = "grad+normal (K6) and kernel integrals (K7)"
+    stages["reinit_plus_gradient_cells_per_s"] = n_act * (REINIT_ITERS + 1) / (
+        (st[:, 1].mean() + st[:, 2].mean()) * 1e-3)
+    clocks = clk.summary()
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": w.dtype, "data": "synthetic",
+        "config": {"workload": f"{w.name}+C4: extruded prism 512^3 effective (128^3 cells x 4^3), "
+                               f"reinit {REINIT_ITERS} + grad/normal/kernel-integral, "
+                               f"{n_part} probes ({args.order} order)",
+                   "n_packages": n_pkg - 2, "active_cells": n_act, "particles": n_part,
+                   "l2": "flushed between steps (512 MiB write, outside the timed events)",
+                   "parallelism": f"zslab{world}" if world > 1 else "1 GPU"},
+        "probes_per_s": n_part / (ms * 1e-3),
+        "stages": stages,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps,
+        "wall_s": t_wall,
+        "roofline": {"kernel": "k_reinit<float>", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
+                     "bytes_per_cell": bytes_per_cell, "cells_per_launch": n_act,
+                     "traffic": ncu_traffic("k_reinit", w.name),
+                     "note": "C2 working set (~83 MB/sweep) is L2-resident across the 20 sweeps"},
+        "clocks": clocks,
+        "gpu_name": torch.cuda.get_device_name(local),
+    }
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(w, n_act)
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------ oracle timing ------
+
+def oracle_sample(w, budget_s: float = 12.0):
+    """Time the oracle's reinit + gradient sweeps on the dense fp64 grid of
+    the workload (tables and initial phi built beforehand, untimed)."""
+    from oracle import oracle as O
+    O.build()
+    threads = len(os.sched_getaffinity(0))
+    O.set_threads(threads)
+    o = O.Oracle(w)
+    t = o.build_tables()
+    phi = o.phi_dense()
+    n_act = (t.n_pkg - 2) * 64
+    sweeps, t0 = 0, time.perf_counter()
+    while True:
+        phi = o.reinit_step(phi, w.cfl)
+        sweeps += 1
+        if time.perf_counter() - t0 > budget_s * 0.7 or sweeps >= REINIT_ITERS:
+            break
+    o.gradient(phi)
+    dt = time.perf_counter() - t0
+    return {"value": n_act * (sweeps + 1) / dt, "unit": UNIT, "cores": O.get_threads(),
+            "kind": "oracle",
+            "sample": f"{sweeps} reinit sweeps + 1 gradient/normal sweep of the dense fp64 oracle "
+                      f"on {w.name} ({n_act} active points each); tables and initial phi built "
+                      f"beforehand (untimed); {dt:.1f} s"}
+
+
+def cpu_baseline(w, n_act):
+    try:
+        return oracle_sample(w)
+    except Exception as e:  # never fail the bench line on the baseline
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
+                "sample": f"failed: {e}"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    w = W.config(args.config)
+    from oracle import oracle as O
+    O.build()
+    threads = len(os.sched_getaffinity(0))
+    O.set_threads(threads)
+    o = O.Oracle(w)
+    t = o.build_tables()
+    phi0 = o.phi_dense()
+    n_act = (t.n_pkg - 2) * 64
+    sweeps = 2
+
+    def step():
+        phi = phi0
+        for _ in range(sweeps):
+            phi = o.reinit_step(phi, w.cfl)
+        o.gradient(phi)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = n_act * (sweeps + 1) / dt
+    sample = (f"{sweeps} reinit sweeps + 1 gradient/normal sweep of the dense fp64 oracle on "
+              f"{w.name} per step ({n_act} active points per sweep); tables/init untimed")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": f"{w.name}: extruded prism 512^3 effective (CPU oracle sample)",
+                      "active_cells": n_act},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.get_threads(),
+                            "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = rank_info()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

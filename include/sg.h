@@ -1,0 +1,260 @@
+/*
+ * sg.h -- C-ABI of the B200-native contiguous sparse-grid hot path.
+ *
+ * Method: F. Gu, X. Hu, "Contiguous Storage of Grid Data for Heterogeneous
+ * Computing" (arXiv 2512.11473).  Citations "P:<line>" refer to the paper's
+ * text (reference PAPER.md), "R-<n>" to the readings listed in DESIGN.md.
+ *
+ * Data structure:
+ *   - a coarse background grid of N[0] x N[1] x N[2] cells of size l_c;
+ *   - cells near the surface are activated (core: |f(centre)| < l_c, P:499-502;
+ *     inner: not core but a 26-neighbour of a core cell) and own one
+ *     data package of 4^3 data points at spacing dx = l_c / 4;
+ *   - packages are stored contiguously, ids 2.. in ascending linear cell order
+ *     (x fastest, z slowest; R-1); ids 0 and 1 are the singular negative and
+ *     positive far-field packages;
+ *   - per background cell a u32 table: package id, or 0/1 = inactive far field
+ *     of that sign (R-5);
+ *   - per package a meta record (linear cell, category) and a
+ *     3x3x3 table of neighbour package ids, slot ox + 3 oy + 9 oz
+ *     for cell offset (ox-1, oy-1, oz-1) (R-8); singular rows are self;
+ *   - field values per package: 64 contiguous values, data index
+ *     i + 4 j + 16 k (x fastest, R-9).  Vector fields are component-major
+ *     inside a package: [package][component][64].
+ *
+ * Conventions for every call:
+ *   - Every function returns sg_status; no C++ exception crosses the ABI.
+ *     On failure sg_last_error() returns a thread-local message valid until
+ *     the next sg_* call on this thread.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Calls are stream-ordered and asynchronous unless noted.
+ *   - Device pointers are plain CUDA device addresses of the current device.
+ *   - The grid handle owns all its device memory (allocated stream-ordered
+ *     from the device's default memory pool) and frees it in sg_destroy.
+ *   - Argument errors are reported before any launch (SG_ERR_ARG); CUDA
+ *     errors, including asynchronous ones from earlier launches, surface as
+ *     SG_ERR_CUDA at the next call that checks.
+ *   - There is no CPU fallback: without a CUDA device every compute call
+ *     returns SG_ERR_CUDA.
+ */
+#ifndef SG_H_
+#define SG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_ABI_VERSION 1
+#define SG_PKG 4        /* package subdivision, "default by 4"        */
+#define SG_MAX_PRIMS 16 /* primitives per geometry                          */
+
+typedef enum {
+    SG_OK = 0,
+    SG_ERR_ARG = 1,    /* invalid argument (null pointer, pkg != 4, n <= 0, ...) */
+    SG_ERR_OOM = 2,    /* device allocation failed                             */
+    SG_ERR_CUDA = 3,   /* CUDA runtime error (incl. no device)                 */
+    SG_ERR_NCCL = 4,   /* reserved for the multi-GPU communicator              */
+    SG_ERR_STATE = 5,  /* wrong call order, e.g. probing grad before sg_gradient */
+    SG_ERR_DOMAIN = 6  /* slab / domain inconsistency                           */
+} sg_status;
+
+typedef enum { SG_F32 = 0, SG_F64 = 1 } sg_dtype;
+
+/* Analytic primitives (stand-in for the triangle-mesh SDF of P:516, which is
+ * out of scope).  Parameters p[] per kind:
+ *   SG_SPHERE      cx cy cz r
+ *   SG_SHELL       cx cy cz r_in r_out
+ *   SG_BOX         cx cy cz bx by bz        (half extents)
+ *   SG_TORUS_X/Y/Z cx cy cz R r             (symmetry axis x / y / z)
+ *   SG_TRIPRISM_Z  ax ay bx by cx cy z0 z1  (triangle ccw in xy, extruded in z)
+ * The union of several primitives is their pointwise min, in order.  The
+ * fp64 evaluation order is fixed and compiled without FMA
+ * contraction so that the tagging decision is reproducible bit for bit. */
+typedef enum {
+    SG_SPHERE = 0,
+    SG_SHELL = 1,
+    SG_BOX = 2,
+    SG_TORUS_X = 3,
+    SG_TORUS_Y = 4,
+    SG_TORUS_Z = 5,
+    SG_TRIPRISM_Z = 6
+} sg_prim_kind;
+
+typedef struct {
+    int32_t kind; /* sg_prim_kind */
+    int32_t pad;
+    double p[12];
+} sg_prim;
+
+typedef struct {
+    const sg_prim* prims; /* host pointer, n_prims entries (1..SG_MAX_PRIMS) */
+    int32_t n_prims;
+    int32_t pad;
+} sg_geometry;
+
+typedef struct {
+    double lower[3];   /* domain lower corner                                  */
+    double cell;       /* background cell size l_c > 0                         */
+    int32_t n[3];      /* background cells per axis, each >= 1; total < 2^32  */
+    int32_t pkg;       /* must be SG_PKG (4)                                   */
+    int32_t dtype;     /* sg_dtype of every field                              */
+    int32_t pad;
+    double far;        /* far-field magnitude; 0 -> 4 l_c max(1, init_scale) (R-4) */
+    double init_scale; /* initial phi = init_scale * f; 0 -> 1                 */
+} sg_desc;
+
+/* z-slab of a multi-GPU partition (whole background planes, R-1).  The rank
+ * owns planes [z_lo, z_hi) and additionally stores one ghost plane on each
+ * side that lies inside the domain.  id_base is the global package id of the
+ * first stored package (2 for the lowest slab); it is the number of active
+ * cells in planes below the first stored plane, plus 2.  NULL slab = the
+ * whole domain on one GPU. */
+typedef struct {
+    int32_t z_lo;
+    int32_t z_hi;
+    int64_t id_base;
+} sg_slab;
+
+typedef struct sg_grid sg_grid;
+
+/* sg_gradient field selection */
+enum {
+    SG_GRAD = 1,   /* grad phi by central difference (Lst. 5)   */
+    SG_NORMAL = 2, /* n = grad phi / |grad phi| (0 where |grad phi| = 0)   */
+    SG_KINT = 4    /* kernel integrals K, G (reading R-14)      */
+};
+
+/* sg_view selectors */
+enum {
+    SG_VIEW_BG = 0,          /* u32 [stored cells]        background table          */
+    SG_VIEW_META_CELL = 1,   /* u32 [n_pkg]               global linear cell index  */
+    SG_VIEW_META_CAT = 2,    /* u8  [n_pkg]               0/1 singular, 2 inner, 3 core */
+    SG_VIEW_NB = 3,          /* u32 [n_pkg][27]           neighbour package ids     */
+    SG_VIEW_PHI = 4,         /* T   [n_pkg][64]           current phi               */
+    SG_VIEW_GRAD = 5,        /* T   [n_pkg][3][64]        grad phi                  */
+    SG_VIEW_NORMAL = 6,      /* T   [n_pkg][3][64]        normal                    */
+    SG_VIEW_KINT = 7,        /* T   [n_pkg][64]           K                         */
+    SG_VIEW_GKINT = 8,       /* T   [n_pkg][3][64]        G = grad K                */
+    SG_VIEW_PLANE_FIRST = 9, /* i64 [stored planes + 1]   first package id per plane */
+    SG_VIEW_PHI_NEXT = 10    /* T   [n_pkg][64]           reinit scratch buffer     */
+};
+
+typedef struct {
+    void* ptr;         /* device pointer, non-owning; NULL if not computed yet */
+    int64_t shape[3];  /* unused trailing dims = 1                             */
+    int32_t ndim;
+    int32_t elem_size; /* bytes per element                                    */
+    int32_t dtype;     /* 0 f32, 1 f64, 2 u32, 3 u8, 4 i64                     */
+    int32_t pad;
+} sg_view_t;
+
+typedef struct {
+    int64_t n_pkg;        /* packages stored, incl. the two singular ones      */
+    int64_t n_core;       /* stored core packages                              */
+    int64_t n_inner;      /* stored inner packages                             */
+    int64_t id_base;      /* global id of local id 2 (sg_slab.id_base)         */
+    int32_t dtype;
+    int32_t z_lo, z_hi;   /* owned background planes                           */
+    int32_t zs_lo, zs_hi; /* stored background planes (owned + ghosts)         */
+    int32_t pad;
+    double dx;            /* data spacing l_c / 4                              */
+    double far;           /* far-field magnitude                               */
+    double kernel_sum;    /* S = sum of kernel weights of the last SG_KINT     */
+    int32_t has_grad, has_normal, has_kint, phi_cur;
+    int64_t device_bytes; /* bytes held by the grid                            */
+    int64_t own_lo;       /* owned local package ids [own_lo, own_hi); ghost   */
+    int64_t own_hi;       /* packages are [2, own_lo) and [own_hi, n_pkg)      */
+} sg_info_t;
+
+/* ---------------------------------------------------------------- calls -- */
+
+/* Build the sparse grid for `geom` (P:499-526 steps 1-5, single layer):
+ *   K1 core tagging at background-cell centres (fp64),
+ *   K2 inner tagging + ordered compaction (ids in linear cell order),
+ *   K3 27-neighbour table (out-of-domain neighbours: 0/1 by the sign of f at
+ *      the virtual cell centre, R-6),
+ *   K4 initial phi = init_scale * f at the 64 data points of each package,
+ *      rounded to dtype; singular packages hold -far / +far.
+ * One host synchronisation reads back the package count (replaces the
+ * paper's USM shared scalar).  slab may be NULL.  On success *out
+ * owns the grid.  Errors: SG_ERR_ARG (null pointers, pkg != 4, n < 1,
+ * cell <= 0, n_prims outside 1..SG_MAX_PRIMS, unknown kind or dtype, more than
+ * 2^32 - 3 stored packages), SG_ERR_DOMAIN (slab outside the domain),
+ * SG_ERR_OOM, SG_ERR_CUDA. */
+sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, const sg_slab* slab,
+                   void* stream, sg_grid** out);
+
+/* `iters` Jacobi sweeps of upwind Godunov reinitialisation on every active
+ * data point (reading R-12; phi' = phi - cfl dx s (|grad phi|_G - 1)),
+ * double-buffered; inactive and singular data stay unchanged.  Neighbours
+ * across package faces are reached through the neighbour table (Lst. 2).
+ * iters >= 0, 0 < cfl <= 0.5.  Asynchronous.  On a slab grid only the owned
+ * packages are updated; the caller refreshes the ghost packages of the
+ * current buffer (SG_VIEW_PHI, contiguous id ranges, see sg_info) between
+ * sweeps, i.e. calls sg_reinit(grid, 1, ...) once per exchange. */
+sg_status sg_reinit(sg_grid* grid, int32_t iters, double cfl, void* stream);
+
+/* Derived fields from the current phi: any OR of SG_GRAD, SG_NORMAL, SG_KINT.
+ * h_ratio = h / dx of the Wendland C2 kernel, in [0.5, 2] (stencil radius
+ * <= 3 < 4, so every tap stays in the 27-neighbourhood).  Asynchronous. */
+sg_status sg_gradient(sg_grid* grid, uint32_t fields, double h_ratio, void* stream);
+
+/* Grid-particle coupling (reading R-15): for each of n positions
+ * (row-major n x 3, grid dtype) look up the containing background cell; an
+ * inactive cell yields its far constant, an active one the trilinear
+ * interpolation of phi (and of grad phi if `grad` != NULL) over the 8
+ * surrounding data points, fetched through the package's neighbour row with
+ * NeighbourIndexShift (Lst. 2).  Positions outside the stored domain or NaN
+ * return (+far, 0) and increment *oob_count (device u64, may be NULL).
+ * pos / phi (n) / grad (n x 3) may be device pointers (asynchronous) or host
+ * pointers, pinned or pageable (then the call stages them through device
+ * buffers in pipelined chunks and returns after the results are in host
+ * memory).  grad != NULL requires a prior sg_gradient with SG_GRAD
+ * (SG_ERR_STATE otherwise).  n == 0 is a no-op. */
+sg_status sg_probe(const sg_grid* grid, int64_t n, const void* pos, void* phi, void* grad,
+                   unsigned long long* oob_count, void* stream);
+
+/* Table-1 workloads of the paper, on the current phi:
+ *   op 0 "sequential": phi += value at every active data point (in place);
+ *   op 1 "stencil": out = 7-point Laplacian of phi at every active data point
+ *        ((sum of 6 neighbours - 6 phi) / dx^2; singular packages 0),
+ *        written to the SG_VIEW_PHI_NEXT buffer (phi is unchanged). */
+sg_status sg_table1(sg_grid* grid, int32_t op, double value, void* stream);
+
+sg_status sg_info(const sg_grid* grid, sg_info_t* info);
+sg_status sg_view(const sg_grid* grid, int32_t what, sg_view_t* view);
+
+/* Release the grid.  sg_destroy synchronises the device first (safe from any
+ * stream); sg_destroy_async frees stream-ordered on `stream` (the caller
+ * guarantees no other stream still uses the grid). */
+void sg_destroy(sg_grid* grid);
+sg_status sg_destroy_async(sg_grid* grid, void* stream);
+
+/* Host-only helper for the z-slab partition (no device use): given per-plane
+ * package counts counts[0..nz) choose nranks contiguous slabs with cut planes
+ * cuts[0..nranks] (cuts[0] = 0, cuts[nranks] = nz) so that each rank's count
+ * is as close as possible to total/nranks: cut r is the smallest plane z with
+ * prefix(z) >= r*total/nranks (ties go to the lowest plane), clamped so every
+ * slab has at least one plane when nz >= nranks.  Returns SG_ERR_ARG if
+ * nranks < 1 or nz < nranks. */
+sg_status sg_balanced_cuts(const int64_t* counts, int32_t nz, int32_t nranks, int32_t* cuts);
+
+/* Per-plane package counts of background planes [z_lo, z_hi) of the whole
+ * domain (tagging only, no package storage): counts is a device i64 array of
+ * z_hi - z_lo entries.  Used to balance the slabs before sg_build. */
+sg_status sg_plane_counts(const sg_desc* desc, const sg_geometry* geom, int32_t z_lo,
+                          int32_t z_hi, int64_t* counts, void* stream);
+
+const char* sg_last_error(void);
+int32_t sg_abi_version(void);
+/* Number of device kernels this library has launched in this process. */
+uint64_t sg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SG_H_ */

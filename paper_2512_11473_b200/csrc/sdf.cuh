@@ -1,0 +1,86 @@
+// sdf.cuh -- fp64 analytic signed distance on the device.
+//
+// Only included by translation units compiled with -fmad=false: every
+// operation below is a separately rounded IEEE double operation in the order
+// written (no FMA contraction, IEEE sqrt/div), which makes the tagging
+// decision |f(centre)| < l_c (reading R-2) reproducible bit for bit
+// against any other IEEE evaluation with the same operation order.
+#pragma once
+
+#include "sg_internal.cuh"
+
+namespace sg {
+
+__device__ __forceinline__ double sd_len3(double ex, double ey, double ez) {
+    return sqrt((ex * ex + ey * ey) + ez * ez);
+}
+
+__device__ __forceinline__ double sd_prim(int kind, const double* p, double x, double y,
+                                          double z) {
+    switch (kind) {
+    case SG_SPHERE:
+        return sd_len3(x - p[0], y - p[1], z - p[2]) - p[3];
+    case SG_SHELL: {
+        const double rm = 0.5 * (p[3] + p[4]);
+        const double hw = 0.5 * (p[4] - p[3]);
+        return fabs(sd_len3(x - p[0], y - p[1], z - p[2]) - rm) - hw;
+    }
+    case SG_BOX: {
+        const double qx = fabs(x - p[0]) - p[3];
+        const double qy = fabs(y - p[1]) - p[4];
+        const double qz = fabs(z - p[2]) - p[5];
+        const double mx = fmax(qx, 0.0), my = fmax(qy, 0.0), mz = fmax(qz, 0.0);
+        return sqrt((mx * mx + my * my) + mz * mz) + fmin(fmax(qx, fmax(qy, qz)), 0.0);
+    }
+    case SG_TORUS_X: {
+        const double ex = x - p[0], ey = y - p[1], ez = z - p[2];
+        const double t = sqrt(ey * ey + ez * ez) - p[3];
+        return sqrt(t * t + ex * ex) - p[4];
+    }
+    case SG_TORUS_Y: {
+        const double ex = x - p[0], ey = y - p[1], ez = z - p[2];
+        const double t = sqrt(ex * ex + ez * ez) - p[3];
+        return sqrt(t * t + ey * ey) - p[4];
+    }
+    case SG_TORUS_Z: {
+        const double ex = x - p[0], ey = y - p[1], ez = z - p[2];
+        const double t = sqrt(ex * ex + ey * ey) - p[3];
+        return sqrt(t * t + ez * ez) - p[4];
+    }
+    case SG_TRIPRISM_Z: {
+        // exact 2-D triangle distance: clamped point-segment distance per
+        // edge; inside iff strictly left of every (ccw) edge
+        double best = 0.0;
+        bool inside = true;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            const int e1 = (e + 1) % 3;
+            const double ux = p[2 * e1] - p[2 * e], uy = p[2 * e1 + 1] - p[2 * e + 1];
+            const double wx = x - p[2 * e], wy = y - p[2 * e + 1];
+            double t = (wx * ux + wy * uy) / (ux * ux + uy * uy);
+            t = fmin(fmax(t, 0.0), 1.0);
+            const double hx = wx - ux * t, hy = wy - uy * t;
+            const double d2 = hx * hx + hy * hy;
+            best = (e == 0) ? d2 : fmin(best, d2);
+            inside = inside && (ux * wy - uy * wx > 0.0);
+        }
+        const double dxy = inside ? -sqrt(best) : sqrt(best);
+        const double zc = 0.5 * (p[6] + p[7]);
+        const double hl = 0.5 * (p[7] - p[6]);
+        const double qz = fabs(z - zc) - hl;
+        const double a = fmax(dxy, 0.0), b = fmax(qz, 0.0);
+        return fmin(fmax(dxy, qz), 0.0) + sqrt(a * a + b * b);
+    }
+    default:
+        return __longlong_as_double(0x7ff8000000000000ULL);  // NaN
+    }
+}
+
+// union of the primitives = pointwise min, in order
+__device__ __forceinline__ double sd_eval(const Geom& g, double x, double y, double z) {
+    double f = sd_prim(g.kind[0], g.p[0], x, y, z);
+    for (int i = 1; i < g.n; ++i) f = fmin(f, sd_prim(g.kind[i], g.p[i], x, y, z));
+    return f;
+}
+
+}  // namespace sg

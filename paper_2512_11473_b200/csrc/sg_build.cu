@@ -1,0 +1,661 @@
+// sg_build.cu -- sg_build (K1-K4), grid lifetime, info/view, slab helpers.
+//
+// Compiled with -fmad=false: the fp64 signed distance (sdf.cuh) and the
+// position arithmetic must be the separately rounded operations of DESIGN.md
+// "O1"/"O2" so that the core predicate and the initial phi are reproducible.
+//
+// Pipeline (steps 1-5 of the initialization, single layer):
+//   K1 k_tag      : f at every background-cell centre -> core / sign flags
+//   K2 k_count    : inner tagging (26-neighbourhood), per-tile active counts
+//      k_scan     : exclusive scan of tile counts (ordered compaction, R-1)
+//      -- one D2H read of the package count (P:468-471 analogue) --
+//      k_scatter  : block scan inside each tile -> ids 2.. in linear order;
+//                   background table, meta (cell, category)
+//      k_planes   : first package id per background plane (slab ranges)
+//   K3 k_nb       : 27-neighbour package table
+//   K4 k_phi_init : phi = init_scale * f at the 64 data points
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+
+#include "sdf.cuh"
+#include "sg_internal.cuh"
+
+namespace sg {
+
+std::atomic<uint64_t> g_launches{0};
+
+static thread_local std::string t_last_error;
+
+void set_last_error(const std::string& m) { t_last_error = m; }
+void clear_last_error() { t_last_error.clear(); }
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    std::string m = std::string(cudaGetErrorName(e)) + " (" + cudaGetErrorString(e) + ") in " +
+                    what + " at " + file + ":" + std::to_string(line);
+    if (e == cudaErrorMemoryAllocation) throw Error(SG_ERR_OOM, m);
+    throw Error(SG_ERR_CUDA, m);
+}
+
+static std::once_flag g_pool_once;
+
+void* dalloc(size_t bytes, cudaStream_t s) {
+    std::call_once(g_pool_once, [] {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+    void* p = nullptr;
+    if (bytes == 0) bytes = 256;
+    SG_CUDA(cudaMallocAsync(&p, bytes, s));
+    return p;
+}
+
+// ------------------------------------------------------------- kernels ---
+
+constexpr int kTB = 256;               // threads per block in the compaction
+constexpr int kCPT = 16;               // cells per thread
+constexpr int kTile = kTB * kCPT;      // cells per tile (one block)
+
+// K1 -- core flag (bit 0) and negative sign (bit 1) per background cell of the
+// tag planes [zt_lo, zt_lo + gridDim.z).  O2: centre = lower + (c + 0.5) l_c.
+__global__ void __launch_bounds__(256) k_tag(GridC gc, Geom geom, int32_t zt_lo,
+                                             uint8_t* __restrict__ flags) {
+    const int cx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int cy = blockIdx.y;
+    const int zl = blockIdx.z;
+    if (cx >= gc.n[0]) return;
+    const int cz = zt_lo + zl;
+    const double x = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
+    const double y = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
+    const double z = gc.lower[2] + ((double)cz + 0.5) * gc.cell;
+    const double f = sd_eval(geom, x, y, z);
+    flags[(int64_t)zl * gc.plane + (int64_t)cy * gc.n[0] + cx] =
+        (uint8_t)((fabs(f) < gc.cell ? 1 : 0) | (f < 0.0 ? 2 : 0));
+}
+
+// category of a stored cell: 3 core, 2 inner (26-neighbour of a core cell,
+// clipped to the domain, R-3), else 0/1 by sign (R-5)
+__device__ __forceinline__ uint8_t cell_category(const GridC& gc, const uint8_t* __restrict__ flags,
+                                                 int32_t zt_lo, int cx, int cy, int cz) {
+    const int64_t nx = gc.n[0];
+    const uint8_t f = flags[(int64_t)(cz - zt_lo) * gc.plane + (int64_t)cy * nx + cx];
+    if (f & 1) return 3;
+    const int z0 = max(cz - 1, 0), z1 = min(cz + 1, gc.n[2] - 1);
+    const int y0 = max(cy - 1, 0), y1 = min(cy + 1, gc.n[1] - 1);
+    const int x0 = max(cx - 1, 0), x1 = min(cx + 1, gc.n[0] - 1);
+    for (int z = z0; z <= z1; ++z)
+        for (int y = y0; y <= y1; ++y) {
+            const uint8_t* row = flags + (int64_t)(z - zt_lo) * gc.plane + (int64_t)y * nx;
+            for (int x = x0; x <= x1; ++x)
+                if (row[x] & 1) return 2;
+        }
+    return (f & 2) ? 0 : 1;
+}
+
+__device__ __forceinline__ void next_cell(const GridC& gc, int& cx, int& cy, int& cz) {
+    if (++cx == gc.n[0]) {
+        cx = 0;
+        if (++cy == gc.n[1]) {
+            cy = 0;
+            ++cz;
+        }
+    }
+}
+
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < (int)(blockDim.x >> 5)) s_warp[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    total = s_warp[(blockDim.x >> 5) - 1];
+    const int before = warp > 0 ? s_warp[warp - 1] : 0;
+    return before + x - v;
+}
+
+// K2a -- category per stored cell + active count per tile of kTile cells
+__global__ void __launch_bounds__(kTB) k_count(GridC gc, int32_t zt_lo, int64_t ncs,
+                                               const uint8_t* __restrict__ flags,
+                                               uint8_t* __restrict__ cat,
+                                               int32_t* __restrict__ tile_count,
+                                               unsigned long long* __restrict__ n_core) {
+    __shared__ int s_warp[32];
+    const int64_t l0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kCPT;
+    int cnt = 0, ncore = 0;
+    if (l0 < ncs) {
+        const int64_t L = (int64_t)gc.zs_lo * gc.plane + l0;
+        int cx = (int)(L % gc.n[0]);
+        int cy = (int)((L / gc.n[0]) % gc.n[1]);
+        int cz = (int)(L / gc.plane);
+        for (int q = 0; q < kCPT; ++q) {
+            const int64_t l = l0 + q;
+            if (l >= ncs) break;
+            const uint8_t c = cell_category(gc, flags, zt_lo, cx, cy, cz);
+            cat[l] = c;
+            cnt += c >= 2;
+            ncore += c == 3;
+            next_cell(gc, cx, cy, cz);
+        }
+    }
+    int total;
+    block_excl_scan(cnt, s_warp, total);
+    __syncthreads();
+    int ctot;
+    block_excl_scan(ncore, s_warp, ctot);
+    if (threadIdx.x == 0) {
+        tile_count[blockIdx.x] = total;
+        if (ctot) atomicAdd(n_core, (unsigned long long)ctot);
+    }
+}
+
+// K2b -- exclusive scan of tile counts (one block; each thread owns a
+// contiguous segment).  out[n] = total.
+__global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, int64_t n,
+                                               int64_t* __restrict__ out) {
+    __shared__ long long s[1024];
+    const int64_t seg = (n + 1023) / 1024;
+    const int64_t b = (int64_t)threadIdx.x * seg, e = min(n, b + seg);
+    long long sum = 0;
+    for (int64_t i = b; i < e; ++i) sum += cnt[i];
+    s[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        long long v = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0;
+        __syncthreads();
+        s[threadIdx.x] += v;
+        __syncthreads();
+    }
+    long long run = s[threadIdx.x] - sum;
+    for (int64_t i = b; i < e; ++i) {
+        out[i] = run;
+        run += cnt[i];
+    }
+    if (threadIdx.x == 1023) out[n] = s[1023];
+}
+
+// K2c -- ordered compaction: ids 2 + (active cells before) in linear order
+__global__ void __launch_bounds__(kTB) k_scatter(GridC gc, int64_t ncs,
+                                                 const uint8_t* __restrict__ cat,
+                                                 const int64_t* __restrict__ tile_off,
+                                                 uint32_t* __restrict__ bg,
+                                                 uint32_t* __restrict__ meta_cell,
+                                                 uint8_t* __restrict__ meta_cat) {
+    __shared__ int s_warp[32];
+    const int64_t l0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kCPT;
+    uint8_t c[kCPT];
+    int cnt = 0;
+    if (l0 + kCPT <= ncs) {
+        const uint4 v = *reinterpret_cast<const uint4*>(cat + l0);
+        memcpy(c, &v, 16);
+    } else {
+        for (int q = 0; q < kCPT; ++q) c[q] = (l0 + q < ncs) ? cat[l0 + q] : 0xFF;
+    }
+#pragma unroll
+    for (int q = 0; q < kCPT; ++q) cnt += (c[q] != 0xFF) && c[q] >= 2;
+    int total;
+    const int ex = block_excl_scan(cnt, s_warp, total);
+    uint32_t id = (uint32_t)(2 + tile_off[blockIdx.x] + ex);
+    uint32_t out[kCPT];
+    const uint32_t Lbase = (uint32_t)((int64_t)gc.zs_lo * gc.plane + l0);
+#pragma unroll
+    for (int q = 0; q < kCPT; ++q) {
+        if (c[q] != 0xFF && c[q] >= 2) {
+            out[q] = id;
+            meta_cell[id] = Lbase + q;
+            meta_cat[id] = c[q];
+            ++id;
+        } else {
+            out[q] = c[q];
+        }
+    }
+    if (l0 + kCPT <= ncs) {
+        uint4* d = reinterpret_cast<uint4*>(bg + l0);
+#pragma unroll
+        for (int q = 0; q < kCPT / 4; ++q)
+            d[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+    } else {
+        for (int q = 0; q < kCPT; ++q)
+            if (l0 + q < ncs) bg[l0 + q] = out[q];
+    }
+}
+
+// first local package id of every stored plane; pf[planes] = n_pkg
+__global__ void k_planes_init(int64_t* pf, int32_t planes, int64_t n_pkg) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i <= planes) pf[i] = n_pkg;
+}
+
+__global__ void k_planes(GridC gc, const uint32_t* __restrict__ meta_cell, int64_t n_pkg,
+                         int64_t* __restrict__ pf) {
+    const int64_t id = 2 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= n_pkg) return;
+    const int p = (int)(meta_cell[id] / (uint64_t)gc.plane) - gc.zs_lo;
+    const int q = id == 2 ? -1 : (int)(meta_cell[id - 1] / (uint64_t)gc.plane) - gc.zs_lo;
+    for (int z = q + 1; z <= p; ++z) pf[z] = id;
+}
+
+// K3 -- neighbour table; one thread per (package, slot).  Neighbours outside
+// the domain take the sign of f at the virtual cell centre (R-6); cells in
+// the domain but outside the stored planes (beyond a ghost plane) take their
+// sign flag (never dereferenced by owned-point stencils).
+__global__ void __launch_bounds__(256) k_nb(GridC gc, Geom geom, int32_t zt_lo,
+                                            const uint8_t* __restrict__ flags,
+                                            const uint32_t* __restrict__ bg,
+                                            const uint32_t* __restrict__ meta_cell,
+                                            int64_t n_pkg, uint32_t* __restrict__ nb) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_pkg * 27) return;
+    const int64_t id = t / 27;
+    const int s = (int)(t - id * 27);
+    if (id < 2) {
+        nb[t] = (uint32_t)id;  // far-field packages neighbour themselves
+        return;
+    }
+    const uint32_t L = meta_cell[id];
+    const int cx = (int)(L % (uint32_t)gc.n[0]);
+    const int cy = (int)((L / (uint32_t)gc.n[0]) % (uint32_t)gc.n[1]);
+    const int cz = (int)(L / (uint32_t)gc.plane);
+    const int qx = cx + s % 3 - 1, qy = cy + (s / 3) % 3 - 1, qz = cz + s / 9 - 1;
+    uint32_t v;
+    if (qx < 0 || qy < 0 || qz < 0 || qx >= gc.n[0] || qy >= gc.n[1] || qz >= gc.n[2]) {
+        const double x = gc.lower[0] + ((double)qx + 0.5) * gc.cell;
+        const double y = gc.lower[1] + ((double)qy + 0.5) * gc.cell;
+        const double z = gc.lower[2] + ((double)qz + 0.5) * gc.cell;
+        v = sd_eval(geom, x, y, z) < 0.0 ? 0u : 1u;
+    } else if (qz >= gc.zs_lo && qz < gc.zs_hi) {
+        v = bg[(int64_t)(qz - gc.zs_lo) * gc.plane + (int64_t)qy * gc.n[0] + qx];
+    } else {
+        v = (flags[(int64_t)(qz - zt_lo) * gc.plane + (int64_t)qy * gc.n[0] + qx] & 2) ? 0u : 1u;
+    }
+    nb[t] = v;
+}
+
+// K4 -- initial level set at the 64 data points of every package:
+// phi = init_scale * f(lower + (I + 0.5) dx) rounded to T (R-11, R-17);
+// singular packages -far / +far in both buffers.
+template <class T>
+__global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
+                                                  const uint32_t* __restrict__ meta_cell,
+                                                  int64_t n_pkg, T* __restrict__ phi0,
+                                                  T* __restrict__ phi1) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_pkg * 64) return;
+    const int64_t id = t >> 6;
+    const int d = (int)(t & 63);
+    if (id < 2) {
+        const T v = (T)(id == 0 ? -gc.far : gc.far);
+        phi0[t] = v;
+        phi1[t] = v;
+        return;
+    }
+    const uint32_t L = meta_cell[id];
+    const int cx = (int)(L % (uint32_t)gc.n[0]);
+    const int cy = (int)((L / (uint32_t)gc.n[0]) % (uint32_t)gc.n[1]);
+    const int cz = (int)(L / (uint32_t)gc.plane);
+    const int64_t ix = 4 * (int64_t)cx + (d & 3), iy = 4 * (int64_t)cy + ((d >> 2) & 3),
+                  iz = 4 * (int64_t)cz + (d >> 4);
+    const double x = gc.lower[0] + ((double)ix + 0.5) * gc.dx;
+    const double y = gc.lower[1] + ((double)iy + 0.5) * gc.dx;
+    const double z = gc.lower[2] + ((double)iz + 0.5) * gc.dx;
+    phi0[t] = (T)(gc.init_scale * sd_eval(geom, x, y, z));
+}
+
+// per-plane active counts for slab balancing (tag planes known)
+__global__ void __launch_bounds__(256) k_plane_count(GridC gc, int32_t zt_lo, int32_t zc_lo,
+                                                     const uint8_t* __restrict__ flags,
+                                                     unsigned long long* __restrict__ counts) {
+    const int cx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int cy = blockIdx.y;
+    const int cz = zc_lo + blockIdx.z;
+    bool act = false;
+    if (cx < gc.n[0]) act = cell_category(gc, flags, zt_lo, cx, cy, cz) >= 2;
+    const unsigned m = __ballot_sync(0xffffffffu, act);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&counts[blockIdx.z], (unsigned long long)__popc(m));
+}
+
+// ------------------------------------------------------------- helpers ---
+
+static GridC make_gridc(const sg_desc* d) {
+    GridC gc{};
+    for (int k = 0; k < 3; ++k) {
+        gc.lower[k] = d->lower[k];
+        gc.n[k] = d->n[k];
+        gc.upper[k] = d->lower[k] + (double)d->n[k] * d->cell;
+    }
+    gc.cell = d->cell;
+    gc.dx = d->cell / 4.0;
+    gc.init_scale = d->init_scale > 0.0 ? d->init_scale : 1.0;
+    gc.far = d->far > 0.0 ? d->far : 4.0 * d->cell * std::max(1.0, gc.init_scale);
+    gc.plane = (int64_t)d->n[0] * d->n[1];
+    return gc;
+}
+
+static void check_desc(const sg_desc* d, const sg_geometry* g) {
+    SG_ARG(d != nullptr && g != nullptr, "sg_build: null desc or geometry");
+    SG_ARG(d->pkg == SG_PKG, "sg_build: desc.pkg must be 4");
+    SG_ARG(d->n[0] >= 1 && d->n[1] >= 1 && d->n[2] >= 1, "sg_build: n must be >= 1");
+    SG_ARG(d->n[1] <= 65535 && d->n[2] <= 65535, "sg_build: n[1], n[2] must be <= 65535");
+    SG_ARG((double)d->n[0] * d->n[1] * d->n[2] < 4294967295.0, "sg_build: more than 2^32-1 cells");
+    SG_ARG(d->cell > 0.0 && std::isfinite(d->cell), "sg_build: cell must be > 0");
+    SG_ARG(d->dtype == SG_F32 || d->dtype == SG_F64, "sg_build: unknown dtype");
+    SG_ARG(d->init_scale >= 0.0 && d->far >= 0.0, "sg_build: negative init_scale or far");
+    SG_ARG(g->prims != nullptr && g->n_prims >= 1 && g->n_prims <= SG_MAX_PRIMS,
+           "sg_build: need 1..16 primitives");
+    for (int i = 0; i < g->n_prims; ++i)
+        SG_ARG(g->prims[i].kind >= SG_SPHERE && g->prims[i].kind <= SG_TRIPRISM_Z,
+               "sg_build: unknown primitive kind");
+}
+
+static Geom make_geom(const sg_geometry* g) {
+    Geom ge{};
+    ge.n = g->n_prims;
+    for (int i = 0; i < g->n_prims; ++i) {
+        ge.kind[i] = g->prims[i].kind;
+        for (int j = 0; j < 12; ++j) ge.p[i][j] = g->prims[i].p[j];
+    }
+    return ge;
+}
+
+static void launch_tag(const GridC& gc, const Geom& geom, int32_t zt_lo, int32_t zt_hi,
+                       uint8_t* flags, cudaStream_t s) {
+    if (zt_hi <= zt_lo) return;
+    dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1], (unsigned)(zt_hi - zt_lo));
+    k_tag<<<grid, 256, 0, s>>>(gc, geom, zt_lo, flags);
+    SG_LAUNCHED();
+}
+
+static int check_device() {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) throw_cuda(e, "cudaGetDevice (no CUDA device?)", __FILE__, __LINE__);
+    return dev;
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+// ------------------------------------------------------------------- ABI ---
+
+extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, const sg_slab* slab,
+                              void* stream, sg_grid** out) {
+    return guard([&] {
+        SG_ARG(out != nullptr, "sg_build: null out");
+        *out = nullptr;
+        check_desc(desc, geom);
+        const int dev = check_device();
+        cudaStream_t s = (cudaStream_t)stream;
+        auto g = std::make_unique<sg_grid>();
+        g->device = dev;
+        g->gc = make_gridc(desc);
+        g->geom = make_geom(geom);
+        g->dtype = desc->dtype;
+        g->esz = desc->dtype == SG_F64 ? 8 : 4;
+        GridC& gc = g->gc;
+        const int nz = desc->n[2];
+        if (slab) {
+            SG_ARG(slab->z_lo >= 0 && slab->z_lo < slab->z_hi && slab->z_hi <= nz,
+                   "sg_build: slab planes outside the domain");
+            SG_ARG(slab->id_base >= 2, "sg_build: slab.id_base must be >= 2");
+            gc.z_lo = slab->z_lo;
+            gc.z_hi = slab->z_hi;
+            g->id_base = slab->id_base;
+        } else {
+            gc.z_lo = 0;
+            gc.z_hi = nz;
+            g->id_base = 2;
+        }
+        gc.zs_lo = std::max(0, gc.z_lo - 1);
+        gc.zs_hi = std::min(nz, gc.z_hi + 1);
+        const int32_t zt_lo = std::max(0, gc.zs_lo - 1), zt_hi = std::min(nz, gc.zs_hi + 1);
+        const int64_t ncs = gc.plane * (gc.zs_hi - gc.zs_lo);
+        g->ncell_stored = ncs;
+
+        // K1: tag planes = stored planes + one on each side (inner tagging
+        // of a stored boundary plane needs the core flags beyond it)
+        uint8_t* flags = (uint8_t*)dalloc((size_t)gc.plane * (zt_hi - zt_lo), s);
+        launch_tag(gc, g->geom, zt_lo, zt_hi, flags, s);
+
+        const int64_t n_tiles = ceil_div(ncs, kTile);
+        uint8_t* cat = (uint8_t*)dalloc((size_t)(n_tiles * kTile), s);
+        int32_t* tile_count = (int32_t*)dalloc(sizeof(int32_t) * n_tiles, s);
+        int64_t* tile_off = (int64_t*)dalloc(sizeof(int64_t) * (n_tiles + 1), s);
+        unsigned long long* d_core = (unsigned long long*)dalloc(sizeof(unsigned long long), s);
+        SG_CUDA(cudaMemsetAsync(d_core, 0, sizeof(unsigned long long), s));
+        k_count<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, zt_lo, ncs, flags, cat, tile_count, d_core);
+        SG_LAUNCHED();
+        k_scan<<<1, 1024, 0, s>>>(tile_count, n_tiles, tile_off);
+        SG_LAUNCHED();
+
+        // the single host synchronisation: package count (and core count)
+        int64_t counts[2];
+        SG_CUDA(cudaMemcpyAsync(&counts[0], tile_off + n_tiles, sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, s));
+        SG_CUDA(cudaMemcpyAsync(&counts[1], d_core, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        SG_CUDA(cudaStreamSynchronize(s));
+        const int64_t n_active = counts[0];
+        SG_ARG(n_active + 2 < 4294967295LL, "sg_build: more than 2^32-3 packages");
+        g->n_pkg = n_active + 2;
+        g->n_core = counts[1];
+        g->n_inner = n_active - counts[1];
+        const int64_t n_pkg = g->n_pkg;
+
+        g->bg = (uint32_t*)g->alloc(sizeof(uint32_t) * ncs, s);
+        g->meta_cell = (uint32_t*)g->alloc(sizeof(uint32_t) * n_pkg, s);
+        g->meta_cat = (uint8_t*)g->alloc((size_t)n_pkg, s);
+        g->nb = (uint32_t*)g->alloc(sizeof(uint32_t) * 27 * n_pkg, s);
+        const int32_t planes = gc.zs_hi - gc.zs_lo;
+        g->plane_first = (int64_t*)g->alloc(sizeof(int64_t) * (planes + 1), s);
+        for (int b = 0; b < 2; ++b) g->phi[b] = g->alloc((size_t)g->esz * 64 * n_pkg, s);
+
+        const uint32_t sing_cell[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
+        const uint8_t sing_cat[2] = {0, 1};
+        SG_CUDA(cudaMemcpyAsync(g->meta_cell, sing_cell, sizeof(sing_cell), cudaMemcpyHostToDevice, s));
+        SG_CUDA(cudaMemcpyAsync(g->meta_cat, sing_cat, sizeof(sing_cat), cudaMemcpyHostToDevice, s));
+
+        k_scatter<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, ncs, cat, tile_off, g->bg, g->meta_cell,
+                                                    g->meta_cat);
+        SG_LAUNCHED();
+        k_planes_init<<<(unsigned)ceil_div(planes + 1, 256), 256, 0, s>>>(g->plane_first, planes,
+                                                                          n_pkg);
+        SG_LAUNCHED();
+        if (n_active > 0) {
+            k_planes<<<(unsigned)ceil_div(n_active, 256), 256, 0, s>>>(gc, g->meta_cell, n_pkg,
+                                                                       g->plane_first);
+            SG_LAUNCHED();
+        }
+        k_nb<<<(unsigned)ceil_div(n_pkg * 27, 256), 256, 0, s>>>(gc, g->geom, zt_lo, flags, g->bg,
+                                                                 g->meta_cell, n_pkg, g->nb);
+        SG_LAUNCHED();
+        const unsigned pb = (unsigned)ceil_div(n_pkg * 64, 256);
+        if (g->dtype == SG_F64)
+            k_phi_init<double><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
+                                                  (double*)g->phi[0], (double*)g->phi[1]);
+        else
+            k_phi_init<float><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
+                                                 (float*)g->phi[0], (float*)g->phi[1]);
+        SG_LAUNCHED();
+        g->cur = 0;
+
+        // owned id range: whole domain -> [2, n_pkg); slab -> plane ranges
+        if (gc.zs_lo == gc.z_lo && gc.zs_hi == gc.z_hi) {
+            g->own_lo = 2;
+            g->own_hi = n_pkg;
+        } else {
+            std::vector<int64_t> pf(planes + 1);
+            SG_CUDA(cudaMemcpyAsync(pf.data(), g->plane_first, sizeof(int64_t) * (planes + 1),
+                                    cudaMemcpyDeviceToHost, s));
+            SG_CUDA(cudaStreamSynchronize(s));
+            g->own_lo = pf[gc.z_lo - gc.zs_lo];
+            g->own_hi = pf[gc.z_hi - gc.zs_lo];
+        }
+
+        SG_CUDA(cudaFreeAsync(flags, s));
+        SG_CUDA(cudaFreeAsync(cat, s));
+        SG_CUDA(cudaFreeAsync(tile_count, s));
+        SG_CUDA(cudaFreeAsync(tile_off, s));
+        SG_CUDA(cudaFreeAsync(d_core, s));
+        *out = g.release();
+    });
+}
+
+static void free_grid(sg_grid* g, cudaStream_t s, bool async) {
+    for (auto& a : g->allocs) {
+        if (async)
+            cudaFreeAsync(a.first, s);
+        else
+            cudaFree(a.first);
+    }
+    g->allocs.clear();
+    delete g;
+}
+
+extern "C" void sg_destroy(sg_grid* grid) {
+    if (!grid) return;
+    cudaDeviceSynchronize();
+    free_grid(grid, 0, false);
+}
+
+extern "C" sg_status sg_destroy_async(sg_grid* grid, void* stream) {
+    return guard([&] {
+        if (!grid) return;
+        free_grid(grid, (cudaStream_t)stream, true);
+        SG_CUDA(cudaGetLastError());
+    });
+}
+
+extern "C" sg_status sg_info(const sg_grid* g, sg_info_t* info) {
+    return guard([&] {
+        SG_ARG(g && info, "sg_info: null argument");
+        std::memset(info, 0, sizeof(*info));
+        info->n_pkg = g->n_pkg;
+        info->n_core = g->n_core;
+        info->n_inner = g->n_inner;
+        info->id_base = g->id_base;
+        info->dtype = g->dtype;
+        info->z_lo = g->gc.z_lo;
+        info->z_hi = g->gc.z_hi;
+        info->zs_lo = g->gc.zs_lo;
+        info->zs_hi = g->gc.zs_hi;
+        info->dx = g->gc.dx;
+        info->far = g->gc.far;
+        info->kernel_sum = g->kernel_sum;
+        info->has_grad = g->has_grad;
+        info->has_normal = g->has_normal;
+        info->has_kint = g->has_kint;
+        info->phi_cur = g->cur;
+        info->device_bytes = g->bytes();
+        info->own_lo = g->own_lo;
+        info->own_hi = g->own_hi;
+    });
+}
+
+extern "C" sg_status sg_view(const sg_grid* g, int32_t what, sg_view_t* v) {
+    return guard([&] {
+        SG_ARG(g && v, "sg_view: null argument");
+        std::memset(v, 0, sizeof(*v));
+        v->shape[0] = v->shape[1] = v->shape[2] = 1;
+        const int fdt = g->dtype == SG_F64 ? 1 : 0;
+        auto set = [&](void* p, int ndim, int64_t a, int64_t b, int64_t c, int es, int dt) {
+            v->ptr = p;
+            v->ndim = ndim;
+            v->shape[0] = a;
+            v->shape[1] = b;
+            v->shape[2] = c;
+            v->elem_size = es;
+            v->dtype = dt;
+        };
+        switch (what) {
+        case SG_VIEW_BG: set(g->bg, 1, g->ncell_stored, 1, 1, 4, 2); break;
+        case SG_VIEW_META_CELL: set(g->meta_cell, 1, g->n_pkg, 1, 1, 4, 2); break;
+        case SG_VIEW_META_CAT: set(g->meta_cat, 1, g->n_pkg, 1, 1, 1, 3); break;
+        case SG_VIEW_NB: set(g->nb, 2, g->n_pkg, 27, 1, 4, 2); break;
+        case SG_VIEW_PHI: set(g->phi[g->cur], 2, g->n_pkg, 64, 1, g->esz, fdt); break;
+        case SG_VIEW_PHI_NEXT: set(g->phi[1 - g->cur], 2, g->n_pkg, 64, 1, g->esz, fdt); break;
+        case SG_VIEW_GRAD: set(g->has_grad ? g->grad : nullptr, 3, g->n_pkg, 3, 64, g->esz, fdt); break;
+        case SG_VIEW_NORMAL:
+            set(g->has_normal ? g->normal : nullptr, 3, g->n_pkg, 3, 64, g->esz, fdt);
+            break;
+        case SG_VIEW_KINT: set(g->has_kint ? g->kint : nullptr, 2, g->n_pkg, 64, 1, g->esz, fdt); break;
+        case SG_VIEW_GKINT:
+            set(g->has_kint ? g->gkint : nullptr, 3, g->n_pkg, 3, 64, g->esz, fdt);
+            break;
+        case SG_VIEW_PLANE_FIRST:
+            set(g->plane_first, 1, g->gc.zs_hi - g->gc.zs_lo + 1, 1, 1, 8, 4);
+            break;
+        default: throw Error(SG_ERR_ARG, "sg_view: unknown selector");
+        }
+    });
+}
+
+extern "C" sg_status sg_balanced_cuts(const int64_t* counts, int32_t nz, int32_t nranks,
+                                      int32_t* cuts) {
+    return guard([&] {
+        SG_ARG(counts && cuts, "sg_balanced_cuts: null argument");
+        SG_ARG(nranks >= 1 && nz >= nranks, "sg_balanced_cuts: need 1 <= nranks <= nz");
+        std::vector<int64_t> pre(nz + 1, 0);
+        for (int z = 0; z < nz; ++z) pre[z + 1] = pre[z] + counts[z];
+        const int64_t total = pre[nz];
+        cuts[0] = 0;
+        cuts[nranks] = nz;
+        for (int r = 1; r < nranks; ++r) {
+            // smallest z with prefix(z) >= r * total / nranks (exact integer
+            // comparison: prefix * nranks >= r * total)
+            int z = 0;
+            while (z < nz && pre[z] * nranks < (int64_t)r * total) ++z;
+            // every slab keeps at least one plane
+            z = std::max(z, cuts[r - 1] + 1);
+            z = std::min(z, nz - (nranks - r));
+            cuts[r] = z;
+        }
+    });
+}
+
+extern "C" sg_status sg_plane_counts(const sg_desc* desc, const sg_geometry* geom, int32_t z_lo,
+                                     int32_t z_hi, int64_t* counts, void* stream) {
+    return guard([&] {
+        check_desc(desc, geom);
+        SG_ARG(counts != nullptr, "sg_plane_counts: null counts");
+        SG_ARG(z_lo >= 0 && z_lo <= z_hi && z_hi <= desc->n[2], "sg_plane_counts: bad plane range");
+        check_device();
+        if (z_hi == z_lo) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        GridC gc = make_gridc(desc);
+        const Geom ge = make_geom(geom);
+        const int32_t zt_lo = std::max(0, z_lo - 1), zt_hi = std::min(desc->n[2], z_hi + 1);
+        uint8_t* flags = (uint8_t*)dalloc((size_t)gc.plane * (zt_hi - zt_lo), s);
+        launch_tag(gc, ge, zt_lo, zt_hi, flags, s);
+        SG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (z_hi - z_lo), s));
+        dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1], (unsigned)(z_hi - z_lo));
+        k_plane_count<<<grid, 256, 0, s>>>(gc, zt_lo, z_lo, flags, (unsigned long long*)counts);
+        SG_LAUNCHED();
+        SG_CUDA(cudaFreeAsync(flags, s));
+    });
+}
+
+extern "C" const char* sg_last_error(void) { return t_last_error.c_str(); }
+extern "C" int32_t sg_abi_version(void) { return SG_ABI_VERSION; }
+extern "C" uint64_t sg_launch_count(void) { return g_launches.load(); }

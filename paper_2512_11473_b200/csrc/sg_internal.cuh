@@ -1,0 +1,142 @@
+// sg_internal.cuh -- private definitions of libsg (grid handle, launch and
+// error plumbing).  Not part of the ABI; see include/sg.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sg.h"
+
+namespace sg {
+
+// Analytic geometry, passed by value to the kernels that evaluate f
+// (parameter space, ~1.6 KB).
+struct Geom {
+    int32_t n;
+    int32_t kind[SG_MAX_PRIMS];
+    double p[SG_MAX_PRIMS][12];
+};
+
+// Grid constants passed by value to every kernel.
+struct GridC {
+    double lower[3];
+    double upper[3];  // lower + n * cell
+    double cell;      // l_c
+    double dx;        // l_c / 4
+    double far;
+    double init_scale;
+    int32_t n[3];
+    int32_t zs_lo, zs_hi;  // stored planes
+    int32_t z_lo, z_hi;    // owned planes
+    int64_t plane;         // n[0] * n[1]
+};
+
+struct Error : std::runtime_error {
+    sg_status st;
+    Error(sg_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+extern std::atomic<uint64_t> g_launches;
+
+void set_last_error(const std::string& m);
+void clear_last_error();
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define SG_CUDA(x)                                                  \
+    do {                                                            \
+        cudaError_t e_ = (x);                                       \
+        if (e_ != cudaSuccess) ::sg::throw_cuda(e_, #x, __FILE__, __LINE__); \
+    } while (0)
+
+// After every kernel launch: surface launch errors, count the launch.
+#define SG_LAUNCHED()                                               \
+    do {                                                            \
+        SG_CUDA(cudaGetLastError());                                \
+        ::sg::g_launches.fetch_add(1, std::memory_order_relaxed);   \
+    } while (0)
+
+#define SG_ARG(cond, msg)                                           \
+    do {                                                            \
+        if (!(cond)) throw ::sg::Error(SG_ERR_ARG, msg);            \
+    } while (0)
+
+template <class F>
+sg_status guard(F&& f) {
+    clear_last_error();
+    try {
+        f();
+        return SG_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.st;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return SG_ERR_OOM;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return SG_ERR_CUDA;
+    }
+}
+
+// Stream-ordered device allocation from the default pool (memory kept in the
+// pool across grids: release threshold raised on first use).
+void* dalloc(size_t bytes, cudaStream_t s);
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace sg
+
+struct sg_grid {
+    sg::GridC gc;
+    sg::Geom geom;
+    int32_t dtype = SG_F32;
+    int32_t esz = 4;
+    int64_t id_base = 2;
+    int64_t n_pkg = 2, n_core = 0, n_inner = 0;
+    int64_t ncell_stored = 0;
+    // topology: background table, meta, neighbour table
+    uint32_t* bg = nullptr;
+    uint32_t* meta_cell = nullptr;
+    uint8_t* meta_cat = nullptr;
+    uint32_t* nb = nullptr;
+    int64_t* plane_first = nullptr;  // [stored planes + 1]
+    // fields
+    void* phi[2] = {nullptr, nullptr};
+    int cur = 0;
+    void* grad = nullptr;
+    void* normal = nullptr;
+    void* kint = nullptr;
+    void* gkint = nullptr;
+    bool has_grad = false, has_normal = false, has_kint = false;
+    double kernel_sum = 0.0;
+    int device = 0;
+    std::vector<std::pair<void*, size_t>> allocs;
+    // owned package range [own_lo, own_hi) in local ids
+    int64_t own_lo = 2, own_hi = 2;
+
+    void* alloc(size_t bytes, cudaStream_t s) {
+        void* p = sg::dalloc(bytes, s);
+        allocs.emplace_back(p, bytes);
+        return p;
+    }
+    int64_t bytes() const {
+        int64_t b = 0;
+        for (auto& a : allocs) b += (int64_t)a.second;
+        return b;
+    }
+};
+
+// kernels / launchers implemented per translation unit
+namespace sg {
+void launch_reinit(sg_grid* g, int32_t iters, double cfl, cudaStream_t s);
+void launch_gradient(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t s);
+void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void* grad,
+                  unsigned long long* oob, cudaStream_t s);
+void launch_table1(sg_grid* g, int32_t op, double value, cudaStream_t s);
+}  // namespace sg

@@ -1,0 +1,315 @@
+"""Thin Python binding of libsg (include/sg.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libsg.so; this module
+only converts Python/torch arguments into the C-ABI's plain pointers and
+sizes.  There is no fallback: if libsg.so is missing, or no CUDA device is
+present, the calls raise.
+
+Low-level functions carry the C names (sg_build, sg_reinit, sg_gradient,
+sg_probe, sg_table1, sg_info, sg_view, sg_destroy, ...).  `Grid` is a small
+convenience wrapper over them that hands out zero-copy torch views.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsg.so")
+
+SG_OK, SG_ERR_ARG, SG_ERR_OOM, SG_ERR_CUDA, SG_ERR_NCCL, SG_ERR_STATE, SG_ERR_DOMAIN = range(7)
+SG_F32, SG_F64 = 0, 1
+SG_GRAD, SG_NORMAL, SG_KINT = 1, 2, 4
+VIEWS = {"bg": 0, "meta_cell": 1, "meta_cat": 2, "nb": 3, "phi": 4, "grad": 5, "normal": 6,
+         "kint": 7, "gkint": 8, "plane_first": 9, "phi_next": 10}
+_STATUS = {0: "SG_OK", 1: "SG_ERR_ARG", 2: "SG_ERR_OOM", 3: "SG_ERR_CUDA", 4: "SG_ERR_NCCL",
+           5: "SG_ERR_STATE", 6: "SG_ERR_DOMAIN"}
+
+# exported symbols declared in include/sg.h (checked by the CPU test suite)
+EXPORTS = ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_info", "sg_view",
+           "sg_destroy", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
+           "sg_last_error", "sg_abi_version", "sg_launch_count")
+
+
+class SgError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class sg_prim(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("p", C.c_double * 12)]
+
+
+class sg_geometry(C.Structure):
+    _fields_ = [("prims", C.POINTER(sg_prim)), ("n_prims", C.c_int32), ("pad", C.c_int32)]
+
+
+class sg_desc(C.Structure):
+    _fields_ = [("lower", C.c_double * 3), ("cell", C.c_double), ("n", C.c_int32 * 3),
+                ("pkg", C.c_int32), ("dtype", C.c_int32), ("pad", C.c_int32),
+                ("far", C.c_double), ("init_scale", C.c_double)]
+
+
+class sg_slab(C.Structure):
+    _fields_ = [("z_lo", C.c_int32), ("z_hi", C.c_int32), ("id_base", C.c_int64)]
+
+
+class sg_view_t(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("shape", C.c_int64 * 3), ("ndim", C.c_int32),
+                ("elem_size", C.c_int32), ("dtype", C.c_int32), ("pad", C.c_int32)]
+
+
+class sg_info_t(C.Structure):
+    _fields_ = [("n_pkg", C.c_int64), ("n_core", C.c_int64), ("n_inner", C.c_int64),
+                ("id_base", C.c_int64), ("dtype", C.c_int32), ("z_lo", C.c_int32),
+                ("z_hi", C.c_int32), ("zs_lo", C.c_int32), ("zs_hi", C.c_int32),
+                ("pad", C.c_int32), ("dx", C.c_double), ("far", C.c_double),
+                ("kernel_sum", C.c_double), ("has_grad", C.c_int32), ("has_normal", C.c_int32),
+                ("has_kint", C.c_int32), ("phi_cur", C.c_int32), ("device_bytes", C.c_int64),
+                ("own_lo", C.c_int64), ("own_hi", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
+
+
+_lib = None
+
+
+def lib():
+    """Load libsg.so (built in-tree by paper_2512_11473_b200.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libsg.so not built: run `python -m paper_2512_11473_b200.build` "
+                              f"({LIB_PATH} missing); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        L.sg_build.argtypes = [C.POINTER(sg_desc), C.POINTER(sg_geometry), C.POINTER(sg_slab), P,
+                               C.POINTER(P)]
+        L.sg_reinit.argtypes = [P, I32, D, P]
+        L.sg_gradient.argtypes = [P, C.c_uint32, D, P]
+        L.sg_probe.argtypes = [P, I64, P, P, P, P, P]
+        L.sg_table1.argtypes = [P, I32, D, P]
+        L.sg_info.argtypes = [P, C.POINTER(sg_info_t)]
+        L.sg_view.argtypes = [P, I32, C.POINTER(sg_view_t)]
+        L.sg_destroy.argtypes = [P]
+        L.sg_destroy.restype = None
+        L.sg_destroy_async.argtypes = [P, P]
+        L.sg_balanced_cuts.argtypes = [P, I32, I32, P]
+        L.sg_plane_counts.argtypes = [C.POINTER(sg_desc), C.POINTER(sg_geometry), I32, I32, P, P]
+        L.sg_last_error.restype = C.c_char_p
+        L.sg_abi_version.restype = I32
+        L.sg_launch_count.restype = C.c_uint64
+        for name in ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_info",
+                     "sg_view", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != SG_OK:
+        raise SgError(st, lib().sg_last_error().decode(errors="replace"))
+
+
+def _stream(stream):
+    """torch.cuda.Stream | int | None -> void*"""
+    if stream is None:
+        try:
+            import torch
+            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except Exception:
+            return C.c_void_p(0)
+    if hasattr(stream, "cuda_stream"):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+def make_desc(w) -> tuple:
+    """Workload-like object (n, cell, lower, dtype, prims, far, init_scale)
+    -> (sg_desc, sg_geometry, keepalive)."""
+    d = sg_desc()
+    for k in range(3):
+        d.lower[k] = float(w.lower[k])
+        d.n[k] = int(w.n[k])
+    d.cell = float(w.cell)
+    d.pkg = 4
+    d.dtype = SG_F64 if w.dtype in ("f64", "float64") else SG_F32
+    d.far = float(getattr(w, "far", 0.0) or 0.0)
+    d.init_scale = float(getattr(w, "init_scale", 1.0) or 1.0)
+    prims = (sg_prim * len(w.prims))()
+    for i, pr in enumerate(w.prims):
+        prims[i].kind = int(pr.kind)
+        for j, v in enumerate(pr.p):
+            prims[i].p[j] = float(v)
+    geom = sg_geometry(C.cast(prims, C.POINTER(sg_prim)), len(w.prims), 0)
+    return d, geom, prims
+
+
+# ------------------------------------------------------------ raw C calls --
+
+def sg_build(desc: sg_desc, geom: sg_geometry, slab: sg_slab | None = None, stream=None) -> int:
+    out = C.c_void_p()
+    _check(lib().sg_build(C.byref(desc), C.byref(geom), C.byref(slab) if slab else None,
+                          _stream(stream), C.byref(out)))
+    return out.value
+
+
+def sg_reinit(grid: int, iters: int, cfl: float = 0.3, stream=None) -> None:
+    _check(lib().sg_reinit(C.c_void_p(grid), int(iters), float(cfl), _stream(stream)))
+
+
+def sg_gradient(grid: int, fields: int = SG_GRAD | SG_NORMAL, h_ratio: float = 1.3,
+                stream=None) -> None:
+    _check(lib().sg_gradient(C.c_void_p(grid), int(fields), float(h_ratio), _stream(stream)))
+
+
+def sg_probe(grid: int, n: int, pos_ptr: int, phi_ptr: int, grad_ptr: int | None = None,
+             oob_ptr: int | None = None, stream=None) -> None:
+    _check(lib().sg_probe(C.c_void_p(grid), int(n), C.c_void_p(pos_ptr), C.c_void_p(phi_ptr),
+                          C.c_void_p(grad_ptr) if grad_ptr else None,
+                          C.c_void_p(oob_ptr) if oob_ptr else None, _stream(stream)))
+
+
+def sg_table1(grid: int, op: int, value: float = 1.0, stream=None) -> None:
+    _check(lib().sg_table1(C.c_void_p(grid), int(op), float(value), _stream(stream)))
+
+
+def sg_info(grid: int) -> dict:
+    info = sg_info_t()
+    _check(lib().sg_info(C.c_void_p(grid), C.byref(info)))
+    return info.as_dict()
+
+
+def sg_view(grid: int, what: int) -> sg_view_t:
+    v = sg_view_t()
+    _check(lib().sg_view(C.c_void_p(grid), int(what), C.byref(v)))
+    return v
+
+
+def sg_destroy(grid: int) -> None:
+    lib().sg_destroy(C.c_void_p(grid))
+
+
+def sg_destroy_async(grid: int, stream=None) -> None:
+    _check(lib().sg_destroy_async(C.c_void_p(grid), _stream(stream)))
+
+
+def sg_balanced_cuts(counts, nranks: int) -> list:
+    import numpy as np
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.int64))
+    cuts = np.zeros(nranks + 1, dtype=np.int32)
+    _check(lib().sg_balanced_cuts(c.ctypes.data_as(C.c_void_p), int(c.size), int(nranks),
+                                  cuts.ctypes.data_as(C.c_void_p)))
+    return [int(v) for v in cuts]
+
+
+def sg_plane_counts(desc: sg_desc, geom: sg_geometry, z_lo: int, z_hi: int, counts_ptr: int,
+                    stream=None) -> None:
+    _check(lib().sg_plane_counts(C.byref(desc), C.byref(geom), int(z_lo), int(z_hi),
+                                 C.c_void_p(counts_ptr), _stream(stream)))
+
+
+def sg_launch_count() -> int:
+    return int(lib().sg_launch_count())
+
+
+def sg_abi_version() -> int:
+    return int(lib().sg_abi_version())
+
+
+# ---------------------------------------------------------------- torch ----
+
+_TORCH_DT = {0: "float32", 1: "float64", 2: "uint32", 3: "uint8", 4: "int64"}
+_TYPESTR = {0: "<f4", 1: "<f8", 2: "<u4", 3: "|u1", 4: "<i8"}
+
+
+class _CAI:
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def view_tensor(grid: int, name: str):
+    """Zero-copy torch view of a device array of the grid (non-owning: valid
+    until the grid is destroyed or, for phi, the next reinit swap)."""
+    import torch
+    v = sg_view(grid, VIEWS[name])
+    if not v.ptr:
+        raise SgError(SG_ERR_STATE, f"view '{name}' not computed yet")
+    shape = [v.shape[i] for i in range(v.ndim)]
+    if v.dtype == 2:  # torch lacks full uint32 support: expose as int32 bits
+        t = torch.as_tensor(_CAI(v.ptr, shape, "<i4"), device="cuda")
+        return t
+    return torch.as_tensor(_CAI(v.ptr, shape, _TYPESTR[v.dtype]), device="cuda")
+
+
+class Grid:
+    """Owning handle around sg_build/sg_destroy with torch-friendly calls."""
+
+    def __init__(self, w, slab: tuple | None = None, stream=None):
+        self.w = w
+        self.desc, self.geom, self._keep = make_desc(w)
+        sl = None
+        if slab is not None:
+            sl = sg_slab(int(slab[0]), int(slab[1]), int(slab[2]))
+        self.handle = sg_build(self.desc, self.geom, sl, stream)
+
+    @property
+    def info(self) -> dict:
+        return sg_info(self.handle)
+
+    def reinit(self, iters: int, cfl: float = 0.3, stream=None):
+        sg_reinit(self.handle, iters, cfl, stream)
+        return self
+
+    def gradient(self, fields: int = SG_GRAD | SG_NORMAL, h_ratio: float = 1.3, stream=None):
+        sg_gradient(self.handle, fields, h_ratio, stream)
+        return self
+
+    def table1(self, op: int, value: float = 1.0, stream=None):
+        sg_table1(self.handle, op, value, stream)
+        return self
+
+    def probe(self, pos, want_grad: bool = True, oob=None, stream=None):
+        """pos: torch tensor (n, 3) of the grid dtype on cuda (or pinned/
+        pageable CPU tensor -> host path).  Returns (phi, grad|None)."""
+        import torch
+        n = int(pos.shape[0])
+        dt = pos.dtype
+        phi = torch.empty(n, dtype=dt, device=pos.device, pin_memory=(pos.device.type == "cpu"
+                                                                        and pos.is_pinned()))
+        grad = None
+        if want_grad:
+            grad = torch.empty((n, 3), dtype=dt, device=pos.device,
+                               pin_memory=(pos.device.type == "cpu" and pos.is_pinned()))
+        sg_probe(self.handle, n, pos.data_ptr(), phi.data_ptr(),
+                 grad.data_ptr() if grad is not None else None,
+                 oob.data_ptr() if oob is not None else None, stream)
+        return phi, grad
+
+    def view(self, name: str):
+        return view_tensor(self.handle, name)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            sg_destroy(self.handle)
+            self.handle = None
+
+    def close_async(self, stream=None):
+        if getattr(self, "handle", None):
+            sg_destroy_async(self.handle, stream)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,90 @@
+"""C-ABI checks that need no GPU: the library loads, exports every function
+include/sg.h declares, the ctypes mirrors match the C struct layouts, and the
+host-only partition helper behaves (no device compute calls here)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "sg.h")
+
+
+@pytest.fixture(scope="module")
+def sg():
+    from paper_2512_11473_b200 import build, sg as S
+    build.build()
+    return S
+
+
+def _declared_functions():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:sg_status|void|const char\*|int32_t|uint64_t)\s+(sg_\w+)\s*\(",
+                                 txt, flags=re.M)))
+
+
+def test_exports_every_declared_symbol(sg):
+    names = _declared_functions()
+    assert len(names) >= 14
+    L = C.CDLL(sg.LIB_PATH)
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(sg.EXPORTS)
+    # exported dynamic symbols of the .so (nm -D)
+    out = subprocess.run(["nm", "-D", "--defined-only", sg.LIB_PATH], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}$", out, flags=re.M), n
+
+
+def test_abi_version(sg):
+    assert sg.sg_abi_version() == 1
+    assert sg.sg_launch_count() == 0
+
+
+def test_ctypes_layout_matches_header(sg, tmp_path):
+    src = tmp_path / "sz.c"
+    src.write_text('#include "sg.h"\n#include <stdio.h>\n#include <stddef.h>\nint main(){printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n",'
+                   'sizeof(sg_prim),sizeof(sg_geometry),sizeof(sg_desc),sizeof(sg_slab),sizeof(sg_view_t),'
+                   'sizeof(sg_info_t),offsetof(sg_info_t,own_hi),offsetof(sg_desc,init_scale));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I" + os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
+    exp = [C.sizeof(sg.sg_prim), C.sizeof(sg.sg_geometry), C.sizeof(sg.sg_desc), C.sizeof(sg.sg_slab),
+           C.sizeof(sg.sg_view_t), C.sizeof(sg.sg_info_t), sg.sg_info_t.own_hi.offset,
+           sg.sg_desc.init_scale.offset]
+    assert got == exp
+
+
+def test_balanced_cuts_host_logic(sg):
+    counts = np.array([0, 0, 5, 10, 10, 10, 5, 0, 0, 0])
+    cuts = sg.sg_balanced_cuts(counts, 2)
+    assert cuts[0] == 0 and cuts[-1] == 10
+    pre = np.concatenate([[0], np.cumsum(counts)])
+    # cut = smallest z with prefix(z) >= total/2
+    assert cuts[1] == int(np.argmax(pre * 2 >= pre[-1]))
+    for r in (1, 3, 4, 8, 10):
+        c = sg.sg_balanced_cuts(counts, r)
+        assert len(c) == r + 1 and all(b > a for a, b in zip(c, c[1:]))
+    with pytest.raises(sg.SgError):
+        sg.sg_balanced_cuts(counts, 11)
+    with pytest.raises(sg.SgError):
+        sg.sg_balanced_cuts(counts, 0)
+    # balance quality on the C3 plane profile of the oracle
+    from oracle.oracle import Oracle
+    import workloads as W
+    t = Oracle(W.config("C2")).build_tables()
+    c = sg.sg_balanced_cuts(t.plane_count, 8)
+    loads = [int(t.plane_count[a:b].sum()) for a, b in zip(c, c[1:])]
+    # whole-plane granularity: no slab exceeds the mean by more than one plane
+    assert max(loads) <= sum(loads) / 8 + int(t.plane_count.max())
+
+
+def test_no_torch_types_in_header():
+    txt = open(HEADER).read()
+    assert "torch" not in re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    assert 'extern "C"' in txt

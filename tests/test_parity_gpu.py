@@ -1,0 +1,352 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Tables (background, meta, neighbours, plane ranges) must be bit-exact.
+Fields use the tolerances of DESIGN.md "Tolerances" (north_star: 1e-5 dx per
+reinit iteration in fp32, 1e-12 relative in fp64).  Oracle inputs never come
+from the GPU: multi-step comparisons feed the ORACLE's state into the GPU.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def sgm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2512_11473_b200 import build
+    build.build()
+    from paper_2512_11473_b200 import sg
+    return sg
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import oracle
+    oracle.build()
+    return oracle
+
+
+def np_dtype(w):
+    return np.float64 if w.dtype == "f64" else np.float32
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def phi_tol(w):
+    return 1e-5 * w.dx if w.dtype == "f32" else None
+
+
+def assert_phi_close(w, got, exp, what=""):
+    got = np.asarray(got, dtype=np.float64)
+    if w.dtype == "f32":
+        err = np.max(np.abs(got - exp)) if got.size else 0.0
+        assert err <= 1e-5 * w.dx, f"{what}: max err {err / w.dx:.3e} dx"
+    else:
+        scale = np.maximum(np.abs(exp), w.dx)
+        err = np.max(np.abs(got - exp) / scale) if got.size else 0.0
+        assert err <= 1e-12, f"{what}: max rel err {err:.3e}"
+
+
+def tables_equal(sgm, O, w):
+    o = O.Oracle(w)
+    t = o.build_tables()
+    g = sgm.Grid(w)
+    info = g.info
+    assert info["n_pkg"] == t.n_pkg
+    assert info["n_core"] == int(np.count_nonzero(t.cat == 3))
+    assert info["n_inner"] == int(np.count_nonzero(t.cat == 2))
+    assert np.array_equal(u32(g.view("bg")), t.bg)
+    assert np.array_equal(u32(g.view("meta_cell")), t.meta_cell)
+    assert np.array_equal(g.view("meta_cat").cpu().numpy(), t.meta_cat)
+    assert np.array_equal(u32(g.view("nb")), t.nb)
+    pf = g.view("plane_first").cpu().numpy()
+    exp_pf = 2 + np.concatenate([[0], np.cumsum(t.plane_count)])
+    assert np.array_equal(pf, exp_pf)
+    return o, t, g
+
+
+# ------------------------------------------------------------------ tables --
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_tables_bit_exact_configs(sgm, O, name):
+    tables_equal(sgm, O, W.config(name))
+
+
+@pytest.mark.parametrize("seed,n", [(0, 8), (1, 13), (2, 16), (3, 24), (4, 9), (5, 20), (6, 17), (7, 31)])
+def test_tables_bit_exact_random_scenes(sgm, O, seed, n):
+    tables_equal(sgm, O, W.random_scene(seed, n, dtype="f64" if seed % 2 else "f32"))
+
+
+def test_tables_nonuniform_grid_and_offset(sgm, O):
+    w = W.Workload("aniso", (23, 9, 14), 0.05, lower=(-0.3, 0.1, -0.2), dtype="f32",
+                   prims=(W.Prim(W.TORUS_Z, (0.25, 0.32, 0.15, 0.25, 0.08)),
+                          W.Prim(W.SPHERE, (0.7, 0.3, 0.4, 0.12))))
+    tables_equal(sgm, O, w)
+
+
+def test_band_touching_domain_boundary(sgm, O):
+    # sphere reaching outside the domain: out-of-domain neighbours by sign (R-6)
+    w = W.Workload("edge", (12, 12, 12), 1 / 12, dtype="f64",
+                   prims=(W.Prim(W.SPHERE, (0.1, 0.5, 0.5, 0.35)),))
+    o, t, g = tables_equal(sgm, O, w)
+    assert (t.nb[2:] <= 1).any()
+    # fields too
+    phi0 = o.phi_dense()
+    gp = g.view("phi").cpu().numpy()
+    assert_phi_close(w, gp, o.to_packages(phi0, -o.far, o.far), "init")
+    g.reinit(1)
+    assert_phi_close(w, g.view("phi").cpu().numpy(),
+                     o.to_packages(o.reinit_step(phi0), -o.far, o.far), "reinit")
+
+
+def test_empty_band_and_single_cell(sgm, O):
+    # geometry entirely outside the domain: no packages, all far field
+    w = W.Workload("empty", (8, 8, 8), 1 / 8, dtype="f32",
+                   prims=(W.Prim(W.SPHERE, (5.0, 5.0, 5.0, 0.3)),))
+    o, t, g = tables_equal(sgm, O, w)
+    assert g.info["n_pkg"] == 2
+    g.reinit(3).gradient(sgm.SG_GRAD | sgm.SG_NORMAL | sgm.SG_KINT)
+    pos = torch.tensor([[0.5, 0.5, 0.5], [0.1, 0.2, 0.3]], dtype=torch.float32, device="cuda")
+    phi, grad = g.probe(pos)
+    assert torch.all(phi == o.far) and torch.all(grad == 0)
+    # n = 1 background cell
+    w1 = W.Workload("one", (1, 1, 1), 0.5, dtype="f64", prims=(W.Prim(W.SPHERE, (0.25, 0.25, 0.25, 0.2)),))
+    o1, t1, g1 = tables_equal(sgm, O, w1)
+    assert g1.info["n_pkg"] == 3
+    g1.reinit(1)
+    assert_phi_close(w1, g1.view("phi").cpu().numpy(),
+                     o1.to_packages(o1.reinit_step(o1.phi_dense()), -o1.far, o1.far))
+
+
+def test_argument_errors(sgm):
+    w = W.config("C1")
+    d, geom, keep = sgm.make_desc(w)
+    d.pkg = 3
+    with pytest.raises(sgm.SgError) as e:
+        sgm.sg_build(d, geom)
+    assert e.value.status == sgm.SG_ERR_ARG
+    g = sgm.Grid(w)
+    with pytest.raises(sgm.SgError):
+        g.reinit(1, cfl=0.7)
+    with pytest.raises(sgm.SgError):
+        g.gradient(sgm.SG_KINT, h_ratio=3.0)
+    pos = torch.zeros((4, 3), dtype=torch.float64, device="cuda")
+    with pytest.raises(sgm.SgError) as e:
+        g.probe(pos, want_grad=True)  # no gradient yet
+    assert e.value.status == sgm.SG_ERR_STATE
+
+
+# ------------------------------------------------------------------ fields --
+
+@pytest.mark.parametrize("name,scale", [("C1", 1.0), ("C1", 2.0), ("C2", 1.0)])
+def test_phi_init(sgm, O, name, scale):
+    w = W.config(name).with_(init_scale=scale)
+    o = O.Oracle(w)
+    o.build_tables()
+    exp = o.to_packages(o.phi_dense(), -o.far, o.far)
+    g = sgm.Grid(w)
+    got = g.view("phi").cpu().numpy()
+    # fp64 SDF with identical operation order on both sides, then RN to dtype
+    assert np.array_equal(got, exp.astype(np_dtype(w)))
+
+
+def _upload(g, w, pk):
+    g.view("phi").copy_(torch.from_numpy(pk.astype(np_dtype(w))))
+
+
+@pytest.mark.parametrize("name,scale", [("C1", 1.0), ("C1", 2.0), ("C2", 1.0), ("C2", 2.0)])
+def test_reinit_per_iteration(sgm, O, name, scale):
+    """One sweep from the same input state, at k = 0 and k = 10 oracle
+    iterations (the oracle state rounded to dtype is uploaded to the GPU)."""
+    w = W.config(name).with_(init_scale=scale)
+    o = O.Oracle(w)
+    o.build_tables()
+    g = sgm.Grid(w)
+    phi = o.phi_dense()
+    dt = np_dtype(w)
+    for k in (0, 10):
+        if k:
+            phi = o.reinit(phi, k)
+        phi_in = phi.astype(dt).astype(np.float64)  # exactly the GPU's input
+        _upload(g, w, o.to_packages(phi_in, -o.far, o.far))
+        exp = o.to_packages(o.reinit_step(phi_in), -o.far, o.far)
+        g.reinit(1)
+        assert_phi_close(w, g.view("phi").cpu().numpy(), exp, f"{name} step {k}")
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_reinit_drift_20(sgm, O, name):
+    """20 GPU sweeps vs 20 oracle sweeps from the same init: flag if the
+    drift exceeds 20 x the per-step tolerance."""
+    w = W.config(name)
+    o = O.Oracle(w)
+    o.build_tables()
+    g = sgm.Grid(w)
+    g.reinit(20)
+    exp = o.to_packages(o.reinit(o.phi_dense(), 20), -o.far, o.far)
+    got = g.view("phi").cpu().numpy().astype(np.float64)
+    if w.dtype == "f32":
+        assert np.max(np.abs(got - exp)) <= 20 * 1e-5 * w.dx
+    else:
+        assert np.max(np.abs(got - exp) / np.maximum(np.abs(exp), w.dx)) <= 20 * 1e-12
+
+
+def _vec_pk(o, dense3):
+    return np.stack([o.to_packages(dense3[c], 0.0, 0.0) for c in range(3)], axis=1)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_gradient_normal_kernel(sgm, O, name):
+    w = W.config(name)
+    o = O.Oracle(w)
+    o.build_tables()
+    phi = o.reinit(o.phi_dense(), 5).astype(np_dtype(w)).astype(np.float64)
+    g = sgm.Grid(w)
+    _upload(g, w, o.to_packages(phi, -o.far, o.far))
+    g.gradient(sgm.SG_GRAD | sgm.SG_NORMAL | sgm.SG_KINT, h_ratio=w.h_ratio)
+    grad, normal = o.gradient(phi)
+    eg, en = _vec_pk(o, grad), _vec_pk(o, normal)
+    gg = g.view("grad").cpu().numpy().astype(np.float64)
+    gn = g.view("normal").cpu().numpy().astype(np.float64)
+    tol = 1e-5 if w.dtype == "f32" else 1e-12
+    assert np.max(np.abs(gg - eg) / np.maximum(1.0, np.abs(eg))) <= tol
+    m = np.linalg.norm(eg, axis=1, keepdims=True) >= 0.5
+    mm = np.broadcast_to(m, en.shape)
+    assert np.max(np.abs(gn - en)[mm]) <= tol
+    K, G = o.kernel_integrals(phi, w.h_ratio)
+    S = O.kernel_taps(w.h_ratio, o.dx)[1].sum()
+    eK = o.to_packages(K, S, 0.0)  # singular packages: S / 0 (R-16)
+    eG = _vec_pk(o, G)
+    gK = g.view("kint").cpu().numpy().astype(np.float64)
+    gG = g.view("gkint").cpu().numpy().astype(np.float64)
+    assert abs(g.info["kernel_sum"] - S) < 1e-12
+    assert np.max(np.abs(gK - eK)) <= tol
+    h = w.h_ratio * w.dx
+    assert np.max(np.abs(gG - eG) / (np.maximum(1.0, h * np.abs(eG)) / h)) <= tol
+
+
+# ------------------------------------------------------------------- probe --
+
+def _probe_compare(sgm, O, w, pos_np, phi_iters=3):
+    o = O.Oracle(w)
+    o.build_tables()
+    phi = o.reinit(o.phi_dense(), phi_iters).astype(np_dtype(w)).astype(np.float64)
+    g = sgm.Grid(w)
+    _upload(g, w, o.to_packages(phi, -o.far, o.far))
+    g.gradient(sgm.SG_GRAD)
+    grad, _ = o.gradient(phi)
+    grad = grad.astype(np_dtype(w)).astype(np.float64)  # the GPU stores grad in dtype
+    # the oracle interpolates the same dtype-rounded grad the GPU stores
+    pos = torch.from_numpy(pos_np).cuda()
+    oob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    gphi, ggrad = g.probe(pos, oob=oob)
+    ephi, egrad, eoob = o.probe(phi, grad, pos_np)
+    gphi = gphi.cpu().numpy().astype(np.float64)
+    ggrad = ggrad.cpu().numpy().astype(np.float64)
+    assert int(oob.item()) == eoob
+    assert_phi_close(w, gphi, ephi, "probe phi")
+    tol = 1e-5 if w.dtype == "f32" else 1e-12
+    assert np.max(np.abs(ggrad - egrad) / np.maximum(1.0, np.abs(egrad))) <= tol
+    return g, o, pos, gphi, ggrad
+
+
+def test_probe_c1_lattice_and_random(sgm, O):
+    w = W.config("C1")
+    lat = W.lattice_particles(w, dtype=np.float64)
+    rnd = W.random_positions(w, 20000, seed=3)
+    bad = np.array([[-0.1, 0.5, 0.5], [0.5, 1.0, 0.5], [np.nan, 0.5, 0.5], [0.5, 0.5, 1.5]])
+    faces = rnd[:2000].copy()
+    faces[:, 0] = np.round(faces[:, 0] / w.cell) * w.cell  # exactly on package faces
+    pos = np.concatenate([lat, rnd, bad, faces])
+    g, o, tpos, gphi, ggrad = _probe_compare(sgm, O, w, pos)
+    # host-buffer path (C-ABI with host pointers) is bitwise the device path
+    hpos = tpos.cpu().pin_memory()
+    hphi, hgrad = g.probe(hpos)
+    assert np.array_equal(hphi.numpy(), gphi) and np.array_equal(hgrad.numpy(), ggrad)
+    pphi, pgrad = g.probe(tpos.cpu())  # pageable
+    assert np.array_equal(pphi.numpy(), gphi)
+
+
+def test_probe_c4_particles_on_c2(sgm, O):
+    """C4: ~19.45 M lattice particles (jittered, sorted) on the C2 grid."""
+    w = W.config("C2")
+    pos = W.lattice_particles(w, seed=0)
+    g, o, tpos, gphi, ggrad = _probe_compare(sgm, O, w, pos)
+    assert pos.shape[0] == 19454436
+    far = np.abs(gphi) == np.float32(o.far)
+    frac_band = 1.0 - far.mean()
+    assert 0.15 < frac_band < 0.23  # ~18.9 % in active cells
+
+
+def test_probe_empty_and_zero(sgm, O):
+    w = W.config("C1")
+    g = sgm.Grid(w)
+    pos = torch.empty((0, 3), dtype=torch.float64, device="cuda")
+    phi, grad = g.probe(pos, want_grad=False)
+    assert phi.numel() == 0
+
+
+# ----------------------------------------------------------- Table 1 ops ---
+
+def test_table1_sequential_and_laplacian(sgm, O):
+    """Sequential: checksum = initial + v * count.  Stencil: the
+    7-point Laplacian of x^2 + y^2 + z^2 is 6 exactly where all six
+    neighbours are band points."""
+    w = W.config("C1")
+    o = O.Oracle(w)
+    t = o.build_tables()
+    g = sgm.Grid(w)
+    phi0 = g.view("phi").clone()
+    g.table1(0, 1.0)
+    d = (g.view("phi") - phi0).cpu().numpy()
+    assert np.all(d[2:] == 1.0) and np.all(d[:2] == 0)
+    m = 4 * w.n[0]
+    I = (np.arange(m) + 0.5) * w.dx
+    Z, Y, X = np.meshgrid(I, I, I, indexing="ij")
+    q = X**2 + Y**2 + Z**2
+    _upload(g, w, o.to_packages(q, -o.far, o.far))
+    g.table1(1)
+    lap = g.view("phi_next").cpu().numpy()
+    # points whose 6 neighbours lie in active cells
+    cb = np.repeat(np.repeat(np.repeat(t.bg.reshape(w.n[::-1]) >= 2, 4, 0), 4, 1), 4, 2)
+    inner = cb.copy()
+    for ax in range(3):
+        inner &= np.roll(cb, 1, ax) & np.roll(cb, -1, ax)
+    lapd = o.to_packages(np.zeros_like(q), 0, 0)
+    mask = o.to_packages(inner.astype(np.float64), 0, 0) > 0
+    assert mask.sum() > 1000
+    assert np.max(np.abs(lap[mask] - 6.0)) < 1e-9
+    assert lapd.shape == lap.shape
+
+
+# ----------------------------------------------------- full size, sampled --
+
+def test_c3_full_size_sampled(sgm, O):
+    """C3 (2048^3 effective): tables bit-exact in full; phi init and the first
+    reinit sweep at sampled points against the oracle's pointwise forms."""
+    w = W.config("C3")
+    o, t, g = tables_equal(sgm, O, w)
+    phi = g.view("phi")
+    rng = np.random.default_rng(11)
+    ids = rng.integers(2, t.n_pkg, 3000)
+    ds = rng.integers(0, 64, 3000)
+    cells = t.meta_cell[ids].astype(np.int64)
+    cx, cy, cz = cells % 512, (cells // 512) % 512, cells // (512 * 512)
+    ix, iy, iz = 4 * cx + (ds & 3), 4 * cy + ((ds >> 2) & 3), 4 * cz + (ds >> 4)
+    got0 = phi.cpu().numpy()[ids, ds]
+    exp0 = np.array([o.phi_point(a, b, c) for a, b, c in zip(ix, iy, iz)])
+    assert np.array_equal(got0, exp0.astype(np.float32))
+    g.reinit(1)
+    got1 = g.view("phi").cpu().numpy()[ids, ds].astype(np.float64)
+    exp1 = np.array([o.reinit_point_from_init(a, b, c, w.cfl) for a, b, c in zip(ix, iy, iz)])
+    # the GPU's input is the fp32-rounded init; the pointwise oracle uses the
+    # fp64 init: allow the input rounding (0.5 ulp of |phi| <= 16 dx) on top
+    assert np.max(np.abs(got1 - exp1)) <= 1e-5 * w.dx + 2 * 16 * w.dx * 2**-24
