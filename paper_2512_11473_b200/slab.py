@@ -1,0 +1,238 @@
+"""Multi-GPU z-slab partition of the sparse grid (north_star: "Packages are
+partitioned across the 8xB200 box in z-slabs of the background grid, with
+NCCL halo exchange of boundary packages ... each reinitialization iteration
+and particles binned to their owning rank").
+
+Plan (host logic, no device compute here):
+  1. every rank counts active packages per background plane of a uniform
+     z-range (sg_plane_counts), the counts are all-gathered;
+  2. balanced cuts (sg_balanced_cuts): rank r owns planes [cuts[r], cuts[r+1]);
+  3. global ids follow the linear cell order (z slowest, R-1), so a rank's
+     stored planes [z_lo-1, z_hi+1) are ONE contiguous global id range
+     starting at id_base = 2 + (packages in planes < z_lo-1);
+  4. halos are whole background planes = contiguous local id ranges: the
+     first owned plane goes to rank r-1's ghost-above plane, the last owned
+     plane to rank r+1's ghost-below plane.  No packing, no index remap.
+
+Per reinit sweep each rank updates its owned packages (sg_reinit(g, 1)) and
+then refreshes the ghost packages of the new current phi buffer with one
+grouped send/recv (torch.distributed P2P over NCCL; any backend works for
+the host-side tests).  Jacobi sweeps are order-independent, so P-GPU results
+are bitwise identical to 1 GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class SlabPlan:
+    rank: int
+    world: int
+    cuts: list          # [world + 1] plane cuts
+    z_lo: int
+    z_hi: int
+    zs_lo: int          # stored planes (owned + ghosts inside the domain)
+    zs_hi: int
+    id_base: int        # global id of local id 2
+
+
+def plan(counts, world: int, rank: int, cuts=None) -> SlabPlan:
+    """counts: per-plane package counts of the whole domain (len nz)."""
+    counts = np.asarray(counts, dtype=np.int64)
+    nz = counts.size
+    if cuts is None:
+        from .sg import sg_balanced_cuts
+        cuts = sg_balanced_cuts(counts, world)
+    z_lo, z_hi = cuts[rank], cuts[rank + 1]
+    zs_lo, zs_hi = max(0, z_lo - 1), min(nz, z_hi + 1)
+    id_base = 2 + int(counts[:zs_lo].sum())
+    return SlabPlan(rank, world, list(cuts), z_lo, z_hi, zs_lo, zs_hi, id_base)
+
+
+@dataclass
+class Halo:
+    """Local id ranges [a, b) of the four halo pieces of one rank."""
+    send_lo: tuple   # first owned plane -> rank - 1
+    send_hi: tuple   # last owned plane  -> rank + 1
+    recv_lo: tuple   # ghost plane below <- rank - 1
+    recv_hi: tuple   # ghost plane above <- rank + 1
+
+
+def halo_ranges(p: SlabPlan, plane_first) -> Halo:
+    """plane_first: local first id of every stored plane (+ end), i.e. the
+    SG_VIEW_PLANE_FIRST array of the rank's grid."""
+    pf = [int(v) for v in plane_first]
+
+    def rng(z):  # local id range of stored plane z
+        i = z - p.zs_lo
+        return (pf[i], pf[i + 1])
+
+    none = (0, 0)
+    has_lo, has_hi = p.rank > 0, p.rank < p.world - 1
+    return Halo(send_lo=rng(p.z_lo) if has_lo else none,
+                send_hi=rng(p.z_hi - 1) if has_hi else none,
+                recv_lo=rng(p.z_lo - 1) if has_lo else none,
+                recv_hi=rng(p.z_hi) if has_hi else none)
+
+
+def exchange(field, halo: Halo, rank: int, world: int, per_pkg: int, group=None):
+    """Refresh the ghost packages of `field` (a tensor whose first dimension
+    is the local package id, flattened to [n_pkg * per_pkg] or shaped
+    [n_pkg, ...]) with one grouped send/recv."""
+    import torch.distributed as dist
+    flat = field.reshape(-1)
+    ops = []
+
+    def sl(r):
+        return flat[r[0] * per_pkg:r[1] * per_pkg]
+
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, sl(halo.send_lo), rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, sl(halo.recv_lo), rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.isend, sl(halo.send_hi), rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, sl(halo.recv_hi), rank + 1, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+def owner_mask(pos, w, p: SlabPlan):
+    """Particles whose containing background plane this rank owns (the
+    binning rule of the probe: OOB on every other rank)."""
+    import torch
+    cz = torch.floor((pos[:, 2].double() - w.lower[2]) / w.cell)
+    return (cz >= p.z_lo) & (cz < p.z_hi)
+
+
+class SlabGrid:
+    """One rank's slab of the global grid plus its halo plan."""
+
+    def __init__(self, w, world: int, rank: int, group=None, stream=None):
+        import torch
+        import torch.distributed as dist
+        from . import sg
+        self.w, self.world, self.rank, self.group = w, world, rank, group
+        nz = w.n[2]
+        desc, geom, keep = sg.make_desc(w)
+        # 1. per-plane counts of a uniform z range, all-gathered
+        lo, hi = rank * nz // world, (rank + 1) * nz // world
+        cnt = torch.zeros(max(1, hi - lo), dtype=torch.int64, device="cuda")
+        sg.sg_plane_counts(desc, geom, lo, hi, cnt.data_ptr(), stream)
+        parts = [torch.zeros(max(1, (r + 1) * nz // world - r * nz // world), dtype=torch.int64,
+                             device="cuda") for r in range(world)]
+        dist.all_gather(parts, cnt, group=group)
+        counts = torch.cat([p[:(r + 1) * nz // world - r * nz // world]
+                            for r, p in enumerate(parts)]).cpu().numpy()
+        self.counts = counts
+        # 2-3. cuts and id base
+        self.plan = plan(counts, world, rank)
+        self.grid = sg.Grid(w, slab=(self.plan.z_lo, self.plan.z_hi, self.plan.id_base),
+                            stream=stream)
+        pf = self.grid.view("plane_first").cpu().numpy()
+        self.halo = halo_ranges(self.plan, pf)
+
+    def exchange(self, name: str):
+        per = 64 if name in ("phi", "kint") else 192
+        exchange(self.grid.view(name), self.halo, self.rank, self.world, per, self.group)
+
+    def reinit(self, iters: int, cfl: float, stream=None):
+        from . import sg
+        for _ in range(iters):
+            sg.sg_reinit(self.grid.handle, 1, cfl, stream)
+            self.exchange("phi")
+
+    def gradient(self, fields: int, h_ratio: float, stream=None):
+        from . import sg
+        sg.sg_gradient(self.grid.handle, fields, h_ratio, stream)
+        if fields & sg.SG_GRAD:
+            self.exchange("grad")
+
+    def close(self):
+        self.grid.close()
+
+
+def bench_slab(args, w, rank, world, local):
+    """bench.py body for N > 1 (torchrun): one z-slab per rank, NCCL halos."""
+    import json
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    import workloads as W
+    from . import sg
+    from bench import METRIC, UNIT, REINIT_ITERS, ClockSampler
+
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    pos_np = W.lattice_particles(w, seed=0, order=args.order,
+                                 dtype=np.float32 if w.dtype == "f32" else np.float64)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    fields = sg.SG_GRAD | sg.SG_NORMAL | sg.SG_KINT
+
+    def step():
+        s = SlabGrid(w, world, rank, stream=stream)
+        s.reinit(REINIT_ITERS, w.cfl, stream)
+        s.gradient(fields, w.h_ratio, stream)
+        return s
+
+    # particles binned to their owner rank (input preparation, untimed)
+    s0 = step()
+    d_pos_all = torch.from_numpy(pos_np).cuda()
+    d_pos = d_pos_all[owner_mask(d_pos_all, w, s0.plan)].contiguous()
+    del d_pos_all
+    n_local = d_pos.shape[0]
+    n_pkg_local = s0.plan and (s0.grid.info["own_hi"] - s0.grid.info["own_lo"])
+    s0.close()
+    d_phi = torch.empty(n_local, dtype=d_pos.dtype, device="cuda")
+    d_grad = torch.empty((n_local, 3), dtype=d_pos.dtype, device="cuda")
+
+    def full_step():
+        s = step()
+        sg.sg_probe(s.grid.handle, n_local, d_pos.data_ptr(), d_phi.data_ptr(), d_grad.data_ptr(),
+                    None, stream)
+        return s
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        full_step().close()
+    torch.cuda.synchronize()
+    l0 = sg.sg_launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            s = full_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            times.append(float(t.item()))
+            s.close()
+    launches = sg.sg_launch_count() - l0
+    tot = torch.tensor([n_pkg_local, n_local], dtype=torch.int64, device="cuda")
+    dist.all_reduce(tot)
+    n_act = int(tot[0].item()) * 64
+    ms = float(np.mean(times))
+    if rank == 0:
+        out = {"metric": METRIC, "value": n_act * (REINIT_ITERS + 1) / (ms * 1e-3), "unit": UNIT,
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": w.dtype, "data": "synthetic",
+               "config": {"workload": f"{w.name}+C4 z-slab partitioned, NCCL halo per sweep",
+                          "active_cells": n_act, "particles": int(tot[1].item()),
+                          "parallelism": f"zslab{world}",
+                          "l2": "flushed between steps (512 MiB write)"},
+               "probes_per_s": int(tot[1].item()) / (ms * 1e-3),
+               "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": None}
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+    _ = time

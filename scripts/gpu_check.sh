@@ -1,0 +1,23 @@
+#!/bin/bash
+# One GPU session: build, smoke, GPU tests, bench, ncu launch list + full captures.
+# Usage (from the repo root, under gpurun): bash scripts/gpu_check.sh [tests|bench|ncu|all]
+set -u
+mkdir -p gpurun_out
+what=${1:-all}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
+python -m paper_2512_11473_b200.build > gpurun_out/build.log 2>&1
+python -c "import oracle.oracle as o; o.build()" >> gpurun_out/build.log 2>&1
+if [[ $what == all || $what == tests ]]; then
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+  timeout 1500 python -m pytest tests -m gpu -q -rf --durations=15 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+fi
+if [[ $what == all || $what == bench ]]; then
+  timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+fi
+if [[ $what == all || $what == ncu ]]; then
+  B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_reinit -s 25 -c 1 -o gpurun_out/prof_reinit $B > gpurun_out/ncu_reinit.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gradient|k_kint|k_probe|k_phi_init|k_count|k_tag|k_nb' -s 7 -c 7 -o gpurun_out/prof_other $B > gpurun_out/ncu_other.log 2>&1
+fi
+ls -la gpurun_out > gpurun_out/ls.txt
