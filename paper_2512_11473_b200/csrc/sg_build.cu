@@ -5,8 +5,9 @@
 // "O1"/"O2" so that the core predicate and the initial phi are reproducible.
 //
 // Pipeline (steps 1-5 of the initialization, single layer):
-//   K1 k_tag      : f at every background-cell centre -> core / sign flags
-//   K2 k_count    : inner tagging (26-neighbourhood), per-tile active counts
+//   K1 k_tag      : f at every background-cell centre -> core / sign bitmasks
+//   K2 k_count    : inner tagging (26-neighbourhood dilation of 32-cell words),
+//                   per-tile active counts
 //      k_scan     : exclusive scan of tile counts (ordered compaction, R-1)
 //      -- one D2H read of the package count (P:468-471 analogue) --
 //      k_scatter  : block scan inside each tile -> ids 2.. in linear order;
@@ -61,54 +62,72 @@ void* dalloc(size_t bytes, cudaStream_t s) {
 
 // ------------------------------------------------------------- kernels ---
 
-constexpr int kTB = 256;               // threads per block in the compaction
-constexpr int kCPT = 16;               // cells per thread
-constexpr int kTile = kTB * kCPT;      // cells per tile (one block)
+constexpr int kTB = 256;  // threads (words) per compaction tile: 8192 cells
 
-// K1 -- core flag (bit 0) and negative sign (bit 1) per background cell of the
-// tag planes [zt_lo, zt_lo + gridDim.z).  O2: centre = lower + (c + 0.5) l_c.
-__global__ void __launch_bounds__(256) k_tag(GridC gc, Geom geom, int32_t zt_lo,
-                                             uint8_t* __restrict__ flags) {
+// Tag bitmasks: per tag plane z and row y, W = ceil(nx / 32) words; bit i of
+// word q is cell x = 32 q + i.  core = |f(centre)| < l_c, neg = f(centre) < 0.
+struct Bits {
+    const uint32_t* core;
+    const uint32_t* neg;
+    int32_t W;
+    int32_t zt_lo;
+    __device__ __forceinline__ int64_t idx(const GridC& gc, int z, int y, int q) const {
+        return ((int64_t)(z - zt_lo) * gc.n[1] + y) * W + q;
+    }
+};
+
+// K1 -- f at every background-cell centre of the tag planes
+// [zt_lo, zt_lo + gridDim.z) (O2: centre = lower + (c + 0.5) l_c); warp ballots
+// pack the core and sign predicates into words.
+__global__ void __launch_bounds__(256) k_tag(GridC gc, Geom geom, int32_t zt_lo, int32_t W,
+                                             uint32_t* __restrict__ core_w,
+                                             uint32_t* __restrict__ neg_w) {
     const int cx = blockIdx.x * blockDim.x + threadIdx.x;
     const int cy = blockIdx.y;
-    const int zl = blockIdx.z;
-    if (cx >= gc.n[0]) return;
-    const int cz = zt_lo + zl;
-    const double x = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
-    const double y = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
-    const double z = gc.lower[2] + ((double)cz + 0.5) * gc.cell;
-    const double f = sd_eval(geom, x, y, z);
-    flags[(int64_t)zl * gc.plane + (int64_t)cy * gc.n[0] + cx] =
-        (uint8_t)((fabs(f) < gc.cell ? 1 : 0) | (f < 0.0 ? 2 : 0));
+    const int cz = zt_lo + (int)blockIdx.z;
+    bool core = false, neg = false;
+    if (cx < gc.n[0]) {
+        const double x = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
+        const double y = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
+        const double z = gc.lower[2] + ((double)cz + 0.5) * gc.cell;
+        const double f = sd_eval(geom, x, y, z);
+        core = fabs(f) < gc.cell;
+        neg = f < 0.0;
+    }
+    const uint32_t cw = __ballot_sync(0xffffffffu, core);
+    const uint32_t nw = __ballot_sync(0xffffffffu, neg);
+    const int q = cx >> 5;
+    if ((threadIdx.x & 31) == 0 && q < W) {
+        const int64_t i = ((int64_t)blockIdx.z * gc.n[1] + cy) * W + q;
+        core_w[i] = cw;
+        neg_w[i] = nw;
+    }
 }
 
-// category of a stored cell: 3 core, 2 inner (26-neighbour of a core cell,
-// clipped to the domain, R-3), else 0/1 by sign (R-5)
-__device__ __forceinline__ uint8_t cell_category(const GridC& gc, const uint8_t* __restrict__ flags,
-                                                 int32_t zt_lo, int cx, int cy, int cz) {
-    const int64_t nx = gc.n[0];
-    const uint8_t f = flags[(int64_t)(cz - zt_lo) * gc.plane + (int64_t)cy * nx + cx];
-    if (f & 1) return 3;
-    const int z0 = max(cz - 1, 0), z1 = min(cz + 1, gc.n[2] - 1);
-    const int y0 = max(cy - 1, 0), y1 = min(cy + 1, gc.n[1] - 1);
-    const int x0 = max(cx - 1, 0), x1 = min(cx + 1, gc.n[0] - 1);
-    for (int z = z0; z <= z1; ++z)
-        for (int y = y0; y <= y1; ++y) {
-            const uint8_t* row = flags + (int64_t)(z - zt_lo) * gc.plane + (int64_t)y * nx;
-            for (int x = x0; x <= x1; ++x)
-                if (row[x] & 1) return 2;
-        }
-    return (f & 2) ? 0 : 1;
+__device__ __forceinline__ uint32_t valid_bits(const GridC& gc, int q, int W) {
+    const int rem = gc.n[0] - 32 * (W - 1);  // cells in the last word of a row
+    return (q < W - 1 || rem == 32) ? 0xffffffffu : ((1u << rem) - 1u);
 }
 
-__device__ __forceinline__ void next_cell(const GridC& gc, int& cx, int& cy, int& cz) {
-    if (++cx == gc.n[0]) {
-        cx = 0;
-        if (++cy == gc.n[1]) {
-            cy = 0;
-            ++cz;
+// active = core dilated by the 26-neighbourhood (R-3, clipped to the domain):
+// OR of the x-dilated words of the 3 x 3 rows around (y, z)
+__device__ __forceinline__ uint32_t active_word(const GridC& gc, const Bits& b, int z, int y,
+                                                int q) {
+    uint32_t act = 0;
+    for (int dz = -1; dz <= 1; ++dz) {
+        const int zz = z + dz;
+        if (zz < 0 || zz >= gc.n[2]) continue;
+        for (int dy = -1; dy <= 1; ++dy) {
+            const int yy = y + dy;
+            if (yy < 0 || yy >= gc.n[1]) continue;
+            const int64_t i = b.idx(gc, zz, yy, q);
+            const uint32_t w = __ldg(b.core + i);
+            const uint32_t wl = q > 0 ? __ldg(b.core + i - 1) : 0u;
+            const uint32_t wr = q < b.W - 1 ? __ldg(b.core + i + 1) : 0u;
+            act |= w | (w << 1) | (wl >> 31) | (w >> 1) | (wr << 31);
         }
     }
+    return act & valid_bits(gc, q, b.W);
 }
 
 __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
@@ -136,29 +155,23 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
     return before + x - v;
 }
 
-// K2a -- category per stored cell + active count per tile of kTile cells
-__global__ void __launch_bounds__(kTB) k_count(GridC gc, int32_t zt_lo, int64_t ncs,
-                                               const uint8_t* __restrict__ flags,
-                                               uint8_t* __restrict__ cat,
+// K2a -- active words of the stored planes + active count per tile of kTB words
+__global__ void __launch_bounds__(kTB) k_count(GridC gc, Bits b, int64_t nwords,
+                                               uint32_t* __restrict__ act_w,
                                                int32_t* __restrict__ tile_count,
                                                unsigned long long* __restrict__ n_core) {
     __shared__ int s_warp[32];
-    const int64_t l0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kCPT;
+    const int64_t t = (int64_t)blockIdx.x * kTB + threadIdx.x;
     int cnt = 0, ncore = 0;
-    if (l0 < ncs) {
-        const int64_t L = (int64_t)gc.zs_lo * gc.plane + l0;
-        int cx = (int)(L % gc.n[0]);
-        int cy = (int)((L / gc.n[0]) % gc.n[1]);
-        int cz = (int)(L / gc.plane);
-        for (int q = 0; q < kCPT; ++q) {
-            const int64_t l = l0 + q;
-            if (l >= ncs) break;
-            const uint8_t c = cell_category(gc, flags, zt_lo, cx, cy, cz);
-            cat[l] = c;
-            cnt += c >= 2;
-            ncore += c == 3;
-            next_cell(gc, cx, cy, cz);
-        }
+    if (t < nwords) {
+        const int q = (int)(t % b.W);
+        const int64_t row = t / b.W;
+        const int y = (int)(row % gc.n[1]);
+        const int z = gc.zs_lo + (int)(row / gc.n[1]);
+        const uint32_t act = active_word(gc, b, z, y, q);
+        act_w[t] = act;
+        cnt = __popc(act);
+        ncore = __popc(__ldg(b.core + b.idx(gc, z, y, q)) & valid_bits(gc, q, b.W));
     }
     int total;
     block_excl_scan(cnt, s_warp, total);
@@ -196,49 +209,40 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, 
     if (threadIdx.x == 1023) out[n] = s[1023];
 }
 
-// K2c -- ordered compaction: ids 2 + (active cells before) in linear order
-__global__ void __launch_bounds__(kTB) k_scatter(GridC gc, int64_t ncs,
-                                                 const uint8_t* __restrict__ cat,
+// K2c -- ordered compaction (R-1): ids 2 + (active cells before) in linear
+// cell order; background table (id, or 0/1 by sign) and meta (cell, category)
+__global__ void __launch_bounds__(kTB) k_scatter(GridC gc, Bits b, int64_t nwords,
+                                                 const uint32_t* __restrict__ act_w,
                                                  const int64_t* __restrict__ tile_off,
                                                  uint32_t* __restrict__ bg,
                                                  uint32_t* __restrict__ meta_cell,
                                                  uint8_t* __restrict__ meta_cat) {
     __shared__ int s_warp[32];
-    const int64_t l0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kCPT;
-    uint8_t c[kCPT];
-    int cnt = 0;
-    if (l0 + kCPT <= ncs) {
-        const uint4 v = *reinterpret_cast<const uint4*>(cat + l0);
-        memcpy(c, &v, 16);
-    } else {
-        for (int q = 0; q < kCPT; ++q) c[q] = (l0 + q < ncs) ? cat[l0 + q] : 0xFF;
-    }
-#pragma unroll
-    for (int q = 0; q < kCPT; ++q) cnt += (c[q] != 0xFF) && c[q] >= 2;
+    const int64_t t = (int64_t)blockIdx.x * kTB + threadIdx.x;
+    const uint32_t act = t < nwords ? act_w[t] : 0u;
     int total;
-    const int ex = block_excl_scan(cnt, s_warp, total);
+    const int ex = block_excl_scan(__popc(act), s_warp, total);
+    if (t >= nwords) return;
+    const int q = (int)(t % b.W);
+    const int64_t row = t / b.W;
+    const int y = (int)(row % gc.n[1]);
+    const int z = gc.zs_lo + (int)(row / gc.n[1]);
+    const int64_t wi = b.idx(gc, z, y, q);
+    const uint32_t core = __ldg(b.core + wi), neg = __ldg(b.neg + wi);
+    const int nbits = min(32, gc.n[0] - 32 * q);
+    const int64_t L0 = ((int64_t)z * gc.n[1] + y) * gc.n[0] + 32 * q;  // global linear cell
+    uint32_t* out = bg + (L0 - (int64_t)gc.zs_lo * gc.plane);
     uint32_t id = (uint32_t)(2 + tile_off[blockIdx.x] + ex);
-    uint32_t out[kCPT];
-    const uint32_t Lbase = (uint32_t)((int64_t)gc.zs_lo * gc.plane + l0);
-#pragma unroll
-    for (int q = 0; q < kCPT; ++q) {
-        if (c[q] != 0xFF && c[q] >= 2) {
-            out[q] = id;
-            meta_cell[id] = Lbase + q;
-            meta_cat[id] = c[q];
+    for (int i = 0; i < nbits; ++i) {
+        const uint32_t m = 1u << i;
+        if (act & m) {
+            out[i] = id;
+            meta_cell[id] = (uint32_t)(L0 + i);
+            meta_cat[id] = (core & m) ? 3 : 2;
             ++id;
         } else {
-            out[q] = c[q];
+            out[i] = (neg & m) ? 0u : 1u;
         }
-    }
-    if (l0 + kCPT <= ncs) {
-        uint4* d = reinterpret_cast<uint4*>(bg + l0);
-#pragma unroll
-        for (int q = 0; q < kCPT / 4; ++q)
-            d[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
-    } else {
-        for (int q = 0; q < kCPT; ++q)
-            if (l0 + q < ncs) bg[l0 + q] = out[q];
     }
 }
 
@@ -257,27 +261,26 @@ __global__ void k_planes(GridC gc, const uint32_t* __restrict__ meta_cell, int64
     for (int z = q + 1; z <= p; ++z) pf[z] = id;
 }
 
-// K3 -- neighbour table; one thread per (package, slot).  Neighbours outside
-// the domain take the sign of f at the virtual cell centre (R-6); cells in
-// the domain but outside the stored planes (beyond a ghost plane) take their
-// sign flag (never dereferenced by owned-point stencils).
-__global__ void __launch_bounds__(256) k_nb(GridC gc, Geom geom, int32_t zt_lo,
-                                            const uint8_t* __restrict__ flags,
+// K3 -- neighbour table; one warp per package, lane s < 27 fills slot s
+// (coalesced 108 B row).  Neighbours outside the domain take the sign of f at
+// the virtual cell centre (R-6); cells in the domain but outside the stored
+// planes (beyond a ghost plane) take their sign bit (never dereferenced by
+// owned-point stencils).
+__global__ void __launch_bounds__(256) k_nb(GridC gc, Geom geom, Bits b,
                                             const uint32_t* __restrict__ bg,
                                             const uint32_t* __restrict__ meta_cell,
                                             int64_t n_pkg, uint32_t* __restrict__ nb) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_pkg * 27) return;
-    const int64_t id = t / 27;
-    const int s = (int)(t - id * 27);
+    const int64_t id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int s = threadIdx.x & 31;
+    if (id >= n_pkg || s >= 27) return;
     if (id < 2) {
-        nb[t] = (uint32_t)id;  // far-field packages neighbour themselves
+        nb[id * 27 + s] = (uint32_t)id;  // far-field packages neighbour themselves
         return;
     }
-    const uint32_t L = meta_cell[id];
-    const int cx = (int)(L % (uint32_t)gc.n[0]);
-    const int cy = (int)((L / (uint32_t)gc.n[0]) % (uint32_t)gc.n[1]);
-    const int cz = (int)(L / (uint32_t)gc.plane);
+    const uint32_t L = __ldg(meta_cell + id);
+    const uint32_t nx = (uint32_t)gc.n[0], ny = (uint32_t)gc.n[1];
+    const uint32_t r = L / nx;
+    const int cx = (int)(L - r * nx), cy = (int)(r % ny), cz = (int)(r / ny);
     const int qx = cx + s % 3 - 1, qy = cy + (s / 3) % 3 - 1, qz = cz + s / 9 - 1;
     uint32_t v;
     if (qx < 0 || qy < 0 || qz < 0 || qx >= gc.n[0] || qy >= gc.n[1] || qz >= gc.n[2]) {
@@ -286,11 +289,11 @@ __global__ void __launch_bounds__(256) k_nb(GridC gc, Geom geom, int32_t zt_lo,
         const double z = gc.lower[2] + ((double)qz + 0.5) * gc.cell;
         v = sd_eval(geom, x, y, z) < 0.0 ? 0u : 1u;
     } else if (qz >= gc.zs_lo && qz < gc.zs_hi) {
-        v = bg[(int64_t)(qz - gc.zs_lo) * gc.plane + (int64_t)qy * gc.n[0] + qx];
+        v = __ldg(bg + (int64_t)(qz - gc.zs_lo) * gc.plane + (int64_t)qy * gc.n[0] + qx);
     } else {
-        v = (flags[(int64_t)(qz - zt_lo) * gc.plane + (int64_t)qy * gc.n[0] + qx] & 2) ? 0u : 1u;
+        v = ((__ldg(b.neg + b.idx(gc, qz, qy, qx >> 5)) >> (qx & 31)) & 1u) ? 0u : 1u;
     }
-    nb[t] = v;
+    nb[id * 27 + s] = v;
 }
 
 // K4 -- initial level set at the 64 data points of every package:
@@ -323,17 +326,18 @@ __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
     phi0[t] = (T)(gc.init_scale * sd_eval(geom, x, y, z));
 }
 
-// per-plane active counts for slab balancing (tag planes known)
-__global__ void __launch_bounds__(256) k_plane_count(GridC gc, int32_t zt_lo, int32_t zc_lo,
-                                                     const uint8_t* __restrict__ flags,
+// per-plane active counts for slab balancing (planes [zc_lo, zc_lo + nplanes))
+__global__ void __launch_bounds__(256) k_plane_count(GridC gc, Bits b, int32_t zc_lo,
+                                                     int64_t nwords,
                                                      unsigned long long* __restrict__ counts) {
-    const int cx = blockIdx.x * blockDim.x + threadIdx.x;
-    const int cy = blockIdx.y;
-    const int cz = zc_lo + blockIdx.z;
-    bool act = false;
-    if (cx < gc.n[0]) act = cell_category(gc, flags, zt_lo, cx, cy, cz) >= 2;
-    const unsigned m = __ballot_sync(0xffffffffu, act);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&counts[blockIdx.z], (unsigned long long)__popc(m));
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nwords) return;
+    const int q = (int)(t % b.W);
+    const int64_t row = t / b.W;
+    const int y = (int)(row % gc.n[1]);
+    const int zl = (int)(row / gc.n[1]);
+    const int c = __popc(active_word(gc, b, zc_lo + zl, y, q));
+    if (c) atomicAdd(&counts[zl], (unsigned long long)c);
 }
 
 // ------------------------------------------------------------- helpers ---
@@ -350,6 +354,10 @@ static GridC make_gridc(const sg_desc* d) {
     gc.init_scale = d->init_scale > 0.0 ? d->init_scale : 1.0;
     gc.far = d->far > 0.0 ? d->far : 4.0 * d->cell * std::max(1.0, gc.init_scale);
     gc.plane = (int64_t)d->n[0] * d->n[1];
+    gc.inv_cell = 1.0 / d->cell;
+    gc.inv_dx = 1.0 / gc.dx;
+    int e = 0;
+    gc.dyadic = std::frexp(d->cell, &e) == 0.5 ? 1 : 0;
     return gc;
 }
 
@@ -380,10 +388,10 @@ static Geom make_geom(const sg_geometry* g) {
 }
 
 static void launch_tag(const GridC& gc, const Geom& geom, int32_t zt_lo, int32_t zt_hi,
-                       uint8_t* flags, cudaStream_t s) {
+                       int32_t W, uint32_t* core_w, uint32_t* neg_w, cudaStream_t s) {
     if (zt_hi <= zt_lo) return;
     dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1], (unsigned)(zt_hi - zt_lo));
-    k_tag<<<grid, 256, 0, s>>>(gc, geom, zt_lo, flags);
+    k_tag<<<grid, 256, 0, s>>>(gc, geom, zt_lo, W, core_w, neg_w);
     SG_LAUNCHED();
 }
 
@@ -436,16 +444,21 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
 
         // K1: tag planes = stored planes + one on each side (inner tagging
         // of a stored boundary plane needs the core flags beyond it)
-        uint8_t* flags = (uint8_t*)dalloc((size_t)gc.plane * (zt_hi - zt_lo), s);
-        launch_tag(gc, g->geom, zt_lo, zt_hi, flags, s);
+        const int32_t W = (int32_t)ceil_div(gc.n[0], 32);
+        const int64_t tag_words = (int64_t)W * gc.n[1] * (zt_hi - zt_lo);
+        uint32_t* core_w = (uint32_t*)dalloc(sizeof(uint32_t) * 2 * tag_words, s);
+        uint32_t* neg_w = core_w + tag_words;
+        launch_tag(gc, g->geom, zt_lo, zt_hi, W, core_w, neg_w, s);
+        const Bits bits{core_w, neg_w, W, zt_lo};
 
-        const int64_t n_tiles = ceil_div(ncs, kTile);
-        uint8_t* cat = (uint8_t*)dalloc((size_t)(n_tiles * kTile), s);
+        const int64_t nwords = (int64_t)W * gc.n[1] * (gc.zs_hi - gc.zs_lo);
+        const int64_t n_tiles = ceil_div(nwords, kTB);
+        uint32_t* act_w = (uint32_t*)dalloc(sizeof(uint32_t) * nwords, s);
         int32_t* tile_count = (int32_t*)dalloc(sizeof(int32_t) * n_tiles, s);
         int64_t* tile_off = (int64_t*)dalloc(sizeof(int64_t) * (n_tiles + 1), s);
         unsigned long long* d_core = (unsigned long long*)dalloc(sizeof(unsigned long long), s);
         SG_CUDA(cudaMemsetAsync(d_core, 0, sizeof(unsigned long long), s));
-        k_count<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, zt_lo, ncs, flags, cat, tile_count, d_core);
+        k_count<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, bits, nwords, act_w, tile_count, d_core);
         SG_LAUNCHED();
         k_scan<<<1, 1024, 0, s>>>(tile_count, n_tiles, tile_off);
         SG_LAUNCHED();
@@ -476,8 +489,8 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         SG_CUDA(cudaMemcpyAsync(g->meta_cell, sing_cell, sizeof(sing_cell), cudaMemcpyHostToDevice, s));
         SG_CUDA(cudaMemcpyAsync(g->meta_cat, sing_cat, sizeof(sing_cat), cudaMemcpyHostToDevice, s));
 
-        k_scatter<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, ncs, cat, tile_off, g->bg, g->meta_cell,
-                                                    g->meta_cat);
+        k_scatter<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, bits, nwords, act_w, tile_off, g->bg,
+                                                    g->meta_cell, g->meta_cat);
         SG_LAUNCHED();
         k_planes_init<<<(unsigned)ceil_div(planes + 1, 256), 256, 0, s>>>(g->plane_first, planes,
                                                                           n_pkg);
@@ -487,7 +500,7 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
                                                                        g->plane_first);
             SG_LAUNCHED();
         }
-        k_nb<<<(unsigned)ceil_div(n_pkg * 27, 256), 256, 0, s>>>(gc, g->geom, zt_lo, flags, g->bg,
+        k_nb<<<(unsigned)ceil_div(n_pkg * 32, 256), 256, 0, s>>>(gc, g->geom, bits, g->bg,
                                                                  g->meta_cell, n_pkg, g->nb);
         SG_LAUNCHED();
         const unsigned pb = (unsigned)ceil_div(n_pkg * 64, 256);
@@ -513,8 +526,8 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
             g->own_hi = pf[gc.z_hi - gc.zs_lo];
         }
 
-        SG_CUDA(cudaFreeAsync(flags, s));
-        SG_CUDA(cudaFreeAsync(cat, s));
+        SG_CUDA(cudaFreeAsync(core_w, s));
+        SG_CUDA(cudaFreeAsync(act_w, s));
         SG_CUDA(cudaFreeAsync(tile_count, s));
         SG_CUDA(cudaFreeAsync(tile_off, s));
         SG_CUDA(cudaFreeAsync(d_core, s));
@@ -646,13 +659,17 @@ extern "C" sg_status sg_plane_counts(const sg_desc* desc, const sg_geometry* geo
         GridC gc = make_gridc(desc);
         const Geom ge = make_geom(geom);
         const int32_t zt_lo = std::max(0, z_lo - 1), zt_hi = std::min(desc->n[2], z_hi + 1);
-        uint8_t* flags = (uint8_t*)dalloc((size_t)gc.plane * (zt_hi - zt_lo), s);
-        launch_tag(gc, ge, zt_lo, zt_hi, flags, s);
+        const int32_t W = (int32_t)ceil_div(gc.n[0], 32);
+        const int64_t tag_words = (int64_t)W * gc.n[1] * (zt_hi - zt_lo);
+        uint32_t* core_w = (uint32_t*)dalloc(sizeof(uint32_t) * 2 * tag_words, s);
+        launch_tag(gc, ge, zt_lo, zt_hi, W, core_w, core_w + tag_words, s);
+        const Bits bits{core_w, core_w + tag_words, W, zt_lo};
         SG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (z_hi - z_lo), s));
-        dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1], (unsigned)(z_hi - z_lo));
-        k_plane_count<<<grid, 256, 0, s>>>(gc, zt_lo, z_lo, flags, (unsigned long long*)counts);
+        const int64_t nwords = (int64_t)W * gc.n[1] * (z_hi - z_lo);
+        k_plane_count<<<(unsigned)ceil_div(nwords, 256), 256, 0, s>>>(gc, bits, z_lo, nwords,
+                                                                      (unsigned long long*)counts);
         SG_LAUNCHED();
-        SG_CUDA(cudaFreeAsync(flags, s));
+        SG_CUDA(cudaFreeAsync(core_w, s));
     });
 }
 

@@ -34,6 +34,8 @@ struct GridC {
     int32_t zs_lo, zs_hi;  // stored planes
     int32_t z_lo, z_hi;    // owned planes
     int64_t plane;         // n[0] * n[1]
+    double inv_cell, inv_dx;
+    int32_t dyadic;        // l_c is a power of two: x / l_c == x * (1 / l_c) exactly
 };
 
 struct Error : std::runtime_error {

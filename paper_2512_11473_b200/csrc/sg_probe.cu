@@ -1,9 +1,9 @@
 // sg_probe.cu -- grid-particle coupling (K8, reading R-15).
 //
-// One thread per particle: containing background cell (fp64 division +
-// floor) -> background table -> far constant (inactive cell) or
-// trilinear interpolation of phi (and grad phi) over the 8 data points around
-// the position.  The corners lie at package-relative shifts in [-1, 4] of the
+// Per particle: containing background cell (fp64 division + floor) ->
+// background table -> far constant (inactive cell) or trilinear
+// interpolation of phi (and grad phi) over the 8 data points around the
+// position (see the phase comments of k_probe).  The corners lie at package-relative shifts in [-1, 4] of the
 // containing package and are resolved through its neighbour row with
 // NeighbourIndexShift (Lst. 2): "position-based random memory
 // access of a data package and may be its neighbors".
@@ -20,6 +20,21 @@
 
 namespace sg {
 
+// (x - lower) / d with the oracle's rounding: for a power-of-two spacing the
+// division is a multiplication by the exact reciprocal.
+__device__ __forceinline__ double qdiv(const GridC& gc, double v, bool cell) {
+    if (gc.dyadic) return v * (cell ? gc.inv_cell : gc.inv_dx);
+    return v / (cell ? gc.cell : gc.dx);
+}
+
+// Phase 1 (one thread per particle): positions staged through shared memory
+// (coalesced), containing cell, background lookup; far-field and OOB
+// particles are finished here.  Band particles are appended to a block list
+// with their package id, corner shifts and weights.
+// Phase 2 (eight lanes per band particle, one per trilinear corner): each
+// lane resolves its corner with Lst. 2 on the package's neighbour row, loads
+// phi and the three gradient components, and the eight weighted values are
+// summed with xor-shuffles.  Outputs leave through shared memory, coalesced.
 template <class T>
 __global__ void __launch_bounds__(256) k_probe(GridC gc, const uint32_t* __restrict__ bg,
                                                const uint32_t* __restrict__ nb,
@@ -28,73 +43,137 @@ __global__ void __launch_bounds__(256) k_probe(GridC gc, const uint32_t* __restr
                                                const T* __restrict__ pos, T* __restrict__ out_phi,
                                                T* __restrict__ out_grad,
                                                unsigned long long* __restrict__ oob) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool bad = false;
-    if (i < n) {
-        const double x[3] = {(double)pos[3 * i], (double)pos[3 * i + 1], (double)pos[3 * i + 2]};
-        int c[3];
+    __shared__ T s_pos[256 * 3];
+    __shared__ T s_phi[256];
+    __shared__ T s_g[256 * 3];
+    __shared__ uint32_t s_pk[256];
+    __shared__ uint16_t s_who[256];
+    __shared__ uint32_t s_sh[256];  // packed shifts s_k + 1 in [0, 4], 3 bits each
+    __shared__ T s_t[256 * 3];
+    __shared__ int s_cnt;
+    const int64_t base = (int64_t)blockIdx.x * 256;
+    const int m = (int)min((int64_t)256, n - base);
+    {
+        // three independent coalesced loads per thread, then the stores
+        const T* src = pos + 3 * base;
+        const int t0 = threadIdx.x;
+        const T a0 = t0 < 3 * m ? src[t0] : T(0);
+        const T a1 = t0 + 256 < 3 * m ? src[t0 + 256] : T(0);
+        const T a2 = t0 + 512 < 3 * m ? src[t0 + 512] : T(0);
+        s_pos[t0] = a0;
+        s_pos[t0 + 256] = a1;
+        s_pos[t0 + 512] = a2;
+    }
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+
+    const int t = threadIdx.x;
+    bool bad = false, band = false;
+    uint32_t b = 0, sh = 0;
+    T tt[3];
+    if (t < m) {
+        const double x[3] = {(double)s_pos[3 * t], (double)s_pos[3 * t + 1],
+                             (double)s_pos[3 * t + 2]};
         bool ok = true;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            // NaN fails both comparisons -> out of bounds
+        for (int k = 0; k < 3; ++k)  // NaN fails both comparisons -> OOB
             ok = ok && (x[k] >= gc.lower[k]) && (x[k] < gc.upper[k]);
-        }
+        int c[3] = {0, 0, 0};
         if (ok) {
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                c[k] = min((int)floor((x[k] - gc.lower[k]) / gc.cell), gc.n[k] - 1);
+                c[k] = min((int)floor(qdiv(gc, x[k] - gc.lower[k], true)), gc.n[k] - 1);
             ok = c[2] >= gc.z_lo && c[2] < gc.z_hi;  // owned planes of a slab
         }
-        T rphi = (T)gc.far, g0 = T(0), g1 = T(0), g2 = T(0);
+        T rphi = (T)gc.far;
         if (!ok) {
             bad = true;
         } else {
-            const uint32_t b =
-                __ldg(bg + ((int64_t)(c[2] - gc.zs_lo) * gc.n[1] + c[1]) * gc.n[0] + c[0]);
+            b = __ldg(bg + ((int64_t)(c[2] - gc.zs_lo) * gc.n[1] + c[1]) * gc.n[0] + c[0]);
             if (b < 2) {
                 rphi = (T)(b == 0 ? -gc.far : gc.far);
             } else {
-                int s[3];
-                T t[3];
+                band = true;
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    const double u = (x[k] - gc.lower[k]) / gc.dx - 0.5;
+                    const double u = qdiv(gc, x[k] - gc.lower[k], false) - 0.5;
                     const double a = floor(u);
-                    t[k] = (T)(u - a);
-                    s[k] = (int)a - 4 * c[k];  // in [-1, 3]
-                }
-                const uint32_t* row = nb + (int64_t)b * 27;
-                rphi = T(0);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int bx = q & 1, by = (q >> 1) & 1, bz = q >> 2;
-                    const int sx = s[0] + bx, sy = s[1] + by, sz = s[2] + bz;  // [-1, 4]
-                    const int ox = (sx + 4) >> 2, oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
-                    const int d = (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
-                    const int64_t pk = __ldg(row + ox + 3 * oy + 9 * oz);
-                    const T w = ((bx ? t[0] : T(1) - t[0]) * (by ? t[1] : T(1) - t[1])) *
-                                (bz ? t[2] : T(1) - t[2]);
-                    rphi += w * __ldg(phi + pk * 64 + d);
-                    if (grad) {
-                        const T* G = grad + pk * 192 + d;
-                        g0 += w * __ldg(G);
-                        g1 += w * __ldg(G + 64);
-                        g2 += w * __ldg(G + 128);
-                    }
+                    tt[k] = (T)(u - a);
+                    sh |= (uint32_t)((int)a - 4 * c[k] + 1) << (3 * k);  // s_k in [-1, 3]
                 }
             }
         }
-        out_phi[i] = rphi;
-        if (out_grad) {
-            out_grad[3 * i] = g0;
-            out_grad[3 * i + 1] = g1;
-            out_grad[3 * i + 2] = g2;
+        if (!band) {
+            s_phi[t] = rphi;
+            s_g[3 * t] = s_g[3 * t + 1] = s_g[3 * t + 2] = T(0);
         }
     }
-    if (oob) {
-        const unsigned m = __ballot_sync(0xffffffffu, bad);
-        if ((threadIdx.x & 31) == 0 && m) atomicAdd(oob, (unsigned long long)__popc(m));
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned bal = __ballot_sync(0xffffffffu, band);
+    int wbase = 0;
+    if (lane == 0 && bal) wbase = atomicAdd(&s_cnt, __popc(bal));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (band) {
+        const int idx = wbase + __popc(bal & ((1u << lane) - 1u));
+        s_pk[idx] = b;
+        s_who[idx] = (uint16_t)t;
+        s_sh[idx] = sh;
+        s_t[3 * idx] = tt[0];
+        s_t[3 * idx + 1] = tt[1];
+        s_t[3 * idx + 2] = tt[2];
     }
+    if (oob) {
+        const unsigned mb = __ballot_sync(0xffffffffu, bad);
+        if (lane == 0 && mb) atomicAdd(oob, (unsigned long long)__popc(mb));
+    }
+    __syncthreads();
+
+    // phase 2: 8 lanes per band particle
+    const int cnt = s_cnt;
+    const int corner = threadIdx.x & 7;
+    const int bx = corner & 1, by = (corner >> 1) & 1, bz = corner >> 2;
+    for (int q0 = 0; q0 < cnt; q0 += 32) {
+        const int q = q0 + (threadIdx.x >> 3);
+        const bool act = q < cnt;
+        T v = T(0), g0 = T(0), g1 = T(0), g2 = T(0);
+        if (act) {
+            const uint32_t shq = s_sh[q];
+            const int sx = (int)(shq & 7) - 1 + bx, sy = (int)((shq >> 3) & 7) - 1 + by,
+                      sz = (int)(shq >> 6) - 1 + bz;  // corner shifts in [-1, 4]
+            const int ox = (sx + 4) >> 2, oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
+            const int d = (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
+            const int64_t pk = __ldg(nb + (int64_t)s_pk[q] * 27 + ox + 3 * oy + 9 * oz);
+            const T tx = s_t[3 * q], ty = s_t[3 * q + 1], tz = s_t[3 * q + 2];
+            const T w = ((bx ? tx : T(1) - tx) * (by ? ty : T(1) - ty)) * (bz ? tz : T(1) - tz);
+            v = w * __ldg(phi + pk * 64 + d);
+            if (grad) {
+                const T* G = grad + pk * 192 + d;
+                g0 = w * __ldg(G);
+                g1 = w * __ldg(G + 64);
+                g2 = w * __ldg(G + 128);
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (grad) {
+                g0 += __shfl_xor_sync(0xffffffffu, g0, o);
+                g1 += __shfl_xor_sync(0xffffffffu, g1, o);
+                g2 += __shfl_xor_sync(0xffffffffu, g2, o);
+            }
+        }
+        if (act && corner == 0) {
+            const int p = s_who[q];
+            s_phi[p] = v;
+            s_g[3 * p] = g0;
+            s_g[3 * p + 1] = g1;
+            s_g[3 * p + 2] = g2;
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < m; q += 256) out_phi[base + q] = s_phi[q];
+    if (out_grad)
+        for (int q = threadIdx.x; q < 3 * m; q += 256) out_grad[3 * base + q] = s_g[q];
 }
 
 template <class T>

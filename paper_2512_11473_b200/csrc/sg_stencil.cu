@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "sg_internal.cuh"
@@ -52,8 +53,10 @@ __device__ __forceinline__ void st_row(double* p, const double (&r)[4]) {
 // neighbour-table slot of the six face neighbours, Lst. 2 offsets (R-8):
 // r = 0..5 -> -x, +x, -y, +y, -z, +z
 __device__ __forceinline__ int face_slot(int r) {
-    // slot = ox + 3 oy + 9 oz, o in {0,1,2}; centre = 13
-    return r == 0 ? 12 : r == 1 ? 14 : r == 2 ? 10 : r == 3 ? 16 : r == 4 ? 4 : 22;
+    // slot = ox + 3 oy + 9 oz, o in {0,1,2}; centre = 13: {12, 14, 10, 16, 4, 22}
+    // packed 5 bits per entry (no branch, no constant-table load)
+    constexpr uint32_t kPack = 12u | 14u << 5 | 10u << 10 | 16u << 15 | 4u << 20 | 22u << 25;
+    return (int)((kPack >> (5 * r)) & 31u);
 }
 
 // The 7-point cross of one x-row: own row c, rows ym/yp/zm/zp and the two
@@ -96,26 +99,43 @@ struct StC {
     T inv_dx, dx2, cdx, inv_2dx;
 };
 
-__device__ __forceinline__ float rs_scale(float p, float dx2) { return p * rsqrtf(fmaf(p, p, dx2)); }
-__device__ __forceinline__ double rs_scale(double p, double dx2) { return p / sqrt(p * p + dx2); }
-
-// O7 (reading R-12): one Jacobi Godunov step at one data point
-template <class T>
-__device__ __forceinline__ T godunov(T p, T xm, T xp, T ym, T yp, T zm, T zp, const StC<T>& c) {
-    if (p == T(0)) return p;
-    const bool pos = p > T(0);
-    T g2 = T(0);
-    const T m[3] = {xm, ym, zm}, q[3] = {xp, yp, zp};
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const T dm = (p - m[a]) * c.inv_dx;  // backward difference a
-        const T dp = (q[a] - p) * c.inv_dx;  // forward difference b
-        const T u = pos ? fmax(dm, T(0)) : fmin(dm, T(0));
-        const T v = pos ? fmin(dp, T(0)) : fmax(dp, T(0));
-        g2 += fmax(u * u, v * v);
-    }
-    const T s = rs_scale(p, c.dx2);
-    return p - c.cdx * s * (sqrt(g2) - T(1));
+// O7 (reading R-12): one Jacobi Godunov step at one data point, in the
+// sign-folded form.  With sigma = sign(phi) the two upwind cases
+//   phi > 0: g_k^2 = max(max(a,0)^2, min(b,0)^2)
+//   phi < 0: g_k^2 = max(min(a,0)^2, max(b,0)^2),
+// a = (phi - phi_{-e})/dx, b = (phi_{+e} - phi)/dx, are one expression:
+//   g_k = max(sigma (phi - phi_{-e}), sigma (phi - phi_{+e}), 0) / dx.
+// phi = 0 gives s = 0 and leaves the point unchanged, as the definition does.
+// fp32: approximate rsqrt/sqrt (MUFU, ~2 ulp) -- well inside 1e-5 dx.
+__device__ __forceinline__ float gd_axis(float ap, uint32_t sg, float m, float q) {
+    const float sm = __uint_as_float(__float_as_uint(m) ^ sg);
+    const float sq = __uint_as_float(__float_as_uint(q) ^ sg);
+    return fmaxf(fmaxf(ap - sm, ap - sq), 0.f);
+}
+__device__ __forceinline__ float godunov(float p, float xm, float xp, float ym, float yp, float zm,
+                                         float zp, const StC<float>& c) {
+    const uint32_t sg = __float_as_uint(p) & 0x80000000u;
+    const float ap = fabsf(p);
+    const float wx = gd_axis(ap, sg, xm, xp);
+    const float wy = gd_axis(ap, sg, ym, yp);
+    const float wz = gd_axis(ap, sg, zm, zp);
+    const float G = fmaf(wx, wx, fmaf(wy, wy, wz * wz));
+    const float g = G > 0.f ? G * rsqrtf(G) : 0.f;  // |grad phi| dx
+    const float s = p * rsqrtf(fmaf(p, p, c.dx2));
+    return fmaf(-c.cdx * s, fmaf(g, c.inv_dx, -1.f), p);
+}
+__device__ __forceinline__ double gd_axis(double ap, double sg, double m, double q) {
+    return fmax(fmax(ap - sg * m, ap - sg * q), 0.0);
+}
+__device__ __forceinline__ double godunov(double p, double xm, double xp, double ym, double yp,
+                                          double zm, double zp, const StC<double>& c) {
+    const double sg = p < 0.0 ? -1.0 : 1.0;
+    const double ap = fabs(p);
+    const double wx = gd_axis(ap, sg, xm, xp) * c.inv_dx;
+    const double wy = gd_axis(ap, sg, ym, yp) * c.inv_dx;
+    const double wz = gd_axis(ap, sg, zm, zp) * c.inv_dx;
+    const double s = p / sqrt(p * p + c.dx2);
+    return p - c.cdx * s * (sqrt(wx * wx + wy * wy + wz * wz) - 1.0);
 }
 
 // K5 -- reinitialisation sweep over packages [lo, hi)
@@ -214,17 +234,20 @@ __global__ void k_add(T* __restrict__ phi, int64_t n4, int64_t off4, T v) {
 // ------------------------------------------------------ kernel integral --
 // K7 (reading R-14): K = sum_o w[o] H(-phi_{I+o}),
 // G = sum_o gw[o] H(-phi_{I+o}) over the taps |o| dx < 2h of a Wendland C2
-// kernel.  Four packages per 256-thread block; each package stages its
-// (4 + 2R)^3 neighbourhood of H(-phi) in shared memory (values fetched through
-// the neighbour row with Lst. 2, shifts in [-R, 3 + R] within [-4, 7]), then
-// every thread accumulates its point over the tap list (taps in shared
-// memory, uniform across the block -> broadcast reads).
-
-template <class T>
-struct Tap {
-    int32_t off;
-    T w, gx, gy, gz;
-};
+// kernel.  The weights depend on o only through s = |o|^2:
+// w[o] = Wt[s], gw[o] = Gt[s] * o (Gt[s] = W'(|o| dx) (-1/|o|) dx^3).
+//
+// Mapping: 16 threads per package, 8 packages per 128-thread block.  Each
+// package stages its (4 + 2R)^3 neighbourhood of H(-phi) in shared memory
+// (values fetched through the package's neighbour row with Lst. 2; shifts in
+// [-R, 3 + R] stay inside [-4, 7]), then every thread produces one x-row of 4
+// outputs: for every (oy, oz) of the stencil it reads one staged row of
+// 4 + 2R values (vector shared loads) and applies all its x-taps to the 4
+// outputs with register-resident weights (taps unrolled at compile time,
+// R = ceil(2 h_ratio) - 1, all |o|^2 <= (R+1)^2 - 1 enumerated; taps outside
+// the support carry weight 0).  Packages whose whole staged neighbourhood is
+// uniformly H = 0 or H = 1 take the closed form K = S H, G = 0 (exact in exact
+// arithmetic since sum gw = 0).
 
 __device__ __forceinline__ float heav(float u, float eps, float inv_eps) {
     if (u < -eps) return 0.f;
@@ -240,54 +263,139 @@ __device__ __forceinline__ double heav(double u, double eps, double inv_eps) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k_kint(const T* __restrict__ in,
-                                              const uint32_t* __restrict__ nb, int64_t lo,
-                                              int64_t hi, const Tap<T>* __restrict__ taps,
-                                              int32_t n_taps, int32_t R, T eps, T* __restrict__ K,
-                                              T* __restrict__ G) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Tap<T>* s_tap = reinterpret_cast<Tap<T>*>(smem_raw);
-    const int RS = 4 + 2 * R;
-    const int vol = RS * RS * RS;
-    T* s_h = reinterpret_cast<T*>(smem_raw + ((sizeof(Tap<T>) * n_taps + 15) & ~size_t(15)));
-    for (int t = threadIdx.x; t < n_taps; t += blockDim.x) s_tap[t] = taps[t];
+struct KintC {
+    T wt[16];  // Wt[s], s = |o|^2
+    T gt[16];  // Gt[s]
+    T S;       // sum of all weights (host, double rounded to T)
+    T eps, inv_eps;
+};
 
-    const int lp = threadIdx.x >> 6;  // package slot in block
-    const int tl = threadIdx.x & 63;  // data point in package
-    const int64_t pkg = lo + (int64_t)blockIdx.x * 4 + lp;
+template <int R>
+struct KGeo {
+    static constexpr int RS = 4 + 2 * R;                 // staged width
+    static constexpr int RSX = (RS + 3) & ~3;            // padded row (16 B multiple)
+    static constexpr int SLICE = RS * RSX + 4;           // padded z-slice (bank shift)
+    static constexpr int VOL = RS * SLICE;               // floats per package
+    static constexpr int S2MAX = (R + 1) * (R + 1) - 1;  // largest |o|^2 enumerated
+};
+
+template <class T, int R>
+__global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
+                                              const uint32_t* __restrict__ nb, int64_t lo,
+                                              int64_t hi, KintC<T> c, T* __restrict__ K,
+                                              T* __restrict__ G) {
+    using Geo = KGeo<R>;
+    constexpr int RS = Geo::RS, RSX = Geo::RSX, SLICE = Geo::SLICE, VOL = Geo::VOL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* s_h = reinterpret_cast<T*>(smem_raw);
+    __shared__ uint32_t s_nb[8][28];
+
+    const int lp = threadIdx.x >> 4;  // package slot in block (0..7)
+    const int r = threadIdx.x & 15;   // x-row (j, k) of this thread
+    const int64_t pkg = lo + (int64_t)blockIdx.x * 8 + lp;
     const bool valid = pkg < hi;
-    T* H = s_h + lp * vol;
-    const T inv_eps = T(1) / eps;
     if (valid) {
-        const uint32_t* row = nb + pkg * 27;
-        for (int q = tl; q < vol; q += 64) {
-            const int lx = q % RS, ly = (q / RS) % RS, lz = q / (RS * RS);
-            const int sx = lx - R, sy = ly - R, sz = lz - R;  // shifts in [-R, 3+R]
-            const int ox = (sx + 4) >> 2, oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
-            const int dx = sx + 4 - 4 * ox, dy = sy + 4 - 4 * oy, dz = sz + 4 - 4 * oz;
-            const uint32_t pk = __ldg(row + ox + 3 * oy + 9 * oz);
-            const T v = __ldg(in + (int64_t)pk * 64 + dx + 4 * dy + 16 * dz);
-            H[q] = heav(-v, eps, inv_eps);
+        s_nb[lp][r] = __ldg(nb + pkg * 27 + r);
+        if (r < 11) s_nb[lp][16 + r] = __ldg(nb + pkg * 27 + 16 + r);
+    }
+    __syncwarp();
+    T* H = s_h + lp * VOL;
+    bool all1 = true, all0 = true;
+    if (valid) {
+        // staged points q = r + 16 m, m < PER; loads issued in batches of 8
+        // so that eight global loads per thread are in flight
+        constexpr int NV = RS * RS * RS, PER = (NV + 15) / 16, BATCH = 8;
+#pragma unroll
+        for (int m0 = 0; m0 < PER; m0 += BATCH) {
+            T v[BATCH];
+            int hi_[BATCH];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const int q = r + 16 * (m0 + u);
+                hi_[u] = -1;
+                if (m0 + u < PER && q < NV) {
+                    const int lx = q % RS, ly = (q / RS) % RS, lz = q / (RS * RS);
+                    const int sx = lx - R, sy = ly - R, sz = lz - R;  // shifts in [-R, 3+R]
+                    const int ox = (sx + 4) >> 2, oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
+                    const int d =
+                        (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
+                    const uint32_t pk = s_nb[lp][ox + 3 * oy + 9 * oz];
+                    v[u] = __ldg(in + (int64_t)pk * 64 + d);
+                    hi_[u] = lz * SLICE + ly * RSX + lx;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                if (hi_[u] >= 0) {
+                    const T h = heav(-v[u], c.eps, c.inv_eps);
+                    H[hi_[u]] = h;
+                    all1 = all1 && (h == T(1));
+                    all0 = all0 && (h == T(0));
+                }
+            }
         }
     }
-    __syncthreads();
-    if (!valid) return;
-    const int i = tl & 3, j = (tl >> 2) & 3, k = tl >> 4;
-    const int ci = (i + R) + RS * ((j + R) + RS * (k + R));
-    T acc = T(0), ax = T(0), ay = T(0), az = T(0);
-    for (int t = 0; t < n_taps; ++t) {
-        const Tap<T> tp = s_tap[t];
-        const T h = H[ci + tp.off];
-        acc += tp.w * h;
-        ax += tp.gx * h;
-        ay += tp.gy * h;
-        az += tp.gz * h;
+    // package-uniform neighbourhood? (16 lanes of a package share a half-warp)
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+        all1 = __shfl_xor_sync(0xffffffffu, (int)all1, o) && all1;
+        all0 = __shfl_xor_sync(0xffffffffu, (int)all0, o) && all0;
     }
-    K[pkg * 64 + tl] = acc;
-    T* g = G + pkg * 192 + tl;
-    g[0] = ax;
-    g[64] = ay;
-    g[128] = az;
+    __syncwarp();
+    if (!valid) return;
+    const int j = r & 3, k = r >> 2;
+    T acc[4], gx[4], gy[4], gz[4];
+    if (all1 || all0) {
+        const T v = all1 ? c.S : T(0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            acc[i] = v;
+            gx[i] = gy[i] = gz[i] = T(0);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = gx[i] = gy[i] = gz[i] = T(0);
+#pragma unroll
+        for (int oz = -R; oz <= R; ++oz) {
+#pragma unroll
+            for (int oy = -R; oy <= R; ++oy) {
+                if (oy * oy + oz * oz > Geo::S2MAX) continue;
+                const T* row = H + (k + R + oz) * SLICE + (j + R + oy) * RSX;
+                T h[RSX];
+#pragma unroll
+                for (int q = 0; q < RSX; q += 4) {
+                    if constexpr (sizeof(T) == 4) {
+                        const float4 v = *reinterpret_cast<const float4*>(row + q);
+                        h[q] = v.x; h[q + 1] = v.y; h[q + 2] = v.z; h[q + 3] = v.w;
+                    } else {
+                        const double2 a = *reinterpret_cast<const double2*>(row + q);
+                        const double2 b = *reinterpret_cast<const double2*>(row + q + 2);
+                        h[q] = a.x; h[q + 1] = a.y; h[q + 2] = b.x; h[q + 3] = b.y;
+                    }
+                }
+#pragma unroll
+                for (int ox = -R; ox <= R; ++ox) {
+                    const int s2 = ox * ox + oy * oy + oz * oz;
+                    if (s2 > Geo::S2MAX) continue;
+                    const T w = c.wt[s2];
+                    const T g = c.gt[s2];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const T hv = h[i + R + ox];
+                        acc[i] = fma(w, hv, acc[i]);
+                        if (ox) gx[i] = fma(g * T(ox), hv, gx[i]);
+                        if (oy) gy[i] = fma(g * T(oy), hv, gy[i]);
+                        if (oz) gz[i] = fma(g * T(oz), hv, gz[i]);
+                    }
+                }
+            }
+        }
+    }
+    st_row(K + pkg * 64 + 4 * r, acc);
+    T* Gp = G + pkg * 192 + 4 * r;
+    st_row(Gp, gx);
+    st_row(Gp + 64, gy);
+    st_row(Gp + 128, gz);
 }
 
 // singular packages (R-16): K = S / 0, G = 0; grad = normal = 0
@@ -316,18 +424,79 @@ static StC<T> stencil_consts(const sg_grid* g, double cfl) {
 }
 
 template <class T>
-static void reinit_t(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
+static void reinit_launch(sg_grid* g, int cur, const StC<T>& c, cudaStream_t s) {
     const int64_t lo = g->own_lo, hi = g->own_hi;
-    const StC<T> c = stencil_consts<T>(g, cfl);
-    for (int it = 0; it < iters; ++it) {
-        if (hi > lo) {
-            const unsigned blocks = (unsigned)ceil_div((hi - lo) * 16, 256);
-            k_reinit<T><<<blocks, 256, 0, s>>>((const T*)g->phi[g->cur], (T*)g->phi[1 - g->cur],
-                                               g->nb, lo, hi, c);
-            SG_LAUNCHED();
-        }
-        g->cur = 1 - g->cur;
+    if (hi <= lo) return;
+    const unsigned blocks = (unsigned)ceil_div((hi - lo) * 16, 256);
+    k_reinit<T><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], (T*)g->phi[1 - cur], g->nb, lo, hi, c);
+}
+
+// Multi-sweep reinit runs as one CUDA graph of `iters` kernel nodes.  The
+// sweeps of an L2-resident band take ~10 us each, so launch gaps matter.
+// Graphs are cached process-wide keyed by every kernel parameter (buffer
+// pointers, id range, iters, start buffer, cfl): a rebuilt grid of the same
+// shape gets the same pool addresses and reuses the instantiated graph.
+struct GraphKey {
+    const void* p0;
+    const void* p1;
+    const void* nb;
+    int64_t lo, hi;
+    int32_t iters, dt;
+    double cfl;
+    bool operator==(const GraphKey& o) const {
+        return p0 == o.p0 && p1 == o.p1 && nb == o.nb && lo == o.lo && hi == o.hi &&
+               iters == o.iters && dt == o.dt && cfl == o.cfl;
     }
+};
+
+static std::mutex g_graph_mu;
+static std::vector<std::pair<GraphKey, cudaGraphExec_t>> g_graphs;  // small LRU
+static cudaStream_t g_capture = nullptr;
+
+template <class T>
+static void reinit_t(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
+    const StC<T> c = stencil_consts<T>(g, cfl);
+    if (iters == 1 || g->own_hi <= g->own_lo) {
+        for (int it = 0; it < iters; ++it) {
+            if (g->own_hi > g->own_lo) {
+                reinit_launch<T>(g, g->cur, c, s);
+                SG_LAUNCHED();
+            }
+            g->cur = 1 - g->cur;
+        }
+        return;
+    }
+    const GraphKey key{g->phi[g->cur], g->phi[1 - g->cur], g->nb, g->own_lo, g->own_hi, iters,
+                       (int32_t)sizeof(T), cfl};
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    cudaGraphExec_t exec = nullptr;
+    for (size_t i = 0; i < g_graphs.size(); ++i)
+        if (g_graphs[i].first == key) {
+            exec = g_graphs[i].second;
+            std::swap(g_graphs[i], g_graphs.back());  // most recent last
+            break;
+        }
+    if (!exec) {
+        if (!g_capture) SG_CUDA(cudaStreamCreateWithFlags(&g_capture, cudaStreamNonBlocking));
+        cudaGraph_t graph;
+        SG_CUDA(cudaStreamBeginCapture(g_capture, cudaStreamCaptureModeThreadLocal));
+        int cur = g->cur;
+        for (int it = 0; it < iters; ++it) {
+            reinit_launch<T>(g, cur, c, g_capture);
+            cur = 1 - cur;
+        }
+        SG_CUDA(cudaStreamEndCapture(g_capture, &graph));
+        SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        SG_CUDA(cudaGraphDestroy(graph));
+        if (g_graphs.size() >= 32) {
+            cudaGraphExecDestroy(g_graphs.front().second);
+            g_graphs.erase(g_graphs.begin());
+        }
+        g_graphs.push_back({key, exec});
+    }
+    SG_CUDA(cudaGraphLaunch(exec, s));
+    g_launches.fetch_add((uint64_t)iters, std::memory_order_relaxed);
+    if (iters & 1) g->cur = 1 - g->cur;
 }
 
 void launch_reinit(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
@@ -339,45 +508,53 @@ void launch_reinit(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
 
 // Wendland C2 weights (reading R-14), evaluated on the host in double:
 // sigma = 21 / (16 pi h^3), q = r / h, W = sigma (1 - q/2)^4 (2q + 1),
-// W' = -5 sigma q (1 - q/2)^3 / h; w[o] = W(|o| dx) dx^3,
-// gw[o] = W'(|o| dx) (-o/|o|) dx^3 for |o| dx < 2h.
+// W' = -5 sigma q (1 - q/2)^3 / h; per |o|^2 = s2 (r = sqrt(s2) dx):
+// Wt[s2] = W(r) dx^3, Gt[s2] = W'(r) (-1/|o|) dx^3 (so gw[o] = Gt[s2] o),
+// both 0 outside the support |o| dx < 2h.  S = sum of w over the taps.
 template <class T>
-static std::vector<Tap<T>> make_taps(double h_ratio, double dx, int R, double* S) {
+static KintC<T> make_kint(double h_ratio, double dx, int R, double* S_out) {
     const double pi = 3.14159265358979323846;
     const double h = h_ratio * dx;
     const double sigma = 21.0 / (16.0 * pi * h * h * h);
-    const int RS = 4 + 2 * R;
-    std::vector<Tap<T>> v;
-    double sum = 0.0;
+    KintC<T> c{};
+    double wt[16] = {0}, S = 0.0;
+    for (int s2 = 0; s2 < 16; ++s2) {
+        const double len = std::sqrt((double)s2);
+        if (!(len * dx < 2.0 * h)) continue;
+        const double q = len * dx / h;
+        const double a = 1.0 - 0.5 * q;
+        wt[s2] = sigma * a * a * a * a * (2.0 * q + 1.0) * dx * dx * dx;
+        const double dW = -5.0 * sigma * q * a * a * a / h * dx * dx * dx;
+        c.wt[s2] = (T)wt[s2];
+        c.gt[s2] = (T)(len > 0 ? -dW / len : 0.0);
+    }
+    // S: the weights summed over every tap o in [-R, R]^3 (multiplicity of
+    // each |o|^2), in double
     for (int oz = -R; oz <= R; ++oz)
         for (int oy = -R; oy <= R; ++oy)
             for (int ox = -R; ox <= R; ++ox) {
-                const double len = std::sqrt((double)(ox * ox + oy * oy + oz * oz));
-                if (!(len * dx < 2.0 * h)) continue;
-                const double q = len * dx / h;
-                const double a = 1.0 - 0.5 * q;
-                const double W = sigma * a * a * a * a * (2.0 * q + 1.0) * dx * dx * dx;
-                const double dW = -5.0 * sigma * q * a * a * a / h * dx * dx * dx;
-                Tap<T> t;
-                t.off = ox + RS * (oy + RS * oz);
-                t.w = (T)W;
-                t.gx = (T)(len > 0 ? dW * (-ox / len) : 0.0);
-                t.gy = (T)(len > 0 ? dW * (-oy / len) : 0.0);
-                t.gz = (T)(len > 0 ? dW * (-oz / len) : 0.0);
-                sum += W;
-                v.push_back(t);
+                const int s2 = ox * ox + oy * oy + oz * oz;
+                if (s2 < 16) S += wt[s2];
             }
-    *S = sum;
-    return v;
+    c.S = (T)S;
+    *S_out = S;
+    c.eps = (T)dx;
+    c.inv_eps = (T)(1.0 / dx);
+    return c;
 }
 
-struct TapCache {
-    double h_ratio = -1;
-    void* dev = nullptr;
-    int32_t n = 0;
-    int32_t R = 0;
-    double S = 0;
-};
+template <class T, int R>
+static void launch_kint_r(sg_grid* g, const T* phi, const KintC<T>& c, cudaStream_t s) {
+    const int64_t lo = g->own_lo, hi = g->own_hi;
+    if (hi <= lo) return;
+    const size_t smem = sizeof(T) * 8 * KGeo<R>::VOL;
+    auto kern = k_kint<T, R>;
+    if (smem > 48 * 1024)
+        SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)ceil_div(hi - lo, 8), 128, smem, s>>>(phi, g->nb, lo, hi, c, (T*)g->kint,
+                                                          (T*)g->gkint);
+    SG_LAUNCHED();
+}
 
 template <class T>
 static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t s) {
@@ -403,29 +580,18 @@ static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t
     if (fields & SG_KINT) {
         // largest |o_k| of a tap: o_k < 2 h_ratio  ->  R = ceil(2 h_ratio) - 1
         const int R = (int)std::ceil(2.0 * h_ratio) - 1;
-        double S = 0;
-        std::vector<Tap<T>> taps = make_taps<T>(h_ratio, g->gc.dx, R, &S);
+        double S = 0.0;
+        const KintC<T> kc = make_kint<T>(h_ratio, g->gc.dx, R, &S);
         if (!g->kint) g->kint = g->alloc((size_t)g->n_pkg * 64 * sizeof(T), s);
         if (!g->gkint) g->gkint = g->alloc(vec_bytes, s);
-        Tap<T>* d_taps = (Tap<T>*)dalloc(sizeof(Tap<T>) * taps.size(), s);
-        SG_CUDA(cudaMemcpyAsync(d_taps, taps.data(), sizeof(Tap<T>) * taps.size(),
-                                cudaMemcpyHostToDevice, s));
-        const int RS = 4 + 2 * R;
-        const size_t smem = ((sizeof(Tap<T>) * taps.size() + 15) & ~size_t(15)) +
-                            sizeof(T) * 4 * RS * RS * RS;
-        auto kern = k_kint<T>;
-        if (smem > 48 * 1024)
-            SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-        if (hi > lo) {
-            kern<<<(unsigned)ceil_div(hi - lo, 4), 256, smem, s>>>(
-                phi, g->nb, lo, hi, d_taps, (int32_t)taps.size(), R, (T)g->gc.dx, (T*)g->kint,
-                (T*)g->gkint);
-            SG_LAUNCHED();
+        switch (R) {
+        case 0: launch_kint_r<T, 0>(g, phi, kc, s); break;
+        case 1: launch_kint_r<T, 1>(g, phi, kc, s); break;
+        case 2: launch_kint_r<T, 2>(g, phi, kc, s); break;
+        default: launch_kint_r<T, 3>(g, phi, kc, s); break;
         }
-        k_singular<T><<<1, 128, 0, s>>>((T*)g->kint, (T*)g->gkint, nullptr, nullptr, (T)S);
+        k_singular<T><<<1, 128, 0, s>>>((T*)g->kint, (T*)g->gkint, nullptr, nullptr, kc.S);
         SG_LAUNCHED();
-        SG_CUDA(cudaFreeAsync(d_taps, s));
         g->has_kint = true;
         g->kernel_sum = S;
     }
