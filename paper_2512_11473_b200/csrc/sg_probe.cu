@@ -27,153 +27,192 @@ __device__ __forceinline__ double qdiv(const GridC& gc, double v, bool cell) {
     return v / (cell ? gc.cell : gc.dx);
 }
 
-// Phase 1 (one thread per particle): positions staged through shared memory
-// (coalesced), containing cell, background lookup; far-field and OOB
-// particles are finished here.  Band particles are appended to a block list
-// with their package id, corner shifts and weights.
-// Phase 2 (eight lanes per band particle, one per trilinear corner): each
-// lane resolves its corner with Lst. 2 on the package's neighbour row, loads
-// phi and the three gradient components, and the eight weighted values are
-// summed with xor-shuffles.  Outputs leave through shared memory, coalesced.
+// Warp-centric, barrier-free: each warp owns a chunk of 128 consecutive
+// particles (4 per lane, 4 independent lookup chains per lane in flight).
+// Phase 1 (lane per particle): positions staged through the warp's shared
+// region (coalesced loads, transposed), containing cell, background lookup;
+// far-field and OOB particles are finished here; band particles are appended
+// to the warp's list with package id, corner shifts and weights.
+// Phase 2 (eight lanes per band particle, one per trilinear corner, two
+// particle groups per pass): each lane resolves its corner with Lst. 2 on the
+// package's neighbour row, loads phi and the three gradient components; the
+// eight weighted values are summed with xor-shuffles.  Results leave through
+// the shared region, coalesced.
+constexpr int kPW = 128;  // particles per warp chunk
+
 template <class T>
-__global__ void __launch_bounds__(256) k_probe(GridC gc, const uint32_t* __restrict__ bg,
+struct ProbeSmem {
+    static constexpr int kWB = sizeof(T) == 4 ? 8 : 4;  // warps per block
+    T io[kWB][4 * kPW];  // staged positions (3 x 128) / results (phi 128 + grad 384)
+    T t[kWB][3 * kPW];   // trilinear fractions of band particles
+    uint32_t pk[kWB][kPW];
+    uint32_t sh[kWB][kPW];  // packed corner shifts s_k + 1 in [0, 4], 3 bits each
+    uint8_t who[kWB][kPW];
+};
+
+template <class T>
+__global__ void __launch_bounds__(32 * ProbeSmem<T>::kWB, 2048 / (32 * ProbeSmem<T>::kWB) / 2)
+k_probe(GridC gc, const uint32_t* __restrict__ bg,
                                                const uint32_t* __restrict__ nb,
                                                const T* __restrict__ phi,
                                                const T* __restrict__ grad, int64_t n,
                                                const T* __restrict__ pos, T* __restrict__ out_phi,
                                                T* __restrict__ out_grad,
                                                unsigned long long* __restrict__ oob) {
-    __shared__ T s_pos[256 * 3];
-    __shared__ T s_phi[256];
-    __shared__ T s_g[256 * 3];
-    __shared__ uint32_t s_pk[256];
-    __shared__ uint16_t s_who[256];
-    __shared__ uint32_t s_sh[256];  // packed shifts s_k + 1 in [0, 4], 3 bits each
-    __shared__ T s_t[256 * 3];
-    __shared__ int s_cnt;
-    const int64_t base = (int64_t)blockIdx.x * 256;
-    const int m = (int)min((int64_t)256, n - base);
+    __shared__ ProbeSmem<T> S;
+    constexpr int kWB = ProbeSmem<T>::kWB;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t base = ((int64_t)blockIdx.x * kWB + w) * kPW;
+    if (base >= n) return;  // whole warp leaves together
+    const int m = (int)min((int64_t)kPW, n - base);
+    T* io = S.io[w];
     {
-        // three independent coalesced loads per thread, then the stores
         const T* src = pos + 3 * base;
-        const int t0 = threadIdx.x;
-        const T a0 = t0 < 3 * m ? src[t0] : T(0);
-        const T a1 = t0 + 256 < 3 * m ? src[t0 + 256] : T(0);
-        const T a2 = t0 + 512 < 3 * m ? src[t0 + 512] : T(0);
-        s_pos[t0] = a0;
-        s_pos[t0 + 256] = a1;
-        s_pos[t0 + 512] = a2;
+        T v[12];
+#pragma unroll
+        for (int u = 0; u < 12; ++u) {
+            const int q = lane + 32 * u;
+            v[u] = q < 3 * m ? src[q] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 12; ++u) io[lane + 32 * u] = v[u];
     }
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
+    __syncwarp();
+    T x[4][3];  // positions in the grid dtype; promoted to double where used
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) x[j][k] = io[3 * (lane + 32 * j) + k];
+    __syncwarp();
 
-    const int t = threadIdx.x;
-    bool bad = false, band = false;
-    uint32_t b = 0, sh = 0;
-    T tt[3];
-    if (t < m) {
-        const double x[3] = {(double)s_pos[3 * t], (double)s_pos[3 * t + 1],
-                             (double)s_pos[3 * t + 2]};
-        bool ok = true;
+    // phase 1: four particles per lane (p = lane + 32 j)
+    uint32_t b[4];
+    bool ok[4];
+    int c[4][3];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        ok[j] = lane + 32 * j < m;
 #pragma unroll
         for (int k = 0; k < 3; ++k)  // NaN fails both comparisons -> OOB
-            ok = ok && (x[k] >= gc.lower[k]) && (x[k] < gc.upper[k]);
-        int c[3] = {0, 0, 0};
-        if (ok) {
+            ok[j] = ok[j] && ((double)x[j][k] >= gc.lower[k]) && ((double)x[j][k] < gc.upper[k]);
 #pragma unroll
-            for (int k = 0; k < 3; ++k)
-                c[k] = min((int)floor(qdiv(gc, x[k] - gc.lower[k], true)), gc.n[k] - 1);
-            ok = c[2] >= gc.z_lo && c[2] < gc.z_hi;  // owned planes of a slab
+        for (int k = 0; k < 3; ++k)
+            c[j][k] = ok[j] ? min((int)floor(qdiv(gc, (double)x[j][k] - gc.lower[k], true)), gc.n[k] - 1) : 0;
+        ok[j] = ok[j] && c[j][2] >= gc.z_lo && c[j][2] < gc.z_hi;  // owned planes of a slab
+        b[j] = ok[j] ? __ldg(bg + ((int64_t)(c[j][2] - gc.zs_lo) * gc.n[1] + c[j][1]) * gc.n[0] +
+                             c[j][0])
+                     : 1u;
+    }
+    int nband = 0;
+    int nbad = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int p = lane + 32 * j;
+        const bool inr = p < m;
+        const bool band = ok[j] && b[j] >= 2;
+        const unsigned bal = __ballot_sync(0xffffffffu, band);
+        nbad += __popc(__ballot_sync(0xffffffffu, inr && !ok[j]));
+        if (band) {
+            const int idx = nband + __popc(bal & ((1u << lane) - 1u));
+            uint32_t sh = 0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double u = qdiv(gc, (double)x[j][k] - gc.lower[k], false) - 0.5;
+                const double a = floor(u);
+                S.t[w][3 * idx + k] = (T)(u - a);
+                sh |= (uint32_t)((int)a - 4 * c[j][k] + 1) << (3 * k);  // s_k in [-1, 3]
+            }
+            S.pk[w][idx] = b[j];
+            S.sh[w][idx] = sh;
+            S.who[w][idx] = (uint8_t)p;
+        } else if (inr) {
+            io[p] = (T)(!ok[j] ? gc.far : (b[j] == 0 ? -gc.far : gc.far));
+            io[kPW + 3 * p] = io[kPW + 3 * p + 1] = io[kPW + 3 * p + 2] = T(0);
         }
-        T rphi = (T)gc.far;
-        if (!ok) {
-            bad = true;
-        } else {
-            b = __ldg(bg + ((int64_t)(c[2] - gc.zs_lo) * gc.n[1] + c[1]) * gc.n[0] + c[0]);
-            if (b < 2) {
-                rphi = (T)(b == 0 ? -gc.far : gc.far);
-            } else {
-                band = true;
+        nband += __popc(bal);
+    }
+    if (oob && lane == 0 && nbad) atomicAdd(oob, (unsigned long long)nbad);
+    __syncwarp();
+
+    // phase 2: 8 lanes per band particle, 4 particles per group, 2 groups per pass
+    const int corner = lane & 7;
+    const int bx = corner & 1, by = (corner >> 1) & 1, bz = corner >> 2;
+    for (int q0 = 0; q0 < nband; q0 += 8) {
+        T v[2], g0[2], g1[2], g2[2];
+        int64_t pk[2];
+        T wgt[2];
+        int d[2];
+        bool act[2];
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const double u = qdiv(gc, x[k] - gc.lower[k], false) - 0.5;
-                    const double a = floor(u);
-                    tt[k] = (T)(u - a);
-                    sh |= (uint32_t)((int)a - 4 * c[k] + 1) << (3 * k);  // s_k in [-1, 3]
+        for (int hh = 0; hh < 2; ++hh) {
+            const int q = q0 + 4 * hh + (lane >> 3);
+            act[hh] = q < nband;
+            pk[hh] = 0;
+            d[hh] = 0;
+            wgt[hh] = T(0);
+            if (act[hh]) {
+                const uint32_t shq = S.sh[w][q];
+                const int sx = (int)(shq & 7) - 1 + bx, sy = (int)((shq >> 3) & 7) - 1 + by,
+                          sz = (int)(shq >> 6) - 1 + bz;  // corner shifts in [-1, 4]
+                const int ox = (sx + 4) >> 2, oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
+                d[hh] = (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
+                pk[hh] = __ldg(nb + (int64_t)S.pk[w][q] * 27 + ox + 3 * oy + 9 * oz);
+                const T tx = S.t[w][3 * q], ty = S.t[w][3 * q + 1], tz = S.t[w][3 * q + 2];
+                wgt[hh] = ((bx ? tx : T(1) - tx) * (by ? ty : T(1) - ty)) * (bz ? tz : T(1) - tz);
+            }
+        }
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            v[hh] = g0[hh] = g1[hh] = g2[hh] = T(0);
+            if (act[hh]) {
+                v[hh] = __ldg(phi + pk[hh] * 64 + d[hh]);
+                if (grad) {
+                    const T* G = grad + pk[hh] * 192 + d[hh];
+                    g0[hh] = __ldg(G);
+                    g1[hh] = __ldg(G + 64);
+                    g2[hh] = __ldg(G + 128);
                 }
             }
         }
-        if (!band) {
-            s_phi[t] = rphi;
-            s_g[3 * t] = s_g[3 * t + 1] = s_g[3 * t + 2] = T(0);
-        }
-    }
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned bal = __ballot_sync(0xffffffffu, band);
-    int wbase = 0;
-    if (lane == 0 && bal) wbase = atomicAdd(&s_cnt, __popc(bal));
-    wbase = __shfl_sync(0xffffffffu, wbase, 0);
-    if (band) {
-        const int idx = wbase + __popc(bal & ((1u << lane) - 1u));
-        s_pk[idx] = b;
-        s_who[idx] = (uint16_t)t;
-        s_sh[idx] = sh;
-        s_t[3 * idx] = tt[0];
-        s_t[3 * idx + 1] = tt[1];
-        s_t[3 * idx + 2] = tt[2];
-    }
-    if (oob) {
-        const unsigned mb = __ballot_sync(0xffffffffu, bad);
-        if (lane == 0 && mb) atomicAdd(oob, (unsigned long long)__popc(mb));
-    }
-    __syncthreads();
-
-    // phase 2: 8 lanes per band particle
-    const int cnt = s_cnt;
-    const int corner = threadIdx.x & 7;
-    const int bx = corner & 1, by = (corner >> 1) & 1, bz = corner >> 2;
-    for (int q0 = 0; q0 < cnt; q0 += 32) {
-        const int q = q0 + (threadIdx.x >> 3);
-        const bool act = q < cnt;
-        T v = T(0), g0 = T(0), g1 = T(0), g2 = T(0);
-        if (act) {
-            const uint32_t shq = s_sh[q];
-            const int sx = (int)(shq & 7) - 1 + bx, sy = (int)((shq >> 3) & 7) - 1 + by,
-                      sz = (int)(shq >> 6) - 1 + bz;  // corner shifts in [-1, 4]
-            const int ox = (sx + 4) >> 2, oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
-            const int d = (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
-            const int64_t pk = __ldg(nb + (int64_t)s_pk[q] * 27 + ox + 3 * oy + 9 * oz);
-            const T tx = s_t[3 * q], ty = s_t[3 * q + 1], tz = s_t[3 * q + 2];
-            const T w = ((bx ? tx : T(1) - tx) * (by ? ty : T(1) - ty)) * (bz ? tz : T(1) - tz);
-            v = w * __ldg(phi + pk * 64 + d);
-            if (grad) {
-                const T* G = grad + pk * 192 + d;
-                g0 = w * __ldg(G);
-                g1 = w * __ldg(G + 64);
-                g2 = w * __ldg(G + 128);
-            }
-        }
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (grad) {
-                g0 += __shfl_xor_sync(0xffffffffu, g0, o);
-                g1 += __shfl_xor_sync(0xffffffffu, g1, o);
-                g2 += __shfl_xor_sync(0xffffffffu, g2, o);
+        for (int hh = 0; hh < 2; ++hh) {
+            v[hh] *= wgt[hh];
+            g0[hh] *= wgt[hh];
+            g1[hh] *= wgt[hh];
+            g2[hh] *= wgt[hh];
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                v[hh] += __shfl_xor_sync(0xffffffffu, v[hh], o);
+                if (grad) {
+                    g0[hh] += __shfl_xor_sync(0xffffffffu, g0[hh], o);
+                    g1[hh] += __shfl_xor_sync(0xffffffffu, g1[hh], o);
+                    g2[hh] += __shfl_xor_sync(0xffffffffu, g2[hh], o);
+                }
+            }
+            const int q = q0 + 4 * hh + (lane >> 3);
+            if (act[hh] && corner == 0) {
+                const int p = S.who[w][q];
+                io[p] = v[hh];
+                io[kPW + 3 * p] = g0[hh];
+                io[kPW + 3 * p + 1] = g1[hh];
+                io[kPW + 3 * p + 2] = g2[hh];
             }
         }
-        if (act && corner == 0) {
-            const int p = s_who[q];
-            s_phi[p] = v;
-            s_g[3 * p] = g0;
-            s_g[3 * p + 1] = g1;
-            s_g[3 * p + 2] = g2;
+    }
+    __syncwarp();
+    // coalesced results
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int p = lane + 32 * j;
+        if (p < m) out_phi[base + p] = io[p];
+    }
+    if (out_grad) {
+#pragma unroll
+        for (int u = 0; u < 12; ++u) {
+            const int q = lane + 32 * u;
+            if (q < 3 * m) out_grad[3 * base + q] = io[kPW + q];
         }
     }
-    __syncthreads();
-    for (int q = threadIdx.x; q < m; q += 256) out_phi[base + q] = s_phi[q];
-    if (out_grad)
-        for (int q = threadIdx.x; q < 3 * m; q += 256) out_grad[3 * base + q] = s_g[q];
 }
 
 template <class T>
@@ -181,7 +220,8 @@ static void probe_dev(const sg_grid* g, int64_t n, const void* pos, void* out_ph
                       void* out_grad, unsigned long long* oob, cudaStream_t s) {
     if (n <= 0) return;
     const T* grad = out_grad ? (const T*)g->grad : nullptr;
-    k_probe<T><<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(
+    constexpr int kWB = ProbeSmem<T>::kWB;
+    k_probe<T><<<(unsigned)ceil_div(n, kPW * kWB), 32 * kWB, 0, s>>>(
         g->gc, g->bg, g->nb, (const T*)g->phi[g->cur], grad, n, (const T*)pos, (T*)out_phi,
         (T*)out_grad, oob);
     SG_LAUNCHED();

@@ -264,9 +264,9 @@ __device__ __forceinline__ double heav(double u, double eps, double inv_eps) {
 
 template <class T>
 struct KintC {
-    T wt[16];  // Wt[s], s = |o|^2
-    T gt[16];  // Gt[s]
-    T S;       // sum of all weights (host, double rounded to T)
+    T wt[16];     // Wt[s], s = |o|^2
+    T gt[4][16];  // m * Gt[s] for |o_k| = m (pre-multiplied: no per-tap multiply)
+    T S;          // sum of all weights (host, double rounded to T)
     T eps, inv_eps;
 };
 
@@ -378,14 +378,16 @@ __global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
                     const int s2 = ox * ox + oy * oy + oz * oz;
                     if (s2 > Geo::S2MAX) continue;
                     const T w = c.wt[s2];
-                    const T g = c.gt[s2];
+                    const T wx = ox > 0 ? c.gt[ox][s2] : -c.gt[-ox][s2];
+                    const T wy = oy > 0 ? c.gt[oy][s2] : -c.gt[-oy][s2];
+                    const T wz = oz > 0 ? c.gt[oz][s2] : -c.gt[-oz][s2];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const T hv = h[i + R + ox];
                         acc[i] = fma(w, hv, acc[i]);
-                        if (ox) gx[i] = fma(g * T(ox), hv, gx[i]);
-                        if (oy) gy[i] = fma(g * T(oy), hv, gy[i]);
-                        if (oz) gz[i] = fma(g * T(oz), hv, gz[i]);
+                        if (ox) gx[i] = fma(wx, hv, gx[i]);
+                        if (oy) gy[i] = fma(wy, hv, gy[i]);
+                        if (oz) gz[i] = fma(wz, hv, gz[i]);
                     }
                 }
             }
@@ -526,7 +528,7 @@ static KintC<T> make_kint(double h_ratio, double dx, int R, double* S_out) {
         wt[s2] = sigma * a * a * a * a * (2.0 * q + 1.0) * dx * dx * dx;
         const double dW = -5.0 * sigma * q * a * a * a / h * dx * dx * dx;
         c.wt[s2] = (T)wt[s2];
-        c.gt[s2] = (T)(len > 0 ? -dW / len : 0.0);
+        for (int m = 0; m < 4; ++m) c.gt[m][s2] = (T)(len > 0 ? m * (-dW / len) : 0.0);
     }
     // S: the weights summed over every tap o in [-R, R]^3 (multiplicity of
     // each |o|^2), in double
