@@ -83,4 +83,95 @@ __device__ __forceinline__ double sd_eval(const Geom& g, double x, double y, dou
     return f;
 }
 
+// f at NZ points sharing (x, y): the terms of each primitive that depend on
+// x and y only are evaluated once per column; each f[k] is the operation
+// sequence of sd_prim / sd_eval above (common-subexpression reuse only, so
+// the result is bit-identical to NZ separate sd_eval calls).
+template <int NZ>
+__device__ __forceinline__ void sd_prim_col(int kind, const double* p, double x, double y,
+                                            const double (&z)[NZ], double (&f)[NZ]) {
+    switch (kind) {
+    case SG_SPHERE:
+    case SG_SHELL: {
+        const double ex = x - p[0], ey = y - p[1];
+        const double exy = ex * ex + ey * ey;
+        const double rm = 0.5 * (p[3] + p[4]);
+        const double hw = 0.5 * (p[4] - p[3]);
+#pragma unroll
+        for (int k = 0; k < NZ; ++k) {
+            const double ez = z[k] - p[2];
+            const double d = sqrt(exy + ez * ez);
+            f[k] = kind == SG_SPHERE ? d - p[3] : fabs(d - rm) - hw;
+        }
+        return;
+    }
+    case SG_BOX: {
+        const double qx = fabs(x - p[0]) - p[3];
+        const double qy = fabs(y - p[1]) - p[4];
+        const double mx = fmax(qx, 0.0), my = fmax(qy, 0.0);
+        const double mxy = mx * mx + my * my;
+#pragma unroll
+        for (int k = 0; k < NZ; ++k) {
+            const double qz = fabs(z[k] - p[2]) - p[5];
+            const double mz = fmax(qz, 0.0);
+            f[k] = sqrt(mxy + mz * mz) + fmin(fmax(qx, fmax(qy, qz)), 0.0);
+        }
+        return;
+    }
+    case SG_TORUS_Z: {
+        const double ex = x - p[0], ey = y - p[1];
+        const double t = sqrt(ex * ex + ey * ey) - p[3];
+#pragma unroll
+        for (int k = 0; k < NZ; ++k) {
+            const double ez = z[k] - p[2];
+            f[k] = sqrt(t * t + ez * ez) - p[4];
+        }
+        return;
+    }
+    case SG_TRIPRISM_Z: {
+        double best = 0.0;
+        bool inside = true;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            const int e1 = (e + 1) % 3;
+            const double ux = p[2 * e1] - p[2 * e], uy = p[2 * e1 + 1] - p[2 * e + 1];
+            const double wx = x - p[2 * e], wy = y - p[2 * e + 1];
+            double t = (wx * ux + wy * uy) / (ux * ux + uy * uy);
+            t = fmin(fmax(t, 0.0), 1.0);
+            const double hx = wx - ux * t, hy = wy - uy * t;
+            const double d2 = hx * hx + hy * hy;
+            best = (e == 0) ? d2 : fmin(best, d2);
+            inside = inside && (ux * wy - uy * wx > 0.0);
+        }
+        const double dxy = inside ? -sqrt(best) : sqrt(best);
+        const double zc = 0.5 * (p[6] + p[7]);
+        const double hl = 0.5 * (p[7] - p[6]);
+        const double a = fmax(dxy, 0.0);
+#pragma unroll
+        for (int k = 0; k < NZ; ++k) {
+            const double qz = fabs(z[k] - zc) - hl;
+            const double b = fmax(qz, 0.0);
+            f[k] = fmin(fmax(dxy, qz), 0.0) + sqrt(a * a + b * b);
+        }
+        return;
+    }
+    default:  // torus x / y: no (x, y)-only term worth sharing
+#pragma unroll
+        for (int k = 0; k < NZ; ++k) f[k] = sd_prim(kind, p, x, y, z[k]);
+        return;
+    }
+}
+
+template <int NZ>
+__device__ __forceinline__ void sd_eval_col(const Geom& g, double x, double y,
+                                            const double (&z)[NZ], double (&f)[NZ]) {
+    sd_prim_col<NZ>(g.kind[0], g.p[0], x, y, z, f);
+    for (int i = 1; i < g.n; ++i) {
+        double fi[NZ];
+        sd_prim_col<NZ>(g.kind[i], g.p[i], x, y, z, fi);
+#pragma unroll
+        for (int k = 0; k < NZ; ++k) f[k] = fmin(f[k], fi[k]);
+    }
+}
+
 }  // namespace sg

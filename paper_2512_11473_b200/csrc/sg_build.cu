@@ -76,31 +76,33 @@ struct Bits {
     }
 };
 
-// K1 -- f at every background-cell centre of the tag planes
-// [zt_lo, zt_lo + gridDim.z) (O2: centre = lower + (c + 0.5) l_c); warp ballots
-// pack the core and sign predicates into words.
-__global__ void __launch_bounds__(256) k_tag(GridC gc, Geom geom, int32_t zt_lo, int32_t W,
-                                             uint32_t* __restrict__ core_w,
+// K1 -- f at every background-cell centre of the tag planes [zt_lo, zt_hi)
+// (O2: centre = lower + (c + 0.5) l_c).  A thread owns an (x, y) column and 4
+// consecutive planes (the (x, y)-only terms of each primitive are shared,
+// bit-identically); warp ballots pack the core and sign predicates into words.
+__global__ void __launch_bounds__(256) k_tag(GridC gc, Geom geom, int32_t zt_lo, int32_t zt_hi,
+                                             int32_t W, uint32_t* __restrict__ core_w,
                                              uint32_t* __restrict__ neg_w) {
     const int cx = blockIdx.x * blockDim.x + threadIdx.x;
     const int cy = blockIdx.y;
-    const int cz = zt_lo + (int)blockIdx.z;
-    bool core = false, neg = false;
-    if (cx < gc.n[0]) {
-        const double x = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
-        const double y = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
-        const double z = gc.lower[2] + ((double)cz + 0.5) * gc.cell;
-        const double f = sd_eval(geom, x, y, z);
-        core = fabs(f) < gc.cell;
-        neg = f < 0.0;
-    }
-    const uint32_t cw = __ballot_sync(0xffffffffu, core);
-    const uint32_t nw = __ballot_sync(0xffffffffu, neg);
+    const int z0 = zt_lo + 4 * (int)blockIdx.z;
+    const double x = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
+    const double y = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
+    double z[4], f[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) z[k] = gc.lower[2] + ((double)(z0 + k) + 0.5) * gc.cell;
+    if (cx < gc.n[0]) sd_eval_col<4>(geom, x, y, z, f);
     const int q = cx >> 5;
-    if ((threadIdx.x & 31) == 0 && q < W) {
-        const int64_t i = ((int64_t)blockIdx.z * gc.n[1] + cy) * W + q;
-        core_w[i] = cw;
-        neg_w[i] = nw;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const bool in = cx < gc.n[0];
+        const uint32_t cw = __ballot_sync(0xffffffffu, in && fabs(f[k]) < gc.cell);
+        const uint32_t nw = __ballot_sync(0xffffffffu, in && f[k] < 0.0);
+        if ((threadIdx.x & 31) == 0 && q < W && z0 + k < zt_hi) {
+            const int64_t i = ((int64_t)(z0 + k - zt_lo) * gc.n[1] + cy) * W + q;
+            core_w[i] = cw;
+            neg_w[i] = nw;
+        }
     }
 }
 
@@ -210,7 +212,10 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, 
 }
 
 // K2c -- ordered compaction (R-1): ids 2 + (active cells before) in linear
-// cell order; background table (id, or 0/1 by sign) and meta (cell, category)
+// cell order; background table (id, or 0/1 by sign) and meta (cell,
+// category).  A thread owns one 32-cell word for the scan; the writes are
+// done warp-cooperatively word by word (lane = bit), so every background-
+// table store is a coalesced 128 B row segment.
 __global__ void __launch_bounds__(kTB) k_scatter(GridC gc, Bits b, int64_t nwords,
                                                  const uint32_t* __restrict__ act_w,
                                                  const int64_t* __restrict__ tile_off,
@@ -222,26 +227,43 @@ __global__ void __launch_bounds__(kTB) k_scatter(GridC gc, Bits b, int64_t nword
     const uint32_t act = t < nwords ? act_w[t] : 0u;
     int total;
     const int ex = block_excl_scan(__popc(act), s_warp, total);
-    if (t >= nwords) return;
-    const int q = (int)(t % b.W);
-    const int64_t row = t / b.W;
-    const int y = (int)(row % gc.n[1]);
-    const int z = gc.zs_lo + (int)(row / gc.n[1]);
-    const int64_t wi = b.idx(gc, z, y, q);
-    const uint32_t core = __ldg(b.core + wi), neg = __ldg(b.neg + wi);
-    const int nbits = min(32, gc.n[0] - 32 * q);
-    const int64_t L0 = ((int64_t)z * gc.n[1] + y) * gc.n[0] + 32 * q;  // global linear cell
-    uint32_t* out = bg + (L0 - (int64_t)gc.zs_lo * gc.plane);
-    uint32_t id = (uint32_t)(2 + tile_off[blockIdx.x] + ex);
-    for (int i = 0; i < nbits; ++i) {
-        const uint32_t m = 1u << i;
-        if (act & m) {
-            out[i] = id;
-            meta_cell[id] = (uint32_t)(L0 + i);
-            meta_cat[id] = (core & m) ? 3 : 2;
-            ++id;
-        } else {
-            out[i] = (neg & m) ? 0u : 1u;
+    uint32_t core = 0, neg = 0, id0 = 0;
+    int nbits = 0;
+    int64_t off = 0, L0 = 0;
+    if (t < nwords) {
+        const int q = (int)(t % b.W);
+        const int64_t row = t / b.W;
+        const int y = (int)(row % gc.n[1]);
+        const int z = gc.zs_lo + (int)(row / gc.n[1]);
+        const int64_t wi = b.idx(gc, z, y, q);
+        core = __ldg(b.core + wi);
+        neg = __ldg(b.neg + wi);
+        nbits = min(32, gc.n[0] - 32 * q);
+        L0 = ((int64_t)z * gc.n[1] + y) * gc.n[0] + 32 * q;  // global linear cell
+        off = L0 - (int64_t)gc.zs_lo * gc.plane;
+        id0 = (uint32_t)(2 + tile_off[blockIdx.x] + ex);
+    }
+    const int lane = threadIdx.x & 31;
+    const uint32_t m = 1u << lane, below = m - 1u;
+    for (int src = 0; src < 32; ++src) {
+        const int nb_ = __shfl_sync(0xffffffffu, nbits, src);
+        if (nb_ == 0) continue;  // warp-uniform
+        const uint32_t a = __shfl_sync(0xffffffffu, act, src);
+        const uint32_t cw = __shfl_sync(0xffffffffu, core, src);
+        const uint32_t nw = __shfl_sync(0xffffffffu, neg, src);
+        const uint32_t i0 = __shfl_sync(0xffffffffu, id0, src);
+        const int64_t o = __shfl_sync(0xffffffffu, off, src);
+        const int64_t l0 = __shfl_sync(0xffffffffu, L0, src);
+        if (lane < nb_) {
+            uint32_t v;
+            if (a & m) {
+                v = i0 + __popc(a & below);
+                meta_cell[v] = (uint32_t)(l0 + lane);
+                meta_cat[v] = (cw & m) ? 3 : 2;
+            } else {
+                v = (nw & m) ? 0u : 1u;
+            }
+            bg[o + lane] = v;
         }
     }
 }
@@ -261,69 +283,95 @@ __global__ void k_planes(GridC gc, const uint32_t* __restrict__ meta_cell, int64
     for (int z = q + 1; z <= p; ++z) pf[z] = id;
 }
 
-// K3 -- neighbour table; one warp per package, lane s < 27 fills slot s
-// (coalesced 108 B row).  Neighbours outside the domain take the sign of f at
-// the virtual cell centre (R-6); cells in the domain but outside the stored
-// planes (beyond a ghost plane) take their sign bit (never dereferenced by
-// owned-point stencils).
-__global__ void __launch_bounds__(256) k_nb(GridC gc, Geom geom, Bits b,
+// Sign of f at a (virtual) cell centre outside the domain (R-6); rare, kept
+// out of line so the neighbour-table kernel stays small.
+__device__ __noinline__ uint32_t virtual_sign(double lx, double ly, double lz, double cell,
+                                              const Geom* __restrict__ geom, int qx, int qy,
+                                              int qz) {
+    const double x = lx + ((double)qx + 0.5) * cell;
+    const double y = ly + ((double)qy + 0.5) * cell;
+    const double z = lz + ((double)qz + 0.5) * cell;
+    return sd_eval(*geom, x, y, z) < 0.0 ? 0u : 1u;
+}
+
+// K3 -- neighbour table; a warp fills the rows of 4 packages (lane s < 27 =
+// slot s; coalesced 108 B rows), the loads of the 4 packages batched.
+// Neighbours outside the domain take the sign of f at the virtual cell centre
+// (R-6); cells in the domain but outside the stored planes (beyond a ghost
+// plane) take their sign bit (never dereferenced by owned-point stencils).
+constexpr int kNbPW = 4;  // packages per warp
+
+__global__ void __launch_bounds__(256) k_nb(GridC gc, const Geom* __restrict__ geom, Bits b,
                                             const uint32_t* __restrict__ bg,
                                             const uint32_t* __restrict__ meta_cell,
                                             int64_t n_pkg, uint32_t* __restrict__ nb) {
-    const int64_t id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t id0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kNbPW;
     const int s = threadIdx.x & 31;
-    if (id >= n_pkg || s >= 27) return;
-    if (id < 2) {
-        nb[id * 27 + s] = (uint32_t)id;  // far-field packages neighbour themselves
-        return;
+    if (id0 >= n_pkg || s >= 27) return;
+    const int ox = s % 3 - 1, oy = (s / 3) % 3 - 1, oz = s / 9 - 1;
+    uint32_t L[kNbPW];
+#pragma unroll
+    for (int u = 0; u < kNbPW; ++u) {
+        const int64_t id = id0 + u;
+        L[u] = (id >= 2 && id < n_pkg) ? __ldg(meta_cell + id) : 0xFFFFFFFFu;
     }
-    const uint32_t L = __ldg(meta_cell + id);
+    uint32_t v[kNbPW];
     const uint32_t nx = (uint32_t)gc.n[0], ny = (uint32_t)gc.n[1];
-    const uint32_t r = L / nx;
-    const int cx = (int)(L - r * nx), cy = (int)(r % ny), cz = (int)(r / ny);
-    const int qx = cx + s % 3 - 1, qy = cy + (s / 3) % 3 - 1, qz = cz + s / 9 - 1;
-    uint32_t v;
-    if (qx < 0 || qy < 0 || qz < 0 || qx >= gc.n[0] || qy >= gc.n[1] || qz >= gc.n[2]) {
-        const double x = gc.lower[0] + ((double)qx + 0.5) * gc.cell;
-        const double y = gc.lower[1] + ((double)qy + 0.5) * gc.cell;
-        const double z = gc.lower[2] + ((double)qz + 0.5) * gc.cell;
-        v = sd_eval(geom, x, y, z) < 0.0 ? 0u : 1u;
-    } else if (qz >= gc.zs_lo && qz < gc.zs_hi) {
-        v = __ldg(bg + (int64_t)(qz - gc.zs_lo) * gc.plane + (int64_t)qy * gc.n[0] + qx);
-    } else {
-        v = ((__ldg(b.neg + b.idx(gc, qz, qy, qx >> 5)) >> (qx & 31)) & 1u) ? 0u : 1u;
+#pragma unroll
+    for (int u = 0; u < kNbPW; ++u) {
+        const int64_t id = id0 + u;
+        v[u] = (uint32_t)id;  // far-field packages neighbour themselves
+        if (id < 2 || id >= n_pkg) continue;
+        const uint32_t r = L[u] / nx;
+        const int qx = (int)(L[u] - r * nx) + ox, qy = (int)(r % ny) + oy, qz = (int)(r / ny) + oz;
+        if (qx < 0 || qy < 0 || qz < 0 || qx >= gc.n[0] || qy >= gc.n[1] || qz >= gc.n[2]) {
+            v[u] = virtual_sign(gc.lower[0], gc.lower[1], gc.lower[2], gc.cell, geom, qx, qy, qz);
+        } else if (qz >= gc.zs_lo && qz < gc.zs_hi) {
+            v[u] = __ldg(bg + (int64_t)(qz - gc.zs_lo) * gc.plane + (int64_t)qy * gc.n[0] + qx);
+        } else {
+            v[u] = ((__ldg(b.neg + b.idx(gc, qz, qy, qx >> 5)) >> (qx & 31)) & 1u) ? 0u : 1u;
+        }
     }
-    nb[id * 27 + s] = v;
+#pragma unroll
+    for (int u = 0; u < kNbPW; ++u)
+        if (id0 + u < n_pkg) nb[(id0 + u) * 27 + s] = v[u];
 }
 
 // K4 -- initial level set at the 64 data points of every package:
 // phi = init_scale * f(lower + (I + 0.5) dx) rounded to T (R-11, R-17);
-// singular packages -far / +far in both buffers.
+// singular packages -far / +far in both buffers.  A thread owns one (i, j)
+// column of a package (4 points sharing x and y).
 template <class T>
 __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
                                                   const uint32_t* __restrict__ meta_cell,
                                                   int64_t n_pkg, T* __restrict__ phi0,
                                                   T* __restrict__ phi1) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_pkg * 64) return;
-    const int64_t id = t >> 6;
-    const int d = (int)(t & 63);
+    if (t >= n_pkg * 16) return;
+    const int64_t id = t >> 4;
+    const int col = (int)(t & 15);  // i + 4 j
     if (id < 2) {
         const T v = (T)(id == 0 ? -gc.far : gc.far);
-        phi0[t] = v;
-        phi1[t] = v;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            phi0[id * 64 + col + 16 * k] = v;
+            phi1[id * 64 + col + 16 * k] = v;
+        }
         return;
     }
-    const uint32_t L = meta_cell[id];
-    const int cx = (int)(L % (uint32_t)gc.n[0]);
-    const int cy = (int)((L / (uint32_t)gc.n[0]) % (uint32_t)gc.n[1]);
-    const int cz = (int)(L / (uint32_t)gc.plane);
-    const int64_t ix = 4 * (int64_t)cx + (d & 3), iy = 4 * (int64_t)cy + ((d >> 2) & 3),
-                  iz = 4 * (int64_t)cz + (d >> 4);
+    const uint32_t L = __ldg(meta_cell + id);
+    const uint32_t nx = (uint32_t)gc.n[0], ny = (uint32_t)gc.n[1];
+    const uint32_t r = L / nx;
+    const int cx = (int)(L - r * nx), cy = (int)(r % ny), cz = (int)(r / ny);
+    const int64_t ix = 4 * (int64_t)cx + (col & 3), iy = 4 * (int64_t)cy + (col >> 2);
     const double x = gc.lower[0] + ((double)ix + 0.5) * gc.dx;
     const double y = gc.lower[1] + ((double)iy + 0.5) * gc.dx;
-    const double z = gc.lower[2] + ((double)iz + 0.5) * gc.dx;
-    phi0[t] = (T)(gc.init_scale * sd_eval(geom, x, y, z));
+    double z[4], f[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) z[k] = gc.lower[2] + ((double)(4 * (int64_t)cz + k) + 0.5) * gc.dx;
+    sd_eval_col<4>(geom, x, y, z, f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) phi0[id * 64 + col + 16 * k] = (T)(gc.init_scale * f[k]);
 }
 
 // per-plane active counts for slab balancing (planes [zc_lo, zc_lo + nplanes))
@@ -390,8 +438,9 @@ static Geom make_geom(const sg_geometry* g) {
 static void launch_tag(const GridC& gc, const Geom& geom, int32_t zt_lo, int32_t zt_hi,
                        int32_t W, uint32_t* core_w, uint32_t* neg_w, cudaStream_t s) {
     if (zt_hi <= zt_lo) return;
-    dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1], (unsigned)(zt_hi - zt_lo));
-    k_tag<<<grid, 256, 0, s>>>(gc, geom, zt_lo, W, core_w, neg_w);
+    dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1],
+              (unsigned)ceil_div(zt_hi - zt_lo, 4));
+    k_tag<<<grid, 256, 0, s>>>(gc, geom, zt_lo, zt_hi, W, core_w, neg_w);
     SG_LAUNCHED();
 }
 
@@ -500,10 +549,12 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
                                                                        g->plane_first);
             SG_LAUNCHED();
         }
-        k_nb<<<(unsigned)ceil_div(n_pkg * 32, 256), 256, 0, s>>>(gc, g->geom, bits, g->bg,
+        Geom* d_geom = (Geom*)dalloc(sizeof(Geom), s);
+        SG_CUDA(cudaMemcpyAsync(d_geom, &g->geom, sizeof(Geom), cudaMemcpyHostToDevice, s));
+        k_nb<<<(unsigned)ceil_div(ceil_div(n_pkg, kNbPW) * 32, 256), 256, 0, s>>>(gc, d_geom, bits, g->bg,
                                                                  g->meta_cell, n_pkg, g->nb);
         SG_LAUNCHED();
-        const unsigned pb = (unsigned)ceil_div(n_pkg * 64, 256);
+        const unsigned pb = (unsigned)ceil_div(n_pkg * 16, 256);
         if (g->dtype == SG_F64)
             k_phi_init<double><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
                                                   (double*)g->phi[0], (double*)g->phi[1]);
@@ -528,6 +579,7 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
 
         SG_CUDA(cudaFreeAsync(core_w, s));
         SG_CUDA(cudaFreeAsync(act_w, s));
+        SG_CUDA(cudaFreeAsync(d_geom, s));
         SG_CUDA(cudaFreeAsync(tile_count, s));
         SG_CUDA(cudaFreeAsync(tile_off, s));
         SG_CUDA(cudaFreeAsync(d_core, s));

@@ -138,22 +138,57 @@ __device__ __forceinline__ double godunov(double p, double xm, double xp, double
     return p - c.cdx * s * (sqrt(wx * wx + wy * wy + wz * wz) - 1.0);
 }
 
-// K5 -- reinitialisation sweep over packages [lo, hi)
+// K5 -- reinitialisation sweep over packages [lo, hi).  Eight threads per
+// package; thread (j, k), k in {0, 1}, owns the two x-rows (j, k) and
+// (j, k + 2), which share their middle z-row (j, k + 1): 9 row loads + 4
+// x-end values for 8 points.  The six face-neighbour ids are loaded by six
+// lanes of the 8-lane group and broadcast with shuffles (Lst. 2 with shifts
+// -1 -> (offset 0, data 3) and 4 -> (offset 2, data 0)).
 template <class T>
 __global__ void __launch_bounds__(256) k_reinit(const T* __restrict__ in, T* __restrict__ out,
-                                                const uint32_t* __restrict__ nb, int64_t lo,
-                                                int64_t hi, StC<T> c) {
-    const int64_t pkg = lo + (((int64_t)blockIdx.x * 256 + threadIdx.x) >> 4);
-    Cross<T> x;
-    if (!load_cross(in, nb, pkg, pkg < hi, x)) return;
-    T o[4];
+                                                const uint32_t* __restrict__ nb, uint32_t lo,
+                                                uint32_t hi, StC<T> c) {
+    const uint32_t pkg = lo + ((blockIdx.x * 256u + threadIdx.x) >> 3);
+    const bool valid = pkg < hi;
+    const int g8 = threadIdx.x & 7;
+    const int j = g8 & 3, k = g8 >> 2;
+    uint32_t f = 0;
+    if (valid && g8 < 6) f = __ldg(nb + (size_t)pkg * 27 + face_slot(g8));
+    const int base = threadIdx.x & 24;
+    const uint32_t nxm = __shfl_sync(0xffffffffu, f, base + 0);
+    const uint32_t nxp = __shfl_sync(0xffffffffu, f, base + 1);
+    const uint32_t nym = __shfl_sync(0xffffffffu, f, base + 2);
+    const uint32_t nyp = __shfl_sync(0xffffffffu, f, base + 3);
+    const uint32_t nzm = __shfl_sync(0xffffffffu, f, base + 4);
+    const uint32_t nzp = __shfl_sync(0xffffffffu, f, base + 5);
+    if (!valid) return;
+    const T* P = in + (size_t)pkg * 64;
+    const int r0 = j + 4 * k, r1 = r0 + 8;  // rows (j, k) and (j, k + 2)
+    T c0[4], c1[4], zlo[4], zmid[4], zhi[4], ym0[4], yp0[4], ym1[4], yp1[4];
+    ld_row(P + 4 * r0, c0);
+    ld_row(P + 4 * r1, c1);
+    ld_row(P + 4 * (r0 + 4), zmid);
+    ld_row(k == 0 ? in + (size_t)nzm * 64 + 4 * (j + 12) : P + 4 * j, zlo);
+    ld_row(k == 0 ? P + 4 * (j + 12) : in + (size_t)nzp * 64 + 4 * j, zhi);
+    ld_row(j > 0 ? P + 4 * (r0 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * k), ym0);
+    ld_row(j < 3 ? P + 4 * (r0 + 1) : in + (size_t)nyp * 64 + 4 * (4 * k), yp0);
+    ld_row(j > 0 ? P + 4 * (r1 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * (k + 2)), ym1);
+    ld_row(j < 3 ? P + 4 * (r1 + 1) : in + (size_t)nyp * 64 + 4 * (4 * (k + 2)), yp1);
+    const T xm0 = __ldg(in + (size_t)nxm * 64 + 4 * r0 + 3);
+    const T xp0 = __ldg(in + (size_t)nxp * 64 + 4 * r0);
+    const T xm1 = __ldg(in + (size_t)nxm * 64 + 4 * r1 + 3);
+    const T xp1 = __ldg(in + (size_t)nxp * 64 + 4 * r1);
+    T o0[4], o1[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const T l = i > 0 ? x.c[i - 1] : x.xm;
-        const T r = i < 3 ? x.c[i + 1] : x.xp;
-        o[i] = godunov(x.c[i], l, r, x.ym[i], x.yp[i], x.zm[i], x.zp[i], c);
+        o0[i] = godunov(c0[i], i > 0 ? c0[i - 1] : xm0, i < 3 ? c0[i + 1] : xp0, ym0[i], yp0[i],
+                        zlo[i], zmid[i], c);
+        o1[i] = godunov(c1[i], i > 0 ? c1[i - 1] : xm1, i < 3 ? c1[i + 1] : xp1, ym1[i], yp1[i],
+                        zmid[i], zhi[i], c);
     }
-    st_row(out + pkg * 64 + 4 * (threadIdx.x & 15), o);
+    T* O = out + (size_t)pkg * 64;
+    st_row(O + 4 * r0, o0);
+    st_row(O + 4 * r1, o1);
 }
 
 // K6 -- gradient by Lst. 5 with the arithmetic-mean regulariser, divided by
@@ -429,8 +464,9 @@ template <class T>
 static void reinit_launch(sg_grid* g, int cur, const StC<T>& c, cudaStream_t s) {
     const int64_t lo = g->own_lo, hi = g->own_hi;
     if (hi <= lo) return;
-    const unsigned blocks = (unsigned)ceil_div((hi - lo) * 16, 256);
-    k_reinit<T><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], (T*)g->phi[1 - cur], g->nb, lo, hi, c);
+    const unsigned blocks = (unsigned)ceil_div((hi - lo) * 8, 256);
+    k_reinit<T><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], (T*)g->phi[1 - cur], g->nb,
+                                       (uint32_t)lo, (uint32_t)hi, c);
 }
 
 // Multi-sweep reinit runs as one CUDA graph of `iters` kernel nodes.  The
