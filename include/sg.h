@@ -20,7 +20,8 @@
  *     for cell offset (ox-1, oy-1, oz-1) (R-8); singular rows are self;
  *   - field values per package: 64 contiguous values, data index
  *     i + 4 j + 16 k (x fastest, R-9).  Vector fields are component-major
- *     inside a package: [package][component][64].
+ *     inside a package: [package][component][64], except the gradient, which
+ *     is stored interleaved with phi as [package][64][4] (see SG_VIEW_GRAD).
  *
  * Conventions for every call:
  *   - Every function returns sg_status; no C++ exception crosses the ABI.
@@ -134,7 +135,9 @@ enum {
     SG_VIEW_META_CAT = 2,    /* u8  [n_pkg]               0/1 singular, 2 inner, 3 core */
     SG_VIEW_NB = 3,          /* u32 [n_pkg][27]           neighbour package ids     */
     SG_VIEW_PHI = 4,         /* T   [n_pkg][64]           current phi               */
-    SG_VIEW_GRAD = 5,        /* T   [n_pkg][3][64]        grad phi                  */
+    SG_VIEW_GRAD = 5,        /* T   [n_pkg][64][4]        (phi, d/dx, d/dy, d/dz): the
+                                phi of the sg_gradient call and grad phi, one
+                                vector per data point (probe layout)            */
     SG_VIEW_NORMAL = 6,      /* T   [n_pkg][3][64]        normal                    */
     SG_VIEW_KINT = 7,        /* T   [n_pkg][64]           K                         */
     SG_VIEW_GKINT = 8,       /* T   [n_pkg][3][64]        G = grad K                */

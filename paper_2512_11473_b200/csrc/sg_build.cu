@@ -660,7 +660,7 @@ extern "C" sg_status sg_view(const sg_grid* g, int32_t what, sg_view_t* v) {
         case SG_VIEW_NB: set(g->nb, 2, g->n_pkg, 27, 1, 4, 2); break;
         case SG_VIEW_PHI: set(g->phi[g->cur], 2, g->n_pkg, 64, 1, g->esz, fdt); break;
         case SG_VIEW_PHI_NEXT: set(g->phi[1 - g->cur], 2, g->n_pkg, 64, 1, g->esz, fdt); break;
-        case SG_VIEW_GRAD: set(g->has_grad ? g->grad : nullptr, 3, g->n_pkg, 3, 64, g->esz, fdt); break;
+        case SG_VIEW_GRAD: set(g->has_grad ? g->grad : nullptr, 3, g->n_pkg, 64, 4, g->esz, fdt); break;
         case SG_VIEW_NORMAL:
             set(g->has_normal ? g->normal : nullptr, 3, g->n_pkg, 3, 64, g->esz, fdt);
             break;

@@ -20,6 +20,16 @@
 
 namespace sg {
 
+__device__ __forceinline__ void ld_vec4(const float* p, float (&v)[4]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+__device__ __forceinline__ void ld_vec4(const double* p, double (&v)[4]) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
 // (x - lower) / d with the oracle's rounding: for a power-of-two spacing the
 // division is a multiplication by the exact reciprocal.
 __device__ __forceinline__ double qdiv(const GridC& gc, double v, bool cell) {
@@ -33,11 +43,11 @@ __device__ __forceinline__ double qdiv(const GridC& gc, double v, bool cell) {
 // region (coalesced loads, transposed), containing cell, background lookup;
 // far-field and OOB particles are finished here; band particles are appended
 // to the warp's list with package id, corner shifts and weights.
-// Phase 2 (eight lanes per band particle, one per trilinear corner, two
-// particle groups per pass): each lane resolves its corner with Lst. 2 on the
-// package's neighbour row, loads phi and the three gradient components; the
-// eight weighted values are summed with xor-shuffles.  Results leave through
-// the shared region, coalesced.
+// Phase 2 (one lane per band particle of the compacted list): the lane
+// resolves its 8 corners with Lst. 2 on the package's neighbour row and loads
+// one (phi, grad) vector per corner from the interleaved gradient layout (or
+// phi alone when no gradient is requested).  Results leave through the
+// shared region, coalesced.
 constexpr int kPW = 128;  // particles per warp chunk
 
 template <class T>
@@ -55,7 +65,7 @@ __global__ void __launch_bounds__(32 * ProbeSmem<T>::kWB, 2048 / (32 * ProbeSmem
 k_probe(GridC gc, const uint32_t* __restrict__ bg,
                                                const uint32_t* __restrict__ nb,
                                                const T* __restrict__ phi,
-                                               const T* __restrict__ grad, int64_t n,
+                                               const T* __restrict__ pg, int64_t n,
                                                const T* __restrict__ pos, T* __restrict__ out_phi,
                                                T* __restrict__ out_grad,
                                                unsigned long long* __restrict__ oob) {
@@ -134,69 +144,54 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
     if (oob && lane == 0 && nbad) atomicAdd(oob, (unsigned long long)nbad);
     __syncwarp();
 
-    // phase 2: 8 lanes per band particle, 4 particles per group, 2 groups per pass
-    const int corner = lane & 7;
-    const int bx = corner & 1, by = (corner >> 1) & 1, bz = corner >> 2;
-    for (int q0 = 0; q0 < nband; q0 += 8) {
-        T v[2], g0[2], g1[2], g2[2];
-        int64_t pk[2];
-        T wgt[2];
-        int d[2];
-        bool act[2];
+    // phase 2: one lane per band particle (compacted list), all 8 corners
+    // resolved by the lane: 8 neighbour-row loads, then 8 vector loads of
+    // (phi, grad) -- two dependent rounds with 8 loads each in flight
+    for (int q0 = 0; q0 < nband; q0 += 32) {
+        const int q = q0 + lane;
+        if (q < nband) {
+            const uint32_t shq = S.sh[w][q];
+            const uint32_t* row = nb + (size_t)S.pk[w][q] * 27;
+            const int s0x = (int)(shq & 7) - 1, s0y = (int)((shq >> 3) & 7) - 1,
+                      s0z = (int)(shq >> 6) - 1;
+            uint32_t pk[8];
+            int d[8];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-            const int q = q0 + 4 * hh + (lane >> 3);
-            act[hh] = q < nband;
-            pk[hh] = 0;
-            d[hh] = 0;
-            wgt[hh] = T(0);
-            if (act[hh]) {
-                const uint32_t shq = S.sh[w][q];
-                const int sx = (int)(shq & 7) - 1 + bx, sy = (int)((shq >> 3) & 7) - 1 + by,
-                          sz = (int)(shq >> 6) - 1 + bz;  // corner shifts in [-1, 4]
+            for (int cc = 0; cc < 8; ++cc) {
+                const int sx = s0x + (cc & 1), sy = s0y + ((cc >> 1) & 1), sz = s0z + (cc >> 2);
                 const int ox = (sx + 4) >> 2, oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
-                d[hh] = (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
-                pk[hh] = __ldg(nb + (int64_t)S.pk[w][q] * 27 + ox + 3 * oy + 9 * oz);
-                const T tx = S.t[w][3 * q], ty = S.t[w][3 * q + 1], tz = S.t[w][3 * q + 2];
-                wgt[hh] = ((bx ? tx : T(1) - tx) * (by ? ty : T(1) - ty)) * (bz ? tz : T(1) - tz);
+                d[cc] = (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
+                pk[cc] = __ldg(row + ox + 3 * oy + 9 * oz);
             }
-        }
+            const T tx = S.t[w][3 * q], ty = S.t[w][3 * q + 1], tz = S.t[w][3 * q + 2];
+            T acc[4] = {T(0), T(0), T(0), T(0)};
+            if (pg) {
+                T v[8][4];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-            v[hh] = g0[hh] = g1[hh] = g2[hh] = T(0);
-            if (act[hh]) {
-                v[hh] = __ldg(phi + pk[hh] * 64 + d[hh]);
-                if (grad) {
-                    const T* G = grad + pk[hh] * 192 + d[hh];
-                    g0[hh] = __ldg(G);
-                    g1[hh] = __ldg(G + 64);
-                    g2[hh] = __ldg(G + 128);
+                for (int cc = 0; cc < 8; ++cc) ld_vec4(pg + ((size_t)pk[cc] * 64 + d[cc]) * 4, v[cc]);
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    const T wgt = (((cc & 1) ? tx : T(1) - tx) * ((cc & 2) ? ty : T(1) - ty)) *
+                                  ((cc & 4) ? tz : T(1) - tz);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[e] += wgt * v[cc][e];
+                }
+            } else {
+                T v[8];
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) v[cc] = __ldg(phi + (size_t)pk[cc] * 64 + d[cc]);
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    const T wgt = (((cc & 1) ? tx : T(1) - tx) * ((cc & 2) ? ty : T(1) - ty)) *
+                                  ((cc & 4) ? tz : T(1) - tz);
+                    acc[0] += wgt * v[cc];
                 }
             }
-        }
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-            v[hh] *= wgt[hh];
-            g0[hh] *= wgt[hh];
-            g1[hh] *= wgt[hh];
-            g2[hh] *= wgt[hh];
-#pragma unroll
-            for (int o = 1; o < 8; o <<= 1) {
-                v[hh] += __shfl_xor_sync(0xffffffffu, v[hh], o);
-                if (grad) {
-                    g0[hh] += __shfl_xor_sync(0xffffffffu, g0[hh], o);
-                    g1[hh] += __shfl_xor_sync(0xffffffffu, g1[hh], o);
-                    g2[hh] += __shfl_xor_sync(0xffffffffu, g2[hh], o);
-                }
-            }
-            const int q = q0 + 4 * hh + (lane >> 3);
-            if (act[hh] && corner == 0) {
-                const int p = S.who[w][q];
-                io[p] = v[hh];
-                io[kPW + 3 * p] = g0[hh];
-                io[kPW + 3 * p + 1] = g1[hh];
-                io[kPW + 3 * p + 2] = g2[hh];
-            }
+            const int p = S.who[w][q];
+            io[p] = acc[0];
+            io[kPW + 3 * p] = acc[1];
+            io[kPW + 3 * p + 1] = acc[2];
+            io[kPW + 3 * p + 2] = acc[3];
         }
     }
     __syncwarp();

@@ -193,7 +193,17 @@ __global__ void __launch_bounds__(256) k_reinit(const T* __restrict__ in, T* __r
 
 // K6 -- gradient by Lst. 5 with the arithmetic-mean regulariser, divided by
 // dx (R-13): (phi_{+1} - phi_{-1}) / (2 dx); optional unit normal.
-// Layout [pkg][component][64].
+// Gradient layout: [pkg][64][4] = (phi, d/dx, d/dy, d/dz) per data point --
+// the probe reads one 16 B vector per trilinear corner.  Normal layout:
+// [pkg][component][64].
+__device__ __forceinline__ void st_vec4(float* p, float a, float b, float c, float d) {
+    *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void st_vec4(double* p, double a, double b, double c, double d) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(a, b);
+    reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
+}
+
 template <class T>
 __global__ void __launch_bounds__(256) k_gradient(const T* __restrict__ in, T* __restrict__ grad,
                                                   T* __restrict__ normal,
@@ -212,11 +222,10 @@ __global__ void __launch_bounds__(256) k_gradient(const T* __restrict__ in, T* _
         gz[i] = (x.zp[i] - x.zm[i]) * c.inv_2dx;
     }
     const int r = threadIdx.x & 15;
-    T* G = grad + pkg * 192 + 4 * r;
     if (grad) {
-        st_row(G, gx);
-        st_row(G + 64, gy);
-        st_row(G + 128, gz);
+        T* G = grad + pkg * 256 + 16 * r;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) st_vec4(G + 4 * i, x.c[i], gx[i], gy[i], gz[i]);
     }
     if (normal) {
         T nx[4], ny[4], nz[4];
@@ -435,15 +444,19 @@ __global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
     st_row(Gp + 128, gz);
 }
 
-// singular packages (R-16): K = S / 0, G = 0; grad = normal = 0
+// singular packages (R-16): K = S / 0, G = 0; grad = normal = 0 (the phi
+// slot of the gradient layout holds the far constants)
 template <class T>
-__global__ void k_singular(T* K, T* G, T* grad, T* normal, T S) {
+__global__ void k_singular(T* K, T* G, T* grad, T* normal, T S, T far) {
     const int t = threadIdx.x;  // 128 threads: two packages x 64
     if (K) K[t] = t < 64 ? S : T(0);
+    if (grad) {
+        grad[4 * t] = t < 64 ? -far : far;
+        grad[4 * t + 1] = grad[4 * t + 2] = grad[4 * t + 3] = T(0);
+    }
     for (int c = 0; c < 3; ++c) {
         const int idx = (t >> 6) * 192 + c * 64 + (t & 63);
         if (G) G[idx] = T(0);
-        if (grad) grad[idx] = T(0);
         if (normal) normal[idx] = T(0);
     }
 }
@@ -600,7 +613,7 @@ static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t
     const T* phi = (const T*)g->phi[g->cur];
     const StC<T> c = stencil_consts<T>(g, 0.0);
     const size_t vec_bytes = (size_t)g->n_pkg * 192 * sizeof(T);
-    if ((fields & SG_GRAD) && !g->grad) g->grad = g->alloc(vec_bytes, s);
+    if ((fields & SG_GRAD) && !g->grad) g->grad = g->alloc((size_t)g->n_pkg * 256 * sizeof(T), s);
     if ((fields & SG_NORMAL) && !g->normal) g->normal = g->alloc(vec_bytes, s);
     if (fields & (SG_GRAD | SG_NORMAL)) {
         T* gp = (fields & SG_GRAD) ? (T*)g->grad : nullptr;
@@ -610,7 +623,7 @@ static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t
             k_gradient<T><<<blocks, 256, 0, s>>>(phi, gp, np, g->nb, lo, hi, c);
             SG_LAUNCHED();
         }
-        k_singular<T><<<1, 128, 0, s>>>(nullptr, nullptr, gp, np, T(0));
+        k_singular<T><<<1, 128, 0, s>>>(nullptr, nullptr, gp, np, T(0), (T)g->gc.far);
         SG_LAUNCHED();
         if (gp) g->has_grad = true;
         if (np) g->has_normal = true;
@@ -628,7 +641,7 @@ static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t
         case 2: launch_kint_r<T, 2>(g, phi, kc, s); break;
         default: launch_kint_r<T, 3>(g, phi, kc, s); break;
         }
-        k_singular<T><<<1, 128, 0, s>>>((T*)g->kint, (T*)g->gkint, nullptr, nullptr, kc.S);
+        k_singular<T><<<1, 128, 0, s>>>((T*)g->kint, (T*)g->gkint, nullptr, nullptr, kc.S, T(0));
         SG_LAUNCHED();
         g->has_kint = true;
         g->kernel_sum = S;

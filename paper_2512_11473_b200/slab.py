@@ -136,7 +136,7 @@ class SlabGrid:
         self.halo = halo_ranges(self.plan, pf)
 
     def exchange(self, name: str):
-        per = 64 if name in ("phi", "kint") else 192
+        per = {"phi": 64, "kint": 64, "grad": 256}.get(name, 192)
         exchange(self.grid.view(name), self.halo, self.rank, self.world, per, self.group)
 
     def reinit(self, iters: int, cfl: float, stream=None):

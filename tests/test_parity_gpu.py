@@ -214,7 +214,9 @@ def test_gradient_normal_kernel(sgm, O, name):
     g.gradient(sgm.SG_GRAD | sgm.SG_NORMAL | sgm.SG_KINT, h_ratio=w.h_ratio)
     grad, normal = o.gradient(phi)
     eg, en = _vec_pk(o, grad), _vec_pk(o, normal)
-    gg = g.view("grad").cpu().numpy().astype(np.float64)
+    g4 = g.view("grad").cpu().numpy().astype(np.float64)  # [n_pkg][64][(phi, gx, gy, gz)]
+    assert np.array_equal(g4[:, :, 0], g.view("phi").cpu().numpy().astype(np.float64))
+    gg = g4[:, :, 1:].transpose(0, 2, 1)
     gn = g.view("normal").cpu().numpy().astype(np.float64)
     tol = 1e-5 if w.dtype == "f32" else 1e-12
     assert np.max(np.abs(gg - eg) / np.maximum(1.0, np.abs(eg))) <= tol

@@ -76,7 +76,7 @@ def test_slabs_bitwise_equal_one_gpu(sgm, name, P):
     full.gradient(fields, w.h_ratio)
     for g in grids:
         g.gradient(fields, w.h_ratio)
-    _exchange_local(grids, halos, "grad", 192)
+    _exchange_local(grids, halos, "grad", 256)
     for name_ in ("phi", "grad", "normal", "kint", "gkint"):
         fv = full.view(name_)
         for p, g in zip(plans, grids):
