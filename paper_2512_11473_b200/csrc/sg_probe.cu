@@ -53,15 +53,14 @@ constexpr int kPW = 128;  // particles per warp chunk
 template <class T>
 struct ProbeSmem {
     static constexpr int kWB = sizeof(T) == 4 ? 8 : 4;  // warps per block
-    T io[kWB][4 * kPW];  // staged positions (3 x 128) / results (phi 128 + grad 384)
-    T t[kWB][3 * kPW];   // trilinear fractions of band particles
-    uint32_t pk[kWB][kPW];
-    uint32_t sh[kWB][kPW];  // packed corner shifts s_k + 1 in [0, 4], 3 bits each
-    uint8_t who[kWB][kPW];
+    T xs[kWB][3 * kPW];  // staged positions
+    T io[kWB][4 * kPW];  // results: phi (128) + grad (384)
+    uint32_t pk[kWB][kPW];  // band list: containing package
+    uint8_t who[kWB][kPW];  // band list: particle slot in the chunk
 };
 
 template <class T>
-__global__ void __launch_bounds__(32 * ProbeSmem<T>::kWB, 2048 / (32 * ProbeSmem<T>::kWB) / 2)
+__global__ void __launch_bounds__(32 * ProbeSmem<T>::kWB, 3)
 k_probe(GridC gc, const uint32_t* __restrict__ bg,
                                                const uint32_t* __restrict__ nb,
                                                const T* __restrict__ phi,
@@ -72,28 +71,37 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
     __shared__ ProbeSmem<T> S;
     constexpr int kWB = ProbeSmem<T>::kWB;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t base = ((int64_t)blockIdx.x * kWB + w) * kPW;
-    if (base >= n) return;  // whole warp leaves together
-    const int m = (int)min((int64_t)kPW, n - base);
+    const int64_t nchunks = (n + kPW - 1) / kPW;
+    const int64_t stride = (int64_t)gridDim.x * kWB;
+    int64_t chunk = (int64_t)blockIdx.x * kWB + w;
     T* io = S.io[w];
-    {
-        const T* src = pos + 3 * base;
-        T v[12];
+    // persistent warps: the positions of the next chunk are loaded while the
+    // current chunk is processed (hides the DRAM latency of the stream)
+    T v[12];
+    auto load_chunk = [&](int64_t ch) {
+        const int64_t b0 = ch * kPW;
+        const int mm = (int)min((int64_t)kPW, n - b0);
+        const T* src = pos + 3 * b0;
 #pragma unroll
         for (int u = 0; u < 12; ++u) {
             const int q = lane + 32 * u;
-            v[u] = q < 3 * m ? src[q] : T(0);
+            v[u] = q < 3 * mm ? src[q] : T(0);
         }
+    };
+    if (chunk < nchunks) load_chunk(chunk);
+    for (; chunk < nchunks; chunk += stride) {
+    const int64_t base = chunk * kPW;
+    const int m = (int)min((int64_t)kPW, n - base);
+    T* xs = S.xs[w];
 #pragma unroll
-        for (int u = 0; u < 12; ++u) io[lane + 32 * u] = v[u];
-    }
+    for (int u = 0; u < 12; ++u) xs[lane + 32 * u] = v[u];
+    if (chunk + stride < nchunks) load_chunk(chunk + stride);
     __syncwarp();
     T x[4][3];  // positions in the grid dtype; promoted to double where used
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) x[j][k] = io[3 * (lane + 32 * j) + k];
-    __syncwarp();
+        for (int k = 0; k < 3; ++k) x[j][k] = xs[3 * (lane + 32 * j) + k];
 
     // phase 1: four particles per lane (p = lane + 32 j)
     uint32_t b[4];
@@ -124,16 +132,7 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
         nbad += __popc(__ballot_sync(0xffffffffu, inr && !ok[j]));
         if (band) {
             const int idx = nband + __popc(bal & ((1u << lane) - 1u));
-            uint32_t sh = 0;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const double u = qdiv(gc, (double)x[j][k] - gc.lower[k], false) - 0.5;
-                const double a = floor(u);
-                S.t[w][3 * idx + k] = (T)(u - a);
-                sh |= (uint32_t)((int)a - 4 * c[j][k] + 1) << (3 * k);  // s_k in [-1, 3]
-            }
             S.pk[w][idx] = b[j];
-            S.sh[w][idx] = sh;
             S.who[w][idx] = (uint8_t)p;
         } else if (inr) {
             io[p] = (T)(!ok[j] ? gc.far : (b[j] == 0 ? -gc.far : gc.far));
@@ -150,10 +149,22 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
     for (int q0 = 0; q0 < nband; q0 += 32) {
         const int q = q0 + lane;
         if (q < nband) {
-            const uint32_t shq = S.sh[w][q];
+            const int p = S.who[w][q];
             const uint32_t* row = nb + (size_t)S.pk[w][q] * 27;
-            const int s0x = (int)(shq & 7) - 1, s0y = (int)((shq >> 3) & 7) - 1,
-                      s0z = (int)(shq >> 6) - 1;
+            // containing cell, lower corner data index a = floor(u),
+            // u = (x - lower)/dx - 1/2, fractions t = u - a (R-15)
+            int sv[3];
+            T tv[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double xd = (double)xs[3 * p + k] - gc.lower[k];
+                const int ck = min((int)floor(qdiv(gc, xd, true)), gc.n[k] - 1);
+                const double u = qdiv(gc, xd, false) - 0.5;
+                const double a = floor(u);
+                tv[k] = (T)(u - a);
+                sv[k] = (int)a - 4 * ck;  // in [-1, 3]
+            }
+            const int s0x = sv[0], s0y = sv[1], s0z = sv[2];
             uint32_t pk[8];
             int d[8];
 #pragma unroll
@@ -163,7 +174,7 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
                 d[cc] = (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
                 pk[cc] = __ldg(row + ox + 3 * oy + 9 * oz);
             }
-            const T tx = S.t[w][3 * q], ty = S.t[w][3 * q + 1], tz = S.t[w][3 * q + 2];
+            const T tx = tv[0], ty = tv[1], tz = tv[2];
             T acc[4] = {T(0), T(0), T(0), T(0)};
             if (pg) {
                 T v[8][4];
@@ -187,7 +198,6 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
                     acc[0] += wgt * v[cc];
                 }
             }
-            const int p = S.who[w][q];
             io[p] = acc[0];
             io[kPW + 3 * p] = acc[1];
             io[kPW + 3 * p + 1] = acc[2];
@@ -208,6 +218,8 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
             if (q < 3 * m) out_grad[3 * base + q] = io[kPW + q];
         }
     }
+    __syncwarp();  // io is restaged by the next chunk
+    }
 }
 
 template <class T>
@@ -216,7 +228,17 @@ static void probe_dev(const sg_grid* g, int64_t n, const void* pos, void* out_ph
     if (n <= 0) return;
     const T* grad = out_grad ? (const T*)g->grad : nullptr;
     constexpr int kWB = ProbeSmem<T>::kWB;
-    k_probe<T><<<(unsigned)ceil_div(n, kPW * kWB), 32 * kWB, 0, s>>>(
+    static int resident[2] = {0, 0};  // blocks per SM x SMs, per dtype
+    int& rb = resident[sizeof(T) == 8];
+    if (!rb) {
+        int dev = 0, sms = 0, per = 0;
+        SG_CUDA(cudaGetDevice(&dev));
+        SG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_probe<T>, 32 * kWB, 0));
+        rb = std::max(1, sms * per);
+    }
+    const int64_t blocks = std::min<int64_t>(ceil_div(n, kPW * kWB), rb);
+    k_probe<T><<<(unsigned)blocks, 32 * kWB, 0, s>>>(
         g->gc, g->bg, g->nb, (const T*)g->phi[g->cur], grad, n, (const T*)pos, (T*)out_phi,
         (T*)out_grad, oob);
     SG_LAUNCHED();

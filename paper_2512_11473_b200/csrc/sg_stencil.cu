@@ -400,38 +400,76 @@ __global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[i] = gx[i] = gy[i] = gz[i] = T(0);
 #pragma unroll
-        for (int oz = -R; oz <= R; ++oz) {
+        // rows (oy, oz) grouped by (|oy|, |oz|) = (a, b): with the sign
+        // butterfly of the (up to) four rows (+-a, +-b)
+        //   S  = sum of the rows            -> K and G_x
+        //   Dy = rows(+a) - rows(-a)        -> G_y  (weight a Gt)
+        //   Dz = rows(+b) - rows(-b)        -> G_z  (weight b Gt)
+        // every tap weight is applied once per group instead of once per row
+        auto load = [&](int oy, int oz, T (&h)[RSX]) {
+            const T* row = H + (k + R + oz) * SLICE + (j + R + oy) * RSX;
 #pragma unroll
-            for (int oy = -R; oy <= R; ++oy) {
-                if (oy * oy + oz * oz > Geo::S2MAX) continue;
-                const T* row = H + (k + R + oz) * SLICE + (j + R + oy) * RSX;
-                T h[RSX];
+            for (int q = 0; q < RSX; q += 4) {
+                if constexpr (sizeof(T) == 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(row + q);
+                    h[q] = v.x; h[q + 1] = v.y; h[q + 2] = v.z; h[q + 3] = v.w;
+                } else {
+                    const double2 a2 = *reinterpret_cast<const double2*>(row + q);
+                    const double2 b2 = *reinterpret_cast<const double2*>(row + q + 2);
+                    h[q] = a2.x; h[q + 1] = a2.y; h[q + 2] = b2.x; h[q + 3] = b2.y;
+                }
+            }
+        };
 #pragma unroll
-                for (int q = 0; q < RSX; q += 4) {
-                    if constexpr (sizeof(T) == 4) {
-                        const float4 v = *reinterpret_cast<const float4*>(row + q);
-                        h[q] = v.x; h[q + 1] = v.y; h[q + 2] = v.z; h[q + 3] = v.w;
-                    } else {
-                        const double2 a = *reinterpret_cast<const double2*>(row + q);
-                        const double2 b = *reinterpret_cast<const double2*>(row + q + 2);
-                        h[q] = a.x; h[q + 1] = a.y; h[q + 2] = b.x; h[q + 3] = b.y;
+        for (int ga = 0; ga <= R; ++ga) {
+#pragma unroll
+            for (int gb = 0; gb <= R; ++gb) {
+                if (ga * ga + gb * gb > Geo::S2MAX) continue;
+                T S[RSX], Dy[RSX], Dz[RSX];
+                if (ga == 0 && gb == 0) {
+                    load(0, 0, S);
+                } else if (gb == 0) {
+                    T p_[RSX], m_[RSX];
+                    load(ga, 0, p_);
+                    load(-ga, 0, m_);
+#pragma unroll
+                    for (int q = 0; q < RSX; ++q) { S[q] = p_[q] + m_[q]; Dy[q] = p_[q] - m_[q]; }
+                } else if (ga == 0) {
+                    T p_[RSX], m_[RSX];
+                    load(0, gb, p_);
+                    load(0, -gb, m_);
+#pragma unroll
+                    for (int q = 0; q < RSX; ++q) { S[q] = p_[q] + m_[q]; Dz[q] = p_[q] - m_[q]; }
+                } else {
+                    T pp[RSX], pm[RSX], mp[RSX], mm[RSX];
+                    load(ga, gb, pp);
+                    load(ga, -gb, pm);
+                    load(-ga, gb, mp);
+                    load(-ga, -gb, mm);
+#pragma unroll
+                    for (int q = 0; q < RSX; ++q) {
+                        const T a1 = pp[q] + pm[q], b1 = mp[q] + mm[q];
+                        const T c1 = pp[q] - pm[q], d1 = mp[q] - mm[q];
+                        S[q] = a1 + b1;
+                        Dy[q] = a1 - b1;
+                        Dz[q] = c1 + d1;
                     }
                 }
 #pragma unroll
                 for (int ox = -R; ox <= R; ++ox) {
-                    const int s2 = ox * ox + oy * oy + oz * oz;
+                    const int s2 = ox * ox + ga * ga + gb * gb;
                     if (s2 > Geo::S2MAX) continue;
                     const T w = c.wt[s2];
                     const T wx = ox > 0 ? c.gt[ox][s2] : -c.gt[-ox][s2];
-                    const T wy = oy > 0 ? c.gt[oy][s2] : -c.gt[-oy][s2];
-                    const T wz = oz > 0 ? c.gt[oz][s2] : -c.gt[-oz][s2];
+                    const T wy = c.gt[ga][s2];
+                    const T wz = c.gt[gb][s2];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const T hv = h[i + R + ox];
+                        const T hv = S[i + R + ox];
                         acc[i] = fma(w, hv, acc[i]);
                         if (ox) gx[i] = fma(wx, hv, gx[i]);
-                        if (oy) gy[i] = fma(wy, hv, gy[i]);
-                        if (oz) gz[i] = fma(wz, hv, gz[i]);
+                        if (ga) gy[i] = fma(wy, Dy[i + R + ox], gy[i]);
+                        if (gb) gz[i] = fma(wz, Dz[i + R + ox], gz[i]);
                     }
                 }
             }
@@ -477,6 +515,8 @@ template <class T>
 static void reinit_launch(sg_grid* g, int cur, const StC<T>& c, cudaStream_t s) {
     const int64_t lo = g->own_lo, hi = g->own_hi;
     if (hi <= lo) return;
+    // (programmatic dependent launch of the next sweep was measured slower:
+    // 21.9 vs 17.7 us per sweep on C2)
     const unsigned blocks = (unsigned)ceil_div((hi - lo) * 8, 256);
     k_reinit<T><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], (T*)g->phi[1 - cur], g->nb,
                                        (uint32_t)lo, (uint32_t)hi, c);
