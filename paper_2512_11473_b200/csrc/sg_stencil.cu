@@ -346,35 +346,69 @@ __global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
     T* H = s_h + lp * VOL;
     bool all1 = true, all0 = true;
     if (valid) {
-        // staged points q = r + 16 m, m < PER; loads issued in batches of 8
-        // so that eight global loads per thread are in flight
-        constexpr int NV = RS * RS * RS, PER = (NV + 15) / 16, BATCH = 8;
+        // staged x-rows (ly, lz) of the region, thread r takes rows r, r+16, ...
+        // A row spans x-shifts [-R, 3+R]: data 4-R..3 of the -x neighbour,
+        // the whole row of the centre column package, data 0..R-1 of the +x
+        // neighbour (Lst. 2) -- three loads per row (vector loads for R = 2).
+        constexpr int NR = RS * RS, RPT = (NR + 15) / 16;
 #pragma unroll
-        for (int m0 = 0; m0 < PER; m0 += BATCH) {
-            T v[BATCH];
-            int hi_[BATCH];
+        for (int m = 0; m < RPT; ++m) {
+            const int rowi = r + 16 * m;
+            if (rowi < NR) {
+                const int ly = rowi % RS, lz = rowi / RS;
+                const int sy = ly - R, sz = lz - R;
+                const int oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
+                const int dyz = 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
+                const uint32_t* slot = &s_nb[lp][3 * oy + 9 * oz];
+                const T* p0 = in + (size_t)slot[0] * 64 + dyz;
+                const T* p1 = in + (size_t)slot[1] * 64 + dyz;
+                const T* p2 = in + (size_t)slot[2] * 64 + dyz;
+                T v[RSX];
+                if constexpr (R == 2 && sizeof(T) == 4) {
+                    const float2 a2 = __ldg(reinterpret_cast<const float2*>(p0 + 2));
+                    const float4 b4 = __ldg(reinterpret_cast<const float4*>(p1));
+                    const float2 c2 = __ldg(reinterpret_cast<const float2*>(p2));
+                    v[0] = a2.x; v[1] = a2.y;
+                    v[2] = b4.x; v[3] = b4.y; v[4] = b4.z; v[5] = b4.w;
+                    v[6] = c2.x; v[7] = c2.y;
+                } else {
 #pragma unroll
-            for (int u = 0; u < BATCH; ++u) {
-                const int q = r + 16 * (m0 + u);
-                hi_[u] = -1;
-                if (m0 + u < PER && q < NV) {
-                    const int lx = q % RS, ly = (q / RS) % RS, lz = q / (RS * RS);
-                    const int sx = lx - R, sy = ly - R, sz = lz - R;  // shifts in [-R, 3+R]
-                    const int ox = (sx + 4) >> 2, oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
-                    const int d =
-                        (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
-                    const uint32_t pk = s_nb[lp][ox + 3 * oy + 9 * oz];
-                    v[u] = __ldg(in + (int64_t)pk * 64 + d);
-                    hi_[u] = lz * SLICE + ly * RSX + lx;
+                    for (int q = 0; q < R; ++q) v[q] = __ldg(p0 + 4 - R + q);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[R + q] = __ldg(p1 + q);
+#pragma unroll
+                    for (int q = 0; q < R; ++q) v[R + 4 + q] = __ldg(p2 + q);
+#pragma unroll
+                    for (int q = RS; q < RSX; ++q) v[q] = T(0);
                 }
-            }
+                // H(-phi): a row with no value inside the smoothing band
+                // |phi| <= eps is a pure select (no sine)
+                bool band = false;
 #pragma unroll
-            for (int u = 0; u < BATCH; ++u) {
-                if (hi_[u] >= 0) {
-                    const T h = heav(-v[u], c.eps, c.inv_eps);
-                    H[hi_[u]] = h;
-                    all1 = all1 && (h == T(1));
-                    all0 = all0 && (h == T(0));
+                for (int q = 0; q < RS; ++q) band = band || (fabs(v[q]) <= c.eps);
+                T h[RSX];
+                if (!band) {
+#pragma unroll
+                    for (int q = 0; q < RSX; ++q) h[q] = v[q] < T(0) ? T(1) : T(0);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < RSX; ++q) h[q] = heav(-v[q], c.eps, c.inv_eps);
+                }
+#pragma unroll
+                for (int q = 0; q < RS; ++q) {
+                    all1 = all1 && (h[q] == T(1));
+                    all0 = all0 && (h[q] == T(0));
+                }
+                T* dst = H + lz * SLICE + ly * RSX;
+#pragma unroll
+                for (int q = 0; q < RSX; q += 4) {
+                    if constexpr (sizeof(T) == 4) {
+                        *reinterpret_cast<float4*>(dst + q) =
+                            make_float4(h[q], h[q + 1], h[q + 2], h[q + 3]);
+                    } else {
+                        reinterpret_cast<double2*>(dst + q)[0] = make_double2(h[q], h[q + 1]);
+                        reinterpret_cast<double2*>(dst + q)[1] = make_double2(h[q + 2], h[q + 3]);
+                    }
                 }
             }
         }

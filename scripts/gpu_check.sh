@@ -14,6 +14,10 @@ fi
 if [[ $what == all || $what == bench ]]; then
   timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 fi
+if [[ $what == all || $what == c3 ]]; then
+  timeout 900 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_reinit|k_gradient|k_kint' -s 26 -c 3 -o gpurun_out/prof_c3 python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_c3.log 2>&1
+fi
 if [[ $what == all || $what == ncu ]]; then
   B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1
