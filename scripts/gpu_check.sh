@@ -25,3 +25,8 @@ if [[ $what == all || $what == ncu ]]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gradient|k_kint|k_probe|k_phi_init|k_count|k_tag|k_nb' -s 7 -c 7 -o gpurun_out/prof_other $B > gpurun_out/ncu_other.log 2>&1
 fi
 ls -la gpurun_out > gpurun_out/ls.txt
+if [[ $what == quick ]]; then
+  timeout 300 python -m pytest tests -m gpu -q -x -k "reinit or slab or c3" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+  timeout 600 python bench.py --no-e2e --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
+  timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+fi
