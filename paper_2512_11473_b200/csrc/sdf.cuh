@@ -57,8 +57,12 @@ __device__ __forceinline__ double sd_prim(int kind, const double* p, double x, d
             const int e1 = (e + 1) % 3;
             const double ux = p[2 * e1] - p[2 * e], uy = p[2 * e1 + 1] - p[2 * e + 1];
             const double wx = x - p[2 * e], wy = y - p[2 * e + 1];
-            double t = (wx * ux + wy * uy) / (ux * ux + uy * uy);
-            t = fmin(fmax(t, 0.0), 1.0);
+            // t = clamp((w.u) / (u.u), 0, 1); the quotient is only needed
+            // strictly inside (0, 1): w.u <= 0 gives t = 0 and w.u >= u.u
+            // gives t = 1 for the correctly rounded quotient too, so the
+            // skipped division changes no bit of the result
+            const double wu = wx * ux + wy * uy, uu = ux * ux + uy * uy;
+            const double t = wu <= 0.0 ? 0.0 : (wu >= uu ? 1.0 : wu / uu);
             const double hx = wx - ux * t, hy = wy - uy * t;
             const double d2 = hx * hx + hy * hy;
             best = (e == 0) ? d2 : fmin(best, d2);
@@ -136,8 +140,12 @@ __device__ __forceinline__ void sd_prim_col(int kind, const double* p, double x,
             const int e1 = (e + 1) % 3;
             const double ux = p[2 * e1] - p[2 * e], uy = p[2 * e1 + 1] - p[2 * e + 1];
             const double wx = x - p[2 * e], wy = y - p[2 * e + 1];
-            double t = (wx * ux + wy * uy) / (ux * ux + uy * uy);
-            t = fmin(fmax(t, 0.0), 1.0);
+            // t = clamp((w.u) / (u.u), 0, 1); the quotient is only needed
+            // strictly inside (0, 1): w.u <= 0 gives t = 0 and w.u >= u.u
+            // gives t = 1 for the correctly rounded quotient too, so the
+            // skipped division changes no bit of the result
+            const double wu = wx * ux + wy * uy, uu = ux * ux + uy * uy;
+            const double t = wu <= 0.0 ? 0.0 : (wu >= uu ? 1.0 : wu / uu);
             const double hx = wx - ux * t, hy = wy - uy * t;
             const double d2 = hx * hx + hy * hy;
             best = (e == 0) ? d2 : fmin(best, d2);

@@ -269,9 +269,14 @@ __global__ void __launch_bounds__(kTB) k_scatter(GridC gc, Bits b, int64_t nword
 }
 
 // first local package id of every stored plane; pf[planes] = n_pkg
-__global__ void k_planes_init(int64_t* pf, int32_t planes, int64_t n_pkg) {
+__global__ void k_planes_init(int64_t* pf, int32_t planes, int64_t n_pkg, uint32_t* meta_cell,
+                              uint8_t* meta_cat) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i <= planes) pf[i] = n_pkg;
+    if (i < 2) {  // singular packages: no cell, category 0 / 1
+        meta_cell[i] = 0xFFFFFFFFu;
+        meta_cat[i] = (uint8_t)i;
+    }
 }
 
 __global__ void k_planes(GridC gc, const uint32_t* __restrict__ meta_cell, int64_t n_pkg,
@@ -525,24 +530,33 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         g->n_inner = n_active - counts[1];
         const int64_t n_pkg = g->n_pkg;
 
-        g->bg = (uint32_t*)g->alloc(sizeof(uint32_t) * ncs, s);
-        g->meta_cell = (uint32_t*)g->alloc(sizeof(uint32_t) * n_pkg, s);
-        g->meta_cat = (uint8_t*)g->alloc((size_t)n_pkg, s);
-        g->nb = (uint32_t*)g->alloc(sizeof(uint32_t) * 27 * n_pkg, s);
+        // one arena for every array of the grid (a single stream-ordered
+        // allocation right after the host sync keeps the device busy)
         const int32_t planes = gc.zs_hi - gc.zs_lo;
-        g->plane_first = (int64_t*)g->alloc(sizeof(int64_t) * (planes + 1), s);
-        for (int b = 0; b < 2; ++b) g->phi[b] = g->alloc((size_t)g->esz * 64 * n_pkg, s);
-
-        const uint32_t sing_cell[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
-        const uint8_t sing_cat[2] = {0, 1};
-        SG_CUDA(cudaMemcpyAsync(g->meta_cell, sing_cell, sizeof(sing_cell), cudaMemcpyHostToDevice, s));
-        SG_CUDA(cudaMemcpyAsync(g->meta_cat, sing_cat, sizeof(sing_cat), cudaMemcpyHostToDevice, s));
+        auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+        const size_t sz_bg = al(sizeof(uint32_t) * ncs), sz_mc = al(sizeof(uint32_t) * n_pkg),
+                     sz_mk = al((size_t)n_pkg), sz_nb = al(sizeof(uint32_t) * 27 * n_pkg),
+                     sz_pf = al(sizeof(int64_t) * (planes + 1)),
+                     sz_phi = al((size_t)g->esz * 64 * n_pkg);
+        char* arena = (char*)g->alloc(sz_bg + sz_mc + sz_mk + sz_nb + sz_pf + 2 * sz_phi, s);
+        g->bg = (uint32_t*)arena;
+        arena += sz_bg;
+        g->meta_cell = (uint32_t*)arena;
+        arena += sz_mc;
+        g->meta_cat = (uint8_t*)arena;
+        arena += sz_mk;
+        g->nb = (uint32_t*)arena;
+        arena += sz_nb;
+        g->plane_first = (int64_t*)arena;
+        arena += sz_pf;
+        g->phi[0] = arena;
+        g->phi[1] = arena + sz_phi;
 
         k_scatter<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, bits, nwords, act_w, tile_off, g->bg,
                                                     g->meta_cell, g->meta_cat);
         SG_LAUNCHED();
-        k_planes_init<<<(unsigned)ceil_div(planes + 1, 256), 256, 0, s>>>(g->plane_first, planes,
-                                                                          n_pkg);
+        k_planes_init<<<(unsigned)ceil_div(planes + 1, 256), 256, 0, s>>>(
+            g->plane_first, planes, n_pkg, g->meta_cell, g->meta_cat);
         SG_LAUNCHED();
         if (n_active > 0) {
             k_planes<<<(unsigned)ceil_div(n_active, 256), 256, 0, s>>>(gc, g->meta_cell, n_pkg,

@@ -5,6 +5,7 @@ set -u
 mkdir -p gpurun_out
 what=${1:-all}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
+(nproc; free -g) >> gpurun_out/gpu.txt 2>&1
 python -m paper_2512_11473_b200.build > gpurun_out/build.log 2>&1
 python -c "import oracle.oracle as o; o.build()" >> gpurun_out/build.log 2>&1
 if [[ $what == all || $what == tests ]]; then
@@ -16,6 +17,7 @@ if [[ $what == all || $what == bench ]]; then
 fi
 if [[ $what == all || $what == c3 ]]; then
   timeout 900 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+  timeout 900 python bench.py --config C5 --steps 5 --warmup 2 --no-cpu-baseline > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_reinit|k_gradient|k_kint' -s 26 -c 3 -o gpurun_out/prof_c3 python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_c3.log 2>&1
 fi
 if [[ $what == all || $what == ncu ]]; then

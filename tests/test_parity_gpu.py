@@ -353,3 +353,35 @@ def test_c3_full_size_sampled(sgm, O):
     # the GPU's input is the fp32-rounded init; the pointwise oracle uses the
     # fp64 init: allow the input rounding (0.5 ulp of |phi| <= 16 dx) on top
     assert np.max(np.abs(got1 - exp1)) <= 1e-5 * w.dx + 2 * 16 * w.dx * 2**-24
+
+
+def test_c5_full_size(sgm, O):
+    """C5 (4096^3 effective, ~10^9 active data points): the whole background
+    table, meta and neighbour table bit-exact against the oracle; phi init and
+    the first reinit sweep at sampled data points."""
+    w = W.config("C5")
+    o = O.Oracle(w)
+    t = o.build_tables()
+    assert t.n_pkg - 2 == 15166440  # SURVEY App. A (tests/golden/tagging_counts.json)
+    g = sgm.Grid(w)
+    info = g.info
+    assert info["n_pkg"] == t.n_pkg
+    assert np.array_equal(g.view("plane_first").cpu().numpy(),
+                          2 + np.concatenate([[0], np.cumsum(t.plane_count)]))
+    assert np.array_equal(u32(g.view("bg")), t.bg)
+    assert np.array_equal(u32(g.view("meta_cell")), t.meta_cell)
+    assert np.array_equal(u32(g.view("nb")), t.nb)
+    rng = np.random.default_rng(13)
+    ids = rng.integers(2, t.n_pkg, 2000)
+    ds = rng.integers(0, 64, 2000)
+    cells = t.meta_cell[ids].astype(np.int64)
+    n = w.n[0]
+    cx, cy, cz = cells % n, (cells // n) % n, cells // (n * n)
+    ix, iy, iz = 4 * cx + (ds & 3), 4 * cy + ((ds >> 2) & 3), 4 * cz + (ds >> 4)
+    got0 = g.view("phi")[torch.from_numpy(ids).cuda(), torch.from_numpy(ds).cuda()].cpu().numpy()
+    exp0 = np.array([o.phi_point(a, b, c) for a, b, c in zip(ix, iy, iz)])
+    assert np.array_equal(got0, exp0.astype(np.float32))
+    g.reinit(1)
+    got1 = g.view("phi")[torch.from_numpy(ids).cuda(), torch.from_numpy(ds).cuda()].cpu().numpy()
+    exp1 = np.array([o.reinit_point_from_init(a, b, c, w.cfl) for a, b, c in zip(ix, iy, iz)])
+    assert np.max(np.abs(got1.astype(np.float64) - exp1)) <= 1e-5 * w.dx + 2 * 16 * w.dx * 2**-24
