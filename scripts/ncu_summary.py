@@ -100,7 +100,8 @@ def reports(tag, out):
                 b = rd * scale.get(units[col["dram__bytes_read.sum"]], 1) + \
                     wr * scale.get(units[col["dram__bytes_write.sum"]], 1)
                 base = name.split("<")[0]
-                traffic.setdefault("C2", {})[base] = b
+                cfg = "C3" if "c3" in os.path.basename(rep) else "C2"
+                traffic.setdefault(cfg, {})[base] = b
             except Exception:
                 pass
     open(os.path.join(ROOT, "profiles", f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
