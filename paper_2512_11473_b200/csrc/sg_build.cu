@@ -411,6 +411,14 @@ static GridC make_gridc(const sg_desc* d) {
     gc.inv_dx = 1.0 / gc.dx;
     int e = 0;
     gc.dyadic = std::frexp(d->cell, &e) == 0.5 ? 1 : 0;
+    gc.idx32 = gc.dyadic && d->dtype == SG_F32;
+    for (int k = 0; k < 3; ++k) {
+        gc.upperf[k] = (float)gc.upper[k];
+        gc.idx32 = gc.idx32 && d->lower[k] == 0.0 && (double)gc.upperf[k] == gc.upper[k] &&
+                   d->n[k] < (1 << 20);
+    }
+    gc.inv_cellf = (float)gc.inv_cell;
+    gc.inv_dxf = (float)gc.inv_dx;
     return gc;
 }
 

@@ -36,6 +36,11 @@ struct GridC {
     int64_t plane;         // n[0] * n[1]
     double inv_cell, inv_dx;
     int32_t dyadic;        // l_c is a power of two: x / l_c == x * (1 / l_c) exactly
+    // fp32 index arithmetic is bit-identical to the fp64 definition when l_c
+    // is a power of two, lower = 0 and upper is a float (see sg_probe.cu)
+    int32_t idx32;
+    float upperf[3];
+    float inv_cellf, inv_dxf;
 };
 
 struct Error : std::runtime_error {

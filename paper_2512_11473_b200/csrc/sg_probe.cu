@@ -30,11 +30,61 @@ __device__ __forceinline__ void ld_vec4(const double* p, double (&v)[4]) {
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
+// Containing background cell of one coordinate and the domain test (R-15:
+// fp64 division and floor).  Fast path (gc.idx32: fp32 positions, l_c a power
+// of two, lower = 0, upper a float): x * 2^e is exact in fp32, so floor and the
+// comparisons are bit-identical to the fp64 definition without fp64 work.
+template <class T>
+__device__ __forceinline__ bool cell_of(const GridC& gc, int k, T x, int& c);
+
+// lower-corner data index a = floor(u), u = (x - lower)/dx - 1/2, and the
+// fraction t = u - a (exact in fp32 on the fast path: u < 2^23)
+template <class T>
+__device__ __forceinline__ void corner_of(const GridC& gc, int k, T x, int& a, T& t);
+
 // (x - lower) / d with the oracle's rounding: for a power-of-two spacing the
 // division is a multiplication by the exact reciprocal.
 __device__ __forceinline__ double qdiv(const GridC& gc, double v, bool cell) {
     if (gc.dyadic) return v * (cell ? gc.inv_cell : gc.inv_dx);
     return v / (cell ? gc.cell : gc.dx);
+}
+
+template <>
+__device__ __forceinline__ bool cell_of<float>(const GridC& gc, int k, float x, int& c) {
+    if (gc.idx32) {
+        c = min((int)floorf(x * gc.inv_cellf), gc.n[k] - 1);
+        return x >= 0.f && x < gc.upperf[k];  // NaN fails both
+    }
+    const double xd = (double)x;
+    c = min((int)floor(qdiv(gc, xd - gc.lower[k], true)), gc.n[k] - 1);
+    return xd >= gc.lower[k] && xd < gc.upper[k];
+}
+template <>
+__device__ __forceinline__ bool cell_of<double>(const GridC& gc, int k, double x, int& c) {
+    c = min((int)floor(qdiv(gc, x - gc.lower[k], true)), gc.n[k] - 1);
+    return x >= gc.lower[k] && x < gc.upper[k];
+}
+template <>
+__device__ __forceinline__ void corner_of<float>(const GridC& gc, int k, float x, int& a, float& t) {
+    if (gc.idx32) {
+        const float u = x * gc.inv_dxf - 0.5f;
+        const float fa = floorf(u);
+        a = (int)fa;
+        t = u - fa;
+        return;
+    }
+    const double u = qdiv(gc, (double)x - gc.lower[k], false) - 0.5;
+    const double fa = floor(u);
+    a = (int)fa;
+    t = (float)(u - fa);
+}
+template <>
+__device__ __forceinline__ void corner_of<double>(const GridC& gc, int k, double x, int& a,
+                                                  double& t) {
+    const double u = qdiv(gc, x - gc.lower[k], false) - 0.5;
+    const double fa = floor(u);
+    a = (int)fa;
+    t = u - fa;
 }
 
 // Warp-centric, barrier-free: each warp owns a chunk of 128 consecutive
@@ -111,11 +161,7 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
     for (int j = 0; j < 4; ++j) {
         ok[j] = lane + 32 * j < m;
 #pragma unroll
-        for (int k = 0; k < 3; ++k)  // NaN fails both comparisons -> OOB
-            ok[j] = ok[j] && ((double)x[j][k] >= gc.lower[k]) && ((double)x[j][k] < gc.upper[k]);
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-            c[j][k] = ok[j] ? min((int)floor(qdiv(gc, (double)x[j][k] - gc.lower[k], true)), gc.n[k] - 1) : 0;
+        for (int k = 0; k < 3; ++k) ok[j] = cell_of<T>(gc, k, x[j][k], c[j][k]) && ok[j];
         ok[j] = ok[j] && c[j][2] >= gc.z_lo && c[j][2] < gc.z_hi;  // owned planes of a slab
         b[j] = ok[j] ? __ldg(bg + ((int64_t)(c[j][2] - gc.zs_lo) * gc.n[1] + c[j][1]) * gc.n[0] +
                              c[j][0])
@@ -157,12 +203,10 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
             T tv[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                const double xd = (double)xs[3 * p + k] - gc.lower[k];
-                const int ck = min((int)floor(qdiv(gc, xd, true)), gc.n[k] - 1);
-                const double u = qdiv(gc, xd, false) - 0.5;
-                const double a = floor(u);
-                tv[k] = (T)(u - a);
-                sv[k] = (int)a - 4 * ck;  // in [-1, 3]
+                int ck, a;
+                cell_of<T>(gc, k, xs[3 * p + k], ck);
+                corner_of<T>(gc, k, xs[3 * p + k], a, tv[k]);
+                sv[k] = a - 4 * ck;  // in [-1, 3]
             }
             const int s0x = sv[0], s0y = sv[1], s0z = sv[2];
             uint32_t pk[8];

@@ -385,3 +385,30 @@ def test_c5_full_size(sgm, O):
     got1 = g.view("phi")[torch.from_numpy(ids).cuda(), torch.from_numpy(ds).cuda()].cpu().numpy()
     exp1 = np.array([o.reinit_point_from_init(a, b, c, w.cfl) for a, b, c in zip(ix, iy, iz)])
     assert np.max(np.abs(got1.astype(np.float64) - exp1)) <= 1e-5 * w.dx + 2 * 16 * w.dx * 2**-24
+
+
+def test_probe_offset_grid_fp32(sgm, O):
+    """fp32 probe on a grid with a non-zero lower corner and a non-dyadic
+    cell size (the general fp64 index path of the kernel)."""
+    w = W.Workload("aniso", (23, 9, 14), 0.05, lower=(-0.3, 0.1, -0.2), dtype="f32",
+                   prims=(W.Prim(W.TORUS_Z, (0.25, 0.32, 0.15, 0.25, 0.08)),
+                          W.Prim(W.SPHERE, (0.7, 0.3, 0.4, 0.12))))
+    rng = np.random.default_rng(21)
+    lo = np.array(w.lower)
+    hi = lo + np.array(w.n) * w.cell
+    pos = rng.uniform(lo - 0.01, hi + 0.01, size=(50000, 3)).astype(np.float32)
+    _probe_compare(sgm, O, w, pos, phi_iters=2)
+
+
+def test_probe_shuffled_c4_matches_lattice(sgm, O):
+    """The probe is a pure per-particle function: a seeded permutation of the
+    C4 particles gives the permuted results bit for bit."""
+    w = W.config("C2")
+    g = sgm.Grid(w)
+    g.reinit(3).gradient(sgm.SG_GRAD)
+    pos = W.lattice_particles(w, seed=0)
+    perm = np.random.default_rng(1).permutation(pos.shape[0])
+    a_phi, a_grad = g.probe(torch.from_numpy(pos).cuda())
+    b_phi, b_grad = g.probe(torch.from_numpy(pos[perm]).cuda())
+    p = torch.from_numpy(perm).cuda()
+    assert torch.equal(a_phi[p], b_phi) and torch.equal(a_grad[p], b_grad)
