@@ -174,6 +174,13 @@ __global__ void __launch_bounds__(kTB) k_count(GridC gc, Bits b, int64_t nwords,
         act_w[t] = act;
         cnt = __popc(act);
         ncore = __popc(__ldg(b.core + b.idx(gc, z, y, q)) & valid_bits(gc, q, b.W));
+        // does an active cell lie on the domain boundary (so that some
+        // neighbour-table entries need the out-of-domain rule R-6)?
+        const int last = gc.n[0] - 1 - 32 * q;  // bit of x = nx - 1 in this word
+        const bool edge = act && (y == 0 || y == gc.n[1] - 1 || z == 0 || z == gc.n[2] - 1 ||
+                                  (q == 0 && (act & 1u)) ||
+                                  (last < 32 && ((act >> last) & 1u)));
+        if (edge) atomicOr(reinterpret_cast<unsigned int*>(n_core + 1), 1u);
     }
     int total;
     block_excl_scan(cnt, s_warp, total);
@@ -306,6 +313,7 @@ __device__ __noinline__ uint32_t virtual_sign(double lx, double ly, double lz, d
 // plane) take their sign bit (never dereferenced by owned-point stencils).
 constexpr int kNbPW = 4;  // packages per warp
 
+template <bool EDGE>
 __global__ void __launch_bounds__(256) k_nb(GridC gc, const Geom* __restrict__ geom, Bits b,
                                             const uint32_t* __restrict__ bg,
                                             const uint32_t* __restrict__ meta_cell,
@@ -329,7 +337,8 @@ __global__ void __launch_bounds__(256) k_nb(GridC gc, const Geom* __restrict__ g
         if (id < 2 || id >= n_pkg) continue;
         const uint32_t r = L[u] / nx;
         const int qx = (int)(L[u] - r * nx) + ox, qy = (int)(r % ny) + oy, qz = (int)(r / ny) + oz;
-        if (qx < 0 || qy < 0 || qz < 0 || qx >= gc.n[0] || qy >= gc.n[1] || qz >= gc.n[2]) {
+        if (EDGE &&
+            (qx < 0 || qy < 0 || qz < 0 || qx >= gc.n[0] || qy >= gc.n[1] || qz >= gc.n[2])) {
             v[u] = virtual_sign(gc.lower[0], gc.lower[1], gc.lower[2], gc.cell, geom, qx, qy, qz);
         } else if (qz >= gc.zs_lo && qz < gc.zs_hi) {
             v[u] = __ldg(bg + (int64_t)(qz - gc.zs_lo) * gc.plane + (int64_t)qy * gc.n[0] + qx);
@@ -457,6 +466,14 @@ static void launch_tag(const GridC& gc, const Geom& geom, int32_t zt_lo, int32_t
     SG_LAUNCHED();
 }
 
+// library-internal side stream (one per process, non-blocking)
+static cudaStream_t side_stream() {
+    static cudaStream_t st = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] { SG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); });
+    return st;
+}
+
 static int check_device() {
     int dev = -1;
     cudaError_t e = cudaGetDevice(&dev);
@@ -518,18 +535,18 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         uint32_t* act_w = (uint32_t*)dalloc(sizeof(uint32_t) * nwords, s);
         int32_t* tile_count = (int32_t*)dalloc(sizeof(int32_t) * n_tiles, s);
         int64_t* tile_off = (int64_t*)dalloc(sizeof(int64_t) * (n_tiles + 1), s);
-        unsigned long long* d_core = (unsigned long long*)dalloc(sizeof(unsigned long long), s);
-        SG_CUDA(cudaMemsetAsync(d_core, 0, sizeof(unsigned long long), s));
+        unsigned long long* d_core = (unsigned long long*)dalloc(2 * sizeof(unsigned long long), s);
+        SG_CUDA(cudaMemsetAsync(d_core, 0, 2 * sizeof(unsigned long long), s));
         k_count<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, bits, nwords, act_w, tile_count, d_core);
         SG_LAUNCHED();
         k_scan<<<1, 1024, 0, s>>>(tile_count, n_tiles, tile_off);
         SG_LAUNCHED();
 
         // the single host synchronisation: package count (and core count)
-        int64_t counts[2];
+        int64_t counts[3];
         SG_CUDA(cudaMemcpyAsync(&counts[0], tile_off + n_tiles, sizeof(int64_t),
                                 cudaMemcpyDeviceToHost, s));
-        SG_CUDA(cudaMemcpyAsync(&counts[1], d_core, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        SG_CUDA(cudaMemcpyAsync(&counts[1], d_core, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         SG_CUDA(cudaStreamSynchronize(s));
         const int64_t n_active = counts[0];
         SG_ARG(n_active + 2 < 4294967295LL, "sg_build: more than 2^32-3 packages");
@@ -571,11 +588,26 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
                                                                        g->plane_first);
             SG_LAUNCHED();
         }
-        Geom* d_geom = (Geom*)dalloc(sizeof(Geom), s);
-        SG_CUDA(cudaMemcpyAsync(d_geom, &g->geom, sizeof(Geom), cudaMemcpyHostToDevice, s));
-        k_nb<<<(unsigned)ceil_div(ceil_div(n_pkg, kNbPW) * 32, 256), 256, 0, s>>>(gc, d_geom, bits, g->bg,
-                                                                 g->meta_cell, n_pkg, g->nb);
+        Geom* d_geom = nullptr;
+        if (counts[2]) {
+            d_geom = (Geom*)dalloc(sizeof(Geom), s);
+            SG_CUDA(cudaMemcpyAsync(d_geom, &g->geom, sizeof(Geom), cudaMemcpyHostToDevice, s));
+        }
+        // K3 (integer / L2 gathers) on a side stream concurrently with K4
+        // (fp64 ALU): they only share read-only inputs
+        cudaStream_t side = side_stream();
+        cudaEvent_t ev_fork, ev_join;
+        SG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        SG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        SG_CUDA(cudaEventRecord(ev_fork, s));
+        SG_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+        const unsigned nbb = (unsigned)ceil_div(ceil_div(n_pkg, kNbPW) * 32, 256);
+        if (counts[2])  // band touches the domain boundary: out-of-domain rule needed
+            k_nb<true><<<nbb, 256, 0, side>>>(gc, d_geom, bits, g->bg, g->meta_cell, n_pkg, g->nb);
+        else
+            k_nb<false><<<nbb, 256, 0, side>>>(gc, d_geom, bits, g->bg, g->meta_cell, n_pkg, g->nb);
         SG_LAUNCHED();
+        SG_CUDA(cudaEventRecord(ev_join, side));
         const unsigned pb = (unsigned)ceil_div(n_pkg * 16, 256);
         if (g->dtype == SG_F64)
             k_phi_init<double><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
@@ -584,6 +616,9 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
             k_phi_init<float><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
                                                  (float*)g->phi[0], (float*)g->phi[1]);
         SG_LAUNCHED();
+        SG_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+        SG_CUDA(cudaEventDestroy(ev_fork));
+        SG_CUDA(cudaEventDestroy(ev_join));
         g->cur = 0;
 
         // owned id range: whole domain -> [2, n_pkg); slab -> plane ranges
@@ -601,7 +636,7 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
 
         SG_CUDA(cudaFreeAsync(core_w, s));
         SG_CUDA(cudaFreeAsync(act_w, s));
-        SG_CUDA(cudaFreeAsync(d_geom, s));
+        if (d_geom) SG_CUDA(cudaFreeAsync(d_geom, s));
         SG_CUDA(cudaFreeAsync(tile_count, s));
         SG_CUDA(cudaFreeAsync(tile_off, s));
         SG_CUDA(cudaFreeAsync(d_core, s));

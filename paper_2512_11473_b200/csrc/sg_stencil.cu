@@ -204,6 +204,11 @@ __device__ __forceinline__ void st_vec4(double* p, double a, double b, double c,
     reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
 }
 
+// 1 / |g| from |g|^2, 0 for g = 0: fp32 via MUFU rsqrt (~2 ulp, inside the
+// 1e-5 normal tolerance), fp64 exactly rounded sqrt and division
+__device__ __forceinline__ float inv_norm(float m2) { return m2 > 0.f ? rsqrtf(m2) : 0.f; }
+__device__ __forceinline__ double inv_norm(double m2) { return m2 > 0.0 ? 1.0 / sqrt(m2) : 0.0; }
+
 template <class T>
 __global__ void __launch_bounds__(256) k_gradient(const T* __restrict__ in, T* __restrict__ grad,
                                                   T* __restrict__ normal,
@@ -231,8 +236,7 @@ __global__ void __launch_bounds__(256) k_gradient(const T* __restrict__ in, T* _
         T nx[4], ny[4], nz[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const T m = sqrt(gx[i] * gx[i] + gy[i] * gy[i] + gz[i] * gz[i]);
-            const T inv = m > T(0) ? T(1) / m : T(0);
+            const T inv = inv_norm(gx[i] * gx[i] + gy[i] * gy[i] + gz[i] * gz[i]);
             nx[i] = gx[i] * inv;
             ny[i] = gy[i] * inv;
             nz[i] = gz[i] * inv;
@@ -297,7 +301,9 @@ __device__ __forceinline__ float heav(float u, float eps, float inv_eps) {
     if (u < -eps) return 0.f;
     if (u > eps) return 1.f;
     const float q = u * inv_eps;
-    return 0.5f * (1.f + q + sinpif(q) * 0.318309886183790672f);
+    // MUFU sine: absolute error <= 2^-21.4 on [-pi, pi] -> |dH| < 1.2e-7,
+    // |dK| < 1.2e-7 S, well inside the fp32 tolerance (1e-5)
+    return 0.5f * (1.f + q + __sinf(3.14159265358979f * q) * 0.318309886183790672f);
 }
 __device__ __forceinline__ double heav(double u, double eps, double inv_eps) {
     if (u < -eps) return 0.0;

@@ -32,3 +32,6 @@ if [[ $what == quick ]]; then
   timeout 600 python bench.py --no-e2e --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
   timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
 fi
+if [[ $what == prof ]]; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_probe|k_kint|k_gradient|k_phi_init|k_nb|k_tag" -s 6 -c 6 -o gpurun_out/prof_b python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_b.log 2>&1
+fi
