@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--order", default="lattice", choices=["lattice", "shuffled"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--slab", action="store_true",
+                   help="z-slab path (NCCL) even at one rank (exercises the multi-GPU code)")
     return p.parse_args()
 
 
@@ -166,8 +168,13 @@ def run_ours(args, rank, world, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     w = W.config(args.config)
-    if world > 1:
+    if world > 1 or args.slab:
         from paper_2512_11473_b200 import slab as SL
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         return SL.bench_slab(args, w, rank, world, local)
     stream = torch.cuda.current_stream()
 

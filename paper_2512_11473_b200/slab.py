@@ -156,83 +156,126 @@ class SlabGrid:
 
 
 def bench_slab(args, w, rank, world, local):
-    """bench.py body for N > 1 (torchrun): one z-slab per rank, NCCL halos."""
+    """bench.py body for z-slab runs (torchrun, one rank per GPU; also usable
+    at world size 1 with --slab to exercise the path): each rank owns a slab,
+    reinit sweeps exchange ghost planes over NCCL, particles are binned to the
+    owner rank.  Times are device events, max over ranks."""
     import json
-    import time
 
     import torch
     import torch.distributed as dist
 
     import workloads as W
     from . import sg
-    from bench import METRIC, UNIT, REINIT_ITERS, ClockSampler
+    from bench import METRIC, UNIT, REINIT_ITERS, ClockSampler, peaks, workload_name
 
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
-    pos_np = W.lattice_particles(w, seed=0, order=args.order,
-                                 dtype=np.float32 if w.dtype == "f32" else np.float64)
+    npdt = np.float32 if w.dtype == "f32" else np.float64
+    pos_np = (W.lattice_particles(w, seed=0, order=args.order, dtype=npdt) if w.particles
+              else np.zeros((0, 3), dtype=npdt))
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     fields = sg.SG_GRAD | sg.SG_NORMAL | sg.SG_KINT
 
-    def step():
-        s = SlabGrid(w, world, rank, stream=stream)
-        s.reinit(REINIT_ITERS, w.cfl, stream)
-        s.gradient(fields, w.h_ratio, stream)
-        return s
-
     # particles binned to their owner rank (input preparation, untimed)
-    s0 = step()
+    s0 = SlabGrid(w, world, rank, stream=stream)
     d_pos_all = torch.from_numpy(pos_np).cuda()
     d_pos = d_pos_all[owner_mask(d_pos_all, w, s0.plan)].contiguous()
     del d_pos_all
-    n_local = d_pos.shape[0]
-    n_pkg_local = s0.plan and (s0.grid.info["own_hi"] - s0.grid.info["own_lo"])
+    n_local = int(d_pos.shape[0])
+    info0 = s0.grid.info
+    n_pkg_local = info0["own_hi"] - info0["own_lo"]
     s0.close()
     d_phi = torch.empty(n_local, dtype=d_pos.dtype, device="cuda")
     d_grad = torch.empty((n_local, 3), dtype=d_pos.dtype, device="cuda")
+    h_pos = d_pos.cpu().pin_memory()
+    h_phi = torch.empty(n_local, dtype=d_pos.dtype).pin_memory()
+    h_grad = torch.empty((n_local, 3), dtype=d_pos.dtype).pin_memory()
 
-    def full_step():
-        s = step()
-        sg.sg_probe(s.grid.handle, n_local, d_pos.data_ptr(), d_phi.data_ptr(), d_grad.data_ptr(),
-                    None, stream)
+    def full_step(ev, host=False):
+        ev[0].record(stream)
+        s = SlabGrid(w, world, rank, stream=stream)
+        ev[1].record(stream)
+        s.reinit(REINIT_ITERS, w.cfl, stream)
+        ev[2].record(stream)
+        s.gradient(fields, w.h_ratio, stream)
+        ev[3].record(stream)
+        if n_local:
+            if host:
+                sg.sg_probe(s.grid.handle, n_local, h_pos.data_ptr(), h_phi.data_ptr(),
+                            h_grad.data_ptr(), None, stream)
+            else:
+                sg.sg_probe(s.grid.handle, n_local, d_pos.data_ptr(), d_phi.data_ptr(),
+                            d_grad.data_ptr(), None, stream)
+        ev[4].record(stream)
         return s
 
-    for _ in range(args.warmup):
-        flush.zero_()
-        full_step().close()
-    torch.cuda.synchronize()
-    l0 = sg.sg_launch_count()
-    times = []
-    with ClockSampler(local) as clk:
+    def mk():
+        return [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+
+    def timed(host):
+        st = []
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            s = full_step()
-            e1.record(stream)
+            ev = mk()
+            s = full_step(ev, host)
             torch.cuda.synchronize()
-            t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+            t = torch.tensor([ev[i].elapsed_time(ev[i + 1]) for i in range(4)], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            times.append(float(t.item()))
+            st.append(t.cpu().numpy())
             s.close()
+        return np.array(st)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        full_step(mk()).close()
+    torch.cuda.synchronize()
+    l0 = sg.sg_launch_count()
+    with ClockSampler(local) as clk:
+        st = timed(False)
     launches = sg.sg_launch_count() - l0
+    e2e = None
+    if not args.no_e2e and n_local:
+        et = timed(True)
     tot = torch.tensor([n_pkg_local, n_local], dtype=torch.int64, device="cuda")
     dist.all_reduce(tot)
     n_act = int(tot[0].item()) * 64
-    ms = float(np.mean(times))
+    n_part = int(tot[1].item())
+    ms = float(st.sum(1).mean())
+    updates = n_act * (REINIT_ITERS + 1)
+    if not args.no_e2e and n_local:
+        e_ms = float(et.sum(1).mean())
+        e2e = {"value": updates / (e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(n_part * 3 * h_pos.element_size()),
+               "d2h_bytes_per_step": int(n_part * 4 * h_pos.element_size()),
+               "ms_per_step": e_ms}
+    reinit_ms = float(st[:, 1].mean()) / REINIT_ITERS
+    esz = 4 if w.dtype == "f32" else 8
+    bpc = 2 * esz + 108 / 64
+    hbm, src = peaks()
+    # per-GPU achieved bandwidth of the sweep (incl. the ghost exchange)
+    achieved = bpc * n_act / world / (reinit_ms * 1e-3) / 1e9
     if rank == 0:
-        out = {"metric": METRIC, "value": n_act * (REINIT_ITERS + 1) / (ms * 1e-3), "unit": UNIT,
+        out = {"metric": METRIC, "value": updates / (ms * 1e-3), "unit": UNIT,
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": w.dtype, "data": "synthetic",
-               "config": {"workload": f"{w.name}+C4 z-slab partitioned, NCCL halo per sweep",
-                          "active_cells": n_act, "particles": int(tot[1].item()),
+               "config": {"workload": workload_name(w, n_part, args.order) +
+                          f", z-slab partitioned over {world} GPUs, NCCL ghost planes per sweep",
+                          "active_cells": n_act, "particles": n_part,
                           "parallelism": f"zslab{world}",
-                          "l2": "flushed between steps (512 MiB write)"},
-               "probes_per_s": int(tot[1].item()) / (ms * 1e-3),
-               "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": None}
+                          "l2": "flushed between steps (512 MiB write, outside the timed events)"},
+               "probes_per_s": n_part / (ms * 1e-3),
+               "stages": {n: {"ms": float(st[:, i].mean())} for i, n in
+                          enumerate(["build", "reinit", "gradient", "probe"])},
+               "e2e": e2e, "gpu_launches": int(launches),
+               "roofline": {"kernel": "k_reinit<float> + ghost exchange", "bound": "hbm",
+                            "achieved": achieved, "peak": hbm, "peak_source": src,
+                            "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                            "note": "per GPU, sweep time max over ranks incl. NCCL exchange"},
+               "clocks": clk.summary()}
         print(json.dumps(out), flush=True)
     dist.destroy_process_group()
-    _ = time
