@@ -93,8 +93,7 @@ __device__ __forceinline__ double sd_eval(const Geom& g, double x, double y, dou
 // the result is bit-identical to NZ separate sd_eval calls).
 template <int NZ>
 __device__ __forceinline__ void sd_prim_col(int kind, const double* p, double x, double y,
-                                            const double (&z)[NZ], double (&f)[NZ],
-                                            const double* cur = nullptr) {
+                                            const double (&z)[NZ], double (&f)[NZ]) {
     switch (kind) {
     case SG_SPHERE:
     case SG_SHELL: {
@@ -102,22 +101,10 @@ __device__ __forceinline__ void sd_prim_col(int kind, const double* p, double x,
         const double exy = ex * ex + ey * ey;
         const double rm = 0.5 * (p[3] + p[4]);
         const double hw = 0.5 * (p[4] - p[3]);
-        const double ro = kind == SG_SPHERE ? p[3] : p[4];  // outer radius
 #pragma unroll
         for (int k = 0; k < NZ; ++k) {
             const double ez = z[k] - p[2];
-            const double d2 = exy + ez * ez;
-            // union early-out: f_prim >= |x - c| - r_out > cur (with a margin
-            // far above the rounding of f_prim) leaves min(cur, f_prim) = cur
-            if (cur) {
-                const double b = cur[k] + ro;
-                const double tb = b * (1.0 + 1e-9) + 1e-12 * ro;
-                if (b > 0.0 && d2 > tb * tb) {
-                    f[k] = __longlong_as_double(0x7ff0000000000000ULL);  // +inf
-                    continue;
-                }
-            }
-            const double d = sqrt(d2);
+            const double d = sqrt(exy + ez * ez);
             f[k] = kind == SG_SPHERE ? d - p[3] : fabs(d - rm) - hw;
         }
         return;
@@ -189,7 +176,7 @@ __device__ __forceinline__ void sd_eval_col(const Geom& g, double x, double y,
     sd_prim_col<NZ>(g.kind[0], g.p[0], x, y, z, f);
     for (int i = 1; i < g.n; ++i) {
         double fi[NZ];
-        sd_prim_col<NZ>(g.kind[i], g.p[i], x, y, z, fi, f);
+        sd_prim_col<NZ>(g.kind[i], g.p[i], x, y, z, fi);
 #pragma unroll
         for (int k = 0; k < NZ; ++k) f[k] = fmin(f[k], fi[k]);
     }
