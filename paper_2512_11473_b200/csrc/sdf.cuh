@@ -182,4 +182,20 @@ __device__ __forceinline__ void sd_eval_col(const Geom& g, double x, double y,
     }
 }
 
+// the same min over the primitives selected by `mask` (bit i = primitive i);
+// callers only drop primitives that provably exceed the minimum
+template <int NZ>
+__device__ __forceinline__ void sd_eval_col_mask(const Geom& g, uint32_t mask, double x, double y,
+                                                 const double (&z)[NZ], double (&f)[NZ]) {
+    bool first = true;
+    for (int i = 0; i < g.n; ++i) {
+        if (!((mask >> i) & 1u)) continue;
+        double fi[NZ];
+        sd_prim_col<NZ>(g.kind[i], g.p[i], x, y, z, fi);
+#pragma unroll
+        for (int k = 0; k < NZ; ++k) f[k] = first ? fi[k] : fmin(f[k], fi[k]);
+        first = false;
+    }
+}
+
 }  // namespace sg

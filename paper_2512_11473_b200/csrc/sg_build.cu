@@ -80,19 +80,37 @@ struct Bits {
 // (O2: centre = lower + (c + 0.5) l_c).  A thread owns an (x, y) column and 4
 // consecutive planes (the (x, y)-only terms of each primitive are shared,
 // bit-identically); warp ballots pack the core and sign predicates into words.
+//
+// Lipschitz cull: the analytic f is a (union of) exact signed distance(s),
+// hence 1-Lipschitz.  A warp covers 32 x 1 x 4 cells whose centres lie within
+// R = |(15.5, 0, 1.5)| l_c of the block centre c.  If |f(c)| > l_c + R + eps
+// (eps far above the rounding of f), no cell of the block is core and every
+// cell has the sign of f(c): the per-cell evaluation is skipped, and the
+// predicates are exactly those the per-cell fp64 evaluation would produce.
 __global__ void __launch_bounds__(256) k_tag(GridC gc, Geom geom, int32_t zt_lo, int32_t zt_hi,
                                              int32_t W, uint32_t* __restrict__ core_w,
                                              uint32_t* __restrict__ neg_w) {
     const int cx = blockIdx.x * blockDim.x + threadIdx.x;
     const int cy = blockIdx.y;
     const int z0 = zt_lo + 4 * (int)blockIdx.z;
-    const double x = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
-    const double y = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
-    double z[4], f[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) z[k] = gc.lower[2] + ((double)(z0 + k) + 0.5) * gc.cell;
-    if (cx < gc.n[0]) sd_eval_col<4>(geom, x, y, z, f);
     const int q = cx >> 5;
+    const double y = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
+    const double fc = sd_eval(geom, gc.lower[0] + (double)(32 * q + 16) * gc.cell, y,
+                              gc.lower[2] + (double)(z0 + 2) * gc.cell);
+    const double R = 15.572411502397436 * gc.cell;  // sqrt(15.5^2 + 1.5^2) l_c
+    const double eps = 1e-9 * (gc.cell + fabs(gc.lower[0]) + fabs(gc.lower[1]) +
+                               fabs(gc.lower[2]) + gc.upper[0] + gc.upper[1] + gc.upper[2]);
+    double f[4];
+    if (fabs(fc) > gc.cell + R + eps) {  // warp-uniform
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f[k] = fc;  // same core (none) and sign predicates
+    } else {
+        const double x = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
+        double z[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) z[k] = gc.lower[2] + ((double)(z0 + k) + 0.5) * gc.cell;
+        if (cx < gc.n[0]) sd_eval_col<4>(geom, x, y, z, f);
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const bool in = cx < gc.n[0];
@@ -383,7 +401,29 @@ __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
     double z[4], f[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) z[k] = gc.lower[2] + ((double)(4 * (int64_t)cz + k) + 0.5) * gc.dx;
-    sd_eval_col<4>(geom, x, y, z, f);
+    if (geom.n == 1) {
+        sd_eval_col<4>(geom, x, y, z, f);
+    } else {
+        // unions: primitives that provably exceed the minimum at every data
+        // point of the package are dropped (1-Lipschitz bound from the
+        // package centre c, data points within R = sqrt(3) 1.5 dx of c)
+        const double pcx = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
+        const double pcy = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
+        const double pcz = gc.lower[2] + ((double)cz + 0.5) * gc.cell;
+        const double R = 2.598076211353316 * gc.dx;
+        const double eps = 1e-9 * (gc.cell + fabs(gc.lower[0]) + fabs(gc.lower[1]) +
+                                   fabs(gc.lower[2]) + gc.upper[0] + gc.upper[1] + gc.upper[2]);
+        double fc[SG_MAX_PRIMS];
+        double m = 0.0;
+        for (int i = 0; i < geom.n; ++i) {
+            fc[i] = sd_prim(geom.kind[i], geom.p[i], pcx, pcy, pcz);
+            m = i == 0 ? fc[i] : fmin(m, fc[i]);
+        }
+        uint32_t mask = 0;
+        for (int i = 0; i < geom.n; ++i)
+            if (fc[i] - R <= m + R + eps) mask |= 1u << i;
+        sd_eval_col_mask<4>(geom, mask, x, y, z, f);
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) phi0[id * 64 + col + 16 * k] = (T)(gc.init_scale * f[k]);
 }
