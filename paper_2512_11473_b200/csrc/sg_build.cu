@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -77,40 +78,92 @@ struct Bits {
 };
 
 // K1 -- f at every background-cell centre of the tag planes [zt_lo, zt_hi)
-// (O2: centre = lower + (c + 0.5) l_c).  A thread owns an (x, y) column and 4
-// consecutive planes (the (x, y)-only terms of each primitive are shared,
-// bit-identically); warp ballots pack the core and sign predicates into words.
+// (O2: centre = lower + (c + 0.5) l_c); warp ballots pack the core and sign
+// predicates into 32-cell words.
 //
+// Work unit: a block of 32 x 1 x 4 cells (one word in 4 consecutive planes);
+// a lane evaluates one (x, y) column of 4 planes (the (x, y)-only terms of
+// each primitive are shared, bit-identically).  A warp owns 32 such blocks
+// along y.
 // Lipschitz cull: the analytic f is a (union of) exact signed distance(s),
-// hence 1-Lipschitz.  A warp covers 32 x 1 x 4 cells whose centres lie within
-// R = |(15.5, 0, 1.5)| l_c of the block centre c.  If |f(c)| > l_c + R + eps
-// (eps far above the rounding of f), no cell of the block is core and every
-// cell has the sign of f(c): the per-cell evaluation is skipped, and the
-// predicates are exactly those the per-cell fp64 evaluation would produce.
+// hence 1-Lipschitz.  The cell centres of a block lie within
+// R = |(15.5, 0, 1.5)| l_c of its centre c.  If |f(c)| > l_c + R + eps (eps far
+// above the rounding of f), no cell of the block is core and every cell has
+// the sign of f(c): the per-cell evaluation is skipped and the predicates are
+// exactly those of the per-cell fp64 evaluation.  The 32 block-centre values
+// of a warp are computed by its 32 lanes in parallel.
+__global__ void __launch_bounds__(128, 4) k_tag_cull(GridC gc, Geom geom, int32_t zt_lo, int32_t zt_hi,
+                                             int32_t W, int32_t cull,
+                                             uint32_t* __restrict__ core_w,
+                                             uint32_t* __restrict__ neg_w) {
+    const int lane = threadIdx.x & 31;
+    const int q = blockIdx.x;                                  // word (32 x-cells)
+    const int y0 = 32 * blockIdx.y;                            // first row of the warp
+    const int z0 = zt_lo + 4 * (4 * (int)blockIdx.z + (threadIdx.x >> 5));  // first plane
+    if (z0 >= zt_hi) return;                                   // warp-uniform
+    const double R = 15.572411502397436 * gc.cell;             // sqrt(15.5^2 + 1.5^2) l_c
+    const double eps = 1e-9 * (gc.cell + fabs(gc.lower[0]) + fabs(gc.lower[1]) +
+                               fabs(gc.lower[2]) + gc.upper[0] + gc.upper[1] + gc.upper[2]);
+    bool skip_mine = false, neg_mine = false;
+    if (cull) {
+        const double fc = sd_eval(geom, gc.lower[0] + (double)(32 * q + 16) * gc.cell,
+                                  gc.lower[1] + ((double)(y0 + lane) + 0.5) * gc.cell,
+                                  gc.lower[2] + (double)(z0 + 2) * gc.cell);
+        skip_mine = fabs(fc) > gc.cell + R + eps;
+        neg_mine = fc < 0.0;
+    }
+    const uint32_t skip = __ballot_sync(0xffffffffu, skip_mine);
+    const uint32_t negb = __ballot_sync(0xffffffffu, neg_mine);
+    const int cx = 32 * q + lane;
+    const bool in = cx < gc.n[0];
+    const uint32_t valid = __ballot_sync(0xffffffffu, in);
+    const int nrows = min(32, gc.n[1] - y0);
+    for (int b = 0; b < nrows; ++b) {
+        const int cy = y0 + b;
+        uint32_t cw[4], nw[4];
+        if ((skip >> b) & 1u) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                cw[k] = 0u;
+                nw[k] = ((negb >> b) & 1u) ? valid : 0u;
+            }
+        } else {
+            const double x = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
+            const double y = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
+            double z[4], f[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) z[k] = gc.lower[2] + ((double)(z0 + k) + 0.5) * gc.cell;
+            if (in) sd_eval_col<4>(geom, x, y, z, f);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                cw[k] = __ballot_sync(0xffffffffu, in && fabs(f[k]) < gc.cell);
+                nw[k] = __ballot_sync(0xffffffffu, in && f[k] < 0.0);
+            }
+        }
+        if (lane < 4 && z0 + lane < zt_hi) {
+            const int k = lane;
+            const int64_t i = ((int64_t)(z0 + k - zt_lo) * gc.n[1] + cy) * W + q;
+            core_w[i] = k == 0 ? cw[0] : k == 1 ? cw[1] : k == 2 ? cw[2] : cw[3];
+            neg_w[i] = k == 0 ? nw[0] : k == 1 ? nw[1] : k == 2 ? nw[2] : nw[3];
+        }
+    }
+}
+
+// K1 without the cull (band-dense domains): a thread owns an (x, y) column of
+// 4 planes, a warp 32 consecutive x-cells.
 __global__ void __launch_bounds__(256) k_tag(GridC gc, Geom geom, int32_t zt_lo, int32_t zt_hi,
                                              int32_t W, uint32_t* __restrict__ core_w,
                                              uint32_t* __restrict__ neg_w) {
     const int cx = blockIdx.x * blockDim.x + threadIdx.x;
     const int cy = blockIdx.y;
     const int z0 = zt_lo + 4 * (int)blockIdx.z;
-    const int q = cx >> 5;
+    const double x = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
     const double y = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
-    const double fc = sd_eval(geom, gc.lower[0] + (double)(32 * q + 16) * gc.cell, y,
-                              gc.lower[2] + (double)(z0 + 2) * gc.cell);
-    const double R = 15.572411502397436 * gc.cell;  // sqrt(15.5^2 + 1.5^2) l_c
-    const double eps = 1e-9 * (gc.cell + fabs(gc.lower[0]) + fabs(gc.lower[1]) +
-                               fabs(gc.lower[2]) + gc.upper[0] + gc.upper[1] + gc.upper[2]);
-    double f[4];
-    if (fabs(fc) > gc.cell + R + eps) {  // warp-uniform
+    double z[4], f[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) f[k] = fc;  // same core (none) and sign predicates
-    } else {
-        const double x = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
-        double z[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) z[k] = gc.lower[2] + ((double)(z0 + k) + 0.5) * gc.cell;
-        if (cx < gc.n[0]) sd_eval_col<4>(geom, x, y, z, f);
-    }
+    for (int k = 0; k < 4; ++k) z[k] = gc.lower[2] + ((double)(z0 + k) + 0.5) * gc.cell;
+    if (cx < gc.n[0]) sd_eval_col<4>(geom, x, y, z, f);
+    const int q = cx >> 5;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const bool in = cx < gc.n[0];
@@ -500,9 +553,21 @@ static Geom make_geom(const sg_geometry* g) {
 static void launch_tag(const GridC& gc, const Geom& geom, int32_t zt_lo, int32_t zt_hi,
                        int32_t W, uint32_t* core_w, uint32_t* neg_w, cudaStream_t s) {
     if (zt_hi <= zt_lo) return;
-    dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1],
-              (unsigned)ceil_div(zt_hi - zt_lo, 4));
-    k_tag<<<grid, 256, 0, s>>>(gc, geom, zt_lo, zt_hi, W, core_w, neg_w);
+    // the cull pays where the band is a small fraction of the domain
+    const int quads = (int)ceil_div(zt_hi - zt_lo, 4);
+    // SG_TAG_CULL=0/1 forces the variant (tests); default by domain size
+    static const int force = [] {
+        const char* e = getenv("SG_TAG_CULL");
+        return e ? atoi(e) : -1;
+    }();
+    const bool cull = force >= 0 ? force == 1 : (double)gc.n[0] * gc.n[1] * gc.n[2] >= (double)(1 << 25);
+    if (cull) {
+        dim3 grid((unsigned)W, (unsigned)ceil_div(gc.n[1], 32), (unsigned)ceil_div(quads, 4));
+        k_tag_cull<<<grid, 128, 0, s>>>(gc, geom, zt_lo, zt_hi, W, 1, core_w, neg_w);
+    } else {
+        dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1], (unsigned)quads);
+        k_tag<<<grid, 256, 0, s>>>(gc, geom, zt_lo, zt_hi, W, core_w, neg_w);
+    }
     SG_LAUNCHED();
 }
 

@@ -412,3 +412,30 @@ def test_probe_shuffled_c4_matches_lattice(sgm, O):
     b_phi, b_grad = g.probe(torch.from_numpy(pos[perm]).cuda())
     p = torch.from_numpy(perm).cuda()
     assert torch.equal(a_phi[p], b_phi) and torch.equal(a_grad[p], b_grad)
+
+
+def test_tables_with_forced_tag_cull(O):
+    """The Lipschitz-culled tagging kernel (default only for >= 2^25 cells) on
+    small scenes with partial words and boundary-touching bands, in a fresh
+    process with SG_TAG_CULL=1: tables bit-exact."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, workloads as W\n"
+        "from oracle.oracle import Oracle\n"
+        "from paper_2512_11473_b200 import sg\n"
+        "for seed, n in [(0, 8), (1, 13), (3, 24), (5, 20), (7, 31), (9, 40)]:\n"
+        "    w = W.random_scene(seed, n)\n"
+        "    t = Oracle(w).build_tables(); g = sg.Grid(w)\n"
+        "    assert np.array_equal(g.view('bg').cpu().numpy().view(np.uint32), t.bg), (seed, n)\n"
+        "    assert np.array_equal(g.view('nb').cpu().numpy().view(np.uint32), t.nb), (seed, n)\n"
+        "w = W.Workload('aniso', (45, 19, 14), 0.05, lower=(-0.3, 0.1, -0.2), prims=(W.Prim(W.TORUS_Z, (0.25, 0.32, 0.15, 0.25, 0.08)),))\n"
+        "t = Oracle(w).build_tables(); g = sg.Grid(w)\n"
+        "assert np.array_equal(g.view('bg').cpu().numpy().view(np.uint32), t.bg)\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, SG_TAG_CULL="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
