@@ -16,6 +16,7 @@
 // 16-lane group and broadcast with warp shuffles.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -145,15 +146,11 @@ __device__ __forceinline__ double godunov(double p, double xm, double xp, double
 // lanes of the 8-lane group and broadcast with shuffles (Lst. 2 with shifts
 // -1 -> (offset 0, data 3) and 4 -> (offset 2, data 0)).
 template <class T>
-__global__ void __launch_bounds__(256) k_reinit(const T* __restrict__ in, T* __restrict__ out,
-                                                const uint32_t* __restrict__ nb, uint32_t lo,
-                                                uint32_t hi, StC<T> c) {
-    const uint32_t pkg = lo + ((blockIdx.x * 256u + threadIdx.x) >> 3);
-    const bool valid = pkg < hi;
+__device__ __forceinline__ void reinit_pkg(const T* __restrict__ in, T* __restrict__ out,
+                                           uint32_t pkg, bool valid, uint32_t f,
+                                           const StC<T>& c) {
     const int g8 = threadIdx.x & 7;
     const int j = g8 & 3, k = g8 >> 2;
-    uint32_t f = 0;
-    if (valid && g8 < 6) f = __ldg(nb + (size_t)pkg * 27 + face_slot(g8));
     const int base = threadIdx.x & 24;
     const uint32_t nxm = __shfl_sync(0xffffffffu, f, base + 0);
     const uint32_t nxp = __shfl_sync(0xffffffffu, f, base + 1);
@@ -189,6 +186,30 @@ __global__ void __launch_bounds__(256) k_reinit(const T* __restrict__ in, T* __r
     T* O = out + (size_t)pkg * 64;
     st_row(O + 4 * r0, o0);
     st_row(O + 4 * r1, o1);
+}
+
+// Persistent grid: an 8-lane group sweeps packages pkg, pkg + G, ...; the
+// face ids of the next package are loaded while the current one is
+// processed, so the face-row gathers do not wait on the neighbour table.
+template <class T>
+__global__ void __launch_bounds__(256) k_reinit(const T* __restrict__ in, T* __restrict__ out,
+                                                const uint32_t* __restrict__ nb, uint32_t lo,
+                                                uint32_t hi, StC<T> c) {
+    const uint32_t G = gridDim.x * 32u;  // package groups in flight
+    uint32_t pkg = lo + ((blockIdx.x * 256u + threadIdx.x) >> 3);
+    const int g8 = threadIdx.x & 7;
+    // warp-uniform trip count: the warp's 4 groups have consecutive ids
+    const uint32_t wfirst = lo + ((blockIdx.x * 256u + (threadIdx.x & ~31u)) >> 3);
+    uint32_t f = 0;
+    if (pkg < hi && g8 < 6) f = __ldg(nb + (size_t)pkg * 27 + face_slot(g8));
+    for (uint32_t w0 = wfirst; w0 < hi; w0 += G) {
+        const uint32_t nxt = pkg + G;
+        uint32_t fn = 0;
+        if (nxt < hi && g8 < 6) fn = __ldg(nb + (size_t)nxt * 27 + face_slot(g8));
+        reinit_pkg(in, out, pkg, pkg < hi, f, c);
+        pkg = nxt;
+        f = fn;
+    }
 }
 
 // K6 -- gradient by Lst. 5 with the arithmetic-mean regulariser, divided by
@@ -557,7 +578,16 @@ static void reinit_launch(sg_grid* g, int cur, const StC<T>& c, cudaStream_t s) 
     if (hi <= lo) return;
     // (programmatic dependent launch of the next sweep was measured slower:
     // 21.9 vs 17.7 us per sweep on C2)
-    const unsigned blocks = (unsigned)ceil_div((hi - lo) * 8, 256);
+    static int resident = 0;
+    if (!resident) {
+        int dev = 0, sms = 0, per = 0;
+        SG_CUDA(cudaGetDevice(&dev));
+        SG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reinit<T>, 256, 0));
+        resident = std::max(1, sms * per);
+    }
+    const unsigned blocks =
+        (unsigned)std::min<int64_t>(ceil_div((hi - lo) * 8, 256), (int64_t)resident);
     k_reinit<T><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], (T*)g->phi[1 - cur], g->nb,
                                        (uint32_t)lo, (uint32_t)hi, c);
 }
