@@ -145,12 +145,16 @@ __device__ __forceinline__ double godunov(double p, double xm, double xp, double
 // x-end values for 8 points.  The six face-neighbour ids are loaded by six
 // lanes of the 8-lane group and broadcast with shuffles (Lst. 2 with shifts
 // -1 -> (offset 0, data 3) and 4 -> (offset 2, data 0)).
+// The 7-point cross of the two x-rows (j, k) and (j, k + 2) of one package
 template <class T>
-__device__ __forceinline__ void reinit_pkg(const T* __restrict__ in, T* __restrict__ out,
-                                           uint32_t pkg, bool valid, uint32_t f,
-                                           const StC<T>& c) {
-    const int g8 = threadIdx.x & 7;
-    const int j = g8 & 3, k = g8 >> 2;
+struct Cross2 {
+    T c0[4], c1[4], zlo[4], zmid[4], zhi[4], ym0[4], yp0[4], ym1[4], yp1[4];
+    T xm0, xp0, xm1, xp1;
+};
+
+template <class T>
+__device__ __forceinline__ void load_cross2(const T* __restrict__ in, uint32_t pkg, bool valid,
+                                            uint32_t f, int j, int k, Cross2<T>& x) {
     const int base = threadIdx.x & 24;
     const uint32_t nxm = __shfl_sync(0xffffffffu, f, base + 0);
     const uint32_t nxp = __shfl_sync(0xffffffffu, f, base + 1);
@@ -160,44 +164,34 @@ __device__ __forceinline__ void reinit_pkg(const T* __restrict__ in, T* __restri
     const uint32_t nzp = __shfl_sync(0xffffffffu, f, base + 5);
     if (!valid) return;
     const T* P = in + (size_t)pkg * 64;
-    const int r0 = j + 4 * k, r1 = r0 + 8;  // rows (j, k) and (j, k + 2)
-    T c0[4], c1[4], zlo[4], zmid[4], zhi[4], ym0[4], yp0[4], ym1[4], yp1[4];
-    ld_row(P + 4 * r0, c0);
-    ld_row(P + 4 * r1, c1);
-    ld_row(P + 4 * (r0 + 4), zmid);
-    ld_row(k == 0 ? in + (size_t)nzm * 64 + 4 * (j + 12) : P + 4 * j, zlo);
-    ld_row(k == 0 ? P + 4 * (j + 12) : in + (size_t)nzp * 64 + 4 * j, zhi);
-    ld_row(j > 0 ? P + 4 * (r0 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * k), ym0);
-    ld_row(j < 3 ? P + 4 * (r0 + 1) : in + (size_t)nyp * 64 + 4 * (4 * k), yp0);
-    ld_row(j > 0 ? P + 4 * (r1 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * (k + 2)), ym1);
-    ld_row(j < 3 ? P + 4 * (r1 + 1) : in + (size_t)nyp * 64 + 4 * (4 * (k + 2)), yp1);
-    const T xm0 = __ldg(in + (size_t)nxm * 64 + 4 * r0 + 3);
-    const T xp0 = __ldg(in + (size_t)nxp * 64 + 4 * r0);
-    const T xm1 = __ldg(in + (size_t)nxm * 64 + 4 * r1 + 3);
-    const T xp1 = __ldg(in + (size_t)nxp * 64 + 4 * r1);
-    T o0[4], o1[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        o0[i] = godunov(c0[i], i > 0 ? c0[i - 1] : xm0, i < 3 ? c0[i + 1] : xp0, ym0[i], yp0[i],
-                        zlo[i], zmid[i], c);
-        o1[i] = godunov(c1[i], i > 0 ? c1[i - 1] : xm1, i < 3 ? c1[i + 1] : xp1, ym1[i], yp1[i],
-                        zmid[i], zhi[i], c);
-    }
-    T* O = out + (size_t)pkg * 64;
-    st_row(O + 4 * r0, o0);
-    st_row(O + 4 * r1, o1);
+    const int r0 = j + 4 * k, r1 = r0 + 8;
+    ld_row(P + 4 * r0, x.c0);
+    ld_row(P + 4 * r1, x.c1);
+    ld_row(P + 4 * (r0 + 4), x.zmid);
+    ld_row(k == 0 ? in + (size_t)nzm * 64 + 4 * (j + 12) : P + 4 * j, x.zlo);
+    ld_row(k == 0 ? P + 4 * (j + 12) : in + (size_t)nzp * 64 + 4 * j, x.zhi);
+    ld_row(j > 0 ? P + 4 * (r0 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * k), x.ym0);
+    ld_row(j < 3 ? P + 4 * (r0 + 1) : in + (size_t)nyp * 64 + 4 * (4 * k), x.yp0);
+    ld_row(j > 0 ? P + 4 * (r1 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * (k + 2)), x.ym1);
+    ld_row(j < 3 ? P + 4 * (r1 + 1) : in + (size_t)nyp * 64 + 4 * (4 * (k + 2)), x.yp1);
+    x.xm0 = __ldg(in + (size_t)nxm * 64 + 4 * r0 + 3);
+    x.xp0 = __ldg(in + (size_t)nxp * 64 + 4 * r0);
+    x.xm1 = __ldg(in + (size_t)nxm * 64 + 4 * r1 + 3);
+    x.xp1 = __ldg(in + (size_t)nxp * 64 + 4 * r1);
 }
 
-// Persistent grid: an 8-lane group sweeps packages pkg, pkg + G, ...; the
-// face ids of the next package are loaded while the current one is
+// Persistent package sweep: an 8-lane group takes packages pkg, pkg + G, ...;
+// the face ids of the next package are loaded while the current one is
 // processed, so the face-row gathers do not wait on the neighbour table.
-template <class T>
-__global__ void __launch_bounds__(256) k_reinit(const T* __restrict__ in, T* __restrict__ out,
-                                                const uint32_t* __restrict__ nb, uint32_t lo,
-                                                uint32_t hi, StC<T> c) {
+// Op(x, pkg, r0, r1) consumes the cross of rows r0 = j + 4k and r1 = r0 + 8.
+template <class T, class Op>
+__global__ void __launch_bounds__(256) k_sweep(const T* __restrict__ in,
+                                               const uint32_t* __restrict__ nb, uint32_t lo,
+                                               uint32_t hi, Op op) {
     const uint32_t G = gridDim.x * 32u;  // package groups in flight
     uint32_t pkg = lo + ((blockIdx.x * 256u + threadIdx.x) >> 3);
     const int g8 = threadIdx.x & 7;
+    const int j = g8 & 3, k = g8 >> 2;
     // warp-uniform trip count: the warp's 4 groups have consecutive ids
     const uint32_t wfirst = lo + ((blockIdx.x * 256u + (threadIdx.x & ~31u)) >> 3);
     uint32_t f = 0;
@@ -206,10 +200,45 @@ __global__ void __launch_bounds__(256) k_reinit(const T* __restrict__ in, T* __r
         const uint32_t nxt = pkg + G;
         uint32_t fn = 0;
         if (nxt < hi && g8 < 6) fn = __ldg(nb + (size_t)nxt * 27 + face_slot(g8));
-        reinit_pkg(in, out, pkg, pkg < hi, f, c);
+        Cross2<T> x;
+        const bool valid = pkg < hi;
+        load_cross2(in, pkg, valid, f, j, k, x);
+        if (valid) op(x, pkg, j + 4 * k, j + 4 * k + 8);
         pkg = nxt;
         f = fn;
     }
+}
+
+// K5 -- one Jacobi Godunov sweep (O7, reading R-12)
+template <class T>
+struct ReinitOp {
+    T* out;
+    StC<T> c;
+    __device__ __forceinline__ void operator()(const Cross2<T>& x, uint32_t pkg, int r0,
+                                               int r1) const {
+        T o0[4], o1[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            o0[i] = godunov(x.c0[i], i > 0 ? x.c0[i - 1] : x.xm0, i < 3 ? x.c0[i + 1] : x.xp0,
+                            x.ym0[i], x.yp0[i], x.zlo[i], x.zmid[i], c);
+            o1[i] = godunov(x.c1[i], i > 0 ? x.c1[i - 1] : x.xm1, i < 3 ? x.c1[i + 1] : x.xp1,
+                            x.ym1[i], x.yp1[i], x.zmid[i], x.zhi[i], c);
+        }
+        T* O = out + (size_t)pkg * 64;
+        st_row(O + 4 * r0, o0);
+        st_row(O + 4 * r1, o1);
+    }
+};
+
+// grid size of a persistent sweep: resident blocks, at most the work
+template <class K>
+static unsigned persistent_blocks(K kernel, int64_t packages) {
+    int dev = 0, sms = 0, per = 0;
+    SG_CUDA(cudaGetDevice(&dev));
+    SG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 256, 0));
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(packages * 8, 256),
+                                                            (int64_t)sms * std::max(per, 1)));
 }
 
 // K6 -- gradient by Lst. 5 with the arithmetic-mean regulariser, divided by
@@ -576,20 +605,12 @@ template <class T>
 static void reinit_launch(sg_grid* g, int cur, const StC<T>& c, cudaStream_t s) {
     const int64_t lo = g->own_lo, hi = g->own_hi;
     if (hi <= lo) return;
-    // (programmatic dependent launch of the next sweep was measured slower:
-    // 21.9 vs 17.7 us per sweep on C2)
-    static int resident = 0;
-    if (!resident) {
-        int dev = 0, sms = 0, per = 0;
-        SG_CUDA(cudaGetDevice(&dev));
-        SG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reinit<T>, 256, 0));
-        resident = std::max(1, sms * per);
-    }
-    const unsigned blocks =
-        (unsigned)std::min<int64_t>(ceil_div((hi - lo) * 8, 256), (int64_t)resident);
-    k_reinit<T><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], (T*)g->phi[1 - cur], g->nb,
-                                       (uint32_t)lo, (uint32_t)hi, c);
+    const ReinitOp<T> op{(T*)g->phi[1 - cur], c};
+    static unsigned blocks_max = 0;  // resident blocks (per instantiation)
+    if (!blocks_max) blocks_max = persistent_blocks(k_sweep<T, ReinitOp<T>>, 1 << 30);
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div((hi - lo) * 8, 256), blocks_max);
+    k_sweep<T, ReinitOp<T>><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], g->nb, (uint32_t)lo,
+                                                   (uint32_t)hi, op);
 }
 
 // Multi-sweep reinit runs as one CUDA graph of `iters` kernel nodes.  The
@@ -729,6 +750,8 @@ static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t
         T* gp = (fields & SG_GRAD) ? (T*)g->grad : nullptr;
         T* np = (fields & SG_NORMAL) ? (T*)g->normal : nullptr;
         if (hi > lo) {
+            // (a persistent 8-lane variant like the reinit sweep measured
+            // slower here: the kernel is bound by its 1.8 KB/package of writes)
             const unsigned blocks = (unsigned)ceil_div((hi - lo) * 16, 256);
             k_gradient<T><<<blocks, 256, 0, s>>>(phi, gp, np, g->nb, lo, hi, c);
             SG_LAUNCHED();
