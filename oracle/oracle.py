@@ -76,6 +76,7 @@ def lib():
         L.or_probe.restype = C.c_int64
         L.or_probe.argtypes = [P, P, C.c_int32, P, P, P, C.c_int64, P, P, P]
         L.or_gather_packages.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_double, P]
+        L.or_table1_dense.argtypes = [P, P, C.c_int32, P, P, C.c_int32, C.c_double, P]
         L.or_set_threads.argtypes = [C.c_int32]
         L.or_get_threads.restype = C.c_int32
         _lib = L
@@ -248,6 +249,14 @@ class Oracle:
         oob = lib().or_probe(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
                              _ptr(g3), n, _ptr(pos), _ptr(out_phi), _ptr(out_grad))
         return out_phi, out_grad, int(oob)
+
+    # Table 1 workloads: op 0 sequential (phi + value), op 1 stencil
+    def table1(self, phi: np.ndarray, op: int, value: float = 0.0) -> np.ndarray:
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        out = np.empty_like(phi)
+        lib().or_table1_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
+                              int(op), float(value), _ptr(out))
+        return out
 
     # layout helper: dense plane -> package-major using the oracle's meta
     def to_packages(self, dense: np.ndarray, far_neg: float, far_pos: float) -> np.ndarray:

@@ -34,6 +34,7 @@
  *                     that use the far constant: parity unpinned
  *   or_kernel_dense   pinned: S closed forms, S/2 at planar interface, sum gw=0
  *   or_probe          pinned: affine reproduction, data-point identity, far/OOB
+ *   or_table1_dense   pinned: Laplacian of x^2+y^2+z^2 = 6, of affine = 0
  */
 #include <math.h>
 #include <stdint.h>
@@ -591,6 +592,36 @@ void or_kernel_dense(const or_grid* g, const or_prim* prims, int32_t n_prims, co
                     for (int a = 0; a < 3; ++a) G[a * plane + I] = gacc[a];
             }
     free(t);
+}
+
+/* ---------------------------------------------------------- Table 1 --- */
+/* The paper's access-pattern benchmark (Table 1):
+ *   "sequential": a minor change to every active value -- phi + value;
+ *   "stencil": the seven-point Laplacian at every active data point,
+ *              (sum of the 6 axis neighbours - 6 phi) / dx^2.
+ * Inactive points: the input value (sequential) / 0 (stencil). */
+void or_table1_dense(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
+                     const double* phi, int32_t op, double value, double* out) {
+    dense_ctx d;
+    dense_init(&d, g, prims, n_prims, bg);
+    const double dx = data_spacing(g);
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t iz = 0; iz < d.m[2]; ++iz)
+        for (int64_t iy = 0; iy < d.m[1]; ++iy)
+            for (int64_t ix = 0; ix < d.m[0]; ++ix) {
+                int64_t I = ix + d.m[0] * (iy + d.m[1] * iz);
+                int act = point_active(&d, ix, iy, iz);
+                if (op == 0) {
+                    out[I] = act ? phi[I] + value : phi[I];
+                } else if (!act) {
+                    out[I] = 0.0;
+                } else {
+                    double s6 = ((dense_get(&d, phi, ix - 1, iy, iz) + dense_get(&d, phi, ix + 1, iy, iz)) +
+                                 (dense_get(&d, phi, ix, iy - 1, iz) + dense_get(&d, phi, ix, iy + 1, iz))) +
+                                (dense_get(&d, phi, ix, iy, iz - 1) + dense_get(&d, phi, ix, iy, iz + 1));
+                    out[I] = (s6 - 6.0 * phi[I]) / (dx * dx);
+                }
+            }
 }
 
 /* ---------------------------------------------------------------- O10 -- */

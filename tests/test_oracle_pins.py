@@ -583,3 +583,28 @@ def test_splitmix64_reference_values():
     assert int(out[0]) == 0xE220A8397B1DCDAF
     assert int(out[1]) == 0x6E789E6AA1B965F4
     assert int(out[2]) == 0x06C45D188009454F
+
+
+def test_table1_laplacian_closed_forms(oracle_lib):
+    """7-point Laplacian: exactly 6 for x^2+y^2+z^2 at points whose
+    six neighbours are band points, 0 for an affine field; the
+    sequential op adds the value at active points only."""
+    w = W.config("C1")
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    m = 4 * w.n[0]
+    I = (np.arange(m) + 0.5) * w.dx
+    Z, Y, X = np.meshgrid(I, I, I, indexing="ij")
+    cb = np.repeat(np.repeat(np.repeat(t.bg.reshape(w.n[::-1]) >= 2, 4, 0), 4, 1), 4, 2)
+    inner = cb.copy()
+    for ax in range(3):
+        inner &= np.roll(cb, 1, ax) & np.roll(cb, -1, ax)
+    lap = o.table1(X**2 + Y**2 + Z**2, 1)
+    assert inner.sum() > 1000
+    assert np.max(np.abs(lap[inner] - 6.0)) < 1e-9
+    assert np.all(lap[~cb] == 0)
+    lap = o.table1(0.3 * X - 0.2 * Y + 0.7 * Z, 1)
+    assert np.max(np.abs(lap[inner])) < 1e-9
+    q = X.copy()
+    out = o.table1(q, 0, 1.0)
+    assert np.array_equal(out[cb], q[cb] + 1.0) and np.array_equal(out[~cb], q[~cb])
