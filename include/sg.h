@@ -223,9 +223,39 @@ sg_status sg_probe(const sg_grid* grid, int64_t n, const void* pos, void* phi, v
 /* Table-1 workloads of the paper, on the current phi:
  *   op 0 "sequential": phi += value at every active data point (in place);
  *   op 1 "stencil": out = 7-point Laplacian of phi at every active data point
- *        ((sum of 6 neighbours - 6 phi) / dx^2; singular packages 0),
- *        written to the SG_VIEW_PHI_NEXT buffer (phi is unchanged). */
+ *        ((sum of 6 neighbours - 6 phi) / dx^2), written to the active
+ *        packages of the SG_VIEW_PHI_NEXT buffer (phi is unchanged; the
+ *        singular packages of that buffer keep the far constants). */
 sg_status sg_table1(sg_grid* grid, int32_t op, double value, void* stream);
+
+/* SPH particle relaxation against the level set (NEXT-2; "the
+ * integral field is interpolated by bi- or tri-linear interpolation to the
+ * particle's position and used in the form of surface force to drive the
+ * particle"; force law and bounding are reading R-21):
+ *   a_i  = -2 ( sum_{j != i} V grad W(x_i - x_j) - G(x_i) ),  V = dp^3,
+ *          Wendland C2 with h = h_ratio dp (pairs from a cell-linked list),
+ *          G = the kernel-gradient integral field interpolated trilinearly;
+ *   dx_i = step dp^2 a_i, its length clamped to max_disp dp;
+ *   bounding: with phi, grad phi probed at the moved position, a particle with
+ *          phi > -surface_offset dp moves by -(phi + surface_offset dp) n,
+ *          n = grad phi / |grad phi|.
+ * One call performs `steps` Jacobi steps (positions double-buffered).  pos is
+ * a device array n x 3 of the grid dtype, updated in place; particles outside
+ * the stored domain are left unchanged.  Requires sg_gradient with SG_GRAD and
+ * SG_KINT (SG_ERR_STATE otherwise).  Pair sums within a cell follow an atomic
+ * binning order: results are reproducible to rounding, not bit for bit. */
+typedef struct {
+    double dp;             /* particle spacing (> 0)                         */
+    double h_ratio;        /* h / dp of the pair kernel, in [0.5, 2]          */
+    double step;           /* dimensionless step (displacement = step dp^2 a) */
+    double max_disp;       /* clamp of the displacement, in units of dp       */
+    double surface_offset; /* bounding offset, in units of dp                 */
+    int32_t steps;         /* >= 0                                            */
+    int32_t pad;
+} sg_relax_params;
+
+sg_status sg_relax(sg_grid* grid, int64_t n, void* pos, const sg_relax_params* params,
+                   void* stream);
 
 sg_status sg_info(const sg_grid* grid, sg_info_t* info);
 sg_status sg_view(const sg_grid* grid, int32_t what, sg_view_t* view);

@@ -77,6 +77,8 @@ def lib():
         L.or_probe.argtypes = [P, P, C.c_int32, P, P, P, C.c_int64, P, P, P]
         L.or_gather_packages.argtypes = [P, P, P, C.c_int64, C.c_double, C.c_double, P]
         L.or_table1_dense.argtypes = [P, P, C.c_int32, P, P, C.c_int32, C.c_double, P]
+        L.or_relax.argtypes = [P, P, C.c_int32, P, P, P, P, C.c_int64, P, C.c_double,
+                               C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32]
         L.or_set_threads.argtypes = [C.c_int32]
         L.or_get_threads.restype = C.c_int32
         _lib = L
@@ -257,6 +259,18 @@ class Oracle:
         lib().or_table1_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
                               int(op), float(value), _ptr(out))
         return out
+
+    # NEXT-2 particle relaxation (reading R-21); pos (n, 3) float64, updated copy
+    def relax(self, phi, grad, G, pos, dp, h_ratio=1.3, step=0.1, max_disp=0.2,
+              surface_offset=0.5, steps=1):
+        pos = np.ascontiguousarray(np.asarray(pos, dtype=np.float64).reshape(-1, 3)).copy()
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        grad = np.ascontiguousarray(grad, dtype=np.float64)
+        G = np.ascontiguousarray(G, dtype=np.float64)
+        lib().or_relax(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi), _ptr(grad),
+                       _ptr(G), pos.shape[0], _ptr(pos), dp, h_ratio, step, max_disp,
+                       surface_offset, int(steps))
+        return pos
 
     # layout helper: dense plane -> package-major using the oracle's meta
     def to_packages(self, dense: np.ndarray, far_neg: float, far_pos: float) -> np.ndarray:

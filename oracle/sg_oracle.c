@@ -694,6 +694,120 @@ int64_t or_probe(const or_grid* g, const or_prim* prims, int32_t n_prims, const 
     return oob;
 }
 
+/* ------------------------------------------------------------ NEXT-2 --- */
+/* SPH particle relaxation against the level set (force law and
+ * bounding: reading R-21 = SPEC S:535-543 with the kernel-gradient integral G
+ * as the surface force).  Per step, for every particle i inside the domain:
+ *   S_i = sum_{j != i, |x_i - x_j| < 2h} V W'(|r|) r / |r|,   r = x_i - x_j,
+ *   a_i = -2 (S_i - G(x_i)),   d_i = step dp^2 a_i, |d_i| clamped to max_d dp,
+ *   x_i' = x_i + d_i;  then with (phi, grad phi) interpolated at x_i':
+ *   if phi > -off dp: x_i' -= (phi + off dp) grad phi / |grad phi|.
+ * All pairs are enumerated (brute force, small n).  Fields are the dense
+ * phi, grad (3 planes) and G (3 planes) of the grid. */
+static void interp_dense(const dense_ctx* d, const double* f3, int ncomp, int64_t plane,
+                         const double x[3], double* out) {
+    const or_grid* g = d->g;
+    const double dx = data_spacing(g);
+    int64_t a[3];
+    double t[3];
+    for (int k = 0; k < 3; ++k) {
+        double u = (x[k] - g->lower[k]) / dx - 0.5;
+        double fl = floor(u);
+        a[k] = (int64_t)fl;
+        t[k] = u - fl;
+    }
+    for (int c = 0; c < ncomp; ++c) out[c] = 0.0;
+    for (int b = 0; b < 8; ++b) {
+        int b0 = b & 1, b1 = (b >> 1) & 1, b2 = (b >> 2) & 1;
+        double w = ((b0 ? t[0] : 1.0 - t[0]) * (b1 ? t[1] : 1.0 - t[1])) * (b2 ? t[2] : 1.0 - t[2]);
+        int64_t ix = a[0] + b0, iy = a[1] + b1, iz = a[2] + b2;
+        int in = ix >= 0 && iy >= 0 && iz >= 0 && ix < d->m[0] && iy < d->m[1] && iz < d->m[2];
+        for (int c = 0; c < ncomp; ++c) {
+            double v;
+            if (ncomp == 1 && c == 0) v = dense_get(d, f3, ix, iy, iz);
+            else v = in ? f3[c * plane + ix + d->m[0] * (iy + d->m[1] * iz)] : 0.0;
+            out[c] += w * v;
+        }
+    }
+}
+
+static int in_domain_pos(const or_grid* g, const double x[3], int64_t c[3]) {
+    for (int k = 0; k < 3; ++k) {
+        double upper = g->lower[k] + (double)g->n[k] * g->cell;
+        if (!(x[k] >= g->lower[k] && x[k] < upper)) return 0;
+        c[k] = (int64_t)floor((x[k] - g->lower[k]) / g->cell);
+        if (c[k] > g->n[k] - 1) c[k] = g->n[k] - 1;
+    }
+    return 1;
+}
+
+void or_relax(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
+              const double* phi, const double* grad3, const double* G3, int64_t n, double* pos,
+              double dp, double h_ratio, double step, double max_disp, double off, int32_t steps) {
+    dense_ctx d;
+    dense_init(&d, g, prims, n_prims, bg);
+    const int64_t plane = d.m[0] * d.m[1] * d.m[2];
+    const double PI = 3.14159265358979323846;
+    const double h = h_ratio * dp;
+    const double sigma = 21.0 / (16.0 * PI * h * h * h);
+    const double V = dp * dp * dp;
+    double* moved = (double*)malloc(sizeof(double) * 3 * (size_t)n);
+    for (int it = 0; it < steps; ++it) {
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t i = 0; i < n; ++i) {
+            const double* xi = pos + 3 * i;
+            int64_t c[3];
+            for (int k = 0; k < 3; ++k) moved[3 * i + k] = xi[k];
+            if (!in_domain_pos(g, xi, c)) continue;
+            double S[3] = {0.0, 0.0, 0.0};
+            for (int64_t j = 0; j < n; ++j) {
+                if (j == i) continue;
+                int64_t cj[3];
+                if (!in_domain_pos(g, pos + 3 * j, cj)) continue;
+                double r[3] = {xi[0] - pos[3 * j], xi[1] - pos[3 * j + 1], xi[2] - pos[3 * j + 2]};
+                double rr = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+                if (!(rr > 0.0 && rr < 2.0 * h)) continue;
+                double q = rr / h, a = 1.0 - 0.5 * q;
+                double dW = -5.0 * sigma * q * a * a * a / h; /* W'(r) */
+                for (int k = 0; k < 3; ++k) S[k] += V * dW * r[k] / rr;
+            }
+            double Gi[3] = {0.0, 0.0, 0.0};
+            if (bg[lin_cell(g, c[0], c[1], c[2])] >= 2) interp_dense(&d, G3, 3, plane, xi, Gi);
+            double dv[3], len = 0.0;
+            for (int k = 0; k < 3; ++k) {
+                dv[k] = step * dp * dp * (-2.0 * (S[k] - Gi[k]));
+                len += dv[k] * dv[k];
+            }
+            len = sqrt(len);
+            double mx = max_disp * dp;
+            double sc = len > mx ? mx / len : 1.0;
+            for (int k = 0; k < 3; ++k) moved[3 * i + k] = xi[k] + dv[k] * sc;
+        }
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i) {
+            double* x = moved + 3 * i;
+            int64_t c[3];
+            if (in_domain_pos(g, x, c)) {
+                uint32_t b = bg[lin_cell(g, c[0], c[1], c[2])];
+                double ph, gv[3] = {0.0, 0.0, 0.0};
+                if (b >= 2) {
+                    interp_dense(&d, phi, 1, plane, x, &ph);
+                    interp_dense(&d, grad3, 3, plane, x, gv);
+                } else {
+                    ph = b == 0 ? -d.far : d.far;
+                }
+                if (ph > -off * dp) {
+                    double m = sqrt(gv[0] * gv[0] + gv[1] * gv[1] + gv[2] * gv[2]);
+                    if (m > 0.0)
+                        for (int k = 0; k < 3; ++k) x[k] -= (ph + off * dp) * gv[k] / m;
+                }
+            }
+            for (int k = 0; k < 3; ++k) pos[3 * i + k] = x[k];
+        }
+    }
+    free(moved);
+}
+
 /* ------------------------------------------------------- layout helper -- */
 /* Gather a dense scalar plane into package-major order using the oracle's
  * own meta table: out[id][i + 4 j + 16 k] = dense[4c + (i,j,k)] (R-9

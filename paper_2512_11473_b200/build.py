@@ -31,6 +31,7 @@ UNITS = {
     # removes the denormal paths around MUFU.RSQ
     "sg_stencil.cu": ["-ftz=true"],
     "sg_probe.cu": ["-ftz=true"],
+    "sg_relax.cu": [],
 }
 
 

@@ -26,7 +26,8 @@ _STATUS = {0: "SG_OK", 1: "SG_ERR_ARG", 2: "SG_ERR_OOM", 3: "SG_ERR_CUDA", 4: "S
            5: "SG_ERR_STATE", 6: "SG_ERR_DOMAIN"}
 
 # exported symbols declared in include/sg.h (checked by the CPU test suite)
-EXPORTS = ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_info", "sg_view",
+EXPORTS = ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax", "sg_info",
+           "sg_view",
            "sg_destroy", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
            "sg_last_error", "sg_abi_version", "sg_launch_count")
 
@@ -53,6 +54,12 @@ class sg_desc(C.Structure):
 
 class sg_slab(C.Structure):
     _fields_ = [("z_lo", C.c_int32), ("z_hi", C.c_int32), ("id_base", C.c_int64)]
+
+
+class sg_relax_params(C.Structure):
+    _fields_ = [("dp", C.c_double), ("h_ratio", C.c_double), ("step", C.c_double),
+                ("max_disp", C.c_double), ("surface_offset", C.c_double), ("steps", C.c_int32),
+                ("pad", C.c_int32)]
 
 
 class sg_view_t(C.Structure):
@@ -91,6 +98,7 @@ def lib():
         L.sg_gradient.argtypes = [P, C.c_uint32, D, P]
         L.sg_probe.argtypes = [P, I64, P, P, P, P, P]
         L.sg_table1.argtypes = [P, I32, D, P]
+        L.sg_relax.argtypes = [P, I64, P, C.POINTER(sg_relax_params), P]
         L.sg_info.argtypes = [P, C.POINTER(sg_info_t)]
         L.sg_view.argtypes = [P, I32, C.POINTER(sg_view_t)]
         L.sg_destroy.argtypes = [P]
@@ -101,7 +109,8 @@ def lib():
         L.sg_last_error.restype = C.c_char_p
         L.sg_abi_version.restype = I32
         L.sg_launch_count.restype = C.c_uint64
-        for name in ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_info",
+        for name in ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
+                     "sg_info",
                      "sg_view", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts"):
             getattr(L, name).restype = C.c_int
         _lib = L
@@ -174,6 +183,14 @@ def sg_probe(grid: int, n: int, pos_ptr: int, phi_ptr: int, grad_ptr: int | None
 
 def sg_table1(grid: int, op: int, value: float = 1.0, stream=None) -> None:
     _check(lib().sg_table1(C.c_void_p(grid), int(op), float(value), _stream(stream)))
+
+
+def sg_relax(grid: int, n: int, pos_ptr: int, dp: float, h_ratio: float = 1.3,
+             step: float = 0.1, max_disp: float = 0.2, surface_offset: float = 0.5,
+             steps: int = 1, stream=None) -> None:
+    p = sg_relax_params(dp, h_ratio, step, max_disp, surface_offset, int(steps), 0)
+    _check(lib().sg_relax(C.c_void_p(grid), int(n), C.c_void_p(pos_ptr), C.byref(p),
+                          _stream(stream)))
 
 
 def sg_info(grid: int) -> dict:
@@ -288,6 +305,13 @@ class Grid:
                  grad.data_ptr() if grad is not None else None,
                  oob.data_ptr() if oob is not None else None, stream)
         return phi, grad
+
+    def relax(self, pos, dp: float, steps: int = 1, h_ratio: float = 1.3, step: float = 0.1,
+              max_disp: float = 0.2, surface_offset: float = 0.5, stream=None):
+        """SPH relaxation steps (NEXT-2) of a device tensor (n, 3), in place."""
+        sg_relax(self.handle, int(pos.shape[0]), pos.data_ptr(), dp, h_ratio, step, max_disp,
+                 surface_offset, steps, stream)
+        return pos
 
     def view(self, name: str):
         return view_tensor(self.handle, name)

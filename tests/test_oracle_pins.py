@@ -608,3 +608,70 @@ def test_table1_laplacian_closed_forms(oracle_lib):
     q = X.copy()
     out = o.table1(q, 0, 1.0)
     assert np.array_equal(out[cb], q[cb] + 1.0) and np.array_equal(out[~cb], q[~cb])
+
+
+# ------------------------------------------------- NEXT-2: relaxation ------
+
+def _relax_world():
+    # a big box: deep inside, phi < -off and G = 0; near the +x face phi is planar
+    return W.Workload("rbox", (16, 16, 16), 1 / 16, dtype="f64",
+                      prims=(W.Prim(W.BOX, (0.5, 0.5, 0.5, 0.3, 0.3, 0.3)),))
+
+
+def _fields(o):
+    phi = o.phi_dense()
+    grad, _ = o.gradient(phi)
+    K, G = o.kernel_integrals(phi, 1.3)
+    return phi, grad, G
+
+
+def test_relax_single_particle_at_rest(oracle_lib):
+    """A lone particle deep inside: no neighbours, G = 0 there, phi < -off:
+    it does not move."""
+    w = _relax_world()
+    o = oracle_lib.Oracle(w)
+    o.build_tables()
+    phi, grad, G = _fields(o)
+    p = np.array([[0.5, 0.5, 0.5]])
+    out = o.relax(phi, grad, G, p, dp=w.dx, steps=3)
+    assert np.array_equal(out, p)
+
+
+def test_relax_pair_moves_apart_symmetrically(oracle_lib):
+    """Two particles 0.5 dp apart deep inside repel along their axis with
+    opposite, equal displacements; the centre of mass is invariant (S:542,
+    S:556)."""
+    w = _relax_world()
+    o = oracle_lib.Oracle(w)
+    o.build_tables()
+    phi, grad, G = _fields(o)
+    dp = w.dx
+    p = np.array([[0.5 - 0.25 * dp, 0.5, 0.5], [0.5 + 0.25 * dp, 0.5, 0.5]])
+    out = o.relax(phi, grad, G, p, dp=dp, step=0.01, steps=1)
+    d = out - p
+    assert d[0, 0] < 0 < d[1, 0]
+    assert abs(d[0, 0] + d[1, 0]) < 1e-15 and np.all(d[:, 1:] == 0)
+    assert abs(out[:, 0].mean() - 0.5) < 1e-15
+    # magnitude from the Wendland C2 derivative at r = 0.5 dp, h = 1.3 dp
+    h = 1.3 * dp
+    q = 0.5 / 1.3
+    sigma = 21 / (16 * math.pi * h**3)
+    dW = -5 * sigma * q * (1 - q / 2) ** 3 / h
+    expect = min(0.01 * dp * dp * 2 * dp**3 * abs(dW), 0.2 * dp)
+    assert abs(d[1, 0] - expect) < 1e-12 * dp
+
+
+def test_relax_bounding_projects_to_offset_level(oracle_lib):
+    """step = 0 isolates the bounding rule: a particle with phi > -off dp on
+    the planar part of the box (phi = x - 0.8) lands exactly on
+    phi = -off dp; particles deeper inside stay."""
+    w = _relax_world()
+    o = oracle_lib.Oracle(w)
+    o.build_tables()
+    phi, grad, G = _fields(o)
+    dp = w.dx
+    p = np.array([[0.8 + 0.3 * dp, 0.5, 0.5], [0.8 - 0.2 * dp, 0.45, 0.52], [0.7, 0.5, 0.5]])
+    out = o.relax(phi, grad, G, p, dp=dp, step=0.0, surface_offset=0.5, steps=1)
+    assert abs(out[0, 0] - (0.8 - 0.5 * dp)) < 1e-12 and abs(out[1, 0] - (0.8 - 0.5 * dp)) < 1e-12
+    assert np.all(out[:2, 1:] == p[:2, 1:])
+    assert np.array_equal(out[2], p[2])

@@ -432,3 +432,53 @@ def test_tables_with_forced_tag_cull(O):
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+# -------------------------------------------------- NEXT-2: relaxation ----
+
+def _relax_setup(sgm, O, w, iters=2):
+    o = O.Oracle(w)
+    o.build_tables()
+    phi = o.reinit(o.phi_dense(), iters).astype(np_dtype(w)).astype(np.float64)
+    g = sgm.Grid(w)
+    _upload(g, w, o.to_packages(phi, -o.far, o.far))
+    g.gradient(sgm.SG_GRAD | sgm.SG_KINT, w.h_ratio)
+    grad, _ = o.gradient(phi)
+    _, G = o.kernel_integrals(phi, w.h_ratio)
+    # the GPU stores grad / G in dtype: the oracle interpolates the same values
+    dt = np_dtype(w)
+    return o, g, phi, grad.astype(dt).astype(np.float64), G.astype(dt).astype(np.float64)
+
+
+def test_relax_c1_fp64(sgm, O):
+    """Three relaxation steps of the C1 lattice particles (dp = dx) against the
+    brute-force oracle (reading R-21)."""
+    w = W.config("C1")
+    o, g, phi, grad, G = _relax_setup(sgm, O, w)
+    pos = W.lattice_particles(w, dtype=np.float64)
+    exp = o.relax(phi, grad, G, pos, dp=w.dx, steps=3)
+    t = torch.from_numpy(pos.copy()).cuda()
+    g.relax(t, dp=w.dx, steps=3)
+    got = t.cpu().numpy()
+    assert np.max(np.abs(got - exp)) <= 1e-10 * w.dx
+    moved = np.linalg.norm(got - pos, axis=1)
+    assert moved.max() > 0.01 * w.dx  # it does something
+    # containment after bounding (S:543): no particle left above -off
+    gp, _ = g.probe(torch.from_numpy(got).cuda(), want_grad=False)
+    assert float(gp.max()) <= -0.5 * w.dx + 1e-12
+
+
+def test_relax_c2_subset_fp32(sgm, O):
+    """fp32: a 20k-particle subset of C4 near the prism's edge and top face."""
+    w = W.config("C2")
+    o, g, phi, grad, G = _relax_setup(sgm, O, w)
+    pos = W.lattice_particles(w, seed=0)
+    sel = (np.abs(pos[:, 0] - 0.5) < 0.03) & (np.abs(pos[:, 1] - 0.3) < 0.03) & (pos[:, 2] > 0.8)
+    pos = np.ascontiguousarray(pos[sel][:20000])
+    assert pos.shape[0] > 2000
+    exp = o.relax(phi, grad, G, pos.astype(np.float64), dp=w.dx, steps=1)
+    t = torch.from_numpy(pos.copy()).cuda()
+    g.relax(t, dp=w.dx, steps=1)
+    got = t.cpu().numpy().astype(np.float64)
+    tol = 4 * np.spacing(np.float32(1.0)) + 1e-5 * w.dx
+    assert np.max(np.abs(got - exp)) <= tol
