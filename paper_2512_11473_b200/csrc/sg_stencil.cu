@@ -362,6 +362,16 @@ __device__ __forceinline__ double heav(double u, double eps, double inv_eps) {
     return 0.5 * (1.0 + q + sinpi(q) * 0.318309886183790672);
 }
 
+// the smoothed Heaviside as selects: both outer branches are exact 0 / 1
+__device__ __forceinline__ float heav_sel(float u, float eps, float inv_eps) {
+    const float q = u * inv_eps;
+    const float sm = 0.5f * (1.f + q + __sinf(3.14159265358979f * q) * 0.318309886183790672f);
+    return u < -eps ? 0.f : (u > eps ? 1.f : sm);
+}
+__device__ __forceinline__ double heav_sel(double u, double eps, double inv_eps) {
+    return heav(u, eps, inv_eps);
+}
+
 template <class T>
 struct KintC {
     T wt[16];     // Wt[s], s = |o|^2
@@ -437,19 +447,10 @@ __global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
 #pragma unroll
                     for (int q = RS; q < RSX; ++q) v[q] = T(0);
                 }
-                // H(-phi): a row with no value inside the smoothing band
-                // |phi| <= eps is a pure select (no sine)
-                bool band = false;
-#pragma unroll
-                for (int q = 0; q < RS; ++q) band = band || (fabs(v[q]) <= c.eps);
+                // H(-phi), branch-free (selects around the smooth part)
                 T h[RSX];
-                if (!band) {
 #pragma unroll
-                    for (int q = 0; q < RSX; ++q) h[q] = v[q] < T(0) ? T(1) : T(0);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < RSX; ++q) h[q] = heav(-v[q], c.eps, c.inv_eps);
-                }
+                for (int q = 0; q < RSX; ++q) h[q] = heav_sel(-v[q], c.eps, c.inv_eps);
 #pragma unroll
                 for (int q = 0; q < RS; ++q) {
                     all1 = all1 && (h[q] == T(1));
