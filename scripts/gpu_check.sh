@@ -18,12 +18,12 @@ fi
 if [[ $what == all || $what == c3 ]]; then
   timeout 900 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
   timeout 900 python bench.py --config C5 --steps 5 --warmup 2 --no-cpu-baseline > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_reinit|k_gradient|k_kint' -s 26 -c 3 -o gpurun_out/prof_c3 python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_c3.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep|k_reinit|k_gradient|k_kint' -s 26 -c 3 -o gpurun_out/prof_c3 python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_c3.log 2>&1
 fi
 if [[ $what == all || $what == ncu ]]; then
   B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_reinit -s 25 -c 1 -o gpurun_out/prof_reinit $B > gpurun_out/ncu_reinit.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_reinit|k_sweep' -s 25 -c 1 -o gpurun_out/prof_reinit $B > gpurun_out/ncu_reinit.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gradient|k_kint|k_probe|k_phi_init|k_count|k_tag|k_nb' -s 7 -c 7 -o gpurun_out/prof_other $B > gpurun_out/ncu_other.log 2>&1
 fi
 ls -la gpurun_out > gpurun_out/ls.txt
