@@ -297,10 +297,10 @@ def run_ours(args, rank, world, local):
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
         "wall_s": t_wall,
-        "roofline": {"kernel": "k_reinit<float>", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": "k_sweep<float, ReinitOp<float>> (reinit sweep)", "bound": "hbm", "achieved": achieved,
                      "peak": hbm, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "bytes_per_cell": bytes_per_cell, "cells_per_launch": n_act,
-                     "traffic": ncu_traffic("k_reinit", w.name),
+                     "traffic": ncu_traffic("k_sweep", w.name),
                      "note": (f"working set per sweep {alg_bytes / 1e6:.0f} MB "
                               + ("< 126 MB L2: L2-resident across the sweeps" if alg_bytes < 126e6
                                  else "> 126 MB L2: streamed from HBM"))},
