@@ -571,6 +571,14 @@ static void launch_tag(const GridC& gc, const Geom& geom, int32_t zt_lo, int32_t
     SG_LAUNCHED();
 }
 
+// pinned host landing buffer of the build's package-count read-back (one
+// per host thread)
+static int64_t* pinned_counts() {
+    static thread_local int64_t* p = nullptr;
+    if (!p) SG_CUDA(cudaHostAlloc((void**)&p, 4 * sizeof(int64_t), cudaHostAllocDefault));
+    return p;
+}
+
 // library-internal side stream (one per process, non-blocking)
 static cudaStream_t side_stream() {
     static cudaStream_t st = nullptr;
@@ -630,28 +638,34 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         // of a stored boundary plane needs the core flags beyond it)
         const int32_t W = (int32_t)ceil_div(gc.n[0], 32);
         const int64_t tag_words = (int64_t)W * gc.n[1] * (zt_hi - zt_lo);
-        uint32_t* core_w = (uint32_t*)dalloc(sizeof(uint32_t) * 2 * tag_words, s);
-        uint32_t* neg_w = core_w + tag_words;
-        launch_tag(gc, g->geom, zt_lo, zt_hi, W, core_w, neg_w, s);
-        const Bits bits{core_w, neg_w, W, zt_lo};
-
         const int64_t nwords = (int64_t)W * gc.n[1] * (gc.zs_hi - gc.zs_lo);
         const int64_t n_tiles = ceil_div(nwords, kTB);
-        uint32_t* act_w = (uint32_t*)dalloc(sizeof(uint32_t) * nwords, s);
-        int32_t* tile_count = (int32_t*)dalloc(sizeof(int32_t) * n_tiles, s);
-        int64_t* tile_off = (int64_t*)dalloc(sizeof(int64_t) * (n_tiles + 1), s);
-        unsigned long long* d_core = (unsigned long long*)dalloc(2 * sizeof(unsigned long long), s);
+        // one scratch block: tag words | active words | tile counts | tile
+        // offsets + [core count, boundary flag] (contiguous: one D2H copy)
+        auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+        const size_t sz_tag = al(sizeof(uint32_t) * 2 * tag_words),
+                     sz_act = al(sizeof(uint32_t) * nwords), sz_cnt = al(sizeof(int32_t) * n_tiles),
+                     sz_off = al(sizeof(int64_t) * (n_tiles + 3));
+        char* scratch = (char*)dalloc(sz_tag + sz_act + sz_cnt + sz_off, s);
+        uint32_t* core_w = (uint32_t*)scratch;
+        uint32_t* neg_w = core_w + tag_words;
+        uint32_t* act_w = (uint32_t*)(scratch + sz_tag);
+        int32_t* tile_count = (int32_t*)(scratch + sz_tag + sz_act);
+        int64_t* tile_off = (int64_t*)(scratch + sz_tag + sz_act + sz_cnt);
+        unsigned long long* d_core = (unsigned long long*)(tile_off + n_tiles + 1);
         SG_CUDA(cudaMemsetAsync(d_core, 0, 2 * sizeof(unsigned long long), s));
+        launch_tag(gc, g->geom, zt_lo, zt_hi, W, core_w, neg_w, s);
+        const Bits bits{core_w, neg_w, W, zt_lo};
         k_count<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, bits, nwords, act_w, tile_count, d_core);
         SG_LAUNCHED();
         k_scan<<<1, 1024, 0, s>>>(tile_count, n_tiles, tile_off);
         SG_LAUNCHED();
 
-        // the single host synchronisation: package count (and core count)
-        int64_t counts[3];
-        SG_CUDA(cudaMemcpyAsync(&counts[0], tile_off + n_tiles, sizeof(int64_t),
+        // the single host synchronisation: package count, core count and the
+        // domain-boundary flag in one 24 B copy into pinned memory
+        int64_t* counts = pinned_counts();
+        SG_CUDA(cudaMemcpyAsync(counts, tile_off + n_tiles, 3 * sizeof(int64_t),
                                 cudaMemcpyDeviceToHost, s));
-        SG_CUDA(cudaMemcpyAsync(&counts[1], d_core, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         SG_CUDA(cudaStreamSynchronize(s));
         const int64_t n_active = counts[0];
         SG_ARG(n_active + 2 < 4294967295LL, "sg_build: more than 2^32-3 packages");
@@ -663,7 +677,6 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         // one arena for every array of the grid (a single stream-ordered
         // allocation right after the host sync keeps the device busy)
         const int32_t planes = gc.zs_hi - gc.zs_lo;
-        auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
         const size_t sz_bg = al(sizeof(uint32_t) * ncs), sz_mc = al(sizeof(uint32_t) * n_pkg),
                      sz_mk = al((size_t)n_pkg), sz_nb = al(sizeof(uint32_t) * 27 * n_pkg),
                      sz_pf = al(sizeof(int64_t) * (planes + 1)),
@@ -701,9 +714,11 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         // K3 (integer / L2 gathers) on a side stream concurrently with K4
         // (fp64 ALU): they only share read-only inputs
         cudaStream_t side = side_stream();
-        cudaEvent_t ev_fork, ev_join;
-        SG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-        SG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+        if (!ev_fork) {
+            SG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+            SG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        }
         SG_CUDA(cudaEventRecord(ev_fork, s));
         SG_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
         const unsigned nbb = (unsigned)ceil_div(ceil_div(n_pkg, kNbPW) * 32, 256);
@@ -722,8 +737,6 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
                                                  (float*)g->phi[0], (float*)g->phi[1]);
         SG_LAUNCHED();
         SG_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
-        SG_CUDA(cudaEventDestroy(ev_fork));
-        SG_CUDA(cudaEventDestroy(ev_join));
         g->cur = 0;
 
         // owned id range: whole domain -> [2, n_pkg); slab -> plane ranges
@@ -739,12 +752,9 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
             g->own_hi = pf[gc.z_hi - gc.zs_lo];
         }
 
-        SG_CUDA(cudaFreeAsync(core_w, s));
-        SG_CUDA(cudaFreeAsync(act_w, s));
+        SG_CUDA(cudaFreeAsync(scratch, s));
         if (d_geom) SG_CUDA(cudaFreeAsync(d_geom, s));
-        SG_CUDA(cudaFreeAsync(tile_count, s));
-        SG_CUDA(cudaFreeAsync(tile_off, s));
-        SG_CUDA(cudaFreeAsync(d_core, s));
+
         *out = g.release();
     });
 }

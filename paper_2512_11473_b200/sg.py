@@ -262,12 +262,27 @@ def view_tensor(grid: int, name: str):
     return torch.as_tensor(_CAI(v.ptr, shape, _TYPESTR[v.dtype]), device="cuda")
 
 
+_DESC_CACHE: dict = {}
+
+
+def _cached_desc(w):
+    """make_desc memoised per (hashable) workload: rebuilding a grid every
+    step does not re-marshal the descriptor."""
+    try:
+        hit = _DESC_CACHE.get(w)
+    except TypeError:  # unhashable workload-like object
+        return make_desc(w)
+    if hit is None:
+        hit = _DESC_CACHE[w] = make_desc(w)
+    return hit
+
+
 class Grid:
     """Owning handle around sg_build/sg_destroy with torch-friendly calls."""
 
     def __init__(self, w, slab: tuple | None = None, stream=None):
         self.w = w
-        self.desc, self.geom, self._keep = make_desc(w)
+        self.desc, self.geom, self._keep = _cached_desc(w)
         sl = None
         if slab is not None:
             sl = sg_slab(int(slab[0]), int(slab[1]), int(slab[2]))
