@@ -52,7 +52,7 @@ __device__ __forceinline__ double qdiv(const GridC& gc, double v, bool cell) {
 template <>
 __device__ __forceinline__ bool cell_of<float>(const GridC& gc, int k, float x, int& c) {
     if (gc.idx32) {
-        c = min((int)floorf(x * gc.inv_cellf), gc.n[k] - 1);
+        c = min(__float2int_rd(x * gc.inv_cellf), gc.n[k] - 1);
         return x >= 0.f && x < gc.upperf[k];  // NaN fails both
     }
     const double xd = (double)x;
@@ -101,10 +101,10 @@ __device__ __forceinline__ void corner_of<double>(const GridC& gc, int k, double
 constexpr int kPW = 128;  // particles per warp chunk
 
 template <class T>
-struct ProbeSmem {
+struct __align__(16) ProbeSmem {
     static constexpr int kWB = sizeof(T) == 4 ? 8 : 4;  // warps per block
-    T xs[kWB][3 * kPW];  // staged positions
-    T io[kWB][4 * kPW];  // results: phi (128) + grad (384)
+    __align__(16) T xs[kWB][3 * kPW];  // staged positions
+    __align__(16) T io[kWB][4 * kPW];  // results: phi (128) + grad (384)
     uint32_t pk[kWB][kPW];  // band list: containing package
     uint8_t who[kWB][kPW];  // band list: particle slot in the chunk
 };
@@ -117,7 +117,7 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
                                                const T* __restrict__ pg, int64_t n,
                                                const T* __restrict__ pos, T* __restrict__ out_phi,
                                                T* __restrict__ out_grad,
-                                               unsigned long long* __restrict__ oob) {
+                                               unsigned long long* __restrict__ oob, bool vec) {
     __shared__ ProbeSmem<T> S;
     constexpr int kWB = ProbeSmem<T>::kWB;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -128,10 +128,24 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
     // persistent warps: the positions of the next chunk are loaded while the
     // current chunk is processed (hides the DRAM latency of the stream)
     T v[12];
+    // 16 B vector staging / write-back for fp32 full chunks when the caller's
+    // buffers are 16 B aligned (chunk offsets are multiples of 512 B)
+    bool vnext = false;
     auto load_chunk = [&](int64_t ch) {
         const int64_t b0 = ch * kPW;
         const int mm = (int)min((int64_t)kPW, n - b0);
         const T* src = pos + 3 * b0;
+        vnext = sizeof(T) == 4 && vec && mm == kPW;
+        if constexpr (sizeof(T) == 4) {
+            if (vnext) {
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    const float4 a = __ldg(reinterpret_cast<const float4*>(src) + lane + 32 * u);
+                    v[4 * u] = a.x; v[4 * u + 1] = a.y; v[4 * u + 2] = a.z; v[4 * u + 3] = a.w;
+                }
+                return;
+            }
+        }
 #pragma unroll
         for (int u = 0; u < 12; ++u) {
             const int q = lane + 32 * u;
@@ -143,8 +157,26 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
     const int64_t base = chunk * kPW;
     const int m = (int)min((int64_t)kPW, n - base);
     T* xs = S.xs[w];
+    const bool vcur = vnext;
+    if constexpr (sizeof(T) == 4) {
+        if (vcur) {
 #pragma unroll
-    for (int u = 0; u < 12; ++u) xs[lane + 32 * u] = v[u];
+            for (int u = 0; u < 3; ++u)
+                reinterpret_cast<float4*>(xs)[lane + 32 * u] =
+                    make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+            // grad staging starts at zero (far-field / OOB particles keep it)
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+                reinterpret_cast<float4*>(io + kPW)[lane + 32 * u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    if (!vcur) {
+#pragma unroll
+        for (int u = 0; u < 12; ++u) {
+            xs[lane + 32 * u] = v[u];
+            io[kPW + lane + 32 * u] = T(0);
+        }
+    }
     if (chunk + stride < nchunks) load_chunk(chunk + stride);
     __syncwarp();
     T x[4][3];  // positions in the grid dtype; promoted to double where used
@@ -182,7 +214,6 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
             S.who[w][idx] = (uint8_t)p;
         } else if (inr) {
             io[p] = (T)(!ok[j] ? gc.far : (b[j] == 0 ? -gc.far : gc.far));
-            io[kPW + 3 * p] = io[kPW + 3 * p + 1] = io[kPW + 3 * p + 2] = T(0);
         }
         nband += __popc(bal);
     }
@@ -250,16 +281,31 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
     }
     __syncwarp();
     // coalesced results
+    bool done = false;
+    if constexpr (sizeof(T) == 4) {
+        if (vcur) {
+            reinterpret_cast<float4*>(out_phi + base)[lane] = reinterpret_cast<const float4*>(io)[lane];
+            if (out_grad) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int p = lane + 32 * j;
-        if (p < m) out_phi[base + p] = io[p];
+                for (int u = 0; u < 3; ++u)
+                    reinterpret_cast<float4*>(out_grad + 3 * base)[lane + 32 * u] =
+                        reinterpret_cast<const float4*>(io + kPW)[lane + 32 * u];
+            }
+            done = true;
+        }
     }
-    if (out_grad) {
+    if (!done) {
 #pragma unroll
-        for (int u = 0; u < 12; ++u) {
-            const int q = lane + 32 * u;
-            if (q < 3 * m) out_grad[3 * base + q] = io[kPW + q];
+        for (int j = 0; j < 4; ++j) {
+            const int p = lane + 32 * j;
+            if (p < m) out_phi[base + p] = io[p];
+        }
+        if (out_grad) {
+#pragma unroll
+            for (int u = 0; u < 12; ++u) {
+                const int q = lane + 32 * u;
+                if (q < 3 * m) out_grad[3 * base + q] = io[kPW + q];
+            }
         }
     }
     __syncwarp();  // io is restaged by the next chunk
@@ -284,7 +330,8 @@ static void probe_dev(const sg_grid* g, int64_t n, const void* pos, void* out_ph
     const int64_t blocks = std::min<int64_t>(ceil_div(n, kPW * kWB), rb);
     k_probe<T><<<(unsigned)blocks, 32 * kWB, 0, s>>>(
         g->gc, g->bg, g->nb, (const T*)g->phi[g->cur], grad, n, (const T*)pos, (T*)out_phi,
-        (T*)out_grad, oob);
+        (T*)out_grad, oob,
+        ((uintptr_t)pos | (uintptr_t)out_phi | (uintptr_t)(out_grad ? out_grad : out_phi)) % 16 == 0);
     SG_LAUNCHED();
 }
 

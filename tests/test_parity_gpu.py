@@ -484,3 +484,21 @@ def test_relax_c2_subset_fp32(sgm, O):
     got = t.cpu().numpy().astype(np.float64)
     tol = 4 * np.spacing(np.float32(1.0)) + 1e-5 * w.dx
     assert np.max(np.abs(got - exp)) <= tol
+
+
+def test_probe_unaligned_buffers(sgm, O):
+    """Buffers that are not 16 B aligned take the scalar staging path: the
+    results equal those of an aligned copy bit for bit."""
+    w = W.config("C2")
+    g = sgm.Grid(w)
+    g.reinit(2).gradient(sgm.SG_GRAD)
+    pos = torch.from_numpy(W.lattice_particles(w, seed=3)[:300001]).cuda()
+    big = torch.empty((pos.shape[0] + 1, 3), dtype=pos.dtype, device="cuda")
+    big[1:] = pos
+    un = big[1:]  # 12 B offset
+    assert un.data_ptr() % 16 != 0
+    a_phi, a_grad = g.probe(pos)
+    b_phi = torch.empty(pos.shape[0] + 1, dtype=pos.dtype, device="cuda")[1:]
+    b_grad = torch.empty((pos.shape[0] + 1, 3), dtype=pos.dtype, device="cuda")[1:]
+    sgm.sg_probe(g.handle, pos.shape[0], un.data_ptr(), b_phi.data_ptr(), b_grad.data_ptr())
+    assert torch.equal(a_phi, b_phi) and torch.equal(a_grad, b_grad)
