@@ -35,3 +35,8 @@ fi
 if [[ $what == prof ]]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_probe|k_kint|k_gradient|k_phi_init|k_nb|k_tag" -s 6 -c 6 -o gpurun_out/prof_b python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_b.log 2>&1
 fi
+if [[ $what == diag3 ]]; then
+  timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+  SG_TAG_CULL=0 timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_nocull.json 2> gpurun_out/bench_c3_nocull.err
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python bench.py --config C3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_c3.log 2>&1
+fi
