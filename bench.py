@@ -113,6 +113,10 @@ class ClockSampler:
             get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
             self._reasons = get
+            # the first NVML queries of a process can be slow and hold driver
+            # locks: take one sample before the timed region starts
+            self._sample()
+            self.sm.clear()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
@@ -122,15 +126,19 @@ class ClockSampler:
     def _run(self):
         nv = self.nv
         while not self._stop.is_set():
-            try:
-                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = self._reasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit:
-                        self.reasons.add(name)
-            except Exception:
-                pass
+            self._sample()
             time.sleep(self.period)
+
+    def _sample(self):
+        nv = self.nv
+        try:
+            self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            r = self._reasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+        except Exception:
+            pass
 
     def __exit__(self, *a):
         self._stop.set()
@@ -293,6 +301,7 @@ def run_ours(args, rank, world, local):
                    "parallelism": f"zslab{world}" if world > 1 else "1 GPU"},
         "probes_per_s": n_part / (ms * 1e-3),
         "stages": stages,
+        "step_ms_min_max": [float(step_ms.min()), float(step_ms.max())],
         "e2e": e2e,
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,

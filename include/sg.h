@@ -71,7 +71,14 @@ typedef enum { SG_F32 = 0, SG_F64 = 1 } sg_dtype;
  *   SG_BOX         cx cy cz bx by bz        (half extents)
  *   SG_TORUS_X/Y/Z cx cy cz R r             (symmetry axis x / y / z)
  *   SG_TRIPRISM_Z  ax ay bx by cx cy z0 z1  (triangle ccw in xy, extruded in z)
- * The union of several primitives is their pointwise min, in order.  The
+ *   SG_LEAK        cx cy cz r margin        (sign-error region, see below)
+ * The union of several primitives is their pointwise min, in order.
+ * SG_LEAK entries are not part of the union: they model the sign errors of a
+ * triangle-mesh SDF on leaky input as a post-operation on the
+ * union value f: f <- -f wherever the point lies strictly inside one of the
+ * leak balls ((x-c).(x-c) < r*r, evaluated as ((ex*ex + ey*ey) + ez*ez))
+ * and |f| >= margin.  The magnitude is untouched; the build (tagging, table,
+ * initial phi) sees the leaky f.  At least one non-leak primitive is needed.  The
  * fp64 evaluation order is fixed and compiled without FMA
  * contraction so that the tagging decision is reproducible bit for bit. */
 typedef enum {
@@ -81,7 +88,8 @@ typedef enum {
     SG_TORUS_X = 3,
     SG_TORUS_Y = 4,
     SG_TORUS_Z = 5,
-    SG_TRIPRISM_Z = 6
+    SG_TRIPRISM_Z = 6,
+    SG_LEAK = 7
 } sg_prim_kind;
 
 typedef struct {
@@ -142,7 +150,13 @@ enum {
     SG_VIEW_KINT = 7,        /* T   [n_pkg][64]           K                         */
     SG_VIEW_GKINT = 8,       /* T   [n_pkg][3][64]        G = grad K                */
     SG_VIEW_PLANE_FIRST = 9, /* i64 [stored planes + 1]   first package id per plane */
-    SG_VIEW_PHI_NEXT = 10    /* T   [n_pkg][64]           reinit scratch buffer     */
+    SG_VIEW_PHI_NEXT = 10,   /* T   [n_pkg][64]           reinit scratch buffer     */
+    /* per-cell bitmasks of the tagging pass, kept for the sign correction:
+     * u32 [tag planes][n1][ceil(n0 / 32)], bit x % 32 of word x / 32 is cell
+     * x of that row; tag planes = stored planes plus one on each side that
+     * lies in the domain (sg_info zs_lo/zs_hi widened by one, clipped) */
+    SG_VIEW_CELL_CORE = 11,  /* |f(centre)| < l_c                                 */
+    SG_VIEW_CELL_NEG = 12    /* f(centre) < 0 (after sg_sign_correct: corrected)  */
 };
 
 typedef struct {
@@ -256,6 +270,37 @@ typedef struct {
 
 sg_status sg_relax(sg_grid* grid, int64_t n, void* pos, const sg_relax_params* params,
                    void* stream);
+
+/* Sign-consistency correction (NEXT-3; "only the sign of level
+ * set for those data points very close to the surface is directly used,
+ * those at other locations are obtained by a two-step diffusion process from
+ * the near interface to the entire domain.  The first coarse step is on the
+ * mesh cells and the second refined one is on the data packages"; reading
+ * R-22).  Both steps are synchronous (Jacobi) sweeps of one majority rule:
+ * an unsigned site with at least one signed face neighbour takes the sign
+ * held by more of its signed face neighbours (a tie leaves it unsigned for
+ * that sweep); a step ends at the first sweep that signs nothing.
+ *   coarse: sites = background cells of the domain (6 face neighbours inside
+ *     the domain).  Core cells keep the sign of f at their centre; all other
+ *     cells start unsigned.  Afterwards the table entry of every inactive
+ *     cell (0/1) and every singular entry of the neighbour table that refers
+ *     to an in-domain cell are rewritten from the corrected cell signs
+ *     (entries for out-of-domain neighbours, R-6, are kept); cells never
+ *     reached keep their sign.
+ *   refined: sites = data points of the active packages (6 face neighbours,
+ *     across package faces through the neighbour table; a neighbour point in
+ *     a singular package is signed: package 0 negative, 1 positive).  Points
+ *     with |phi| < tau (compared in the grid dtype) keep their sign; all
+ *     other active points start unsigned.  Finally phi <- -|phi| / +|phi| at
+ *     every signed point; points never reached keep phi.
+ * tau > 0 (typically dx).  max_sweeps > 0 caps each step, <= 0 means no cap.
+ * sweeps (host int32[2], may be NULL) receives the number of sweeps of the
+ * coarse and the refined step that signed at least one site.  Operates on
+ * the current phi buffer in place and clears has_grad/has_normal/has_kint.
+ * Single-domain grids only (SG_ERR_ARG for a slab grid).  The host
+ * synchronises with `stream` once per batch of sweeps (convergence test). */
+sg_status sg_sign_correct(sg_grid* grid, double tau, int32_t max_sweeps, int32_t* sweeps,
+                          void* stream);
 
 sg_status sg_info(const sg_grid* grid, sg_info_t* info);
 sg_status sg_view(const sg_grid* grid, int32_t what, sg_view_t* view);

@@ -79,6 +79,8 @@ def lib():
         L.or_table1_dense.argtypes = [P, P, C.c_int32, P, P, C.c_int32, C.c_double, P]
         L.or_relax.argtypes = [P, P, C.c_int32, P, P, P, P, C.c_int64, P, C.c_double,
                                C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32]
+        L.or_sign_correct.argtypes = [P, P, C.c_int32, P, P, P, C.c_int64, P, P, P,
+                                      C.c_double, C.c_int32, P]
         L.or_set_threads.argtypes = [C.c_int32]
         L.or_get_threads.restype = C.c_int32
         _lib = L
@@ -273,6 +275,24 @@ class Oracle:
         return pos
 
     # layout helper: dense plane -> package-major using the oracle's meta
+    def sign_correct(self, phi: np.ndarray, tau: float | None = None, max_sweeps: int = 0):
+        """NEXT-3 sign-consistency correction (R-22) on copies of this oracle's
+        tables and of the dense phi.  Returns (bg, nb, cell_neg u8[ncell],
+        phi, (coarse_sweeps, refined_sweeps)).  For an fp32 comparison pass
+        phi and tau already rounded to float32 (the trust decision is then
+        taken in the kernel's precision)."""
+        t = self.tables if self.tables is not None else self.build_tables()
+        bg = t.bg.copy()
+        nb = np.ascontiguousarray(t.nb.copy())
+        cell_neg = np.empty(t.cat.size, np.uint8)
+        out = np.ascontiguousarray(np.array(phi, dtype=np.float64, copy=True))
+        tau = self.dx if tau is None else float(tau)
+        sw = (C.c_int32 * 2)()
+        lib().or_sign_correct(self.g, self.prims, self.n_prims, _ptr(t.cat), _ptr(bg),
+                              _ptr(t.meta_cell), t.n_pkg, _ptr(nb), _ptr(cell_neg), _ptr(out),
+                              tau, int(max_sweeps), sw)
+        return bg, nb, cell_neg, out, (int(sw[0]), int(sw[1]))
+
     def to_packages(self, dense: np.ndarray, far_neg: float, far_pos: float) -> np.ndarray:
         t = self.tables if self.tables is not None else self.build_tables()
         dense = np.ascontiguousarray(dense, dtype=np.float64)

@@ -35,6 +35,11 @@
  *   or_kernel_dense   pinned: S closed forms, S/2 at planar interface, sum gw=0
  *   or_probe          pinned: affine reproduction, data-point identity, far/OOB
  *   or_table1_dense   pinned: Laplacian of x^2+y^2+z^2 = 6, of affine = 0
+ *   or_sdf leak post-op / or_sign_correct
+ *                     pinned: on leaky spheres / tori the corrected signs equal
+ *                     the closed-form containment sign at every data point and
+ *                     cell, magnitudes are unchanged, a watertight input is a
+ *                     fixed point, hand-computed 1-D flood and tie examples
  */
 #include <math.h>
 #include <stdint.h>
@@ -54,7 +59,8 @@ enum {
     OR_TORUS_X = 3,    /* p = cx cy cz R r, symmetry axis x      */
     OR_TORUS_Y = 4,    /* p = cx cy cz R r, symmetry axis y      */
     OR_TORUS_Z = 5,    /* p = cx cy cz R r, symmetry axis z      */
-    OR_TRIPRISM_Z = 6  /* p = ax ay bx by cx cy z0 z1 (ccw in xy) */
+    OR_TRIPRISM_Z = 6, /* p = ax ay bx by cx cy z0 z1 (ccw in xy) */
+    OR_LEAK = 7        /* p = cx cy cz r margin: sign-error ball   */
 };
 
 typedef struct {
@@ -144,14 +150,27 @@ static double sdf_prim(const or_prim* q, const double x[3]) {
     }
 }
 
-/* union = min over primitives, in order */
+/* union = min over the primitives, in order; then the leak post-operation
+ * (include/sg.h SG_LEAK; models the wrong signs of a triangle-mesh SDF on
+ * leaky input): f -> -f strictly inside any leak ball where
+ * |f| >= margin. */
 double or_sdf(const or_prim* prims, int32_t n_prims, const double x[3]) {
     double f = INFINITY;
+    int first = 1;
     for (int i = 0; i < n_prims; ++i) {
+        if (prims[i].kind == OR_LEAK) continue;
         double g = sdf_prim(&prims[i], x);
-        f = (i == 0) ? g : fmin(f, g);
+        f = first ? g : fmin(f, g);
+        first = 0;
     }
-    return f;
+    int flip = 0;
+    for (int i = 0; i < n_prims; ++i) {
+        if (prims[i].kind != OR_LEAK) continue;
+        const double* l = prims[i].p;
+        double ex = x[0] - l[0], ey = x[1] - l[1], ez = x[2] - l[2];
+        if ((ex * ex + ey * ey) + ez * ez < l[3] * l[3] && fabs(f) >= l[4]) flip = 1;
+    }
+    return flip ? -f : f;
 }
 
 void or_sdf_batch(const or_prim* prims, int32_t n_prims, int64_t n, const double* x,
@@ -809,6 +828,180 @@ void or_relax(const or_grid* g, const or_prim* prims, int32_t n_prims, const uin
 }
 
 /* ------------------------------------------------------- layout helper -- */
+/* ---------------------------------------------------------- NEXT-3 -- */
+/* Sign-consistency correction ("only the sign of level set for
+ * those data points very close to the surface is directly used, those at
+ * other locations are obtained by a two-step diffusion process from the near
+ * interface to the entire domain.  The first coarse step is on the mesh cells
+ * and the second refined one is on the data packages."), reading R-22:
+ *
+ * Rule (both steps): synchronous sweeps; an unsigned site with at least one
+ * signed face neighbour takes the sign held by more of its signed face
+ * neighbours, a tie leaves it unsigned in that sweep; a step ends at the
+ * first sweep that signs nothing (or after max_sweeps > 0 sweeps).
+ *
+ * Coarse step: sites = background cells, face neighbours inside the domain.
+ * Core cells (cat 3) are signed by f at their centre, all others unsigned.
+ * Then every inactive cell's table entry becomes 0 (negative) / 1, and every
+ * singular neighbour-table entry of an in-domain cell is re-read from the
+ * table.  cell_neg (optional, ncell bytes) receives the final cell signs
+ * (cells never reached keep the sign of f at their centre).
+ *
+ * Refined step: sites = data points of active cells on the dense grid.
+ * Points with |phi| < tau keep their sign; all other active points start
+ * unsigned.  A neighbour point in an inactive in-domain cell is signed by the
+ * table (0 negative); outside the domain by f at the virtual cell centre
+ * (R-6).  Finally phi = -|phi| or +|phi| at every signed active point.
+ * sweeps[0..1] = number of sweeps of each step that signed something. */
+void or_sign_correct(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint8_t* cat,
+                     uint32_t* bg, const uint32_t* meta_cell, int64_t n_pkg, uint32_t* nb,
+                     uint8_t* cell_neg, double* phi, double tau, int32_t max_sweeps,
+                     int32_t* sweeps) {
+    const int64_t nx = g->n[0], ny = g->n[1], nz = g->n[2];
+    const int64_t ncell = nx * ny * nz;
+    static const int off[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
+
+    /* coarse step on the cells */
+    uint8_t* known = (uint8_t*)malloc((size_t)ncell);
+    uint8_t* neg = (uint8_t*)malloc((size_t)ncell);
+    uint8_t* known2 = (uint8_t*)malloc((size_t)ncell);
+    uint8_t* neg2 = (uint8_t*)malloc((size_t)ncell);
+    for (int64_t cz = 0; cz < nz; ++cz)
+        for (int64_t cy = 0; cy < ny; ++cy)
+            for (int64_t cx = 0; cx < nx; ++cx) {
+                int64_t L = lin_cell(g, cx, cy, cz);
+                double x[3];
+                cell_centre(g, cx, cy, cz, x);
+                known[L] = cat[L] == 3;
+                neg[L] = or_sdf(prims, n_prims, x) < 0.0;
+            }
+    int32_t sw = 0;
+    for (;;) {
+        if (max_sweeps > 0 && sw >= max_sweeps) break;
+        int64_t signed_now = 0;
+        for (int64_t cz = 0; cz < nz; ++cz)
+            for (int64_t cy = 0; cy < ny; ++cy)
+                for (int64_t cx = 0; cx < nx; ++cx) {
+                    int64_t L = lin_cell(g, cx, cy, cz);
+                    known2[L] = known[L];
+                    neg2[L] = neg[L];
+                    if (known[L]) continue;
+                    int vn = 0, vp = 0;
+                    for (int d = 0; d < 6; ++d) {
+                        int64_t qx = cx + off[d][0], qy = cy + off[d][1], qz = cz + off[d][2];
+                        if (!in_domain(g, qx, qy, qz)) continue;
+                        int64_t Q = lin_cell(g, qx, qy, qz);
+                        if (!known[Q]) continue;
+                        if (neg[Q]) vn++;
+                        else vp++;
+                    }
+                    if (vn != vp) {
+                        known2[L] = 1;
+                        neg2[L] = vn > vp;
+                        signed_now++;
+                    }
+                }
+        if (signed_now == 0) break;
+        sw++;
+        memcpy(known, known2, (size_t)ncell);
+        memcpy(neg, neg2, (size_t)ncell);
+    }
+    sweeps[0] = sw;
+    for (int64_t L = 0; L < ncell; ++L)
+        if (bg[L] < 2) bg[L] = neg[L] ? 0u : 1u;
+    for (int64_t id = 2; id < n_pkg; ++id) {
+        int64_t L = meta_cell[id];
+        int64_t cx = L % nx, cy = (L / nx) % ny, cz = L / (nx * ny);
+        for (int s = 0; s < 27; ++s) {
+            int64_t qx = cx + s % 3 - 1, qy = cy + (s / 3) % 3 - 1, qz = cz + s / 9 - 1;
+            if (nb[id * 27 + s] < 2 && in_domain(g, qx, qy, qz))
+                nb[id * 27 + s] = bg[lin_cell(g, qx, qy, qz)];
+        }
+    }
+    if (cell_neg) memcpy(cell_neg, neg, (size_t)ncell);
+    free(known);
+    free(neg);
+    free(known2);
+    free(neg2);
+
+    /* refined step on the data points of active cells */
+    const int64_t mx = PKG * nx, my = PKG * ny, mz = PKG * nz;
+    const int64_t np = mx * my * mz;
+    known = (uint8_t*)calloc((size_t)np, 1);
+    neg = (uint8_t*)calloc((size_t)np, 1);
+    known2 = (uint8_t*)calloc((size_t)np, 1);
+    neg2 = (uint8_t*)calloc((size_t)np, 1);
+#define PIDX(ix, iy, iz) ((ix) + mx * ((iy) + my * (iz)))
+#define ACTIVE(ix, iy, iz) (bg[lin_cell(g, (ix) / PKG, (iy) / PKG, (iz) / PKG)] >= 2)
+    for (int64_t iz = 0; iz < mz; ++iz)
+        for (int64_t iy = 0; iy < my; ++iy)
+            for (int64_t ix = 0; ix < mx; ++ix) {
+                if (!ACTIVE(ix, iy, iz)) continue;
+                double v = phi[PIDX(ix, iy, iz)];
+                known[PIDX(ix, iy, iz)] = fabs(v) < tau;
+                neg[PIDX(ix, iy, iz)] = v < 0.0;
+            }
+    sw = 0;
+    for (;;) {
+        if (max_sweeps > 0 && sw >= max_sweeps) break;
+        int64_t signed_now = 0;
+        memcpy(known2, known, (size_t)np);
+        memcpy(neg2, neg, (size_t)np);
+        for (int64_t iz = 0; iz < mz; ++iz)
+            for (int64_t iy = 0; iy < my; ++iy)
+                for (int64_t ix = 0; ix < mx; ++ix) {
+                    int64_t I = PIDX(ix, iy, iz);
+                    if (!ACTIVE(ix, iy, iz) || known[I]) continue;
+                    int vn = 0, vp = 0;
+                    for (int d = 0; d < 6; ++d) {
+                        int64_t jx = ix + off[d][0], jy = iy + off[d][1], jz = iz + off[d][2];
+                        int kn, ng;
+                        if (jx < 0 || jy < 0 || jz < 0 || jx >= mx || jy >= my || jz >= mz) {
+                            kn = 1;
+                            ng = far_pkg_virtual(g, prims, n_prims, fdiv4(jx), fdiv4(jy),
+                                                 fdiv4(jz)) == 0;
+                        } else if (!ACTIVE(jx, jy, jz)) {
+                            kn = 1;
+                            ng = bg[lin_cell(g, jx / PKG, jy / PKG, jz / PKG)] == 0;
+                        } else {
+                            kn = known[PIDX(jx, jy, jz)];
+                            ng = neg[PIDX(jx, jy, jz)];
+                        }
+                        if (!kn) continue;
+                        if (ng) vn++;
+                        else vp++;
+                    }
+                    if (vn != vp) {
+                        known2[I] = 1;
+                        neg2[I] = vn > vp;
+                        signed_now++;
+                    }
+                }
+        if (signed_now == 0) break;
+        sw++;
+        memcpy(known, known2, (size_t)np);
+        memcpy(neg, neg2, (size_t)np);
+    }
+    sweeps[1] = sw;
+    for (int64_t iz = 0; iz < mz; ++iz)
+        for (int64_t iy = 0; iy < my; ++iy)
+            for (int64_t ix = 0; ix < mx; ++ix) {
+                int64_t I = PIDX(ix, iy, iz);
+                if (ACTIVE(ix, iy, iz)) {
+                    if (known[I]) phi[I] = neg[I] ? -fabs(phi[I]) : fabs(phi[I]);
+                } else { /* inactive point: far constant of the corrected cell sign */
+                    phi[I] = bg[lin_cell(g, ix / PKG, iy / PKG, iz / PKG)] == 0 ? -fabs(phi[I])
+                                                                               : fabs(phi[I]);
+                }
+            }
+#undef PIDX
+#undef ACTIVE
+    free(known);
+    free(neg);
+    free(known2);
+    free(neg2);
+}
+
 /* Gather a dense scalar plane into package-major order using the oracle's
  * own meta table: out[id][i + 4 j + 16 k] = dense[4c + (i,j,k)] (R-9
  * canonical order).  Singular packages take `far_neg` / `far_pos`. */

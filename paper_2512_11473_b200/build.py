@@ -32,6 +32,7 @@ UNITS = {
     "sg_stencil.cu": ["-ftz=true"],
     "sg_probe.cu": ["-ftz=true"],
     "sg_relax.cu": [],
+    "sg_sign.cu": [],
 }
 
 

@@ -80,11 +80,24 @@ __device__ __forceinline__ double sd_prim(int kind, const double* p, double x, d
     }
 }
 
+// SG_LEAK post-operation (include/sg.h): f <- -f strictly inside any leak
+// ball where |f| >= margin
+__device__ __forceinline__ double sd_leak(const Geom& g, double x, double y, double z,
+                                          double f) {
+    bool flip = false;
+    for (int i = 0; i < g.n_leak; ++i) {
+        const double* l = g.leak[i];
+        const double ex = x - l[0], ey = y - l[1], ez = z - l[2];
+        flip = flip || (((ex * ex + ey * ey) + ez * ez < l[3] * l[3]) && fabs(f) >= l[4]);
+    }
+    return flip ? -f : f;
+}
+
 // union of the primitives = pointwise min, in order
 __device__ __forceinline__ double sd_eval(const Geom& g, double x, double y, double z) {
     double f = sd_prim(g.kind[0], g.p[0], x, y, z);
     for (int i = 1; i < g.n; ++i) f = fmin(f, sd_prim(g.kind[i], g.p[i], x, y, z));
-    return f;
+    return g.n_leak ? sd_leak(g, x, y, z, f) : f;
 }
 
 // f at NZ points sharing (x, y): the terms of each primitive that depend on
@@ -180,6 +193,10 @@ __device__ __forceinline__ void sd_eval_col(const Geom& g, double x, double y,
 #pragma unroll
         for (int k = 0; k < NZ; ++k) f[k] = fmin(f[k], fi[k]);
     }
+    if (g.n_leak) {
+#pragma unroll
+        for (int k = 0; k < NZ; ++k) f[k] = sd_leak(g, x, y, z[k], f[k]);
+    }
 }
 
 // the same min over the primitives selected by `mask` (bit i = primitive i);
@@ -195,6 +212,10 @@ __device__ __forceinline__ void sd_eval_col_mask(const Geom& g, uint32_t mask, d
 #pragma unroll
         for (int k = 0; k < NZ; ++k) f[k] = first ? fi[k] : fmin(f[k], fi[k]);
         first = false;
+    }
+    if (g.n_leak) {
+#pragma unroll
+        for (int k = 0; k < NZ; ++k) f[k] = sd_leak(g, x, y, z[k], f[k]);
     }
 }
 

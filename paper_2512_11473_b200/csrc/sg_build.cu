@@ -535,17 +535,32 @@ static void check_desc(const sg_desc* d, const sg_geometry* g) {
     SG_ARG(d->init_scale >= 0.0 && d->far >= 0.0, "sg_build: negative init_scale or far");
     SG_ARG(g->prims != nullptr && g->n_prims >= 1 && g->n_prims <= SG_MAX_PRIMS,
            "sg_build: need 1..16 primitives");
-    for (int i = 0; i < g->n_prims; ++i)
-        SG_ARG(g->prims[i].kind >= SG_SPHERE && g->prims[i].kind <= SG_TRIPRISM_Z,
+    int n_union = 0;
+    for (int i = 0; i < g->n_prims; ++i) {
+        SG_ARG(g->prims[i].kind >= SG_SPHERE && g->prims[i].kind <= SG_LEAK,
                "sg_build: unknown primitive kind");
+        if (g->prims[i].kind == SG_LEAK) {
+            const double* l = g->prims[i].p;
+            SG_ARG(l[3] >= 0.0 && l[4] >= 0.0, "sg_build: leak radius and margin must be >= 0");
+        } else {
+            ++n_union;
+        }
+    }
+    SG_ARG(n_union >= 1, "sg_build: need at least one non-leak primitive");
 }
 
+// union primitives in their given order; SG_LEAK entries to the post-op list
 static Geom make_geom(const sg_geometry* g) {
     Geom ge{};
-    ge.n = g->n_prims;
     for (int i = 0; i < g->n_prims; ++i) {
-        ge.kind[i] = g->prims[i].kind;
-        for (int j = 0; j < 12; ++j) ge.p[i][j] = g->prims[i].p[j];
+        if (g->prims[i].kind == SG_LEAK) {
+            for (int j = 0; j < 5; ++j) ge.leak[ge.n_leak][j] = g->prims[i].p[j];
+            ++ge.n_leak;
+        } else {
+            ge.kind[ge.n] = g->prims[i].kind;
+            for (int j = 0; j < 12; ++j) ge.p[ge.n][j] = g->prims[i].p[j];
+            ++ge.n;
+        }
     }
     return ge;
 }
@@ -560,7 +575,11 @@ static void launch_tag(const GridC& gc, const Geom& geom, int32_t zt_lo, int32_t
         const char* e = getenv("SG_TAG_CULL");
         return e ? atoi(e) : -1;
     }();
-    const bool cull = force >= 0 ? force == 1 : (double)gc.n[0] * gc.n[1] * gc.n[2] >= (double)(1 << 25);
+    // (leak balls flip signs inside a block: the cull's block-uniform sign
+    // does not hold there, so leaky geometries always take the plain kernel)
+    const bool cull = geom.n_leak == 0 &&
+                      (force >= 0 ? force == 1
+                                  : (double)gc.n[0] * gc.n[1] * gc.n[2] >= (double)(1 << 25));
     if (cull) {
         dim3 grid((unsigned)W, (unsigned)ceil_div(gc.n[1], 32), (unsigned)ceil_div(quads, 4));
         k_tag_cull<<<grid, 128, 0, s>>>(gc, geom, zt_lo, zt_hi, W, 1, core_w, neg_w);
@@ -640,18 +659,24 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         const int64_t tag_words = (int64_t)W * gc.n[1] * (zt_hi - zt_lo);
         const int64_t nwords = (int64_t)W * gc.n[1] * (gc.zs_hi - gc.zs_lo);
         const int64_t n_tiles = ceil_div(nwords, kTB);
-        // one scratch block: tag words | active words | tile counts | tile
-        // offsets + [core count, boundary flag] (contiguous: one D2H copy)
+        // the tag bitmasks stay with the grid (sign correction); one scratch
+        // block: active words | tile counts | tile offsets + [core count,
+        // boundary flag] (contiguous: one D2H copy)
         auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
         const size_t sz_tag = al(sizeof(uint32_t) * 2 * tag_words),
                      sz_act = al(sizeof(uint32_t) * nwords), sz_cnt = al(sizeof(int32_t) * n_tiles),
                      sz_off = al(sizeof(int64_t) * (n_tiles + 3));
-        char* scratch = (char*)dalloc(sz_tag + sz_act + sz_cnt + sz_off, s);
-        uint32_t* core_w = (uint32_t*)scratch;
+        uint32_t* core_w = (uint32_t*)g->alloc(sz_tag, s);
         uint32_t* neg_w = core_w + tag_words;
-        uint32_t* act_w = (uint32_t*)(scratch + sz_tag);
-        int32_t* tile_count = (int32_t*)(scratch + sz_tag + sz_act);
-        int64_t* tile_off = (int64_t*)(scratch + sz_tag + sz_act + sz_cnt);
+        g->cell_core = core_w;
+        g->cell_neg = neg_w;
+        g->tag_W = W;
+        g->zt_lo = zt_lo;
+        g->zt_hi = zt_hi;
+        char* scratch = (char*)dalloc(sz_act + sz_cnt + sz_off, s);
+        uint32_t* act_w = (uint32_t*)scratch;
+        int32_t* tile_count = (int32_t*)(scratch + sz_act);
+        int64_t* tile_off = (int64_t*)(scratch + sz_act + sz_cnt);
         unsigned long long* d_core = (unsigned long long*)(tile_off + n_tiles + 1);
         SG_CUDA(cudaMemsetAsync(d_core, 0, 2 * sizeof(unsigned long long), s));
         launch_tag(gc, g->geom, zt_lo, zt_hi, W, core_w, neg_w, s);
@@ -842,6 +867,12 @@ extern "C" sg_status sg_view(const sg_grid* g, int32_t what, sg_view_t* v) {
             break;
         case SG_VIEW_PLANE_FIRST:
             set(g->plane_first, 1, g->gc.zs_hi - g->gc.zs_lo + 1, 1, 1, 8, 4);
+            break;
+        case SG_VIEW_CELL_CORE:
+            set(g->cell_core, 3, g->zt_hi - g->zt_lo, g->gc.n[1], g->tag_W, 4, 2);
+            break;
+        case SG_VIEW_CELL_NEG:
+            set(g->cell_neg, 3, g->zt_hi - g->zt_lo, g->gc.n[1], g->tag_W, 4, 2);
             break;
         default: throw Error(SG_ERR_ARG, "sg_view: unknown selector");
         }

@@ -17,9 +17,11 @@ namespace sg {
 // Analytic geometry, passed by value to the kernels that evaluate f
 // (parameter space, ~1.6 KB).
 struct Geom {
-    int32_t n;
+    int32_t n;       // union primitives (kinds other than SG_LEAK), in order
+    int32_t n_leak;  // SG_LEAK post-operations (sign-error balls)
     int32_t kind[SG_MAX_PRIMS];
     double p[SG_MAX_PRIMS][12];
+    double leak[SG_MAX_PRIMS][5];  // cx cy cz r margin
 };
 
 // Grid constants passed by value to every kernel.
@@ -113,6 +115,10 @@ struct sg_grid {
     uint8_t* meta_cat = nullptr;
     uint32_t* nb = nullptr;
     int64_t* plane_first = nullptr;  // [stored planes + 1]
+    // tagging bitmasks kept for the sign correction: [tag planes][n1][W]
+    uint32_t* cell_core = nullptr;
+    uint32_t* cell_neg = nullptr;
+    int32_t tag_W = 0, zt_lo = 0, zt_hi = 0;
     // fields
     void* phi[2] = {nullptr, nullptr};
     int cur = 0;

@@ -21,13 +21,14 @@ SG_OK, SG_ERR_ARG, SG_ERR_OOM, SG_ERR_CUDA, SG_ERR_NCCL, SG_ERR_STATE, SG_ERR_DO
 SG_F32, SG_F64 = 0, 1
 SG_GRAD, SG_NORMAL, SG_KINT = 1, 2, 4
 VIEWS = {"bg": 0, "meta_cell": 1, "meta_cat": 2, "nb": 3, "phi": 4, "grad": 5, "normal": 6,
-         "kint": 7, "gkint": 8, "plane_first": 9, "phi_next": 10}
+         "kint": 7, "gkint": 8, "plane_first": 9, "phi_next": 10, "cell_core": 11,
+         "cell_neg": 12}
 _STATUS = {0: "SG_OK", 1: "SG_ERR_ARG", 2: "SG_ERR_OOM", 3: "SG_ERR_CUDA", 4: "SG_ERR_NCCL",
            5: "SG_ERR_STATE", 6: "SG_ERR_DOMAIN"}
 
 # exported symbols declared in include/sg.h (checked by the CPU test suite)
-EXPORTS = ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax", "sg_info",
-           "sg_view",
+EXPORTS = ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
+           "sg_sign_correct", "sg_info", "sg_view",
            "sg_destroy", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
            "sg_last_error", "sg_abi_version", "sg_launch_count")
 
@@ -99,6 +100,7 @@ def lib():
         L.sg_probe.argtypes = [P, I64, P, P, P, P, P]
         L.sg_table1.argtypes = [P, I32, D, P]
         L.sg_relax.argtypes = [P, I64, P, C.POINTER(sg_relax_params), P]
+        L.sg_sign_correct.argtypes = [P, D, I32, C.POINTER(I32), P]
         L.sg_info.argtypes = [P, C.POINTER(sg_info_t)]
         L.sg_view.argtypes = [P, I32, C.POINTER(sg_view_t)]
         L.sg_destroy.argtypes = [P]
@@ -110,6 +112,7 @@ def lib():
         L.sg_abi_version.restype = I32
         L.sg_launch_count.restype = C.c_uint64
         for name in ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
+                     "sg_sign_correct",
                      "sg_info",
                      "sg_view", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts"):
             getattr(L, name).restype = C.c_int
@@ -191,6 +194,15 @@ def sg_relax(grid: int, n: int, pos_ptr: int, dp: float, h_ratio: float = 1.3,
     p = sg_relax_params(dp, h_ratio, step, max_disp, surface_offset, int(steps), 0)
     _check(lib().sg_relax(C.c_void_p(grid), int(n), C.c_void_p(pos_ptr), C.byref(p),
                           _stream(stream)))
+
+
+def sg_sign_correct(grid: int, tau: float, max_sweeps: int = 0, stream=None) -> tuple:
+    """Sign-consistency correction (NEXT-3); returns the (coarse, refined)
+    numbers of sweeps that signed something."""
+    sw = (C.c_int32 * 2)()
+    _check(lib().sg_sign_correct(C.c_void_p(grid), float(tau), int(max_sweeps), sw,
+                                 _stream(stream)))
+    return int(sw[0]), int(sw[1])
 
 
 def sg_info(grid: int) -> dict:
@@ -327,6 +339,12 @@ class Grid:
         sg_relax(self.handle, int(pos.shape[0]), pos.data_ptr(), dp, h_ratio, step, max_disp,
                  surface_offset, steps, stream)
         return pos
+
+    def sign_correct(self, tau: float | None = None, max_sweeps: int = 0, stream=None) -> tuple:
+        """Sign-consistency correction (NEXT-3); tau defaults to dx."""
+        if tau is None:
+            tau = self.info["dx"]
+        return sg_sign_correct(self.handle, tau, max_sweeps, stream)
 
     def view(self, name: str):
         return view_tensor(self.handle, name)

@@ -40,3 +40,12 @@ if [[ $what == diag3 ]]; then
   SG_TAG_CULL=0 timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_nocull.json 2> gpurun_out/bench_c3_nocull.err
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python bench.py --config C3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_c3.log 2>&1
 fi
+if [[ $what == sign ]]; then
+  timeout 900 python -m pytest tests/test_sign_gpu.py -q -x -rf > gpurun_out/pytest_sign.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_sign.log
+  timeout 600 python scripts/sign_bench.py C2 C3 > gpurun_out/sign_bench.json 2> gpurun_out/sign_bench.err
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_sign.csv python scripts/sign_bench.py C2 > gpurun_out/ncu_sign.log 2>&1
+fi
+if [[ $what == signprof ]]; then
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_cell_sweep|k_pt_sweep|k_pt_apply|k_nb_fix|k_bg_fix' -s 120 -c 6 -o gpurun_out/prof_sign python scripts/sign_bench.py C3 > gpurun_out/ncu_signprof.log 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 700 --log-file gpurun_out/launches_sign_c3.csv python scripts/sign_bench.py C3 > gpurun_out/ncu_sign_c3.log 2>&1
+fi

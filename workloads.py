@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 # Primitive kinds: numbers are part of the C-ABI (include/sg.h sg_prim_kind).
-SPHERE, SHELL, BOX, TORUS_X, TORUS_Y, TORUS_Z, TRIPRISM_Z = range(7)
+SPHERE, SHELL, BOX, TORUS_X, TORUS_Y, TORUS_Z, TRIPRISM_Z, LEAK = range(8)
 
 
 @dataclass(frozen=True)
@@ -102,6 +102,19 @@ CONFIGS = {
 
 def config(name: str) -> Workload:
     return CONFIGS[name]
+
+
+# Leak balls (cx, cy, cz, r) in the unit domain of the configs: one inside
+# the body, one straddling its surface, one in the far field (a stand-in for
+# the sign errors of a mesh SDF on leaky input; SG_LEAK in sg.h).
+LEAK_BALLS = ((0.5, 0.5, 0.5, 0.2), (0.78, 0.42, 0.55, 0.15), (0.12, 0.85, 0.2, 0.1))
+
+
+def leaky(w: Workload, balls=LEAK_BALLS, margin_cells: float = 1.0) -> Workload:
+    """`w` with SG_LEAK sign-error balls appended; the sign of f flips inside
+    a ball where |f| >= margin_cells * l_c (core cells stay correct)."""
+    leaks = tuple(Prim(LEAK, tuple(b) + (margin_cells * w.cell,)) for b in balls)
+    return w.with_(name=w.name + "L", prims=tuple(w.prims) + leaks)
 
 
 # ------------------------------------------------------------ random scenes --
