@@ -302,6 +302,31 @@ sg_status sg_relax(sg_grid* grid, int64_t n, void* pos, const sg_relax_params* p
 sg_status sg_sign_correct(sg_grid* grid, double tau, int32_t max_sweeps, int32_t* sweeps,
                           void* stream);
 
+/* Small-feature cleaning (NEXT-3; "we reimplemented the
+ * level-set cleaning algorithms (only on the finest layer) in Ref.
+ * [yu2023level] so that it can be run on GPU"; the criterion is not restated
+ * in the paper, reading R-23 takes the stand-in of SPEC S:476-484).  Rounds
+ * of:
+ *   1. K = kernel integral of the current phi (as sg_gradient SG_KINT with
+ *      h_ratio; S = sum of the kernel weights, so K / S is the fraction of
+ *      the kernel support inside the body);
+ *   2. every active data point inside the body within dx of the surface
+ *      (-dx < phi < 0) with K < threshold * S (compared in the grid dtype)
+ *      is raised to phi = +dx (the thin feature is carved away); if no point
+ *      was raised the call ends;
+ *   3. reinit_iters reinitialisation sweeps (sg_reinit with cfl).
+ * At most max_rounds rounds.  modified (host int64[max_rounds], may be NULL)
+ * receives the number of raised points per round (0 for rounds not run);
+ * rounds (may be NULL) the number of rounds that raised something.  The host
+ * synchronises with `stream` once per round.  Afterwards K / G
+ * (SG_VIEW_KINT) describe the final phi only if the last round raised
+ * nothing; grad / normal are stale.  Single-domain grids only (SG_ERR_ARG
+ * for a slab grid); h_ratio in [0.5, 2], threshold in [0, 1], cfl in
+ * (0, 0.5]. */
+sg_status sg_clean(sg_grid* grid, double h_ratio, double threshold, int32_t reinit_iters,
+                   double cfl, int32_t max_rounds, int32_t* rounds, int64_t* modified,
+                   void* stream);
+
 sg_status sg_info(const sg_grid* grid, sg_info_t* info);
 sg_status sg_view(const sg_grid* grid, int32_t what, sg_view_t* view);
 

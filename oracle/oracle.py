@@ -81,6 +81,9 @@ def lib():
                                C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32]
         L.or_sign_correct.argtypes = [P, P, C.c_int32, P, P, P, C.c_int64, P, P, P,
                                       C.c_double, C.c_int32, P]
+        L.or_clean.restype = C.c_int32
+        L.or_clean.argtypes = [P, P, C.c_int32, P, P, C.c_double, C.c_double, C.c_int32,
+                               C.c_double, C.c_int32, P]
         L.or_set_threads.argtypes = [C.c_int32]
         L.or_get_threads.restype = C.c_int32
         _lib = L
@@ -292,6 +295,19 @@ class Oracle:
                               _ptr(t.meta_cell), t.n_pkg, _ptr(nb), _ptr(cell_neg), _ptr(out),
                               tau, int(max_sweeps), sw)
         return bg, nb, cell_neg, out, (int(sw[0]), int(sw[1]))
+
+    def clean(self, phi: np.ndarray, threshold: float = 0.4, max_rounds: int = 5,
+              h_ratio: float | None = None, reinit_iters: int | None = None,
+              cfl: float | None = None):
+        """NEXT-3 small-feature cleaning (R-23) of a copy of the dense phi.
+        Returns (phi, rounds, modified per round)."""
+        out = np.ascontiguousarray(np.array(phi, dtype=np.float64, copy=True))
+        mods = np.zeros(max(1, max_rounds), np.int64)
+        r = lib().or_clean(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(out),
+                           self.w.h_ratio if h_ratio is None else float(h_ratio), float(threshold),
+                           self.w.iters if reinit_iters is None else int(reinit_iters),
+                           self.w.cfl if cfl is None else float(cfl), int(max_rounds), _ptr(mods))
+        return out, int(r), [int(v) for v in mods[:max_rounds]]
 
     def to_packages(self, dense: np.ndarray, far_neg: float, far_pos: float) -> np.ndarray:
         t = self.tables if self.tables is not None else self.build_tables()

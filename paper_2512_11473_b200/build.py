@@ -33,6 +33,7 @@ UNITS = {
     "sg_probe.cu": ["-ftz=true"],
     "sg_relax.cu": [],
     "sg_sign.cu": [],
+    "sg_clean.cu": [],
 }
 
 

@@ -28,7 +28,7 @@ _STATUS = {0: "SG_OK", 1: "SG_ERR_ARG", 2: "SG_ERR_OOM", 3: "SG_ERR_CUDA", 4: "S
 
 # exported symbols declared in include/sg.h (checked by the CPU test suite)
 EXPORTS = ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
-           "sg_sign_correct", "sg_info", "sg_view",
+           "sg_sign_correct", "sg_clean", "sg_info", "sg_view",
            "sg_destroy", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
            "sg_last_error", "sg_abi_version", "sg_launch_count")
 
@@ -101,6 +101,7 @@ def lib():
         L.sg_table1.argtypes = [P, I32, D, P]
         L.sg_relax.argtypes = [P, I64, P, C.POINTER(sg_relax_params), P]
         L.sg_sign_correct.argtypes = [P, D, I32, C.POINTER(I32), P]
+        L.sg_clean.argtypes = [P, D, D, I32, D, I32, C.POINTER(I32), C.POINTER(I64), P]
         L.sg_info.argtypes = [P, C.POINTER(sg_info_t)]
         L.sg_view.argtypes = [P, I32, C.POINTER(sg_view_t)]
         L.sg_destroy.argtypes = [P]
@@ -112,7 +113,7 @@ def lib():
         L.sg_abi_version.restype = I32
         L.sg_launch_count.restype = C.c_uint64
         for name in ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
-                     "sg_sign_correct",
+                     "sg_sign_correct", "sg_clean",
                      "sg_info",
                      "sg_view", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts"):
             getattr(L, name).restype = C.c_int
@@ -203,6 +204,16 @@ def sg_sign_correct(grid: int, tau: float, max_sweeps: int = 0, stream=None) -> 
     _check(lib().sg_sign_correct(C.c_void_p(grid), float(tau), int(max_sweeps), sw,
                                  _stream(stream)))
     return int(sw[0]), int(sw[1])
+
+
+def sg_clean(grid: int, h_ratio: float = 1.3, threshold: float = 0.4, reinit_iters: int = 20,
+             cfl: float = 0.3, max_rounds: int = 5, stream=None) -> tuple:
+    """Small-feature cleaning (NEXT-3); returns (rounds, [raised per round])."""
+    r = C.c_int32(0)
+    mods = (C.c_int64 * max(1, int(max_rounds)))()
+    _check(lib().sg_clean(C.c_void_p(grid), float(h_ratio), float(threshold), int(reinit_iters),
+                          float(cfl), int(max_rounds), C.byref(r), mods, _stream(stream)))
+    return int(r.value), [int(mods[i]) for i in range(int(max_rounds))]
 
 
 def sg_info(grid: int) -> dict:
@@ -345,6 +356,14 @@ class Grid:
         if tau is None:
             tau = self.info["dx"]
         return sg_sign_correct(self.handle, tau, max_sweeps, stream)
+
+    def clean(self, threshold: float = 0.4, max_rounds: int = 5, h_ratio: float | None = None,
+              reinit_iters: int | None = None, cfl: float | None = None, stream=None) -> tuple:
+        """Small-feature cleaning (NEXT-3); returns (rounds, raised per round)."""
+        w = self.w
+        return sg_clean(self.handle, w.h_ratio if h_ratio is None else h_ratio, threshold,
+                        w.iters if reinit_iters is None else reinit_iters,
+                        w.cfl if cfl is None else cfl, max_rounds, stream)
 
     def view(self, name: str):
         return view_tensor(self.handle, name)

@@ -49,3 +49,7 @@ if [[ $what == signprof ]]; then
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_cell_sweep|k_pt_sweep|k_pt_apply|k_nb_fix|k_bg_fix' -s 120 -c 6 -o gpurun_out/prof_sign python scripts/sign_bench.py C3 > gpurun_out/ncu_signprof.log 2>&1
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 700 --log-file gpurun_out/launches_sign_c3.csv python scripts/sign_bench.py C3 > gpurun_out/ncu_sign_c3.log 2>&1
 fi
+if [[ $what == clean ]]; then
+  timeout 900 python -m pytest tests/test_clean_gpu.py tests/test_sign_gpu.py -q -x -rf > gpurun_out/pytest_clean.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_clean.log
+  timeout 600 python scripts/clean_bench.py C2 FIN128 > gpurun_out/clean_bench.json 2> gpurun_out/clean_bench.err
+fi

@@ -104,6 +104,19 @@ def config(name: str) -> Workload:
     return CONFIGS[name]
 
 
+def fins(n: int = 32, dtype: str = "f64", thin: float = 0.5, thick: float = 4.0) -> Workload:
+    """Small-feature scene (SPEC S:482-483 examples): a slab z in [0.2, 0.4]
+    spanning the domain in x and y, with two walls on top (z up to 0.6, across
+    the domain in x): one `thin` h thick at y = 0.3, one `thick` h thick at
+    y = 0.7 (h = h_ratio dx, h_ratio 1.3)."""
+    cell = 1.0 / n
+    h = 1.3 * cell / 4.0
+    return Workload(f"FIN{n}", (n, n, n), cell, dtype=dtype,
+                    prims=(Prim(BOX, (0.5, 0.5, 0.3, 1.0, 1.0, 0.1)),
+                           Prim(BOX, (0.5, 0.3, 0.5, 1.0, 0.5 * thin * h, 0.1)),
+                           Prim(BOX, (0.5, 0.7, 0.5, 1.0, 0.5 * thick * h, 0.1))))
+
+
 # Leak balls (cx, cy, cz, r) in the unit domain of the configs: one inside
 # the body, one straddling its surface, one in the far field (a stand-in for
 # the sign errors of a mesh SDF on leaky input, P:528-531; SG_LEAK in sg.h).
