@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "sg_internal.cuh"
@@ -139,6 +140,59 @@ __device__ __forceinline__ double godunov(double p, double xm, double xp, double
     return p - c.cdx * s * (sqrt(wx * wx + wy * wy + wz * wz) - 1.0);
 }
 
+// fp32 row form of the same sign-folded step, written for the Blackwell
+// paired-FP32 pipe: with a_i = -sign(p_i)/dx and b_i = |p_i|/dx the two upwind
+// differences of one axis are (a m + b, a q + b) / 1 and
+// w = max(., ., 0) is one 3-input FMNMX.  The y / z neighbours of points
+// i, i+1 sit in aligned register pairs of their float4 rows, so they (and
+// |grad|^2, the sign factor and the update) go through FFMA2 / FMUL2; the x
+// neighbours are not pair-aligned and stay scalar.  sqrt / rsqrt: MUFU
+// (~2 ulp), inside the 1e-5 dx tolerance.  Same formula as godunov() above:
+// out = p + cdx s (1 - |grad phi|), s = p / sqrt(p^2 + dx^2).
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void godunov_row(const float (&p)[4], float xm, float xp,
+                                            const float (&ym)[4], const float (&yp)[4],
+                                            const float (&zm)[4], const float (&zp)[4],
+                                            const StC<float>& c, float (&o)[4]) {
+    float a[4], b[4], wx[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        a[i] = p[i] < 0.f ? c.inv_dx : -c.inv_dx;
+        b[i] = fabsf(p[i]) * c.inv_dx;
+        const float m = i > 0 ? p[i - 1] : xm, q = i < 3 ? p[i + 1] : xp;
+        wx[i] = max3f(fmaf(a[i], m, b[i]), fmaf(a[i], q, b[i]), 0.f);
+    }
+    const float2 dx2 = make_float2(c.dx2, c.dx2), cdx = make_float2(c.cdx, c.cdx);
+#pragma unroll
+    for (int h = 0; h < 4; h += 2) {
+        const float2 A = make_float2(a[h], a[h + 1]), B = make_float2(b[h], b[h + 1]);
+        const float2 tym = __ffma2_rn(A, make_float2(ym[h], ym[h + 1]), B);
+        const float2 typ = __ffma2_rn(A, make_float2(yp[h], yp[h + 1]), B);
+        const float2 tzm = __ffma2_rn(A, make_float2(zm[h], zm[h + 1]), B);
+        const float2 tzp = __ffma2_rn(A, make_float2(zp[h], zp[h + 1]), B);
+        const float2 WX = make_float2(wx[h], wx[h + 1]);
+        const float2 WY = make_float2(max3f(tym.x, typ.x, 0.f), max3f(tym.y, typ.y, 0.f));
+        const float2 WZ = make_float2(max3f(tzm.x, tzp.x, 0.f), max3f(tzm.y, tzp.y, 0.f));
+        const float2 G = __ffma2_rn(WX, WX, __ffma2_rn(WY, WY, __fmul2_rn(WZ, WZ)));
+        const float2 t = make_float2(1.f - sqrt_approx(G.x), 1.f - sqrt_approx(G.y));
+        const float2 P = make_float2(p[h], p[h + 1]);
+        const float2 r2 = __ffma2_rn(P, P, dx2);
+        const float2 cs = __fmul2_rn(__fmul2_rn(P, cdx), make_float2(rsqrtf(r2.x), rsqrtf(r2.y)));
+        const float2 out = __ffma2_rn(cs, t, P);
+        o[h] = out.x;
+        o[h + 1] = out.y;
+    }
+}
+
 // K5 -- reinitialisation sweep over packages [lo, hi).  Eight threads per
 // package; thread (j, k), k in {0, 1}, owns the two x-rows (j, k) and
 // (j, k + 2), which share their middle z-row (j, k + 1): 9 row loads + 4
@@ -217,12 +271,17 @@ struct ReinitOp {
     __device__ __forceinline__ void operator()(const Cross2<T>& x, uint32_t pkg, int r0,
                                                int r1) const {
         T o0[4], o1[4];
+        if constexpr (std::is_same<T, float>::value) {
+            godunov_row(x.c0, x.xm0, x.xp0, x.ym0, x.yp0, x.zlo, x.zmid, c, o0);
+            godunov_row(x.c1, x.xm1, x.xp1, x.ym1, x.yp1, x.zmid, x.zhi, c, o1);
+        } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             o0[i] = godunov(x.c0[i], i > 0 ? x.c0[i - 1] : x.xm0, i < 3 ? x.c0[i + 1] : x.xp0,
                             x.ym0[i], x.yp0[i], x.zlo[i], x.zmid[i], c);
             o1[i] = godunov(x.c1[i], i > 0 ? x.c1[i - 1] : x.xm1, i < 3 ? x.c1[i + 1] : x.xp1,
                             x.ym1[i], x.yp1[i], x.zmid[i], x.zhi[i], c);
+        }
         }
         T* O = out + (size_t)pkg * 64;
         st_row(O + 4 * r0, o0);
