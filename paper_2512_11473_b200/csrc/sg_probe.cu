@@ -110,7 +110,7 @@ struct __align__(16) ProbeSmem {
 };
 
 template <class T>
-__global__ void __launch_bounds__(32 * ProbeSmem<T>::kWB, 3)
+__global__ void __launch_bounds__(32 * ProbeSmem<T>::kWB, 4)
 k_probe(GridC gc, const uint32_t* __restrict__ bg,
                                                const uint32_t* __restrict__ nb,
                                                const T* __restrict__ phi,

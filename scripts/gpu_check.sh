@@ -53,3 +53,8 @@ if [[ $what == clean ]]; then
   timeout 900 python -m pytest tests/test_clean_gpu.py tests/test_sign_gpu.py -q -x -rf > gpurun_out/pytest_clean.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_clean.log
   timeout 600 python scripts/clean_bench.py C2 FIN128 > gpurun_out/clean_bench.json 2> gpurun_out/clean_bench.err
 fi
+if [[ $what == probe ]]; then
+  timeout 600 python -m pytest tests -m gpu -q -x -k "probe or smoke or c5 or slab" > gpurun_out/pytest_probe.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_probe.log
+  timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
+  timeout 600 python bench.py --no-cpu-baseline --order shuffled > gpurun_out/bench_shuf.json 2> /dev/null
+fi
