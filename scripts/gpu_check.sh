@@ -58,3 +58,8 @@ if [[ $what == probe ]]; then
   timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
   timeout 600 python bench.py --no-cpu-baseline --order shuffled > gpurun_out/bench_shuf.json 2> /dev/null
 fi
+if [[ $what == kint ]]; then
+  timeout 600 python -m pytest tests -m gpu -q -x -k "kernel or gradient or relax or clean or smoke" > gpurun_out/pytest_kint.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_kint.log
+  timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench.json 2> gpurun_out/bench.err
+  timeout 600 ncu --metrics gpu__time_duration.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum --clock-control none --csv -k regex:k_kint --log-file gpurun_out/launch_kint.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+fi
