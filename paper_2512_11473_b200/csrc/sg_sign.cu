@@ -10,7 +10,8 @@
 // Both steps are bit-parallel Jacobi sweeps over (known, negative) bitmasks:
 //   coarse  one thread per 32-cell word of the tagging bitmasks [z][y][W]:
 //           x neighbours by shifts with the carry bit of the adjacent word,
-//           y / z neighbours are the words one row / plane away;
+//           y / z neighbours are the words one row / plane away; only words
+//           next to the previous sweep's changes are visited (u8 stamps);
 //   refined one thread per package, a u64 per mask (bit i + 4 j + 16 k, the
 //           data layout): in-package neighbours by shifts, the face bits of
 //           the 6 face-neighbour packages through the neighbour table (Lst. 2
@@ -108,18 +109,31 @@ __global__ void __launch_bounds__(256) k_cell_unpack(uint32_t nwords, const uint
     if (t < nwords) neg[t] = st[t].y;
 }
 
+// One coarse sweep, frontier-restricted at word granularity: a 32-cell word
+// is visited only if its u8 stamp says that it or one of the words whose
+// cells touch its cells changed in the previous sweep, i.e.
+// (u8)(stamp - sweep) <= 1 (every word is stamped 0 initially; a stamp of the
+// next sweep written by another thread during this one also passes, and a
+// stale stamp that aliases mod 256 only causes a harmless extra visit: the
+// update is a pure function of the input buffer).  A skipped word cannot
+// change and its output-buffer value is still current, because a word that
+// changed is re-visited (and re-written) in the next sweep.
 __global__ void __launch_bounds__(256) k_cell_sweep(int32_t nx, uint32_t W, uint32_t ny, uint32_t nz,
-                                                    uint32_t nwords, const uint2* __restrict__ in,
+                                                    uint32_t nwords, int32_t sweep,
+                                                    const uint2* __restrict__ in,
                                                     uint2* __restrict__ out,
+                                                    uint8_t* __restrict__ stamp,
                                                     const int* __restrict__ prev,
                                                     int* __restrict__ cur) {
     if (prev && *prev == 0) return;  // converged: nothing to do (block-uniform)
+    const uint8_t s8 = (uint8_t)sweep, n8 = (uint8_t)(sweep + 1);
+    const uint32_t pl = W * ny;
     bool changed = false;
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nwords;
          t += gridDim.x * blockDim.x) {
+        if ((uint8_t)(stamp[t] - s8) > 1u) continue;
         const uint32_t row = t / W, q = t - row * W;
         const uint32_t z = row / ny, y = row - z * ny;
-        const uint32_t pl = W * ny;
         const uint2 c = in[t];
         const uint2 zero = make_uint2(0u, 0u);
         const uint2 l = q > 0 ? in[t - 1] : zero;
@@ -147,7 +161,16 @@ __global__ void __launch_bounds__(256) k_cell_sweep(int32_t nx, uint32_t W, uint
         const uint32_t valid = tail >= 32 ? 0xffffffffu : ((1u << tail) - 1u);
         const uint32_t upd = ~c.x & (tn | tp) & valid;
         out[t] = make_uint2(c.x | upd, (c.y & ~upd) | (upd & tn));
-        changed |= upd != 0u;
+        if (upd) {
+            changed = true;
+            stamp[t] = n8;
+            if ((upd & 1u) && q > 0) stamp[t - 1] = n8;
+            if ((upd >> 31) && q + 1 < W) stamp[t + 1] = n8;
+            if (y > 0) stamp[t - W] = n8;
+            if (y + 1 < ny) stamp[t + W] = n8;
+            if (z > 0) stamp[t - pl] = n8;
+            if (z + 1 < nz) stamp[t + pl] = n8;
+        }
     }
     raise_flag(changed, cur);
 }
@@ -335,11 +358,13 @@ extern "C" sg_status sg_sign_correct(sg_grid* g, double tau, int32_t max_sweeps,
         const int64_t n_pkg = g->n_pkg;
         SG_ARG(nwords < (1LL << 31), "sg_sign_correct: too many cells");
         const size_t cw = sizeof(uint2) * (size_t)nwords, pw = sizeof(uint64_t) * (size_t)n_pkg;
-        char* tmp = (char*)dalloc(2 * cw + 4 * pw + 256 * sizeof(int), s);
+        char* tmp = (char*)dalloc(2 * cw + 4 * pw + 256 * sizeof(int) + (size_t)nwords, s);
         uint2* cs[2] = {(uint2*)tmp, (uint2*)(tmp + cw)};
         uint64_t* pk[2] = {(uint64_t*)(tmp + 2 * cw), (uint64_t*)(tmp + 2 * cw + pw)};
         uint64_t* pn[2] = {(uint64_t*)(tmp + 2 * cw + 2 * pw), (uint64_t*)(tmp + 2 * cw + 3 * pw)};
         int* dflags = (int*)(tmp + 2 * cw + 4 * pw);
+        uint8_t* stamp = (uint8_t*)(dflags + 256);
+        SG_CUDA(cudaMemsetAsync(stamp, 0, (size_t)nwords, s));
 
         // coarse: core cells signed by f(centre), the rest unsigned
         const unsigned cb = (unsigned)ceil_div(nwords, 256);
@@ -349,8 +374,8 @@ extern "C" sg_status sg_sign_correct(sg_grid* g, double tau, int32_t max_sweeps,
         const int c_sweeps = run_sweeps(
             [&](int j, const int* prev, int* cur) {
                 k_cell_sweep<<<cbs, 256, 0, s>>>(gc.n[0], (uint32_t)W, (uint32_t)ny, (uint32_t)nzt,
-                                                (uint32_t)nwords, cs[j & 1], cs[(j + 1) & 1], prev,
-                                                cur);
+                                                (uint32_t)nwords, j, cs[j & 1], cs[(j + 1) & 1],
+                                                stamp, prev, cur);
                 SG_LAUNCHED();
             },
             max_sweeps, dflags, s);
