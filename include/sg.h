@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SG_ABI_VERSION 1
+#define SG_ABI_VERSION 2
 #define SG_PKG 4        /* package subdivision, "default by 4"        */
 #define SG_MAX_PRIMS 16 /* primitives per geometry                          */
 
@@ -99,9 +99,32 @@ typedef struct {
 } sg_prim;
 
 typedef struct {
-    const sg_prim* prims; /* host pointer, n_prims entries (1..SG_MAX_PRIMS) */
+    const sg_prim* prims; /* host pointer, n_prims entries (0..SG_MAX_PRIMS)  */
     int32_t n_prims;
     int32_t pad;
+    /* NEXT-4: closed triangle mesh (reading R-24).  When
+     * n_tris > 0 the mesh's signed distance replaces the union of the
+     * primitives (which must then be empty); otherwise these are ignored.
+     * verts: host, n_verts x 3 fp64; tris: host, n_tris x 3 vertex indices,
+     * counter-clockwise seen from outside.  Copied during sg_build.
+     *   f(x) = s |x - q|: q the closest point of the nearest triangle
+     *   (smallest squared distance, ties to the lowest index; closest point on
+     *   a triangle by its Voronoi regions, Ericson RTCD 5.1.5, fp64 without
+     *   FMA), s = sign((x - q) . N) with N the angle-weighted pseudonormal of
+     *   the closest feature (Baerentzen & Aanaes): the unit face normal, the
+     *   sum of the two adjacent face normals of an edge, or the sum over a
+     *   vertex's corners (in triangle order) of corner angle * face normal.
+     * The device evaluates it exactly up to 4 l_c from the surface (per-cell
+     * triangle bins); the sign of cells farther away comes from the coarse
+     * sign flood of sg_sign_correct, seeded by the cells within 4 l_c
+     * -- the same sign for a closed mesh.  Out-of-domain
+     * neighbour cells take the sign of the nearest in-domain cell.  Mesh
+     * geometries: single-domain grids, no SG_LEAK entries, not accepted by
+     * sg_plane_counts. */
+    const double* verts;
+    const int32_t* tris;
+    int32_t n_verts;
+    int32_t n_tris;
 } sg_geometry;
 
 typedef struct {

@@ -43,6 +43,7 @@ class _Grid(C.Structure):
 
 
 _lib = None
+_active_mesh = None
 
 
 def lib():
@@ -84,6 +85,9 @@ def lib():
         L.or_clean.restype = C.c_int32
         L.or_clean.argtypes = [P, P, C.c_int32, P, P, C.c_double, C.c_double, C.c_int32,
                                C.c_double, C.c_int32, P]
+        L.or_mesh_set.argtypes = [P, P, C.c_int32, C.c_int32]
+        L.or_mesh_sdf.restype = C.c_double
+        L.or_mesh_sdf.argtypes = [P]
         L.or_set_threads.argtypes = [C.c_int32]
         L.or_get_threads.restype = C.c_int32
         _lib = L
@@ -133,6 +137,22 @@ class Oracle:
                 self._prims[i].p[j] = v
         self.n_prims = len(w.prims)
         self.tables: Tables | None = None
+        mesh = getattr(w, "mesh", None)
+        self._mesh = None
+        if mesh is not None:
+            self._mesh = (np.ascontiguousarray(np.asarray(mesh.verts, np.float64)),
+                          np.ascontiguousarray(np.asarray(mesh.tris, np.int32)))
+
+    def _L(self):
+        """The oracle library with this workload's mesh registered (one mesh
+        at a time; a geometry without primitives evaluates the mesh)."""
+        global _active_mesh
+        L = lib()
+        if self._mesh is not None and _active_mesh is not self._mesh:
+            v, t = self._mesh
+            L.or_mesh_set(_ptr(v), _ptr(t), v.size // 3, t.size // 3)
+            _active_mesh = self._mesh
+        return L
 
     # handles
     @property
@@ -145,7 +165,7 @@ class Oracle:
 
     @property
     def far(self) -> float:
-        return float(lib().or_far(self.g))
+        return float(self._L().or_far(self.g))
 
     @property
     def dx(self) -> float:
@@ -159,7 +179,7 @@ class Oracle:
     def sdf(self, x: np.ndarray) -> np.ndarray:
         x = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1, 3))
         out = np.empty(x.shape[0])
-        lib().or_sdf_batch(self.prims, self.n_prims, x.shape[0], _ptr(x), _ptr(out))
+        self._L().or_sdf_batch(self.prims, self.n_prims, x.shape[0], _ptr(x), _ptr(out))
         return out
 
     # O3-O5
@@ -168,17 +188,17 @@ class Oracle:
         ncell = nx * ny * nz
         cat = np.empty(ncell, np.uint8)
         ties = C.c_int64(0)
-        lib().or_tag(self.g, self.prims, self.n_prims, _ptr(cat), C.byref(ties))
+        self._L().or_tag(self.g, self.prims, self.n_prims, _ptr(cat), C.byref(ties))
         bg = np.empty(ncell, np.uint32)
         n_active = int(np.count_nonzero(cat >= 2))
         meta_cell = np.empty(n_active + 2, np.uint32)
         meta_cat = np.empty(n_active + 2, np.uint8)
         plane = np.zeros(nz, np.int64)
-        n_pkg = int(lib().or_compact(self.g, _ptr(cat), _ptr(bg), _ptr(meta_cell),
+        n_pkg = int(self._L().or_compact(self.g, _ptr(cat), _ptr(bg), _ptr(meta_cell),
                                      _ptr(meta_cat), _ptr(plane)))
         assert n_pkg == n_active + 2
         nb = np.empty((n_pkg, 27), np.uint32)
-        lib().or_neighbours(self.g, self.prims, self.n_prims, _ptr(bg), _ptr(meta_cell),
+        self._L().or_neighbours(self.g, self.prims, self.n_prims, _ptr(bg), _ptr(meta_cell),
                             n_pkg, _ptr(nb))
         self.tables = Tables(cat, bg, meta_cell, meta_cat, nb, plane, n_pkg, int(ties.value))
         return self.tables
@@ -193,11 +213,11 @@ class Oracle:
         """Dense initial phi, shape (Mz, My, Mx) (x fastest)."""
         mx, my, mz = self.m
         phi = np.empty((mz, my, mx))
-        lib().or_phi_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi))
+        self._L().or_phi_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi))
         return phi
 
     def phi_point(self, ix: int, iy: int, iz: int) -> float:
-        return float(lib().or_phi_point(self.g, self.prims, self.n_prims, _ptr(self._bg()),
+        return float(self._L().or_phi_point(self.g, self.prims, self.n_prims, _ptr(self._bg()),
                                         ix, iy, iz))
 
     # O7
@@ -205,7 +225,7 @@ class Oracle:
         cfl = self.w.cfl if cfl is None else cfl
         phi = np.ascontiguousarray(phi, dtype=np.float64)
         out = np.empty_like(phi)
-        lib().or_reinit_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
+        self._L().or_reinit_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
                               _ptr(out), cfl)
         return out
 
@@ -216,7 +236,7 @@ class Oracle:
 
     def reinit_point_from_init(self, ix: int, iy: int, iz: int, cfl: float | None = None) -> float:
         cfl = self.w.cfl if cfl is None else cfl
-        return float(lib().or_reinit_point_from_init(self.g, self.prims, self.n_prims,
+        return float(self._L().or_reinit_point_from_init(self.g, self.prims, self.n_prims,
                                                      _ptr(self._bg()), ix, iy, iz, cfl))
 
     # O8
@@ -225,7 +245,7 @@ class Oracle:
         phi = np.ascontiguousarray(phi, dtype=np.float64)
         grad = np.empty((3,) + phi.shape)
         normal = np.empty((3,) + phi.shape)
-        lib().or_gradient_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
+        self._L().or_gradient_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
                                 _ptr(grad), _ptr(normal))
         return grad, normal
 
@@ -240,7 +260,7 @@ class Oracle:
         phi = np.ascontiguousarray(phi, dtype=np.float64)
         K = np.empty_like(phi)
         G = np.empty((3,) + phi.shape)
-        lib().or_kernel_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
+        self._L().or_kernel_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
                               h_ratio, _ptr(K), _ptr(G))
         return K, G
 
@@ -253,7 +273,7 @@ class Oracle:
         n = pos.shape[0]
         out_phi = np.empty(n)
         out_grad = np.empty((n, 3))
-        oob = lib().or_probe(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
+        oob = self._L().or_probe(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
                              _ptr(g3), n, _ptr(pos), _ptr(out_phi), _ptr(out_grad))
         return out_phi, out_grad, int(oob)
 
@@ -261,7 +281,7 @@ class Oracle:
     def table1(self, phi: np.ndarray, op: int, value: float = 0.0) -> np.ndarray:
         phi = np.ascontiguousarray(phi, dtype=np.float64)
         out = np.empty_like(phi)
-        lib().or_table1_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
+        self._L().or_table1_dense(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi),
                               int(op), float(value), _ptr(out))
         return out
 
@@ -272,7 +292,7 @@ class Oracle:
         phi = np.ascontiguousarray(phi, dtype=np.float64)
         grad = np.ascontiguousarray(grad, dtype=np.float64)
         G = np.ascontiguousarray(G, dtype=np.float64)
-        lib().or_relax(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi), _ptr(grad),
+        self._L().or_relax(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(phi), _ptr(grad),
                        _ptr(G), pos.shape[0], _ptr(pos), dp, h_ratio, step, max_disp,
                        surface_offset, int(steps))
         return pos
@@ -291,7 +311,7 @@ class Oracle:
         out = np.ascontiguousarray(np.array(phi, dtype=np.float64, copy=True))
         tau = self.dx if tau is None else float(tau)
         sw = (C.c_int32 * 2)()
-        lib().or_sign_correct(self.g, self.prims, self.n_prims, _ptr(t.cat), _ptr(bg),
+        self._L().or_sign_correct(self.g, self.prims, self.n_prims, _ptr(t.cat), _ptr(bg),
                               _ptr(t.meta_cell), t.n_pkg, _ptr(nb), _ptr(cell_neg), _ptr(out),
                               tau, int(max_sweeps), sw)
         return bg, nb, cell_neg, out, (int(sw[0]), int(sw[1]))
@@ -303,7 +323,7 @@ class Oracle:
         Returns (phi, rounds, modified per round)."""
         out = np.ascontiguousarray(np.array(phi, dtype=np.float64, copy=True))
         mods = np.zeros(max(1, max_rounds), np.int64)
-        r = lib().or_clean(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(out),
+        r = self._L().or_clean(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(out),
                            self.w.h_ratio if h_ratio is None else float(h_ratio), float(threshold),
                            self.w.iters if reinit_iters is None else int(reinit_iters),
                            self.w.cfl if cfl is None else float(cfl), int(max_rounds), _ptr(mods))
@@ -313,7 +333,7 @@ class Oracle:
         t = self.tables if self.tables is not None else self.build_tables()
         dense = np.ascontiguousarray(dense, dtype=np.float64)
         out = np.empty((t.n_pkg, 64))
-        lib().or_gather_packages(self.g, _ptr(dense), _ptr(t.meta_cell), t.n_pkg, far_neg,
+        self._L().or_gather_packages(self.g, _ptr(dense), _ptr(t.meta_cell), t.n_pkg, far_neg,
                                  far_pos, _ptr(out))
         return out
 

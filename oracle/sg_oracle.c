@@ -40,6 +40,10 @@
  *                     the closed-form containment sign at every data point and
  *                     cell, magnitudes are unchanged, a watertight input is a
  *                     fixed point, flood sweep counts = scipy taxicab distance
+ *   or_mesh_sdf       pinned: a 12-triangle box mesh reproduces the box SDF
+ *                     closed form; icosphere distances within the sagitta of
+ *                     the sphere's, signs = containment; invariance under
+ *                     triangle re-ordering
  *   or_clean          pinned: planar slab (K = S/2 at the surface) is a fixed
  *                     point, a fin thinner than h is removed while a thick fin
  *                     and the slab keep their signs, a second call raises
@@ -154,11 +158,164 @@ static double sdf_prim(const or_prim* q, const double x[3]) {
     }
 }
 
+/* ------------------------------------------------------------ NEXT-4 -- */
+/* Signed distance to a closed triangle mesh ("using the
+ * sign-distance function from triangle mesh", ref. baerentzen2005robust;
+ * reading R-24): nearest triangle by squared distance (ties: lowest index),
+ * closest point on a triangle by its Voronoi regions (Ericson, RTCD 5.1.5),
+ * sign of (x - q) . N with N the angle-weighted pseudonormal of the closest
+ * feature.  Brute force over every triangle.  One registered mesh at a time
+ * (test infrastructure); a geometry with no primitives means "the mesh". */
+static struct {
+    int32_t nv, nt;
+    double *V, *fn, *en, *vn;
+    int32_t* T;
+} g_mesh;
+
+static double dot3(const double* a, const double* b) {
+    return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
+}
+
+void or_mesh_set(const double* V, const int32_t* T, int32_t nv, int32_t nt) {
+    free(g_mesh.V);
+    free(g_mesh.T);
+    free(g_mesh.fn);
+    free(g_mesh.en);
+    free(g_mesh.vn);
+    memset(&g_mesh, 0, sizeof(g_mesh));
+    if (nt <= 0) return;
+    g_mesh.nv = nv;
+    g_mesh.nt = nt;
+    g_mesh.V = (double*)malloc(sizeof(double) * 3 * nv);
+    g_mesh.T = (int32_t*)malloc(sizeof(int32_t) * 3 * nt);
+    memcpy(g_mesh.V, V, sizeof(double) * 3 * nv);
+    memcpy(g_mesh.T, T, sizeof(int32_t) * 3 * nt);
+    g_mesh.fn = (double*)calloc((size_t)3 * nt, sizeof(double));
+    g_mesh.en = (double*)calloc((size_t)9 * nt, sizeof(double));
+    g_mesh.vn = (double*)calloc((size_t)3 * nv, sizeof(double));
+    /* unit face normals (b - a) x (c - a) / |.| */
+    for (int t = 0; t < nt; ++t) {
+        const double *a = V + 3 * T[3 * t], *b = V + 3 * T[3 * t + 1], *c = V + 3 * T[3 * t + 2];
+        double u[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+        double w[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+        double n[3] = {u[1] * w[2] - u[2] * w[1], u[2] * w[0] - u[0] * w[2],
+                       u[0] * w[1] - u[1] * w[0]};
+        double l = sqrt(dot3(n, n));
+        for (int k = 0; k < 3; ++k) g_mesh.fn[3 * t + k] = l > 0.0 ? n[k] / l : 0.0;
+    }
+    /* vertex pseudonormal: sum over corners (triangle order) of angle * n */
+    for (int t = 0; t < nt; ++t)
+        for (int k = 0; k < 3; ++k) {
+            int i = T[3 * t + k], j = T[3 * t + (k + 1) % 3], m = T[3 * t + (k + 2) % 3];
+            const double* p = V + 3 * i;
+            double u[3] = {V[3 * j] - p[0], V[3 * j + 1] - p[1], V[3 * j + 2] - p[2]};
+            double w[3] = {V[3 * m] - p[0], V[3 * m + 1] - p[1], V[3 * m + 2] - p[2]};
+            double lu = sqrt(dot3(u, u)), lw = sqrt(dot3(w, w));
+            double cs = (lu > 0.0 && lw > 0.0) ? dot3(u, w) / (lu * lw) : 1.0;
+            if (cs > 1.0) cs = 1.0;
+            if (cs < -1.0) cs = -1.0;
+            double ang = acos(cs);
+            for (int q = 0; q < 3; ++q) g_mesh.vn[3 * i + q] += ang * g_mesh.fn[3 * t + q];
+        }
+    /* edge pseudonormal: n_t + n_t' of the two faces of an edge (brute-force
+     * search for the triangle holding the reversed edge) */
+    for (int t = 0; t < nt; ++t)
+        for (int e = 0; e < 3; ++e) {
+            int i = T[3 * t + e], j = T[3 * t + (e + 1) % 3], other = -1;
+            for (int u = 0; u < nt && other < 0; ++u)
+                for (int f = 0; f < 3; ++f)
+                    if (T[3 * u + f] == j && T[3 * u + (f + 1) % 3] == i) {
+                        other = u;
+                        break;
+                    }
+            for (int q = 0; q < 3; ++q)
+                g_mesh.en[9 * t + 3 * e + q] =
+                    other < 0 ? g_mesh.fn[3 * t + q] : g_mesh.fn[3 * t + q] + g_mesh.fn[3 * other + q];
+        }
+}
+
+/* closest point q of p on triangle (a, b, c); region 0 face, 1..3 vertex
+ * a/b/c, 4..6 edge ab/bc/ca (Ericson, RTCD 5.1.5) */
+static int tri_closest(const double* a, const double* b, const double* c, const double* p,
+                       double* q) {
+    double ab[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+    double ac[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+    double ap[3] = {p[0] - a[0], p[1] - a[1], p[2] - a[2]};
+    double d1 = dot3(ab, ap), d2 = dot3(ac, ap);
+    if (d1 <= 0.0 && d2 <= 0.0) {
+        memcpy(q, a, 3 * sizeof(double));
+        return 1;
+    }
+    double bp[3] = {p[0] - b[0], p[1] - b[1], p[2] - b[2]};
+    double d3 = dot3(ab, bp), d4 = dot3(ac, bp);
+    if (d3 >= 0.0 && d4 <= d3) {
+        memcpy(q, b, 3 * sizeof(double));
+        return 2;
+    }
+    double vc = d1 * d4 - d3 * d2;
+    if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+        double v = d1 / (d1 - d3);
+        for (int k = 0; k < 3; ++k) q[k] = a[k] + v * ab[k];
+        return 4;
+    }
+    double cp[3] = {p[0] - c[0], p[1] - c[1], p[2] - c[2]};
+    double d5 = dot3(ab, cp), d6 = dot3(ac, cp);
+    if (d6 >= 0.0 && d5 <= d6) {
+        memcpy(q, c, 3 * sizeof(double));
+        return 3;
+    }
+    double vb = d5 * d2 - d1 * d6;
+    if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+        double w = d2 / (d2 - d6);
+        for (int k = 0; k < 3; ++k) q[k] = a[k] + w * ac[k];
+        return 6;
+    }
+    double va = d3 * d6 - d5 * d4;
+    if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+        double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        for (int k = 0; k < 3; ++k) q[k] = b[k] + w * (c[k] - b[k]);
+        return 5;
+    }
+    double den = 1.0 / ((va + vb) + vc);
+    double v = vb * den, w = vc * den;
+    for (int k = 0; k < 3; ++k) q[k] = (a[k] + ab[k] * v) + ac[k] * w;
+    return 0;
+}
+
+double or_mesh_sdf(const double x[3]) {
+    double best = 0.0, bq[3] = {0.0, 0.0, 0.0};
+    int bt = -1, breg = 0;
+    for (int t = 0; t < g_mesh.nt; ++t) {
+        const int32_t* tv = g_mesh.T + 3 * t;
+        double q[3];
+        int reg = tri_closest(g_mesh.V + 3 * tv[0], g_mesh.V + 3 * tv[1], g_mesh.V + 3 * tv[2], x, q);
+        double e0 = x[0] - q[0], e1 = x[1] - q[1], e2 = x[2] - q[2];
+        double d2 = (e0 * e0 + e1 * e1) + e2 * e2;
+        if (bt < 0 || d2 < best) {
+            best = d2;
+            bt = t;
+            breg = reg;
+            memcpy(bq, q, sizeof(bq));
+        }
+    }
+    if (bt < 0) return INFINITY;
+    double d = sqrt(best);
+    const double* N;
+    if (breg == 0) N = g_mesh.fn + 3 * bt;
+    else if (breg <= 3) N = g_mesh.vn + 3 * g_mesh.T[3 * bt + breg - 1];
+    else N = g_mesh.en + 9 * bt + 3 * (breg - 4);
+    double s = ((x[0] - bq[0]) * N[0] + (x[1] - bq[1]) * N[1]) + (x[2] - bq[2]) * N[2];
+    return s < 0.0 ? -d : d;
+}
+
+static int mesh_mode(int32_t n_prims) { return n_prims == 0 && g_mesh.nt > 0; }
+
 /* union = min over the primitives, in order; then the leak post-operation
  * (include/sg.h SG_LEAK; models the wrong signs of a triangle-mesh SDF on
  * leaky input): f -> -f strictly inside any leak ball where
  * |f| >= margin. */
 double or_sdf(const or_prim* prims, int32_t n_prims, const double x[3]) {
+    if (mesh_mode(n_prims)) return or_mesh_sdf(x);
     double f = INFINITY;
     int first = 1;
     for (int i = 0; i < n_prims; ++i) {
@@ -304,6 +461,11 @@ int64_t or_compact(const or_grid* g, const uint8_t* cat, uint32_t* bg, uint32_t*
 static inline uint32_t far_pkg_virtual(const or_grid* g, const or_prim* prims, int32_t n_prims,
                                        int64_t cx, int64_t cy, int64_t cz) {
     double x[3];
+    if (mesh_mode(n_prims)) { /* R-24: sign of the nearest in-domain cell */
+        cx = cx < 0 ? 0 : (cx >= g->n[0] ? g->n[0] - 1 : cx);
+        cy = cy < 0 ? 0 : (cy >= g->n[1] ? g->n[1] - 1 : cy);
+        cz = cz < 0 ? 0 : (cz >= g->n[2] ? g->n[2] - 1 : cz);
+    }
     cell_centre(g, cx, cy, cz, x);
     return or_sdf(prims, n_prims, x) < 0.0 ? 0u : 1u;
 }

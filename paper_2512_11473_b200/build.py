@@ -34,6 +34,7 @@ UNITS = {
     "sg_relax.cu": [],
     "sg_sign.cu": [],
     "sg_clean.cu": [],
+    "sg_mesh.cu": ["-fmad=false"],
 }
 
 

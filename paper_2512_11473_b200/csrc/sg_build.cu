@@ -410,7 +410,14 @@ __global__ void __launch_bounds__(256) k_nb(GridC gc, const Geom* __restrict__ g
         const int qx = (int)(L[u] - r * nx) + ox, qy = (int)(r % ny) + oy, qz = (int)(r / ny) + oz;
         if (EDGE &&
             (qx < 0 || qy < 0 || qz < 0 || qx >= gc.n[0] || qy >= gc.n[1] || qz >= gc.n[2])) {
-            v[u] = virtual_sign(gc.lower[0], gc.lower[1], gc.lower[2], gc.cell, geom, qx, qy, qz);
+            if (geom->mesh_nt) {  // mesh: sign of the nearest in-domain cell
+                const int cx = min(max(qx, 0), gc.n[0] - 1), cy = min(max(qy, 0), gc.n[1] - 1);
+                const int cz = min(max(qz, 0), gc.n[2] - 1);
+                v[u] = ((__ldg(b.neg + b.idx(gc, cz, cy, cx >> 5)) >> (cx & 31)) & 1u) ? 0u : 1u;
+            } else {
+                v[u] = virtual_sign(gc.lower[0], gc.lower[1], gc.lower[2], gc.cell, geom, qx, qy,
+                                    qz);
+            }
         } else if (qz >= gc.zs_lo && qz < gc.zs_hi) {
             v[u] = __ldg(bg + (int64_t)(qz - gc.zs_lo) * gc.plane + (int64_t)qy * gc.n[0] + qx);
         } else {
@@ -533,8 +540,16 @@ static void check_desc(const sg_desc* d, const sg_geometry* g) {
     SG_ARG(d->cell > 0.0 && std::isfinite(d->cell), "sg_build: cell must be > 0");
     SG_ARG(d->dtype == SG_F32 || d->dtype == SG_F64, "sg_build: unknown dtype");
     SG_ARG(d->init_scale >= 0.0 && d->far >= 0.0, "sg_build: negative init_scale or far");
-    SG_ARG(g->prims != nullptr && g->n_prims >= 1 && g->n_prims <= SG_MAX_PRIMS,
-           "sg_build: need 1..16 primitives");
+    SG_ARG(g->n_prims >= 0 && g->n_prims <= SG_MAX_PRIMS && (g->n_prims == 0 || g->prims),
+           "sg_build: need 0..16 primitives");
+    if (g->n_tris > 0) {
+        SG_ARG(g->n_prims == 0, "sg_build: a mesh geometry takes no primitives");
+        SG_ARG(g->verts != nullptr && g->tris != nullptr && g->n_verts >= 3,
+               "sg_build: mesh needs vertices and triangles");
+        for (int64_t i = 0; i < 3LL * g->n_tris; ++i)
+            SG_ARG(g->tris[i] >= 0 && g->tris[i] < g->n_verts, "sg_build: triangle index out of range");
+        return;
+    }
     int n_union = 0;
     for (int i = 0; i < g->n_prims; ++i) {
         SG_ARG(g->prims[i].kind >= SG_SPHERE && g->prims[i].kind <= SG_LEAK,
@@ -546,7 +561,7 @@ static void check_desc(const sg_desc* d, const sg_geometry* g) {
             ++n_union;
         }
     }
-    SG_ARG(n_union >= 1, "sg_build: need at least one non-leak primitive");
+    SG_ARG(n_union >= 1, "sg_build: need at least one non-leak primitive (or a mesh)");
 }
 
 // union primitives in their given order; SG_LEAK entries to the post-op list
@@ -679,7 +694,21 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         int64_t* tile_off = (int64_t*)(scratch + sz_act + sz_cnt);
         unsigned long long* d_core = (unsigned long long*)(tile_off + n_tiles + 1);
         SG_CUDA(cudaMemsetAsync(d_core, 0, 2 * sizeof(unsigned long long), s));
-        launch_tag(gc, g->geom, zt_lo, zt_hi, W, core_w, neg_w, s);
+        const bool mesh = geom->n_tris > 0;
+        MeshDev md;
+        if (mesh) {
+            // NEXT-4: exact distances near the surface from per-cell triangle
+            // bins; signs of the cells beyond the bin radius by the coarse
+            // sign flood, seeded by the cells within it
+            SG_ARG(slab == nullptr, "sg_build: mesh geometries need a single-domain grid");
+            md = mesh_prepare(gc, geom, g->geom, s);
+            uint32_t* known_w = (uint32_t*)dalloc(sizeof(uint32_t) * tag_words, s);
+            launch_tag_mesh(gc, g->geom, W, core_w, neg_w, known_w, s);
+            cell_flood(gc.n[0], W, gc.n[1], zt_hi - zt_lo, known_w, neg_w, s);
+            SG_CUDA(cudaFreeAsync(known_w, s));
+        } else {
+            launch_tag(gc, g->geom, zt_lo, zt_hi, W, core_w, neg_w, s);
+        }
         const Bits bits{core_w, neg_w, W, zt_lo};
         k_count<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, bits, nwords, act_w, tile_count, d_core);
         SG_LAUNCHED();
@@ -754,13 +783,17 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         SG_LAUNCHED();
         SG_CUDA(cudaEventRecord(ev_join, side));
         const unsigned pb = (unsigned)ceil_div(n_pkg * 16, 256);
-        if (g->dtype == SG_F64)
-            k_phi_init<double><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
-                                                  (double*)g->phi[0], (double*)g->phi[1]);
-        else
-            k_phi_init<float><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
-                                                 (float*)g->phi[0], (float*)g->phi[1]);
-        SG_LAUNCHED();
+        if (mesh) {
+            launch_phi_init_mesh(gc, g->geom, g->meta_cell, n_pkg, g->dtype, g->phi[0], g->phi[1], s);
+        } else {
+            if (g->dtype == SG_F64)
+                k_phi_init<double><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
+                                                      (double*)g->phi[0], (double*)g->phi[1]);
+            else
+                k_phi_init<float><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
+                                                     (float*)g->phi[0], (float*)g->phi[1]);
+            SG_LAUNCHED();
+        }
         SG_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
         g->cur = 0;
 
@@ -779,6 +812,10 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
 
         SG_CUDA(cudaFreeAsync(scratch, s));
         if (d_geom) SG_CUDA(cudaFreeAsync(d_geom, s));
+        if (mesh) {
+            mesh_release(md, s);
+            g->geom.mesh_nt = 0;  // device mesh arrays are gone
+        }
 
         *out = g.release();
     });
@@ -906,6 +943,7 @@ extern "C" sg_status sg_plane_counts(const sg_desc* desc, const sg_geometry* geo
                                      int32_t z_hi, int64_t* counts, void* stream) {
     return guard([&] {
         check_desc(desc, geom);
+        SG_ARG(geom->n_tris == 0, "sg_plane_counts: mesh geometries are single-domain only");
         SG_ARG(counts != nullptr, "sg_plane_counts: null counts");
         SG_ARG(z_lo >= 0 && z_lo <= z_hi && z_hi <= desc->n[2], "sg_plane_counts: bad plane range");
         check_device();

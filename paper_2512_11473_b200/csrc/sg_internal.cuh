@@ -22,6 +22,18 @@ struct Geom {
     int32_t kind[SG_MAX_PRIMS];
     double p[SG_MAX_PRIMS][12];
     double leak[SG_MAX_PRIMS][5];  // cx cy cz r margin
+    // NEXT-4 closed triangle mesh (device arrays, valid during sg_build);
+    // mesh_nt == 0: the union of the primitives is the geometry
+    int32_t mesh_nt = 0, mesh_nv = 0;
+    const double* mv = nullptr;         // [nv][3] vertices
+    const int32_t* mt = nullptr;        // [nt][3] ccw from outside
+    const double* mfn = nullptr;        // [nt][3] unit face normals
+    const double* men = nullptr;        // [nt][3 edges][3] edge pseudonormals
+    const double* mvn = nullptr;        // [nv][3] vertex pseudonormals
+    const double* msph = nullptr;       // [nt][4] bounding sphere (centroid, radius)
+    const uint32_t* bin_off = nullptr;  // [cells + 1] CSR of triangles per cell
+    const uint32_t* bin_tri = nullptr;
+    double mesh_rb = 0.0;               // bin radius: exact below it
 };
 
 // Grid constants passed by value to every kernel.
@@ -152,4 +164,22 @@ void launch_gradient(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t s
 void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void* grad,
                   unsigned long long* oob, cudaStream_t s);
 void launch_table1(sg_grid* g, int32_t op, double value, cudaStream_t s);
+
+// NEXT-4 triangle mesh (sg_mesh.cu): device copies, pseudonormals, per-cell
+// triangle bins; fills the mesh fields of `g`
+struct MeshDev {
+    std::vector<void*> allocs;
+    uint32_t bin_entries = 0;
+};
+MeshDev mesh_prepare(const GridC& gc, const sg_geometry* geom, Geom& g, cudaStream_t s);
+void mesh_release(MeshDev& m, cudaStream_t s);
+void launch_tag_mesh(const GridC& gc, const Geom& g, int32_t W, uint32_t* core_w, uint32_t* neg_w,
+                     uint32_t* known_w, cudaStream_t s);
+void launch_phi_init_mesh(const GridC& gc, const Geom& g, const uint32_t* meta_cell,
+                          int64_t n_pkg, int32_t dtype, void* phi0, void* phi1, cudaStream_t s);
+// coarse sign flood of the sign correction (sg_sign.cu) on tagging bitmasks
+// [nz][ny][W]: cells with a known bit keep their neg bit, the others take it
+// from the flood; returns the number of sweeps that signed something
+int cell_flood(int32_t nx, int32_t W, int32_t ny, int32_t nz, const uint32_t* known, uint32_t* neg,
+               cudaStream_t s);
 }  // namespace sg

@@ -340,6 +340,35 @@ static int run_sweeps(F&& launch, int cap, int* dflags, cudaStream_t s) {
     return signed_sweeps;
 }
 
+// coarse flood on tagging bitmasks for the mesh build (see sg_internal.cuh)
+int cell_flood(int32_t nx, int32_t W, int32_t ny, int32_t nz, const uint32_t* known, uint32_t* neg,
+               cudaStream_t s) {
+    const int64_t nwords = (int64_t)W * ny * nz;
+    SG_ARG(nwords < (1LL << 31), "cell flood: too many cells");
+    const size_t cw = sizeof(uint2) * (size_t)nwords;
+    char* tmp = (char*)dalloc(2 * cw + 256 * sizeof(int) + (size_t)nwords, s);
+    uint2* cs[2] = {(uint2*)tmp, (uint2*)(tmp + cw)};
+    int* dflags = (int*)(tmp + 2 * cw);
+    uint8_t* stamp = (uint8_t*)(dflags + 256);
+    SG_CUDA(cudaMemsetAsync(stamp, 0, (size_t)nwords, s));
+    const unsigned cb = (unsigned)ceil_div(nwords, 256);
+    k_cell_pack<<<cb, 256, 0, s>>>((uint32_t)nwords, known, neg, cs[0]);
+    SG_LAUNCHED();
+    const unsigned cbs = sweep_blocks(nwords);
+    const int sw = run_sweeps(
+        [&](int j, const int* prev, int* cur) {
+            k_cell_sweep<<<cbs, 256, 0, s>>>(nx, (uint32_t)W, (uint32_t)ny, (uint32_t)nz,
+                                            (uint32_t)nwords, j, cs[j & 1], cs[(j + 1) & 1],
+                                            stamp, prev, cur);
+            SG_LAUNCHED();
+        },
+        0, dflags, s);
+    k_cell_unpack<<<cb, 256, 0, s>>>((uint32_t)nwords, cs[sw & 1], neg);
+    SG_LAUNCHED();
+    SG_CUDA(cudaFreeAsync(tmp, s));
+    return sw;
+}
+
 }  // namespace sg
 
 using namespace sg;

@@ -44,7 +44,9 @@ class sg_prim(C.Structure):
 
 
 class sg_geometry(C.Structure):
-    _fields_ = [("prims", C.POINTER(sg_prim)), ("n_prims", C.c_int32), ("pad", C.c_int32)]
+    _fields_ = [("prims", C.POINTER(sg_prim)), ("n_prims", C.c_int32), ("pad", C.c_int32),
+                ("verts", C.POINTER(C.c_double)), ("tris", C.POINTER(C.c_int32)),
+                ("n_verts", C.c_int32), ("n_tris", C.c_int32)]
 
 
 class sg_desc(C.Structure):
@@ -151,13 +153,23 @@ def make_desc(w) -> tuple:
     d.dtype = SG_F64 if w.dtype in ("f64", "float64") else SG_F32
     d.far = float(getattr(w, "far", 0.0) or 0.0)
     d.init_scale = float(getattr(w, "init_scale", 1.0) or 1.0)
-    prims = (sg_prim * len(w.prims))()
+    prims = (sg_prim * max(1, len(w.prims)))()
     for i, pr in enumerate(w.prims):
         prims[i].kind = int(pr.kind)
         for j, v in enumerate(pr.p):
             prims[i].p[j] = float(v)
     geom = sg_geometry(C.cast(prims, C.POINTER(sg_prim)), len(w.prims), 0)
-    return d, geom, prims
+    keep = [prims]
+    mesh = getattr(w, "mesh", None)
+    if mesh is not None:
+        verts = (C.c_double * len(mesh.verts))(*mesh.verts)
+        tris = (C.c_int32 * len(mesh.tris))(*mesh.tris)
+        geom.verts = C.cast(verts, C.POINTER(C.c_double))
+        geom.tris = C.cast(tris, C.POINTER(C.c_int32))
+        geom.n_verts = len(mesh.verts) // 3
+        geom.n_tris = len(mesh.tris) // 3
+        keep += [verts, tris]
+    return d, geom, keep
 
 
 # ------------------------------------------------------------ raw C calls --

@@ -63,3 +63,8 @@ if [[ $what == kint ]]; then
   timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench.json 2> gpurun_out/bench.err
   timeout 600 ncu --metrics gpu__time_duration.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum --clock-control none --csv -k regex:k_kint --log-file gpurun_out/launch_kint.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 fi
+if [[ $what == mesh ]]; then
+  timeout 900 python -m pytest tests/test_mesh_gpu.py -q -x -rf > gpurun_out/pytest_mesh.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_mesh.log
+  timeout 600 python scripts/mesh_bench.py 4 5 6 > gpurun_out/mesh_bench.json 2> gpurun_out/mesh_bench.err
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_mesh.csv python scripts/mesh_bench.py 5 > /dev/null 2>&1
+fi

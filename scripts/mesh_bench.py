@@ -1,0 +1,40 @@
+"""Build time of triangle-mesh geometries (NEXT-4): icospheres at the C2
+resolution (128^3 cells x 4^3), fp32.  One JSON line per mesh.
+
+python scripts/mesh_bench.py [levels ...]
+"""
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import workloads as W  # noqa: E402
+from paper_2512_11473_b200 import sg  # noqa: E402
+
+
+def run(level, n=128, reps=5):
+    w = W.mesh_workload(f"ico{level}", W.icosphere(level, rot=0.4), n, "f32")
+    stream = torch.cuda.current_stream()
+    ms = []
+    for k in range(reps + 2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        g = sg.Grid(w, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if k >= 2:
+            ms.append(e0.elapsed_time(e1))
+        info = g.info
+        g.close()
+    t = sorted(ms)[len(ms) // 2]
+    return {"mesh": f"icosphere level {level}", "triangles": w.mesh.n_tris, "grid": f"{n}^3 cells",
+            "active_points": (info["n_pkg"] - 2) * 64, "build_ms": t, "ms_all": ms,
+            "note": "sg_build incl. mesh upload, pseudonormals (host), binning, tagging, sign "
+                    "flood, compaction, neighbours, initial phi"}
+
+
+if __name__ == "__main__":
+    for lv in [int(a) for a in sys.argv[1:]] or [4, 5, 6]:
+        print(json.dumps(run(lv)), flush=True)

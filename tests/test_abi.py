@@ -42,7 +42,7 @@ def test_exports_every_declared_symbol(sg):
 
 
 def test_abi_version(sg):
-    assert sg.sg_abi_version() == 1
+    assert sg.sg_abi_version() == 2
     assert sg.sg_launch_count() == 0
 
 

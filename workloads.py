@@ -30,6 +30,23 @@ class Prim:
 
 
 @dataclass(frozen=True)
+class Mesh:
+    """Closed triangle mesh (NEXT-4 input): vertex coordinates flattened
+    (x0, y0, z0, x1, ...) and triangles as vertex-index triples flattened,
+    counter-clockwise seen from outside (outward normals)."""
+    verts: tuple
+    tris: tuple
+
+    @property
+    def n_verts(self) -> int:
+        return len(self.verts) // 3
+
+    @property
+    def n_tris(self) -> int:
+        return len(self.tris) // 3
+
+
+@dataclass(frozen=True)
 class Workload:
     name: str
     n: tuple  # background cells per axis
@@ -44,6 +61,7 @@ class Workload:
     h_ratio: float = 1.3
     particles: str = ""  # "" | "prism_lattice" | "sphere_lattice"
     notes: str = ""
+    mesh: Mesh | None = None  # NEXT-4: replaces the union of prims when set
 
     @property
     def dx(self) -> float:
@@ -115,6 +133,63 @@ def fins(n: int = 32, dtype: str = "f64", thin: float = 0.5, thick: float = 4.0)
                     prims=(Prim(BOX, (0.5, 0.5, 0.3, 1.0, 1.0, 0.1)),
                            Prim(BOX, (0.5, 0.3, 0.5, 1.0, 0.5 * thin * h, 0.1)),
                            Prim(BOX, (0.5, 0.7, 0.5, 1.0, 0.5 * thick * h, 0.1))))
+
+
+# ------------------------------------------------------------- meshes -------
+
+def icosphere(level: int, c=(0.5, 0.5, 0.5), r: float = 0.3, rot: float = 0.0) -> Mesh:
+    """Icosahedron subdivided `level` times, vertices projected onto the
+    sphere (c, r) (20 * 4^level triangles, ccw from outside); `rot` rotates it
+    about the axis (1, 2, 3) so no edge is grid-aligned."""
+    t = (1.0 + 5 ** 0.5) / 2.0
+    v = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t),
+         (0, 1, -t), (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    v = [np.asarray(p, float) / np.linalg.norm(p) for p in v]
+    f = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4),
+         (11, 10, 2), (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8),
+         (3, 8, 9), (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    for _ in range(level):
+        mid = {}
+
+        def m(a, b):
+            k = (min(a, b), max(a, b))
+            if k not in mid:
+                p = v[a] + v[b]
+                v.append(p / np.linalg.norm(p))
+                mid[k] = len(v) - 1
+            return mid[k]
+        nf = []
+        for a, b, cc in f:
+            ab, bc, ca = m(a, b), m(b, cc), m(cc, a)
+            nf += [(a, ab, ca), (b, bc, ab), (cc, ca, bc), (ab, bc, ca)]
+        f = nf
+    P = np.array(v)
+    if rot:
+        k = np.array([1.0, 2.0, 3.0]) / 14 ** 0.5
+        K = np.array([[0, -k[2], k[1]], [k[2], 0, -k[0]], [-k[1], k[0], 0]])
+        R = np.eye(3) + math.sin(rot) * K + (1 - math.cos(rot)) * K @ K
+        P = P @ R.T
+    P = np.asarray(c) + r * P
+    return Mesh(tuple(float(x) for x in P.ravel()), tuple(int(i) for tri in f for i in tri))
+
+
+def box_mesh(c=(0.5, 0.5, 0.5), b=(0.2, 0.15, 0.25)) -> Mesh:
+    """Axis-aligned box of half extents b as 12 triangles (ccw from outside)."""
+    V = [(c[0] + sx * b[0], c[1] + sy * b[1], c[2] + sz * b[2])
+         for sz in (-1, 1) for sy in (-1, 1) for sx in (-1, 1)]
+    # vertex index = ix + 2 iy + 4 iz
+    F = [(0, 2, 3), (0, 3, 1),  # z-
+         (4, 5, 7), (4, 7, 6),  # z+
+         (0, 1, 5), (0, 5, 4),  # y-
+         (2, 6, 7), (2, 7, 3),  # y+
+         (0, 4, 6), (0, 6, 2),  # x-
+         (1, 3, 7), (1, 7, 5)]  # x+
+    return Mesh(tuple(float(x) for p in V for x in p), tuple(i for t in F for i in t))
+
+
+def mesh_workload(name: str, mesh: Mesh, n: int, dtype: str = "f64") -> Workload:
+    """A mesh geometry on an n^3 grid of the unit domain (NEXT-4)."""
+    return Workload(name, (n, n, n), 1.0 / n, dtype=dtype, mesh=mesh)
 
 
 # Leak balls (cx, cy, cz, r) in the unit domain of the configs: one inside
