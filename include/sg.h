@@ -227,6 +227,24 @@ typedef struct {
 sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, const sg_slab* slab,
                    void* stream, sg_grid** out);
 
+/* NEXT-4 multi-resolution ("several layers with successively
+ * doubled resolutions are established ... subsequent layers that each with
+ * doubled resolution are initialized based on the preceding coarser layer";
+ * "For successive layers, only the cells covered by the coarse
+ * core cells will be evaluated"): build the layer with cell size
+ * parent.cell / 2 and 2 n cells per axis (same lower corner, dtype,
+ * init_scale and far setting) of `geom` from `parent`.  Cells under a parent
+ * core cell are evaluated; every other cell takes its parent cell's sign
+ * (after sg_sign_correct on the parent: the corrected sign).  The result is
+ * the grid a direct sg_build at the finer resolution gives: a fine core cell
+ * (|f| < l_f) always has a core parent (|f(parent centre)| < l_f +
+ * sqrt(3)/2 l_f < 2 l_f), and a non-core parent cell has one sign over its
+ * whole cell.  For a mesh geometry no cell beyond the bin radius is ever
+ * evaluated, so no sign flood runs on refined layers.  Single-domain parent
+ * grids; the parent must stay alive during the call.  Errors as sg_build. */
+sg_status sg_build_refined(const sg_grid* parent, const sg_geometry* geom, void* stream,
+                           sg_grid** out);
+
 /* `iters` Jacobi sweeps of upwind Godunov reinitialisation on every active
  * data point (reading R-12; phi' = phi - cfl dx s (|grad phi|_G - 1)),
  * double-buffered; inactive and singular data stay unchanged.  Neighbours

@@ -149,6 +149,42 @@ __global__ void __launch_bounds__(128, 4) k_tag_cull(GridC gc, Geom geom, int32_
     }
 }
 
+// K1 of a refined layer (NEXT-4 multi-resolution: "For
+// successive layers, only the cells covered by the coarse core cells will be
+// evaluated"): a fine cell under a parent core cell is evaluated; any other
+// takes its parent cell's sign.  Equal to full tagging: a fine core cell
+// (|f| < l_f) has |f(parent centre)| < l_f + sqrt(3)/2 l_f < 2 l_f, a core
+// parent; a non-core parent (|f| >= 2 l_f at its centre) has one sign over
+// its whole cell (1-Lipschitz, half-diagonal sqrt(3) l_f).
+__global__ void __launch_bounds__(256) k_tag_refine(GridC gc, Geom geom, int32_t W, ParentBits pb,
+                                                    uint32_t* __restrict__ core_w,
+                                                    uint32_t* __restrict__ neg_w) {
+    const int cx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int cy = blockIdx.y, cz = blockIdx.z;
+    const bool in = cx < gc.n[0];
+    bool core = false, neg = false;
+    if (in) {
+        const int px = cx >> 1;
+        const int64_t pw = ((int64_t)(cz >> 1) * (gc.n[1] >> 1) + (cy >> 1)) * pb.W + (px >> 5);
+        const bool pc = (__ldg(pb.core + pw) >> (px & 31)) & 1u;
+        neg = (__ldg(pb.neg + pw) >> (px & 31)) & 1u;
+        if (pc) {
+            const double f = sd_eval(geom, gc.lower[0] + ((double)cx + 0.5) * gc.cell,
+                                     gc.lower[1] + ((double)cy + 0.5) * gc.cell,
+                                     gc.lower[2] + ((double)cz + 0.5) * gc.cell);
+            core = fabs(f) < gc.cell;
+            neg = f < 0.0;
+        }
+    }
+    const uint32_t cw = __ballot_sync(0xffffffffu, in && core);
+    const uint32_t nw = __ballot_sync(0xffffffffu, in && neg);
+    if ((threadIdx.x & 31) == 0 && cx < gc.n[0]) {
+        const int64_t i = ((int64_t)cz * gc.n[1] + cy) * W + (cx >> 5);
+        core_w[i] = cw;
+        neg_w[i] = nw;
+    }
+}
+
 // K1 without the cull (band-dense domains): a thread owns an (x, y) column of
 // 4 planes, a warp 32 consecutive x-cells.
 __global__ void __launch_bounds__(256) k_tag(GridC gc, Geom geom, int32_t zt_lo, int32_t zt_hi,
@@ -634,15 +670,16 @@ using namespace sg;
 
 // ------------------------------------------------------------------- ABI ---
 
-extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, const sg_slab* slab,
-                              void* stream, sg_grid** out) {
-    return guard([&] {
+static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_slab* slab,
+                       const sg_grid* parent, void* stream, sg_grid** out) {
+    {
         SG_ARG(out != nullptr, "sg_build: null out");
         *out = nullptr;
         check_desc(desc, geom);
         const int dev = check_device();
         cudaStream_t s = (cudaStream_t)stream;
         auto g = std::make_unique<sg_grid>();
+        g->desc = *desc;
         g->device = dev;
         g->gc = make_gridc(desc);
         g->geom = make_geom(geom);
@@ -696,7 +733,17 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         SG_CUDA(cudaMemsetAsync(d_core, 0, 2 * sizeof(unsigned long long), s));
         const bool mesh = geom->n_tris > 0;
         MeshDev md;
-        if (mesh) {
+        if (parent) {
+            const ParentBits pb{parent->cell_core, parent->cell_neg, parent->tag_W};
+            if (mesh) {
+                md = mesh_prepare(gc, geom, g->geom, s);
+                launch_tag_refine_mesh(gc, g->geom, W, pb, core_w, neg_w, s);
+            } else {
+                dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1], (unsigned)gc.n[2]);
+                k_tag_refine<<<grid, 256, 0, s>>>(gc, g->geom, W, pb, core_w, neg_w);
+                SG_LAUNCHED();
+            }
+        } else if (mesh) {
             // NEXT-4: exact distances near the surface from per-cell triangle
             // bins; signs of the cells beyond the bin radius by the coarse
             // sign flood, seeded by the cells within it
@@ -818,6 +865,28 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
         }
 
         *out = g.release();
+    }
+}
+
+extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, const sg_slab* slab,
+                              void* stream, sg_grid** out) {
+    return guard([&] { build_impl(desc, geom, slab, nullptr, stream, out); });
+}
+
+extern "C" sg_status sg_build_refined(const sg_grid* parent, const sg_geometry* geom, void* stream,
+                                      sg_grid** out) {
+    return guard([&] {
+        SG_ARG(parent != nullptr && geom != nullptr, "sg_build_refined: null argument");
+        SG_ARG(parent->gc.zs_lo == 0 && parent->gc.zs_hi == parent->gc.n[2] && parent->id_base == 2,
+               "sg_build_refined: single-domain parent grids only");
+        sg_desc d = parent->desc;
+        d.cell = 0.5 * parent->desc.cell;
+        for (int k = 0; k < 3; ++k) {
+            SG_ARG(parent->desc.n[k] <= (1 << 30), "sg_build_refined: grid too large");
+            d.n[k] = 2 * parent->desc.n[k];
+        }
+        // a default far field scales with the layer's cell size (R-4)
+        build_impl(&d, geom, nullptr, parent, stream, out);
     });
 }
 

@@ -114,6 +114,7 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 }  // namespace sg
 
 struct sg_grid {
+    sg_desc desc;  // as built (the refined layer derives its own from it)
     sg::GridC gc;
     sg::Geom geom;
     int32_t dtype = SG_F32;
@@ -175,6 +176,15 @@ MeshDev mesh_prepare(const GridC& gc, const sg_geometry* geom, Geom& g, cudaStre
 void mesh_release(MeshDev& m, cudaStream_t s);
 void launch_tag_mesh(const GridC& gc, const Geom& g, int32_t W, uint32_t* core_w, uint32_t* neg_w,
                      uint32_t* known_w, cudaStream_t s);
+// NEXT-4 multi-resolution: tagging of a layer refined from `parent` (cells
+// under a parent core cell evaluated, the others inherit the parent's sign)
+struct ParentBits {
+    const uint32_t* core;
+    const uint32_t* neg;
+    int32_t W;  // words per parent row
+};
+void launch_tag_refine_mesh(const GridC& gc, const Geom& g, int32_t W, ParentBits pb,
+                            uint32_t* core_w, uint32_t* neg_w, cudaStream_t s);
 void launch_phi_init_mesh(const GridC& gc, const Geom& g, const uint32_t* meta_cell,
                           int64_t n_pkg, int32_t dtype, void* phi0, void* phi1, cudaStream_t s);
 // coarse sign flood of the sign correction (sg_sign.cu) on tagging bitmasks

@@ -307,6 +307,47 @@ __global__ void __launch_bounds__(256) k_tag_mesh(GridC gc, Geom g, int32_t W,
     }
 }
 
+// K1 of a refined layer for a mesh (NEXT-4 multi-resolution):
+// only cells under a parent core cell are evaluated (all within 2.9 l_c < rb
+// of the surface: exact); the others take the sign of their parent cell
+__global__ void __launch_bounds__(256) k_tag_refine_mesh(GridC gc, Geom g, int32_t W, ParentBits pb,
+                                                         uint32_t* __restrict__ core_w,
+                                                         uint32_t* __restrict__ neg_w) {
+    const int cx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int cy = blockIdx.y, cz = blockIdx.z;
+    const bool in = cx < gc.n[0];
+    bool core = false, neg = false;
+    if (in) {
+        const int px = cx >> 1;
+        const int64_t pw = ((int64_t)(cz >> 1) * (gc.n[1] >> 1) + (cy >> 1)) * pb.W + (px >> 5);
+        const bool pc = (__ldg(pb.core + pw) >> (px & 31)) & 1u;
+        neg = (__ldg(pb.neg + pw) >> (px & 31)) & 1u;
+        if (pc) {
+            const double p[3] = {gc.lower[0] + ((double)cx + 0.5) * gc.cell,
+                                 gc.lower[1] + ((double)cy + 0.5) * gc.cell,
+                                 gc.lower[2] + ((double)cz + 0.5) * gc.cell};
+            bool known;
+            const double f = mesh_sdf(g, ((int64_t)cz * gc.n[1] + cy) * gc.n[0] + cx, p, known);
+            core = fabs(f) < gc.cell;
+            neg = f < 0.0;
+        }
+    }
+    const uint32_t cw = __ballot_sync(0xffffffffu, in && core);
+    const uint32_t nw = __ballot_sync(0xffffffffu, in && neg);
+    if ((threadIdx.x & 31) == 0 && cx < gc.n[0]) {
+        const int64_t i = ((int64_t)cz * gc.n[1] + cy) * W + (cx >> 5);
+        core_w[i] = cw;
+        neg_w[i] = nw;
+    }
+}
+
+void launch_tag_refine_mesh(const GridC& gc, const Geom& g, int32_t W, ParentBits pb,
+                            uint32_t* core_w, uint32_t* neg_w, cudaStream_t s) {
+    dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1], (unsigned)gc.n[2]);
+    k_tag_refine_mesh<<<grid, 256, 0, s>>>(gc, g, W, pb, core_w, neg_w);
+    SG_LAUNCHED();
+}
+
 // K4 for a mesh: phi = init_scale * f at the 64 data points of each active
 // package (every such point is within 3.4 l_c < rb of the surface: exact).
 // One 64-thread block per package, a thread per data point; the package's

@@ -27,7 +27,7 @@ _STATUS = {0: "SG_OK", 1: "SG_ERR_ARG", 2: "SG_ERR_OOM", 3: "SG_ERR_CUDA", 4: "S
            5: "SG_ERR_STATE", 6: "SG_ERR_DOMAIN"}
 
 # exported symbols declared in include/sg.h (checked by the CPU test suite)
-EXPORTS = ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
+EXPORTS = ("sg_build", "sg_build_refined", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
            "sg_sign_correct", "sg_clean", "sg_info", "sg_view",
            "sg_destroy", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
            "sg_last_error", "sg_abi_version", "sg_launch_count")
@@ -97,6 +97,7 @@ def lib():
         P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
         L.sg_build.argtypes = [C.POINTER(sg_desc), C.POINTER(sg_geometry), C.POINTER(sg_slab), P,
                                C.POINTER(P)]
+        L.sg_build_refined.argtypes = [P, C.POINTER(sg_geometry), P, C.POINTER(P)]
         L.sg_reinit.argtypes = [P, I32, D, P]
         L.sg_gradient.argtypes = [P, C.c_uint32, D, P]
         L.sg_probe.argtypes = [P, I64, P, P, P, P, P]
@@ -114,7 +115,7 @@ def lib():
         L.sg_last_error.restype = C.c_char_p
         L.sg_abi_version.restype = I32
         L.sg_launch_count.restype = C.c_uint64
-        for name in ("sg_build", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
+        for name in ("sg_build", "sg_build_refined", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
                      "sg_sign_correct", "sg_clean",
                      "sg_info",
                      "sg_view", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts"):
@@ -315,13 +316,26 @@ def _cached_desc(w):
 class Grid:
     """Owning handle around sg_build/sg_destroy with torch-friendly calls."""
 
-    def __init__(self, w, slab: tuple | None = None, stream=None):
+    def __init__(self, w, slab: tuple | None = None, stream=None, parent=None):
         self.w = w
         self.desc, self.geom, self._keep = _cached_desc(w)
+        if parent is not None:  # NEXT-4: layer refined from `parent`
+            out = C.c_void_p()
+            _check(lib().sg_build_refined(C.c_void_p(parent.handle), C.byref(self.geom),
+                                          _stream(stream), C.byref(out)))
+            self.handle = out.value
+            return
         sl = None
         if slab is not None:
             sl = sg_slab(int(slab[0]), int(slab[1]), int(slab[2]))
         self.handle = sg_build(self.desc, self.geom, sl, stream)
+
+    def refined(self, stream=None) -> "Grid":
+        """The next finer layer (cell / 2, 2 n cells per axis) built from this
+        grid (NEXT-4 multi-resolution, sg_build_refined)."""
+        w = self.w
+        wf = w.with_(name=w.name + "r", n=tuple(2 * k for k in w.n), cell=0.5 * w.cell)
+        return Grid(wf, stream=stream, parent=self)
 
     @property
     def info(self) -> dict:

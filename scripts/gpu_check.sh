@@ -65,6 +65,8 @@ if [[ $what == kint ]]; then
 fi
 if [[ $what == mesh ]]; then
   timeout 900 python -m pytest tests/test_mesh_gpu.py -q -x -rf > gpurun_out/pytest_mesh.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_mesh.log
+  timeout 900 python -m pytest tests/test_refine_gpu.py -q -x -rf > gpurun_out/pytest_refine.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_refine.log
   timeout 600 python scripts/mesh_bench.py 4 5 6 > gpurun_out/mesh_bench.json 2> gpurun_out/mesh_bench.err
+  timeout 600 python scripts/mesh_bench.py chain 4 5 6 >> gpurun_out/mesh_bench.json 2>> gpurun_out/mesh_bench.err
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_mesh.csv python scripts/mesh_bench.py 5 > /dev/null 2>&1
 fi
