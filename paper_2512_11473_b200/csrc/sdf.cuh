@@ -15,6 +15,15 @@ __device__ __forceinline__ double sd_len3(double ex, double ey, double ez) {
     return sqrt((ex * ex + ey * ey) + ez * ez);
 }
 
+// sqrt(a*a + b*b) for a, b >= 0 with the IEEE result: in binary floating
+// point sqrt(fl(x*x)) == |x| when x*x neither overflows nor underflows, so a
+// zero term (exactly representable: 0*0 = +0) lets the square root go
+__device__ __forceinline__ double hyp2(double a, double b) {
+    if (b == 0.0 && (a == 0.0 || (a > 1e-150 && a < 1e150))) return a;
+    if (a == 0.0 && b > 1e-150 && b < 1e150) return b;
+    return sqrt(a * a + b * b);
+}
+
 __device__ __forceinline__ double sd_prim(int kind, const double* p, double x, double y,
                                           double z) {
     switch (kind) {
@@ -73,7 +82,7 @@ __device__ __forceinline__ double sd_prim(int kind, const double* p, double x, d
         const double hl = 0.5 * (p[7] - p[6]);
         const double qz = fabs(z - zc) - hl;
         const double a = fmax(dxy, 0.0), b = fmax(qz, 0.0);
-        return fmin(fmax(dxy, qz), 0.0) + sqrt(a * a + b * b);
+        return fmin(fmax(dxy, qz), 0.0) + hyp2(a, b);
     }
     default:
         return __longlong_as_double(0x7ff8000000000000ULL);  // NaN
@@ -172,7 +181,7 @@ __device__ __forceinline__ void sd_prim_col(int kind, const double* p, double x,
         for (int k = 0; k < NZ; ++k) {
             const double qz = fabs(z[k] - zc) - hl;
             const double b = fmax(qz, 0.0);
-            f[k] = fmin(fmax(dxy, qz), 0.0) + sqrt(a * a + b * b);
+            f[k] = fmin(fmax(dxy, qz), 0.0) + hyp2(a, b);
         }
         return;
     }
