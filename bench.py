@@ -166,6 +166,14 @@ def workload_name(w, n_part, order):
     return s
 
 
+def run_config(w, n_pkg, n_part, order, world):
+    """The `config` object of the JSON line (shared by both arms)."""
+    return {"workload": workload_name(w, n_part, order),
+            "n_packages": n_pkg - 2, "active_cells": (n_pkg - 2) * 64, "particles": n_part,
+            "l2": "flushed between steps (512 MiB write, outside the timed events)",
+            "parallelism": f"zslab{world}" if world > 1 else "1 GPU"}
+
+
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -295,10 +303,7 @@ def run_ours(args, rank, world, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": w.dtype, "data": "synthetic",
-        "config": {"workload": workload_name(w, n_part, args.order),
-                   "n_packages": n_pkg - 2, "active_cells": n_act, "particles": n_part,
-                   "l2": "flushed between steps (512 MiB write, outside the timed events)",
-                   "parallelism": f"zslab{world}" if world > 1 else "1 GPU"},
+        "config": run_config(w, n_pkg, n_part, args.order, world),
         "probes_per_s": n_part / (ms * 1e-3),
         "stages": stages,
         "step_ms_min_max": [float(step_ms.min()), float(step_ms.max())],
@@ -385,13 +390,17 @@ def run_reference(args, rank, world):
     dt = (time.perf_counter() - t0) / args.steps
     value = n_act * (sweeps + 1) / dt
     sample = (f"{sweeps} reinit sweeps + 1 gradient/normal sweep of the dense fp64 oracle on "
-              f"{w.name} per step ({n_act} active points per sweep); tables/init untimed")
+              f"{w.name} per step ({n_act} active points per sweep); tables/init untimed; the "
+              f"GPU step also builds the grid, runs {REINIT_ITERS} sweeps and probes")
+    n_part = 0
+    if w.particles:  # the same particle set the GPU arm probes (count only)
+        npdt = np.float32 if w.dtype == "f32" else np.float64
+        n_part = int(W.lattice_particles(w, seed=0, order=args.order, dtype=npdt).shape[0])
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic",
-           "config": {"workload": f"{w.name}: extruded prism 512^3 effective (CPU oracle sample)",
-                      "active_cells": n_act},
+           "config": run_config(w, t.n_pkg, n_part, args.order, world),
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.get_threads(),
                             "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
