@@ -670,6 +670,23 @@ using namespace sg;
 
 // ------------------------------------------------------------------- ABI ---
 
+// frees everything a failed build allocated (stream-ordered, errors ignored)
+struct BuildGuard {
+    sg_grid* g;
+    cudaStream_t s;
+    std::vector<void*> tmp;
+    MeshDev* md = nullptr;
+    bool done = false;
+    ~BuildGuard() {
+        if (done) return;
+        for (void* p : tmp) cudaFreeAsync(p, s);
+        if (md)
+            for (void* p : md->allocs) cudaFreeAsync(p, s);
+        if (g)
+            for (auto& a : g->allocs) cudaFreeAsync(a.first, s);
+    }
+};
+
 static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_slab* slab,
                        const sg_grid* parent, void* stream, sg_grid** out) {
     {
@@ -679,6 +696,7 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         const int dev = check_device();
         cudaStream_t s = (cudaStream_t)stream;
         auto g = std::make_unique<sg_grid>();
+        BuildGuard guard_mem{g.get(), s};
         g->desc = *desc;
         g->device = dev;
         g->gc = make_gridc(desc);
@@ -726,6 +744,7 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         g->zt_lo = zt_lo;
         g->zt_hi = zt_hi;
         char* scratch = (char*)dalloc(sz_act + sz_cnt + sz_off, s);
+        guard_mem.tmp.push_back(scratch);
         uint32_t* act_w = (uint32_t*)scratch;
         int32_t* tile_count = (int32_t*)(scratch + sz_act);
         int64_t* tile_off = (int64_t*)(scratch + sz_act + sz_cnt);
@@ -733,6 +752,7 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         SG_CUDA(cudaMemsetAsync(d_core, 0, 2 * sizeof(unsigned long long), s));
         const bool mesh = geom->n_tris > 0;
         MeshDev md;
+        guard_mem.md = &md;
         if (parent) {
             const ParentBits pb{parent->cell_core, parent->cell_neg, parent->tag_W};
             if (mesh) {
@@ -810,6 +830,7 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         Geom* d_geom = nullptr;
         if (counts[2]) {
             d_geom = (Geom*)dalloc(sizeof(Geom), s);
+            guard_mem.tmp.push_back(d_geom);
             SG_CUDA(cudaMemcpyAsync(d_geom, &g->geom, sizeof(Geom), cudaMemcpyHostToDevice, s));
         }
         // K3 (integer / L2 gathers) on a side stream concurrently with K4
@@ -864,6 +885,7 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
             g->geom.mesh_nt = 0;  // device mesh arrays are gone
         }
 
+        guard_mem.done = true;
         *out = g.release();
     }
 }

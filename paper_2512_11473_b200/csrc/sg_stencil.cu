@@ -549,7 +549,6 @@ __global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
     } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[i] = gx[i] = gy[i] = gz[i] = T(0);
-#pragma unroll
         // rows (oy, oz) grouped by (|oy|, |oz|) = (a, b): with the sign
         // butterfly of the (up to) four rows (+-a, +-b)
         //   S  = sum of the rows            -> K and G_x
