@@ -70,3 +70,10 @@ if [[ $what == mesh ]]; then
   timeout 600 python scripts/mesh_bench.py chain 4 5 6 >> gpurun_out/mesh_bench.json 2>> gpurun_out/mesh_bench.err
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_mesh.csv python scripts/mesh_bench.py 5 > /dev/null 2>&1
 fi
+if [[ $what == reinit4 ]]; then
+  timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or c3 or c5 or smoke or clean or sign" > gpurun_out/pytest_r4.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_r4.log
+  timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench.json 2> gpurun_out/bench.err
+  SG_REINIT8=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench8.json 2> /dev/null
+  timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> /dev/null
+  SG_REINIT8=1 timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3_8.json 2> /dev/null
+fi
