@@ -60,6 +60,17 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> str:
     if not force and up_to_date():
         return LIB
+    # one builder at a time (e.g. every rank of a torchrun job calls build())
+    import fcntl
+    os.makedirs(BUILD, exist_ok=True)
+    with open(os.path.join(BUILD, ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and up_to_date():
+            return LIB
+        return _build_locked(verbose, ptxas_info)
+
+
+def _build_locked(verbose: bool, ptxas_info: bool) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
     objs = []
