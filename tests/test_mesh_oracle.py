@@ -86,3 +86,34 @@ def test_box_mesh_grid_tables_equal_box_primitive(oracle_lib):
     np.testing.assert_array_equal(tm.bg, tp.bg)
     np.testing.assert_array_equal(tm.nb, tp.nb)
     np.testing.assert_allclose(om.phi_dense(), op.phi_dense(), rtol=0, atol=1e-12)
+
+
+def test_stl_round_trip(tmp_path, oracle_lib):
+    """STL (the paper's input) in and out: a box mesh written as binary
+    STL (fp32 coordinates) and as ASCII reads back to the same closed mesh,
+    whose SDF is still the box closed form."""
+    c, b = (0.5, 0.5, 0.5), (0.25, 0.125, 0.375)  # fp32-exact corners
+    m = W.box_mesh(c, b)
+    p = tmp_path / "box.stl"
+    W.write_stl(str(p), m)
+    r = W.read_stl(str(p))
+    assert r.n_tris == 12 and r.n_verts == 8
+    V = np.array(r.verts).reshape(-1, 3)
+    T = np.array(r.tris).reshape(-1, 3)
+    tri = V[T]
+    nrm = np.cross(tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0])
+    assert np.all((nrm * (tri.mean(1) - np.asarray(c))).sum(1) > 0)  # outward
+    asc = tmp_path / "box_ascii.stl"
+    with open(asc, "w") as fh:
+        fh.write("solid box\n")
+        for t in tri:
+            fh.write(" facet normal 0 0 0\n  outer loop\n")
+            for v in t:
+                fh.write(f"   vertex {float(v[0])!r} {float(v[1])!r} {float(v[2])!r}\n")
+            fh.write("  endloop\n endfacet\n")
+        fh.write("endsolid box\n")
+    r2 = W.read_stl(str(asc))
+    assert r2 == r
+    o = oracle_lib.Oracle(W.mesh_workload("stl", r, 8))
+    x = np.random.default_rng(6).uniform(0, 1, (5000, 3))
+    np.testing.assert_allclose(o.sdf(x), _box_sdf(x, c, b), rtol=0, atol=1e-12)

@@ -187,6 +187,44 @@ def box_mesh(c=(0.5, 0.5, 0.5), b=(0.2, 0.15, 0.25)) -> Mesh:
     return Mesh(tuple(float(x) for p in V for x in p), tuple(i for t in F for i in t))
 
 
+def read_stl(path: str, scale: float = 1.0, offset=(0.0, 0.0, 0.0)) -> Mesh:
+    """Closed triangle mesh from an STL file (binary or ASCII), the paper's
+    input format (P:474).  Vertices are merged by exact coordinate equality;
+    facet normals in the file are ignored (orientation comes from the vertex
+    order, counter-clockwise from outside); x -> scale * x + offset."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    tris = None
+    if len(data) >= 84:
+        n = int(np.frombuffer(data[80:84], "<u4")[0])
+        if 84 + 50 * n == len(data):  # binary
+            rec = np.frombuffer(data[84:], dtype=np.dtype([("n", "<f4", 3), ("v", "<f4", (3, 3)),
+                                                          ("a", "<u2")]), count=n)
+            tris = rec["v"].astype(np.float64)
+    if tris is None:  # ASCII
+        vals = [list(map(float, ln.split()[1:4])) for ln in data.decode("ascii", "replace").splitlines()
+                if ln.strip().startswith("vertex")]
+        tris = np.asarray(vals, np.float64).reshape(-1, 3, 3)
+    pts = tris.reshape(-1, 3) * scale + np.asarray(offset, np.float64)
+    uniq, inv = np.unique(pts, axis=0, return_inverse=True)
+    return Mesh(tuple(float(x) for x in uniq.ravel()), tuple(int(i) for i in inv.ravel()))
+
+
+def write_stl(path: str, mesh: Mesh) -> None:
+    """Binary STL of `mesh` (facet normals from the vertex order)."""
+    V = np.asarray(mesh.verts, np.float64).reshape(-1, 3)
+    T = np.asarray(mesh.tris, np.int64).reshape(-1, 3)
+    rec = np.zeros(len(T), dtype=np.dtype([("n", "<f4", 3), ("v", "<f4", (3, 3)), ("a", "<u2")]))
+    tri = V[T]
+    nrm = np.cross(tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0])
+    rec["n"] = nrm / np.maximum(np.linalg.norm(nrm, axis=1, keepdims=True), 1e-300)
+    rec["v"] = tri
+    with open(path, "wb") as fh:
+        fh.write(b"sgrid-b200 binary STL".ljust(80, b" "))
+        fh.write(np.uint32(len(T)).tobytes())
+        fh.write(rec.tobytes())
+
+
 def mesh_workload(name: str, mesh: Mesh, n: int, dtype: str = "f64") -> Workload:
     """A mesh geometry on an n^3 grid of the unit domain (NEXT-4)."""
     return Workload(name, (n, n, n), 1.0 / n, dtype=dtype, mesh=mesh)
