@@ -797,15 +797,55 @@ static void launch_kint_r(sg_grid* g, const T* phi, const KintC<T>& c, cudaStrea
     SG_LAUNCHED();
 }
 
+// library-internal side stream and fork/join events (one per host thread)
+static cudaStream_t grad_side_stream() {
+    static cudaStream_t st = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] { SG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); });
+    return st;
+}
+
 template <class T>
 static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t s) {
     const int64_t lo = g->own_lo, hi = g->own_hi;
     const T* phi = (const T*)g->phi[g->cur];
     const StC<T> c = stencil_consts<T>(g, 0.0);
     const size_t vec_bytes = (size_t)g->n_pkg * 192 * sizeof(T);
+    const bool want_g = fields & (SG_GRAD | SG_NORMAL), want_k = fields & SG_KINT;
     if ((fields & SG_GRAD) && !g->grad) g->grad = g->alloc((size_t)g->n_pkg * 256 * sizeof(T), s);
     if ((fields & SG_NORMAL) && !g->normal) g->normal = g->alloc(vec_bytes, s);
-    if (fields & (SG_GRAD | SG_NORMAL)) {
+    if (want_k && !g->kint) g->kint = g->alloc((size_t)g->n_pkg * 64 * sizeof(T), s);
+    if (want_k && !g->gkint) g->gkint = g->alloc(vec_bytes, s);
+    // K6 (HBM-write bound) and K7 (FP32 / shared-memory bound) only read phi:
+    // the kernel integrals run on a side stream concurrently with the gradient
+    cudaStream_t sk = s;
+    static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (want_g && want_k) {
+        if (!ev_fork) {
+            SG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+            SG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        }
+        sk = grad_side_stream();
+        SG_CUDA(cudaEventRecord(ev_fork, s));
+        SG_CUDA(cudaStreamWaitEvent(sk, ev_fork, 0));
+    }
+    if (want_k) {
+        // largest |o_k| of a tap: o_k < 2 h_ratio  ->  R = ceil(2 h_ratio) - 1
+        const int R = (int)std::ceil(2.0 * h_ratio) - 1;
+        double S = 0.0;
+        const KintC<T> kc = make_kint<T>(h_ratio, g->gc.dx, R, &S);
+        switch (R) {
+        case 0: launch_kint_r<T, 0>(g, phi, kc, sk); break;
+        case 1: launch_kint_r<T, 1>(g, phi, kc, sk); break;
+        case 2: launch_kint_r<T, 2>(g, phi, kc, sk); break;
+        default: launch_kint_r<T, 3>(g, phi, kc, sk); break;
+        }
+        k_singular<T><<<1, 128, 0, sk>>>((T*)g->kint, (T*)g->gkint, nullptr, nullptr, kc.S, T(0));
+        SG_LAUNCHED();
+        g->has_kint = true;
+        g->kernel_sum = S;
+    }
+    if (want_g) {
         T* gp = (fields & SG_GRAD) ? (T*)g->grad : nullptr;
         T* np = (fields & SG_NORMAL) ? (T*)g->normal : nullptr;
         if (hi > lo) {
@@ -820,23 +860,9 @@ static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t
         if (gp) g->has_grad = true;
         if (np) g->has_normal = true;
     }
-    if (fields & SG_KINT) {
-        // largest |o_k| of a tap: o_k < 2 h_ratio  ->  R = ceil(2 h_ratio) - 1
-        const int R = (int)std::ceil(2.0 * h_ratio) - 1;
-        double S = 0.0;
-        const KintC<T> kc = make_kint<T>(h_ratio, g->gc.dx, R, &S);
-        if (!g->kint) g->kint = g->alloc((size_t)g->n_pkg * 64 * sizeof(T), s);
-        if (!g->gkint) g->gkint = g->alloc(vec_bytes, s);
-        switch (R) {
-        case 0: launch_kint_r<T, 0>(g, phi, kc, s); break;
-        case 1: launch_kint_r<T, 1>(g, phi, kc, s); break;
-        case 2: launch_kint_r<T, 2>(g, phi, kc, s); break;
-        default: launch_kint_r<T, 3>(g, phi, kc, s); break;
-        }
-        k_singular<T><<<1, 128, 0, s>>>((T*)g->kint, (T*)g->gkint, nullptr, nullptr, kc.S, T(0));
-        SG_LAUNCHED();
-        g->has_kint = true;
-        g->kernel_sum = S;
+    if (sk != s) {
+        SG_CUDA(cudaEventRecord(ev_join, sk));
+        SG_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
     }
 }
 
