@@ -77,3 +77,10 @@ if [[ $what == reinit4 ]]; then
   timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> /dev/null
   SG_REINIT8=1 timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3_8.json 2> /dev/null
 fi
+if [[ $what == probe2 ]]; then
+  timeout 600 python -m pytest tests -m gpu -q -x -k "probe or smoke or slab or relax" > gpurun_out/pytest_p2.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_p2.log
+  for v in 0 1; do
+    SG_PROBE_V1=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_v$v.json 2> /dev/null
+    SG_PROBE_V1=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e --order shuffled > gpurun_out/bench_s$v.json 2> /dev/null
+  done
+fi
