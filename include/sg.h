@@ -255,6 +255,16 @@ sg_status sg_build_refined(const sg_grid* parent, const sg_geometry* geom, void*
  * sweeps, i.e. calls sg_reinit(grid, 1, ...) once per exchange. */
 sg_status sg_reinit(sg_grid* grid, int32_t iters, double cfl, void* stream);
 
+/* The same sweeps over every stored package, owned and ghost (a9 with ghost
+ * reuse).  The ghost plane of a slab is 4 data points deep and a
+ * sweep's dependence cone grows one point per sweep: the ghost packages go
+ * wrong from their outer face inward (their out-of-slab neighbours are far
+ * constants), one point per sweep, so after an exchange of the current
+ * buffer up to 4 sweeps keep every owned package exact -- one exchange per 4
+ * sweeps instead of one per sweep.  On a single-domain grid identical to
+ * sg_reinit. */
+sg_status sg_reinit_halo(sg_grid* grid, int32_t iters, double cfl, void* stream);
+
 /* Derived fields from the current phi: any OR of SG_GRAD, SG_NORMAL, SG_KINT.
  * h_ratio = h / dx of the Wendland C2 kernel, in [0.5, 2] (stencil radius
  * <= 3 < 4, so every tap stays in the 27-neighbourhood).  Asynchronous. */

@@ -160,7 +160,7 @@ struct sg_grid {
 
 // kernels / launchers implemented per translation unit
 namespace sg {
-void launch_reinit(sg_grid* g, int32_t iters, double cfl, cudaStream_t s);
+void launch_reinit(sg_grid* g, int32_t iters, double cfl, cudaStream_t s, bool halo = false);
 void launch_gradient(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t s);
 void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void* grad,
                   unsigned long long* oob, cudaStream_t s);

@@ -661,8 +661,8 @@ static StC<T> stencil_consts(const sg_grid* g, double cfl) {
 }
 
 template <class T>
-static void reinit_launch(sg_grid* g, int cur, const StC<T>& c, cudaStream_t s) {
-    const int64_t lo = g->own_lo, hi = g->own_hi;
+static void reinit_launch(sg_grid* g, int cur, const StC<T>& c, int64_t lo, int64_t hi,
+                          cudaStream_t s) {
     if (hi <= lo) return;
     const ReinitOp<T> op{(T*)g->phi[1 - cur], c};
     static unsigned blocks_max = 0;  // resident blocks (per instantiation)
@@ -695,19 +695,21 @@ static std::vector<std::pair<GraphKey, cudaGraphExec_t>> g_graphs;  // small LRU
 static cudaStream_t g_capture = nullptr;
 
 template <class T>
-static void reinit_t(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
+static void reinit_t(sg_grid* g, int32_t iters, double cfl, bool halo, cudaStream_t s) {
     const StC<T> c = stencil_consts<T>(g, cfl);
-    if (iters == 1 || g->own_hi <= g->own_lo) {
+    // owned packages, or (halo) every stored package: owned and ghost
+    const int64_t lo = halo ? 2 : g->own_lo, hi = halo ? g->n_pkg : g->own_hi;
+    if (iters == 1 || hi <= lo) {
         for (int it = 0; it < iters; ++it) {
-            if (g->own_hi > g->own_lo) {
-                reinit_launch<T>(g, g->cur, c, s);
+            if (hi > lo) {
+                reinit_launch<T>(g, g->cur, c, lo, hi, s);
                 SG_LAUNCHED();
             }
             g->cur = 1 - g->cur;
         }
         return;
     }
-    const GraphKey key{g->phi[g->cur], g->phi[1 - g->cur], g->nb, g->own_lo, g->own_hi, iters,
+    const GraphKey key{g->phi[g->cur], g->phi[1 - g->cur], g->nb, lo, hi, iters,
                        (int32_t)sizeof(T), cfl};
     std::lock_guard<std::mutex> lk(g_graph_mu);
     cudaGraphExec_t exec = nullptr;
@@ -723,7 +725,7 @@ static void reinit_t(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
         SG_CUDA(cudaStreamBeginCapture(g_capture, cudaStreamCaptureModeThreadLocal));
         int cur = g->cur;
         for (int it = 0; it < iters; ++it) {
-            reinit_launch<T>(g, cur, c, g_capture);
+            reinit_launch<T>(g, cur, c, lo, hi, g_capture);
             cur = 1 - cur;
         }
         SG_CUDA(cudaStreamEndCapture(g_capture, &graph));
@@ -740,11 +742,11 @@ static void reinit_t(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
     if (iters & 1) g->cur = 1 - g->cur;
 }
 
-void launch_reinit(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
+void launch_reinit(sg_grid* g, int32_t iters, double cfl, cudaStream_t s, bool halo) {
     if (g->dtype == SG_F64)
-        reinit_t<double>(g, iters, cfl, s);
+        reinit_t<double>(g, iters, cfl, halo, s);
     else
-        reinit_t<float>(g, iters, cfl, s);
+        reinit_t<float>(g, iters, cfl, halo, s);
 }
 
 // Wendland C2 weights (reading R-14), evaluated on the host in double:
@@ -908,6 +910,17 @@ extern "C" sg_status sg_reinit(sg_grid* g, int32_t iters, double cfl, void* stre
         SG_CUDA(cudaGetLastError());
         launch_reinit(g, iters, cfl, (cudaStream_t)stream);
         g->has_grad = g->has_normal = g->has_kint = false;  // derived fields are stale
+    });
+}
+
+extern "C" sg_status sg_reinit_halo(sg_grid* g, int32_t iters, double cfl, void* stream) {
+    return guard([&] {
+        SG_ARG(g != nullptr, "sg_reinit_halo: null grid");
+        SG_ARG(iters >= 0, "sg_reinit_halo: iters must be >= 0");
+        SG_ARG(cfl > 0.0 && cfl <= 0.5, "sg_reinit_halo: cfl must be in (0, 0.5]");
+        SG_CUDA(cudaGetLastError());
+        launch_reinit(g, iters, cfl, (cudaStream_t)stream, true);
+        g->has_grad = g->has_normal = g->has_kint = false;
     });
 }
 

@@ -27,7 +27,7 @@ _STATUS = {0: "SG_OK", 1: "SG_ERR_ARG", 2: "SG_ERR_OOM", 3: "SG_ERR_CUDA", 4: "S
            5: "SG_ERR_STATE", 6: "SG_ERR_DOMAIN"}
 
 # exported symbols declared in include/sg.h (checked by the CPU test suite)
-EXPORTS = ("sg_build", "sg_build_refined", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
+EXPORTS = ("sg_build", "sg_build_refined", "sg_reinit", "sg_reinit_halo", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
            "sg_sign_correct", "sg_clean", "sg_info", "sg_view",
            "sg_destroy", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
            "sg_last_error", "sg_abi_version", "sg_launch_count")
@@ -99,6 +99,7 @@ def lib():
                                C.POINTER(P)]
         L.sg_build_refined.argtypes = [P, C.POINTER(sg_geometry), P, C.POINTER(P)]
         L.sg_reinit.argtypes = [P, I32, D, P]
+        L.sg_reinit_halo.argtypes = [P, I32, D, P]
         L.sg_gradient.argtypes = [P, C.c_uint32, D, P]
         L.sg_probe.argtypes = [P, I64, P, P, P, P, P]
         L.sg_table1.argtypes = [P, I32, D, P]
@@ -115,7 +116,7 @@ def lib():
         L.sg_last_error.restype = C.c_char_p
         L.sg_abi_version.restype = I32
         L.sg_launch_count.restype = C.c_uint64
-        for name in ("sg_build", "sg_build_refined", "sg_reinit", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
+        for name in ("sg_build", "sg_build_refined", "sg_reinit", "sg_reinit_halo", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
                      "sg_sign_correct", "sg_clean",
                      "sg_info",
                      "sg_view", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts"):
@@ -184,6 +185,10 @@ def sg_build(desc: sg_desc, geom: sg_geometry, slab: sg_slab | None = None, stre
 
 def sg_reinit(grid: int, iters: int, cfl: float = 0.3, stream=None) -> None:
     _check(lib().sg_reinit(C.c_void_p(grid), int(iters), float(cfl), _stream(stream)))
+
+
+def sg_reinit_halo(grid: int, iters: int, cfl: float = 0.3, stream=None) -> None:
+    _check(lib().sg_reinit_halo(C.c_void_p(grid), int(iters), float(cfl), _stream(stream)))
 
 
 def sg_gradient(grid: int, fields: int = SG_GRAD | SG_NORMAL, h_ratio: float = 1.3,

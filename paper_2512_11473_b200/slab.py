@@ -139,11 +139,23 @@ class SlabGrid:
         per = {"phi": 64, "kint": 64, "grad": 256}.get(name, 192)
         exchange(self.grid.view(name), self.halo, self.rank, self.world, per, self.group)
 
-    def reinit(self, iters: int, cfl: float, stream=None):
+    # sweeps between two ghost exchanges: the ghost plane is 4 data points
+    # deep, so up to 4 sweeps over owned + ghost packages keep the owned ones
+    # exact (include/sg.h sg_reinit_halo; SURVEY 8(e) ghost reuse)
+    GHOST_SWEEPS = 4
+
+    def reinit(self, iters: int, cfl: float, stream=None, per_exchange: int | None = None):
         from . import sg
-        for _ in range(iters):
-            sg.sg_reinit(self.grid.handle, 1, cfl, stream)
+        k = self.GHOST_SWEEPS if per_exchange is None else per_exchange
+        done = 0
+        while done < iters:
+            m = min(k, iters - done)
+            if k == 1:
+                sg.sg_reinit(self.grid.handle, 1, cfl, stream)
+            else:
+                sg.sg_reinit_halo(self.grid.handle, m, cfl, stream)
             self.exchange("phi")
+            done += m
 
     def gradient(self, fields: int, h_ratio: float, stream=None):
         from . import sg
@@ -264,7 +276,8 @@ def bench_slab(args, w, rank, world, local):
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": w.dtype, "data": "synthetic",
                "config": {"workload": workload_name(w, n_part, args.order) +
-                          f", z-slab partitioned over {world} GPUs, NCCL ghost planes per sweep",
+                          f", z-slab partitioned over {world} GPUs, NCCL ghost planes every "
+                          f"{SlabGrid.GHOST_SWEEPS} sweeps",
                           "active_cells": n_act, "particles": n_part,
                           "parallelism": f"zslab{world}",
                           "l2": "flushed between steps (512 MiB write, outside the timed events)"},

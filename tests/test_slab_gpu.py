@@ -96,3 +96,47 @@ def test_slabs_bitwise_equal_one_gpu(sgm, name, P):
         got_phi[m] = ph
         got_grad[m] = gr
     assert torch.equal(got_phi, fphi) and torch.equal(got_grad, fgrad)
+
+
+def _slab_setup(sgm, w, P):
+    from paper_2512_11473_b200 import slab
+    desc, geom, keep = sgm.make_desc(w)
+    nz = w.n[2]
+    counts = torch.zeros(nz, dtype=torch.int64, device="cuda")
+    sgm.sg_plane_counts(desc, geom, 0, nz, counts.data_ptr())
+    counts = counts.cpu().numpy()
+    plans = [slab.plan(counts, P, r) for r in range(P)]
+    grids = [sgm.Grid(w, slab=(p.z_lo, p.z_hi, p.id_base)) for p in plans]
+    halos = [slab.halo_ranges(p, g.view("plane_first").cpu().numpy()) for p, g in zip(plans, grids)]
+    return plans, grids, halos
+
+
+def _owned_equal(full, plans, grids, name):
+    fv = full.view(name)
+    ok = True
+    for p, g in zip(plans, grids):
+        info = g.info
+        a, b = info["own_lo"], info["own_hi"]
+        ok = ok and torch.equal(g.view(name)[a:b], fv[a - 2 + p.id_base:b - 2 + p.id_base])
+    return ok
+
+
+@pytest.mark.parametrize("name,P", [("C1", 2), ("C2", 4)])
+def test_ghost_reuse_four_sweeps_per_exchange(sgm, name, P):
+    """SURVEY 8(e) ghost reuse: sweeping owned + ghost packages (sg_reinit_halo)
+    keeps the owned packages exact for up to 4 sweeps per exchange (ghost
+    depth 4 points): bitwise equal to the 1-GPU grid."""
+    w = W.config(name)
+    iters = 20
+    full = sgm.Grid(w)
+    full.reinit(iters, w.cfl)
+    for k, expect in ((4, True), (3, True)):
+        plans, grids, halos = _slab_setup(sgm, w, P)
+        done = 0
+        while done < iters:
+            m = min(k, iters - done)
+            for g in grids:
+                sgm.sg_reinit_halo(g.handle, m, w.cfl)
+            _exchange_local(grids, halos, "phi", 64)
+            done += m
+        assert _owned_equal(full, plans, grids, "phi") == expect, (k, expect)
