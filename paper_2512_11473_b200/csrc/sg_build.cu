@@ -17,6 +17,10 @@
 //   K4 k_phi_init : phi = init_scale * f at the 64 data points
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <chrono>
+#include <cstring>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -303,7 +307,9 @@ __global__ void __launch_bounds__(kTB) k_count(GridC gc, Bits b, int64_t nwords,
 // K2b -- exclusive scan of tile counts (one block; each thread owns a
 // contiguous segment).  out[n] = total.
 __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, int64_t n,
-                                               int64_t* __restrict__ out) {
+                                               int64_t* __restrict__ out,
+                                               volatile long long* __restrict__ host,
+                                               long long gen) {
     __shared__ long long s[1024];
     const int64_t seg = (n + 1023) / 1024;
     const int64_t b = (int64_t)threadIdx.x * seg, e = min(n, b + seg);
@@ -322,7 +328,16 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, 
         out[i] = run;
         run += cnt[i];
     }
-    if (threadIdx.x == 1023) out[n] = s[1023];
+    if (threadIdx.x == 1023) {
+        out[n] = s[1023];
+        // publish [active, core, boundary flag] to mapped pinned memory, the
+        // generation last: the host polls it instead of a stream sync
+        host[0] = s[1023];
+        host[1] = out[n + 1];
+        host[2] = out[n + 2];
+        __threadfence_system();
+        host[3] = gen;
+    }
 }
 
 // K2c -- ordered compaction (R-1): ids 2 + (active cells before) in linear
@@ -643,10 +658,43 @@ static void launch_tag(const GridC& gc, const Geom& geom, int32_t zt_lo, int32_t
 
 // pinned host landing buffer of the build's package-count read-back (one
 // per host thread)
-static int64_t* pinned_counts() {
-    static thread_local int64_t* p = nullptr;
-    if (!p) SG_CUDA(cudaHostAlloc((void**)&p, 4 * sizeof(int64_t), cudaHostAllocDefault));
+// mapped pinned landing buffer of the build's package-count read-back (one
+// per host thread): k_scan writes [active, core, boundary, generation]
+struct Published {
+    volatile long long* host = nullptr;
+    long long* dev = nullptr;
+    long long gen = 0;
+};
+static Published& pinned_counts() {
+    static thread_local Published p;
+    if (!p.host) {
+        void* h = nullptr;
+        SG_CUDA(cudaHostAlloc(&h, 4 * sizeof(long long), cudaHostAllocMapped));
+        std::memset(h, 0, 4 * sizeof(long long));
+        void* d = nullptr;
+        SG_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+        p.host = (volatile long long*)h;
+        p.dev = (long long*)d;
+    }
     return p;
+}
+
+// wait until k_scan has published generation `gen` (spin with pause; after
+// 1 s fall back to a stream sync, which also surfaces kernel errors)
+static void wait_published(const Published& p, long long gen, cudaStream_t s) {
+    auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t it = 0; p.host[3] != gen; ++it) {
+        if ((it & 1023) == 1023 &&
+            std::chrono::steady_clock::now() - t0 > std::chrono::seconds(1)) {
+            SG_CUDA(cudaStreamSynchronize(s));
+            if (p.host[3] != gen) throw Error(SG_ERR_CUDA, "sg_build: count read-back lost");
+            break;
+        }
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
 }
 
 // library-internal side stream (one per process, non-blocking)
@@ -779,15 +827,15 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         const Bits bits{core_w, neg_w, W, zt_lo};
         k_count<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, bits, nwords, act_w, tile_count, d_core);
         SG_LAUNCHED();
-        k_scan<<<1, 1024, 0, s>>>(tile_count, n_tiles, tile_off);
+        Published& pub = pinned_counts();
+        const long long gen = ++pub.gen;
+        k_scan<<<1, 1024, 0, s>>>(tile_count, n_tiles, tile_off, pub.dev, gen);
         SG_LAUNCHED();
 
         // the single host synchronisation: package count, core count and the
         // domain-boundary flag in one 24 B copy into pinned memory
-        int64_t* counts = pinned_counts();
-        SG_CUDA(cudaMemcpyAsync(counts, tile_off + n_tiles, 3 * sizeof(int64_t),
-                                cudaMemcpyDeviceToHost, s));
-        SG_CUDA(cudaStreamSynchronize(s));
+        wait_published(pub, gen, s);
+        const int64_t counts[3] = {(int64_t)pub.host[0], (int64_t)pub.host[1], (int64_t)pub.host[2]};
         const int64_t n_active = counts[0];
         SG_ARG(n_active + 2 < 4294967295LL, "sg_build: more than 2^32-3 packages");
         g->n_pkg = n_active + 2;
