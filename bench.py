@@ -314,6 +314,7 @@ def run_ours(args, rank, world, local):
         "roofline": {"kernel": "k_sweep<float, ReinitOp<float>> (reinit sweep)", "bound": "hbm", "achieved": achieved,
                      "peak": hbm, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "bytes_per_cell": bytes_per_cell, "cells_per_launch": n_act,
+                     "peak_nominal": 8000.0, "frac_nominal": achieved / 8000.0,
                      "traffic": ncu_traffic("k_sweep", w.name),
                      "note": (f"working set per sweep {alg_bytes / 1e6:.0f} MB "
                               + ("< 126 MB L2: L2-resident across the sweeps" if alg_bytes < 126e6
