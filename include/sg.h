@@ -344,6 +344,11 @@ sg_status sg_relax(sg_grid* grid, int64_t n, void* pos, const sg_relax_params* p
  *     with |phi| < tau (compared in the grid dtype) keep their sign; all
  *     other active points start unsigned.  Finally phi <- -|phi| / +|phi| at
  *     every signed point; points never reached keep phi.
+ * On a layer built by sg_build_refined the coarse step revisits only the
+ * cells evaluated on that layer (under a parent core cell): every other cell
+ * carries its parent's sign and starts signed ("only on the coarsest
+ * layer all cells are evaluated.  For refined layers, the operation is
+ * limited to inner cells or data packages").
  * tau > 0 (typically dx).  max_sweeps > 0 caps each step, <= 0 means no cap.
  * sweeps (host int32[2], may be NULL) receives the number of sweeps of the
  * coarse and the refined step that signed at least one site.  Operates on

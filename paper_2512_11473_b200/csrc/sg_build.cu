@@ -162,15 +162,16 @@ __global__ void __launch_bounds__(128, 4) k_tag_cull(GridC gc, Geom geom, int32_
 // its whole cell (1-Lipschitz, half-diagonal sqrt(3) l_f).
 __global__ void __launch_bounds__(256) k_tag_refine(GridC gc, Geom geom, int32_t W, ParentBits pb,
                                                     uint32_t* __restrict__ core_w,
-                                                    uint32_t* __restrict__ neg_w) {
+                                                    uint32_t* __restrict__ neg_w,
+                                                    uint32_t* __restrict__ eval_w) {
     const int cx = blockIdx.x * blockDim.x + threadIdx.x;
     const int cy = blockIdx.y, cz = blockIdx.z;
     const bool in = cx < gc.n[0];
-    bool core = false, neg = false;
+    bool core = false, neg = false, pc = false;
     if (in) {
         const int px = cx >> 1;
         const int64_t pw = ((int64_t)(cz >> 1) * (gc.n[1] >> 1) + (cy >> 1)) * pb.W + (px >> 5);
-        const bool pc = (__ldg(pb.core + pw) >> (px & 31)) & 1u;
+        pc = (__ldg(pb.core + pw) >> (px & 31)) & 1u;
         neg = (__ldg(pb.neg + pw) >> (px & 31)) & 1u;
         if (pc) {
             const double f = sd_eval(geom, gc.lower[0] + ((double)cx + 0.5) * gc.cell,
@@ -182,10 +183,12 @@ __global__ void __launch_bounds__(256) k_tag_refine(GridC gc, Geom geom, int32_t
     }
     const uint32_t cw = __ballot_sync(0xffffffffu, in && core);
     const uint32_t nw = __ballot_sync(0xffffffffu, in && neg);
+    const uint32_t ew = __ballot_sync(0xffffffffu, in && pc);
     if ((threadIdx.x & 31) == 0 && cx < gc.n[0]) {
         const int64_t i = ((int64_t)cz * gc.n[1] + cy) * W + (cx >> 5);
         core_w[i] = cw;
         neg_w[i] = nw;
+        eval_w[i] = ew;
     }
 }
 
@@ -803,12 +806,15 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         guard_mem.md = &md;
         if (parent) {
             const ParentBits pb{parent->cell_core, parent->cell_neg, parent->tag_W};
+            // cells evaluated here (under a parent core cell): the sign
+            // correction of a refined layer revisits only these
+            g->cell_eval = (uint32_t*)g->alloc(sizeof(uint32_t) * tag_words, s);
             if (mesh) {
                 md = mesh_prepare(gc, geom, g->geom, s);
-                launch_tag_refine_mesh(gc, g->geom, W, pb, core_w, neg_w, s);
+                launch_tag_refine_mesh(gc, g->geom, W, pb, core_w, neg_w, g->cell_eval, s);
             } else {
                 dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1], (unsigned)gc.n[2]);
-                k_tag_refine<<<grid, 256, 0, s>>>(gc, g->geom, W, pb, core_w, neg_w);
+                k_tag_refine<<<grid, 256, 0, s>>>(gc, g->geom, W, pb, core_w, neg_w, g->cell_eval);
                 SG_LAUNCHED();
             }
         } else if (mesh) {

@@ -131,6 +131,7 @@ struct sg_grid {
     // tagging bitmasks kept for the sign correction: [tag planes][n1][W]
     uint32_t* cell_core = nullptr;
     uint32_t* cell_neg = nullptr;
+    uint32_t* cell_eval = nullptr;  // refined layer: cells under a parent core cell
     int32_t tag_W = 0, zt_lo = 0, zt_hi = 0;
     // fields
     void* phi[2] = {nullptr, nullptr};
@@ -184,7 +185,7 @@ struct ParentBits {
     int32_t W;  // words per parent row
 };
 void launch_tag_refine_mesh(const GridC& gc, const Geom& g, int32_t W, ParentBits pb,
-                            uint32_t* core_w, uint32_t* neg_w, cudaStream_t s);
+                            uint32_t* core_w, uint32_t* neg_w, uint32_t* eval_w, cudaStream_t s);
 void launch_phi_init_mesh(const GridC& gc, const Geom& g, const uint32_t* meta_cell,
                           int64_t n_pkg, int32_t dtype, void* phi0, void* phi1, cudaStream_t s);
 // coarse sign flood of the sign correction (sg_sign.cu) on tagging bitmasks

@@ -312,15 +312,16 @@ __global__ void __launch_bounds__(256) k_tag_mesh(GridC gc, Geom g, int32_t W,
 // of the surface: exact); the others take the sign of their parent cell
 __global__ void __launch_bounds__(256) k_tag_refine_mesh(GridC gc, Geom g, int32_t W, ParentBits pb,
                                                          uint32_t* __restrict__ core_w,
-                                                         uint32_t* __restrict__ neg_w) {
+                                                         uint32_t* __restrict__ neg_w,
+                                                         uint32_t* __restrict__ eval_w) {
     const int cx = blockIdx.x * blockDim.x + threadIdx.x;
     const int cy = blockIdx.y, cz = blockIdx.z;
     const bool in = cx < gc.n[0];
-    bool core = false, neg = false;
+    bool core = false, neg = false, pc = false;
     if (in) {
         const int px = cx >> 1;
         const int64_t pw = ((int64_t)(cz >> 1) * (gc.n[1] >> 1) + (cy >> 1)) * pb.W + (px >> 5);
-        const bool pc = (__ldg(pb.core + pw) >> (px & 31)) & 1u;
+        pc = (__ldg(pb.core + pw) >> (px & 31)) & 1u;
         neg = (__ldg(pb.neg + pw) >> (px & 31)) & 1u;
         if (pc) {
             const double p[3] = {gc.lower[0] + ((double)cx + 0.5) * gc.cell,
@@ -334,17 +335,19 @@ __global__ void __launch_bounds__(256) k_tag_refine_mesh(GridC gc, Geom g, int32
     }
     const uint32_t cw = __ballot_sync(0xffffffffu, in && core);
     const uint32_t nw = __ballot_sync(0xffffffffu, in && neg);
+    const uint32_t ew = __ballot_sync(0xffffffffu, in && pc);
     if ((threadIdx.x & 31) == 0 && cx < gc.n[0]) {
         const int64_t i = ((int64_t)cz * gc.n[1] + cy) * W + (cx >> 5);
         core_w[i] = cw;
         neg_w[i] = nw;
+        eval_w[i] = ew;
     }
 }
 
 void launch_tag_refine_mesh(const GridC& gc, const Geom& g, int32_t W, ParentBits pb,
-                            uint32_t* core_w, uint32_t* neg_w, cudaStream_t s) {
+                            uint32_t* core_w, uint32_t* neg_w, uint32_t* eval_w, cudaStream_t s) {
     dim3 grid((unsigned)ceil_div(gc.n[0], 256), (unsigned)gc.n[1], (unsigned)gc.n[2]);
-    k_tag_refine_mesh<<<grid, 256, 0, s>>>(gc, g, W, pb, core_w, neg_w);
+    k_tag_refine_mesh<<<grid, 256, 0, s>>>(gc, g, W, pb, core_w, neg_w, eval_w);
     SG_LAUNCHED();
 }
 

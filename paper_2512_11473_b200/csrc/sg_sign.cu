@@ -96,11 +96,24 @@ static unsigned sweep_blocks(int64_t items) {
 // ------------------------------------------------------------- coarse ----
 
 // cell state: .x known bits, .y negative bits of one 32-cell word
+// known bits: core cells, plus (refined layer, eval != nullptr) every valid
+// cell that was not evaluated on this layer -- it carries its parent's
+// corrected sign (on refined layers the correction is limited to the
+// cells near the surface)
 __global__ void __launch_bounds__(256) k_cell_pack(uint32_t nwords, const uint32_t* __restrict__ core,
                                                    const uint32_t* __restrict__ neg,
-                                                   uint2* __restrict__ st) {
+                                                   uint2* __restrict__ st,
+                                                   const uint32_t* __restrict__ eval = nullptr,
+                                                   int32_t nx = 0, uint32_t W = 1) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < nwords) st[t] = make_uint2(core[t], neg[t]);
+    if (t >= nwords) return;
+    uint32_t k = core[t];
+    if (eval) {
+        const int tail = nx - 32 * (int)(t % W);
+        const uint32_t valid = tail >= 32 ? 0xffffffffu : ((1u << tail) - 1u);
+        k |= valid & ~eval[t];
+    }
+    st[t] = make_uint2(k, neg[t]);
 }
 
 __global__ void __launch_bounds__(256) k_cell_unpack(uint32_t nwords, const uint2* __restrict__ st,
@@ -397,7 +410,8 @@ extern "C" sg_status sg_sign_correct(sg_grid* g, double tau, int32_t max_sweeps,
 
         // coarse: core cells signed by f(centre), the rest unsigned
         const unsigned cb = (unsigned)ceil_div(nwords, 256);
-        k_cell_pack<<<cb, 256, 0, s>>>((uint32_t)nwords, g->cell_core, g->cell_neg, cs[0]);
+        k_cell_pack<<<cb, 256, 0, s>>>((uint32_t)nwords, g->cell_core, g->cell_neg, cs[0],
+                                       g->cell_eval, gc.n[0], (uint32_t)W);
         SG_LAUNCHED();
         const unsigned cbs = sweep_blocks(nwords);
         const int c_sweeps = run_sweeps(

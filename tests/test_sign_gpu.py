@@ -146,3 +146,26 @@ def test_sign_correct_rejects_slab_grid(sgm):
         g.sign_correct()
     with pytest.raises(sgm.SgError):
         g.sign_correct(tau=-1.0)
+
+
+@pytest.mark.parametrize("base,levels", [("C2", 2), ("C3", 1)])
+def test_multires_leaky_chain_equals_watertight(sgm, base, levels):
+    """P:528-535 across layers: correct the coarsest leaky layer over all
+    cells, refine, correct each refined layer over its evaluated cells only;
+    the finest layer equals the watertight direct build bit for bit."""
+    w0 = W.config(base)
+    f = 2 ** levels
+    wc = w0.with_(n=tuple(k // f for k in w0.n), cell=w0.cell * f)
+    leaky = W.leaky(wc)
+    g = sgm.Grid(leaky)
+    sw = g.sign_correct()
+    for _ in range(levels):
+        g = g.refined()
+        sw_fine = g.sign_correct()
+        assert sw_fine[0] <= 2 * sw[0]
+    ref = _grid_state(sgm.Grid(w0))
+    got = _grid_state(g)
+    assert np.array_equal(got[0], ref[0])
+    assert np.array_equal(got[1], ref[1])
+    phi_bits_equal(got[2], ref[2].astype(np.float64))
+    assert np.array_equal(got[3], ref[3])
