@@ -84,3 +84,20 @@ if [[ $what == probe2 ]]; then
     SG_PROBE_V1=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e --order shuffled > gpurun_out/bench_s$v.json 2> /dev/null
   done
 fi
+if [[ $what == fuse ]]; then
+  timeout 600 python -m pytest tests -m gpu -q -x -k "gradient or kernel or fused or probe or relax or clean or smoke" > gpurun_out/pytest_fuse.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_fuse.log
+  for v in 1 0; do
+    SG_FUSE_GRAD=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_fuse$v.json 2> /dev/null
+    SG_FUSE_GRAD=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_fuse$v.json 2> /dev/null
+  done
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python bench.py --config C3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_c3.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_kint" -s 1 -c 1 -o gpurun_out/prof_kint python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_kint.log 2>&1
+fi
+if [[ $what == pdl ]]; then
+  timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or smoke or clean" > gpurun_out/pytest_pdl.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pdl.log
+  for v in 1 0; do
+    SG_PDL=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_pdl$v.json 2> /dev/null
+    SG_PDL=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_pdl$v.json 2> /dev/null
+  done
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_probe|k_kint|k_gradient" -s 3 -c 3 -o gpurun_out/prof_pkg python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_pkg.log 2>&1
+fi
