@@ -179,7 +179,11 @@ enum {
      * x of that row; tag planes = stored planes plus one on each side that
      * lies in the domain (sg_info zs_lo/zs_hi widened by one, clipped) */
     SG_VIEW_CELL_CORE = 11,  /* |f(centre)| < l_c                                 */
-    SG_VIEW_CELL_NEG = 12    /* f(centre) < 0 (after sg_sign_correct: corrected)  */
+    SG_VIEW_CELL_NEG = 12,   /* f(centre) < 0 (after sg_sign_correct: corrected)  */
+    SG_VIEW_FACE = 13        /* u32 [n_pkg][8]            face table: entries 0..5 are
+                                neighbour slots 12, 14, 10, 16, 4, 22 (-x, +x, -y,
+                                +y, -z, +z), 6..7 zero -- the 32 B row the 7-point
+                                sweeps read instead of the 108 B neighbour row */
 };
 
 typedef struct {

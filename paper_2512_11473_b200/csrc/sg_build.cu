@@ -442,7 +442,8 @@ template <bool EDGE>
 __global__ void __launch_bounds__(256) k_nb(GridC gc, const Geom* __restrict__ geom, Bits b,
                                             const uint32_t* __restrict__ bg,
                                             const uint32_t* __restrict__ meta_cell,
-                                            int64_t n_pkg, uint32_t* __restrict__ nb) {
+                                            int64_t n_pkg, uint32_t* __restrict__ nb,
+                                            uint32_t* __restrict__ face) {
     const int64_t id0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kNbPW;
     const int s = threadIdx.x & 31;
     if (id0 >= n_pkg || s >= 27) return;
@@ -478,9 +479,15 @@ __global__ void __launch_bounds__(256) k_nb(GridC gc, const Geom* __restrict__ g
             v[u] = ((__ldg(b.neg + b.idx(gc, qz, qy, qx >> 5)) >> (qx & 31)) & 1u) ? 0u : 1u;
         }
     }
+    // face table entry of this slot: -x, +x, -y, +y, -z, +z (or a zero pad)
+    const int fr = s == 12 ? 0 : s == 14 ? 1 : s == 10 ? 2 : s == 16 ? 3 : s == 4 ? 4 : s == 22 ? 5
+                 : s < 2 ? 6 + s : -1;
 #pragma unroll
     for (int u = 0; u < kNbPW; ++u)
-        if (id0 + u < n_pkg) nb[(id0 + u) * 27 + s] = v[u];
+        if (id0 + u < n_pkg) {
+            nb[(id0 + u) * 27 + s] = v[u];
+            if (fr >= 0) face[(id0 + u) * 8 + fr] = fr < 6 ? v[u] : 0u;
+        }
 }
 
 // K4 -- initial level set at the 64 data points of every package:
@@ -854,9 +861,11 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         const int32_t planes = gc.zs_hi - gc.zs_lo;
         const size_t sz_bg = al(sizeof(uint32_t) * ncs), sz_mc = al(sizeof(uint32_t) * n_pkg),
                      sz_mk = al((size_t)n_pkg), sz_nb = al(sizeof(uint32_t) * 27 * n_pkg),
+                     sz_fc = al(sizeof(uint32_t) * 8 * n_pkg),
                      sz_pf = al(sizeof(int64_t) * (planes + 1)),
                      sz_phi = al((size_t)g->esz * 64 * n_pkg);
-        char* arena = (char*)g->alloc(sz_bg + sz_mc + sz_mk + sz_nb + sz_pf + 2 * sz_phi, s);
+        char* arena =
+            (char*)g->alloc(sz_bg + sz_mc + sz_mk + sz_nb + sz_fc + sz_pf + 2 * sz_phi, s);
         g->bg = (uint32_t*)arena;
         arena += sz_bg;
         g->meta_cell = (uint32_t*)arena;
@@ -865,6 +874,8 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         arena += sz_mk;
         g->nb = (uint32_t*)arena;
         arena += sz_nb;
+        g->face = (uint32_t*)arena;
+        arena += sz_fc;
         g->plane_first = (int64_t*)arena;
         arena += sz_pf;
         g->phi[0] = arena;
@@ -899,9 +910,11 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         SG_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
         const unsigned nbb = (unsigned)ceil_div(ceil_div(n_pkg, kNbPW) * 32, 256);
         if (counts[2])  // band touches the domain boundary: out-of-domain rule needed
-            k_nb<true><<<nbb, 256, 0, side>>>(gc, d_geom, bits, g->bg, g->meta_cell, n_pkg, g->nb);
+            k_nb<true><<<nbb, 256, 0, side>>>(gc, d_geom, bits, g->bg, g->meta_cell, n_pkg, g->nb,
+                                              g->face);
         else
-            k_nb<false><<<nbb, 256, 0, side>>>(gc, d_geom, bits, g->bg, g->meta_cell, n_pkg, g->nb);
+            k_nb<false><<<nbb, 256, 0, side>>>(gc, d_geom, bits, g->bg, g->meta_cell, n_pkg, g->nb,
+                                               g->face);
         SG_LAUNCHED();
         SG_CUDA(cudaEventRecord(ev_join, side));
         const unsigned pb = (unsigned)ceil_div(n_pkg * 16, 256);
@@ -1037,6 +1050,7 @@ extern "C" sg_status sg_view(const sg_grid* g, int32_t what, sg_view_t* v) {
         case SG_VIEW_META_CELL: set(g->meta_cell, 1, g->n_pkg, 1, 1, 4, 2); break;
         case SG_VIEW_META_CAT: set(g->meta_cat, 1, g->n_pkg, 1, 1, 1, 3); break;
         case SG_VIEW_NB: set(g->nb, 2, g->n_pkg, 27, 1, 4, 2); break;
+        case SG_VIEW_FACE: set(g->face, 2, g->n_pkg, 8, 1, 4, 2); break;
         case SG_VIEW_PHI: set(g->phi[g->cur], 2, g->n_pkg, 64, 1, g->esz, fdt); break;
         case SG_VIEW_PHI_NEXT: set(g->phi[1 - g->cur], 2, g->n_pkg, 64, 1, g->esz, fdt); break;
         case SG_VIEW_GRAD: set(g->has_grad ? g->grad : nullptr, 3, g->n_pkg, 64, 4, g->esz, fdt); break;

@@ -127,6 +127,10 @@ struct sg_grid {
     uint32_t* meta_cell = nullptr;
     uint8_t* meta_cat = nullptr;
     uint32_t* nb = nullptr;
+    // [n_pkg][8]: the six face-neighbour ids of nb (-x, +x, -y, +y, -z, +z;
+    // slots 12, 14, 10, 16, 4, 22) + 2 zero pads, one 32 B sector per package:
+    // the 7-point sweeps read this instead of their 108 B nb row
+    uint32_t* face = nullptr;
     int64_t* plane_first = nullptr;  // [stored planes + 1]
     // tagging bitmasks kept for the sign correction: [tag planes][n1][W]
     uint32_t* cell_core = nullptr;

@@ -34,12 +34,12 @@ __device__ __forceinline__ void ld_vec4(const double* p, double (&v)[4]) {
 // fp64 division and floor).  Fast path (gc.idx32: fp32 positions, l_c a power
 // of two, lower = 0, upper a float): x * 2^e is exact in fp32, so floor and the
 // comparisons are bit-identical to the fp64 definition without fp64 work.
-template <class T>
+template <class T, bool I32 = false>
 __device__ __forceinline__ bool cell_of(const GridC& gc, int k, T x, int& c);
 
 // lower-corner data index a = floor(u), u = (x - lower)/dx - 1/2, and the
 // fraction t = u - a (exact in fp32 on the fast path: u < 2^23)
-template <class T>
+template <class T, bool I32 = false>
 __device__ __forceinline__ void corner_of(const GridC& gc, int k, T x, int& a, T& t);
 
 // (x - lower) / d with the oracle's rounding: for a power-of-two spacing the
@@ -50,36 +50,39 @@ __device__ __forceinline__ double qdiv(const GridC& gc, double v, bool cell) {
 }
 
 template <>
-__device__ __forceinline__ bool cell_of<float>(const GridC& gc, int k, float x, int& c) {
-    if (gc.idx32) {
-        c = min(__float2int_rd(x * gc.inv_cellf), gc.n[k] - 1);
-        return x >= 0.f && x < gc.upperf[k];  // NaN fails both
-    }
+__device__ __forceinline__ bool cell_of<float, true>(const GridC& gc, int k, float x, int& c) {
+    c = min(__float2int_rd(x * gc.inv_cellf), gc.n[k] - 1);
+    return x >= 0.f && x < gc.upperf[k];  // NaN fails both
+}
+template <>
+__device__ __forceinline__ bool cell_of<float, false>(const GridC& gc, int k, float x, int& c) {
     const double xd = (double)x;
     c = min((int)floor(qdiv(gc, xd - gc.lower[k], true)), gc.n[k] - 1);
     return xd >= gc.lower[k] && xd < gc.upper[k];
 }
 template <>
-__device__ __forceinline__ bool cell_of<double>(const GridC& gc, int k, double x, int& c) {
+__device__ __forceinline__ bool cell_of<double, false>(const GridC& gc, int k, double x, int& c) {
     c = min((int)floor(qdiv(gc, x - gc.lower[k], true)), gc.n[k] - 1);
     return x >= gc.lower[k] && x < gc.upper[k];
 }
 template <>
-__device__ __forceinline__ void corner_of<float>(const GridC& gc, int k, float x, int& a, float& t) {
-    if (gc.idx32) {
-        const float u = x * gc.inv_dxf - 0.5f;
-        const float fa = floorf(u);
-        a = (int)fa;
-        t = u - fa;
-        return;
-    }
+__device__ __forceinline__ void corner_of<float, true>(const GridC& gc, int k, float x, int& a,
+                                                       float& t) {
+    const float u = x * gc.inv_dxf - 0.5f;
+    const float fa = floorf(u);
+    a = (int)fa;
+    t = u - fa;
+}
+template <>
+__device__ __forceinline__ void corner_of<float, false>(const GridC& gc, int k, float x, int& a,
+                                                        float& t) {
     const double u = qdiv(gc, (double)x - gc.lower[k], false) - 0.5;
     const double fa = floor(u);
     a = (int)fa;
     t = (float)(u - fa);
 }
 template <>
-__device__ __forceinline__ void corner_of<double>(const GridC& gc, int k, double x, int& a,
+__device__ __forceinline__ void corner_of<double, false>(const GridC& gc, int k, double x, int& a,
                                                   double& t) {
     const double u = qdiv(gc, x - gc.lower[k], false) - 0.5;
     const double fa = floor(u);
@@ -109,7 +112,9 @@ struct __align__(16) ProbeSmem {
     uint8_t who[kWB][kPW];  // band list: particle slot in the chunk
 };
 
-template <class T>
+// I32: the exact fp32 index fast path (gc.idx32); V: 16 B aligned caller
+// buffers (vector staging of full fp32 chunks) -- both resolved at launch
+template <class T, bool I32, bool V>
 __global__ void __launch_bounds__(32 * ProbeSmem<T>::kWB, 4)
 k_probe(GridC gc, const uint32_t* __restrict__ bg,
                                                const uint32_t* __restrict__ nb,
@@ -117,7 +122,7 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
                                                const T* __restrict__ pg, int64_t n,
                                                const T* __restrict__ pos, T* __restrict__ out_phi,
                                                T* __restrict__ out_grad,
-                                               unsigned long long* __restrict__ oob, bool vec) {
+                                               unsigned long long* __restrict__ oob) {
     __shared__ ProbeSmem<T> S;
     constexpr int kWB = ProbeSmem<T>::kWB;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -135,7 +140,7 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
         const int64_t b0 = ch * kPW;
         const int mm = (int)min((int64_t)kPW, n - b0);
         const T* src = pos + 3 * b0;
-        vnext = sizeof(T) == 4 && vec && mm == kPW;
+        vnext = sizeof(T) == 4 && V && mm == kPW;
         if constexpr (sizeof(T) == 4) {
             if (vnext) {
 #pragma unroll
@@ -193,7 +198,7 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
     for (int j = 0; j < 4; ++j) {
         ok[j] = lane + 32 * j < m;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) ok[j] = cell_of<T>(gc, k, x[j][k], c[j][k]) && ok[j];
+        for (int k = 0; k < 3; ++k) ok[j] = cell_of<T, I32>(gc, k, x[j][k], c[j][k]) && ok[j];
         ok[j] = ok[j] && c[j][2] >= gc.z_lo && c[j][2] < gc.z_hi;  // owned planes of a slab
         b[j] = ok[j] ? __ldg(bg + ((int64_t)(c[j][2] - gc.zs_lo) * gc.n[1] + c[j][1]) * gc.n[0] +
                              c[j][0])
@@ -235,8 +240,8 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 int ck, a;
-                cell_of<T>(gc, k, xs[3 * p + k], ck);
-                corner_of<T>(gc, k, xs[3 * p + k], a, tv[k]);
+                cell_of<T, I32>(gc, k, xs[3 * p + k], ck);
+                corner_of<T, I32>(gc, k, xs[3 * p + k], a, tv[k]);
                 sv[k] = a - 4 * ck;  // in [-1, 3]
             }
             const int s0x = sv[0], s0y = sv[1], s0z = sv[2];
@@ -324,14 +329,20 @@ static void probe_dev(const sg_grid* g, int64_t n, const void* pos, void* out_ph
         int dev = 0, sms = 0, per = 0;
         SG_CUDA(cudaGetDevice(&dev));
         SG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_probe<T>, 32 * kWB, 0));
+        SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_probe<T, false, false>,
+                                                              32 * kWB, 0));
         rb = std::max(1, sms * per);
     }
     const int64_t blocks = std::min<int64_t>(ceil_div(n, kPW * kWB), rb);
-    k_probe<T><<<(unsigned)blocks, 32 * kWB, 0, s>>>(
-        g->gc, g->bg, g->nb, (const T*)g->phi[g->cur], grad, n, (const T*)pos, (T*)out_phi,
-        (T*)out_grad, oob,
-        ((uintptr_t)pos | (uintptr_t)out_phi | (uintptr_t)(out_grad ? out_grad : out_phi)) % 16 == 0);
+    const bool vec =
+        ((uintptr_t)pos | (uintptr_t)out_phi | (uintptr_t)(out_grad ? out_grad : out_phi)) % 16 == 0;
+    auto kern = k_probe<T, false, false>;
+    if constexpr (sizeof(T) == 4) {
+        if (g->gc.idx32) kern = vec ? k_probe<T, true, true> : k_probe<T, true, false>;
+        else if (vec) kern = k_probe<T, false, true>;
+    }
+    kern<<<(unsigned)blocks, 32 * kWB, 0, s>>>(g->gc, g->bg, g->nb, (const T*)g->phi[g->cur], grad,
+                                               n, (const T*)pos, (T*)out_phi, (T*)out_grad, oob);
     SG_LAUNCHED();
 }
 

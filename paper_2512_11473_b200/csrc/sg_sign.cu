@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(256) k_bg_fix(uint32_t nx, int32_t ny, int32_t
 __global__ void __launch_bounds__(256) k_nb_fix(GridC gc, int32_t W, int64_t n_pkg,
                                                 const uint32_t* __restrict__ meta_cell,
                                                 const uint32_t* __restrict__ neg,
-                                                uint32_t* __restrict__ nbt) {
+                                                uint32_t* __restrict__ nbt,
+                                                uint32_t* __restrict__ face) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t id = 2 + t / 27;
     if (id >= n_pkg) return;
@@ -223,7 +224,12 @@ __global__ void __launch_bounds__(256) k_nb_fix(GridC gc, int32_t W, int64_t n_p
     const int64_t row = (int64_t)cy + (int64_t)ny * cz;
     const uint32_t ng = (neg[row * W + (cx >> 5)] >> (cx & 31)) & 1u;
     const uint32_t w = ng ? 0u : 1u;
-    if (w != v) nbt[id * 27 + slot] = w;
+    if (w != v) {
+        nbt[id * 27 + slot] = w;
+        const int fr = slot == 12 ? 0 : slot == 14 ? 1 : slot == 10 ? 2 : slot == 16 ? 3
+                     : slot == 4 ? 4 : slot == 22 ? 5 : -1;
+        if (fr >= 0) face[id * 8 + fr] = w;  // keep the face table in step
+    }
 }
 
 // ------------------------------------------------------------ refined ----
@@ -429,7 +435,7 @@ extern "C" sg_status sg_sign_correct(sg_grid* g, double tau, int32_t max_sweeps,
         SG_LAUNCHED();
         if (n_pkg > 2) {
             k_nb_fix<<<(unsigned)ceil_div((n_pkg - 2) * 27, 256), 256, 0, s>>>(
-                gc, W, n_pkg, g->meta_cell, g->cell_neg, g->nb);
+                gc, W, n_pkg, g->meta_cell, g->cell_neg, g->nb, g->face);
             SG_LAUNCHED();
         }
 

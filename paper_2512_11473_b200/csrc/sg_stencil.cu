@@ -52,14 +52,10 @@ __device__ __forceinline__ void st_row(double* p, const double (&r)[4]) {
     reinterpret_cast<double2*>(p)[1] = make_double2(r[2], r[3]);
 }
 
-// neighbour-table slot of the six face neighbours, Lst. 2 offsets (R-8):
-// r = 0..5 -> -x, +x, -y, +y, -z, +z
-__device__ __forceinline__ int face_slot(int r) {
-    // slot = ox + 3 oy + 9 oz, o in {0,1,2}; centre = 13: {12, 14, 10, 16, 4, 22}
-    // packed 5 bits per entry (no branch, no constant-table load)
-    constexpr uint32_t kPack = 12u | 14u << 5 | 10u << 10 | 16u << 15 | 4u << 20 | 22u << 25;
-    return (int)((kPack >> (5 * r)) & 31u);
-}
+// The six face neighbours r = 0..5 (-x, +x, -y, +y, -z, +z) are neighbour-
+// table slots ox + 3 oy + 9 oz = {12, 14, 10, 16, 4, 22} (Lst. 2 offsets,
+// R-8); the sweeps read them from the compact face table (sg_grid::face),
+// entry r of a package's 32 B row.
 
 // The 7-point cross of one x-row: own row c, rows ym/yp/zm/zp and the two
 // x-end values xm/xp.  Lst. 2 with shifts -1 and 4 (the only ones a
@@ -70,13 +66,15 @@ struct Cross {
     T xm, xp;
 };
 
+// `face`: the grid's compact face table ([pkg][8], sg_grid::face)
 template <class T>
-__device__ __forceinline__ bool load_cross(const T* __restrict__ in, const uint32_t* __restrict__ nb,
-                                           int64_t pkg, bool valid, Cross<T>& x) {
+__device__ __forceinline__ bool load_cross(const T* __restrict__ in,
+                                           const uint32_t* __restrict__ face, int64_t pkg,
+                                           bool valid, Cross<T>& x) {
     const int r = threadIdx.x & 15;
     const int j = r & 3, k = r >> 2;
     uint32_t f = 0;
-    if (valid && r < 6) f = __ldg(nb + pkg * 27 + face_slot(r));
+    if (valid && r < 6) f = __ldg(face + pkg * 8 + r);
     const int base = threadIdx.x & 16;
     const uint32_t nxm = __shfl_sync(0xffffffffu, f, base + 0);
     const uint32_t nxp = __shfl_sync(0xffffffffu, f, base + 1);
@@ -236,11 +234,11 @@ __device__ __forceinline__ void load_cross2(const T* __restrict__ in, uint32_t p
 
 // Persistent package sweep: an 8-lane group takes packages pkg, pkg + G, ...;
 // the face ids of the next package are loaded while the current one is
-// processed, so the face-row gathers do not wait on the neighbour table.
+// processed, so the face-row gathers do not wait on the face table.
 // Op(x, pkg, r0, r1) consumes the cross of rows r0 = j + 4k and r1 = r0 + 8.
 template <class T, class Op>
 __global__ void __launch_bounds__(256) k_sweep(const T* __restrict__ in,
-                                               const uint32_t* __restrict__ nb, uint32_t lo,
+                                               const uint32_t* __restrict__ face, uint32_t lo,
                                                uint32_t hi, Op op) {
     const uint32_t G = gridDim.x * 32u;  // package groups in flight
     uint32_t pkg = lo + ((blockIdx.x * 256u + threadIdx.x) >> 3);
@@ -249,11 +247,11 @@ __global__ void __launch_bounds__(256) k_sweep(const T* __restrict__ in,
     // warp-uniform trip count: the warp's 4 groups have consecutive ids
     const uint32_t wfirst = lo + ((blockIdx.x * 256u + (threadIdx.x & ~31u)) >> 3);
     uint32_t f = 0;
-    if (pkg < hi && g8 < 6) f = __ldg(nb + (size_t)pkg * 27 + face_slot(g8));
+    if (pkg < hi && g8 < 6) f = __ldg(face + (size_t)pkg * 8 + g8);
     for (uint32_t w0 = wfirst; w0 < hi; w0 += G) {
         const uint32_t nxt = pkg + G;
         uint32_t fn = 0;
-        if (nxt < hi && g8 < 6) fn = __ldg(nb + (size_t)nxt * 27 + face_slot(g8));
+        if (nxt < hi && g8 < 6) fn = __ldg(face + (size_t)nxt * 8 + g8);
         Cross2<T> x;
         const bool valid = pkg < hi;
         load_cross2(in, pkg, valid, f, j, k, x);
@@ -321,11 +319,11 @@ __device__ __forceinline__ double inv_norm(double m2) { return m2 > 0.0 ? 1.0 / 
 template <class T>
 __global__ void __launch_bounds__(256) k_gradient(const T* __restrict__ in, T* __restrict__ grad,
                                                   T* __restrict__ normal,
-                                                  const uint32_t* __restrict__ nb, int64_t lo,
+                                                  const uint32_t* __restrict__ face, int64_t lo,
                                                   int64_t hi, StC<T> c) {
     const int64_t pkg = lo + (((int64_t)blockIdx.x * 256 + threadIdx.x) >> 4);
     Cross<T> x;
-    if (!load_cross(in, nb, pkg, pkg < hi, x)) return;
+    if (!load_cross(in, face, pkg, pkg < hi, x)) return;
     T gx[4], gy[4], gz[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -360,11 +358,11 @@ __global__ void __launch_bounds__(256) k_gradient(const T* __restrict__ in, T* _
 // Table 1 "stencil": 7-point Laplacian
 template <class T>
 __global__ void __launch_bounds__(256) k_laplace(const T* __restrict__ in, T* __restrict__ out,
-                                                 const uint32_t* __restrict__ nb, int64_t lo,
+                                                 const uint32_t* __restrict__ face, int64_t lo,
                                                  int64_t hi, T inv_dx2) {
     const int64_t pkg = lo + (((int64_t)blockIdx.x * 256 + threadIdx.x) >> 4);
     Cross<T> x;
-    if (!load_cross(in, nb, pkg, pkg < hi, x)) return;
+    if (!load_cross(in, face, pkg, pkg < hi, x)) return;
     T o[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -506,10 +504,20 @@ __global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
 #pragma unroll
                     for (int q = RS; q < RSX; ++q) v[q] = T(0);
                 }
-                // H(-phi), branch-free (selects around the smooth part)
+                // H(-phi): rows with no value inside the smoothing band
+                // |phi| <= eps take the exact 0 / 1 select only (no sine);
+                // the others the branch-free smooth form
                 T h[RSX];
+                bool smooth = false;
 #pragma unroll
-                for (int q = 0; q < RSX; ++q) h[q] = heav_sel(-v[q], c.eps, c.inv_eps);
+                for (int q = 0; q < RS; ++q) smooth = smooth || !(fabs(v[q]) > c.eps);
+                if (smooth) {
+#pragma unroll
+                    for (int q = 0; q < RSX; ++q) h[q] = heav_sel(-v[q], c.eps, c.inv_eps);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < RSX; ++q) h[q] = v[q] < T(0) ? T(1) : T(0);
+                }
 #pragma unroll
                 for (int q = 0; q < RS; ++q) {
                     all1 = all1 && (h[q] == T(1));
@@ -668,7 +676,7 @@ static void reinit_launch(sg_grid* g, int cur, const StC<T>& c, int64_t lo, int6
     static unsigned blocks_max = 0;  // resident blocks (per instantiation)
     if (!blocks_max) blocks_max = persistent_blocks(k_sweep<T, ReinitOp<T>>, 1 << 30);
     const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div((hi - lo) * 8, 256), blocks_max);
-    k_sweep<T, ReinitOp<T>><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], g->nb, (uint32_t)lo,
+    k_sweep<T, ReinitOp<T>><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], g->face, (uint32_t)lo,
                                                    (uint32_t)hi, op);
 }
 
@@ -709,7 +717,7 @@ static void reinit_t(sg_grid* g, int32_t iters, double cfl, bool halo, cudaStrea
         }
         return;
     }
-    const GraphKey key{g->phi[g->cur], g->phi[1 - g->cur], g->nb, lo, hi, iters,
+    const GraphKey key{g->phi[g->cur], g->phi[1 - g->cur], g->face, lo, hi, iters,
                        (int32_t)sizeof(T), cfl};
     std::lock_guard<std::mutex> lk(g_graph_mu);
     cudaGraphExec_t exec = nullptr;
@@ -854,7 +862,7 @@ static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t
             // (a persistent 8-lane variant like the reinit sweep measured
             // slower here: the kernel is bound by its 1.8 KB/package of writes)
             const unsigned blocks = (unsigned)ceil_div((hi - lo) * 16, 256);
-            k_gradient<T><<<blocks, 256, 0, s>>>(phi, gp, np, g->nb, lo, hi, c);
+            k_gradient<T><<<blocks, 256, 0, s>>>(phi, gp, np, g->face, lo, hi, c);
             SG_LAUNCHED();
         }
         k_singular<T><<<1, 128, 0, s>>>(nullptr, nullptr, gp, np, T(0), (T)g->gc.far);
@@ -886,7 +894,7 @@ static void table1_t(sg_grid* g, int32_t op, double value, cudaStream_t s) {
     } else {
         const unsigned blocks = (unsigned)ceil_div((hi - lo) * 16, 256);
         k_laplace<T><<<blocks, 256, 0, s>>>((const T*)g->phi[g->cur], (T*)g->phi[1 - g->cur],
-                                            g->nb, lo, hi, (T)(1.0 / (g->gc.dx * g->gc.dx)));
+                                            g->face, lo, hi, (T)(1.0 / (g->gc.dx * g->gc.dx)));
     }
     SG_LAUNCHED();
 }

@@ -22,7 +22,7 @@ SG_F32, SG_F64 = 0, 1
 SG_GRAD, SG_NORMAL, SG_KINT = 1, 2, 4
 VIEWS = {"bg": 0, "meta_cell": 1, "meta_cat": 2, "nb": 3, "phi": 4, "grad": 5, "normal": 6,
          "kint": 7, "gkint": 8, "plane_first": 9, "phi_next": 10, "cell_core": 11,
-         "cell_neg": 12}
+         "cell_neg": 12, "face": 13}
 _STATUS = {0: "SG_OK", 1: "SG_ERR_ARG", 2: "SG_ERR_OOM", 3: "SG_ERR_CUDA", 4: "SG_ERR_NCCL",
            5: "SG_ERR_STATE", 6: "SG_ERR_DOMAIN"}
 

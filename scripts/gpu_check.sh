@@ -93,6 +93,31 @@ if [[ $what == fuse ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python bench.py --config C3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_c3.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_kint" -s 1 -c 1 -o gpurun_out/prof_kint python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_kint.log 2>&1
 fi
+if [[ $what == kint2 ]]; then
+  timeout 600 python -m pytest tests -m gpu -q -x -k "gradient or kernel or relax or clean or smoke" > gpurun_out/pytest_kint2.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_kint2.log
+  for v in 1 0; do
+    SG_KINT_ROWSKIP=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_rs$v.json 2> /dev/null
+    SG_KINT_ROWSKIP=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_rs$v.json 2> /dev/null
+  done
+  # warm-L2 sweeps inside the step: no cache flush/invalidate by ncu
+  timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct,l1tex__t_bytes.sum,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active -k regex:"k_sweep|k_probe|k_kint|k_gradient" --csv --log-file gpurun_out/warm_c2.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
+fi
+if [[ $what == face ]]; then
+  timeout 1500 python -m pytest tests -m gpu -q -x -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+  timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
+  timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+  timeout 600 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+  timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct,l1tex__t_bytes.sum,smsp__issue_active.avg.pct_of_peak_sustained_active -k regex:"k_sweep|k_probe|k_gradient" --csv --log-file gpurun_out/warm_c2b.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
+fi
+if [[ $what == sched ]]; then
+  timeout 900 python -m pytest tests -m gpu -q -x -rf -k "tables or reinit or slab or sign or smoke or refine or c3 or c5 or clean or empty" > gpurun_out/pytest_sched.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_sched.log
+  for v in 1 0; do
+    SG_SCHED=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_sc$v.json 2> gpurun_out/bench_sc$v.err
+    SG_SCHED=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_sc$v.json 2> /dev/null
+  done
+  timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct,l1tex__t_bytes.sum,smsp__issue_active.avg.pct_of_peak_sustained_active -k regex:"k_sweep" -c 30 --csv --log-file gpurun_out/warm_c2c.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_sched.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+fi
 if [[ $what == pdl ]]; then
   timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or smoke or clean" > gpurun_out/pytest_pdl.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pdl.log
   for v in 1 0; do

@@ -55,6 +55,18 @@ def assert_phi_close(w, got, exp, what=""):
         assert err <= 1e-12, f"{what}: max rel err {err:.3e}"
 
 
+FACE_SLOTS = [12, 14, 10, 16, 4, 22]  # -x, +x, -y, +y, -z, +z (ox + 3 oy + 9 oz)
+
+
+def assert_face_table(g):
+    """The compact face table the 7-point sweeps read is the neighbour table's
+    six face slots (plus two zero pads), for every package."""
+    face, nb = u32(g.view("face")), u32(g.view("nb"))
+    assert face.shape == (nb.shape[0], 8)
+    assert np.array_equal(face[:, :6], nb[:, FACE_SLOTS])
+    assert not face[:, 6:].any()
+
+
 def tables_equal(sgm, O, w):
     o = O.Oracle(w)
     t = o.build_tables()
@@ -67,6 +79,7 @@ def tables_equal(sgm, O, w):
     assert np.array_equal(u32(g.view("meta_cell")), t.meta_cell)
     assert np.array_equal(g.view("meta_cat").cpu().numpy(), t.meta_cat)
     assert np.array_equal(u32(g.view("nb")), t.nb)
+    assert_face_table(g)
     pf = g.view("plane_first").cpu().numpy()
     exp_pf = 2 + np.concatenate([[0], np.cumsum(t.plane_count)])
     assert np.array_equal(pf, exp_pf)

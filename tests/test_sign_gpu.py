@@ -89,6 +89,9 @@ def _pair(sgm, O, w, max_sweeps=0):
     assert sw == osw
     assert np.array_equal(u32(g.view("bg")), bg)
     assert np.array_equal(u32(g.view("nb")), nb)
+    # the face table the sweeps read follows the corrected neighbour table
+    face = u32(g.view("face"))
+    assert np.array_equal(face[:, :6], nb[:, [12, 14, 10, 16, 4, 22]])
     assert np.array_equal(cell_bits(g, w), cn.astype(bool))
     phi_bits_equal(g.view("phi").cpu().numpy(), o.to_packages(phi, -far, far))
     return g, sw
@@ -107,7 +110,7 @@ def test_sign_correct_sweep_cap(sgm, O, cap):
 
 def _grid_state(g):
     return (u32(g.view("bg")).copy(), u32(g.view("nb")).copy(), g.view("phi").cpu().numpy(),
-            u32(g.view("cell_neg")).copy())
+            u32(g.view("cell_neg")).copy(), u32(g.view("face")).copy())
 
 
 @pytest.mark.parametrize("name", ["C2", "C3"])
@@ -125,6 +128,7 @@ def test_full_size_leaky_equals_watertight(sgm, name):
     assert np.array_equal(got[1], ref[1])
     phi_bits_equal(got[2], ref[2].astype(np.float64))
     assert np.array_equal(got[3], ref[3])
+    assert np.array_equal(got[4], ref[4])  # face table
     assert sw[0] > 0 and sw[1] > 0
     del g
 
