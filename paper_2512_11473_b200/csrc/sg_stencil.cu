@@ -204,32 +204,62 @@ struct Cross2 {
     T xm0, xp0, xm1, xp1;
 };
 
+// The four 8-lane groups of a warp hold consecutive packages pkg0 .. pkg0+3
+// (k_sweep), and lane (j, k) of every group owns the same rows (j, k), (j, k+2).
+// When the x-face neighbour of a package is the next (previous) id -- an
+// x-run of active cells, the common case -- its x = 0 (x = 3) values are
+// already in the registers of the same lane of the next (previous) group:
+// they come by a shuffle of 8 lanes instead of four scalar loads, which cut
+// 16-of-256-byte sector fetches from the L2.  `next_ok`: package pkg + 1 is
+// processed by the next group in this iteration (pkg + 1 < hi).
 template <class T>
 __device__ __forceinline__ void load_cross2(const T* __restrict__ in, uint32_t pkg, bool valid,
-                                            uint32_t f, int j, int k, Cross2<T>& x) {
+                                            bool next_ok, uint32_t f, int j, int k,
+                                            Cross2<T>& x) {
     const int base = threadIdx.x & 24;
+    const int grp = (threadIdx.x >> 3) & 3;
     const uint32_t nxm = __shfl_sync(0xffffffffu, f, base + 0);
     const uint32_t nxp = __shfl_sync(0xffffffffu, f, base + 1);
     const uint32_t nym = __shfl_sync(0xffffffffu, f, base + 2);
     const uint32_t nyp = __shfl_sync(0xffffffffu, f, base + 3);
     const uint32_t nzm = __shfl_sync(0xffffffffu, f, base + 4);
     const uint32_t nzp = __shfl_sync(0xffffffffu, f, base + 5);
-    if (!valid) return;
-    const T* P = in + (size_t)pkg * 64;
-    const int r0 = j + 4 * k, r1 = r0 + 8;
-    ld_row(P + 4 * r0, x.c0);
-    ld_row(P + 4 * r1, x.c1);
-    ld_row(P + 4 * (r0 + 4), x.zmid);
-    ld_row(k == 0 ? in + (size_t)nzm * 64 + 4 * (j + 12) : P + 4 * j, x.zlo);
-    ld_row(k == 0 ? P + 4 * (j + 12) : in + (size_t)nzp * 64 + 4 * j, x.zhi);
-    ld_row(j > 0 ? P + 4 * (r0 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * k), x.ym0);
-    ld_row(j < 3 ? P + 4 * (r0 + 1) : in + (size_t)nyp * 64 + 4 * (4 * k), x.yp0);
-    ld_row(j > 0 ? P + 4 * (r1 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * (k + 2)), x.ym1);
-    ld_row(j < 3 ? P + 4 * (r1 + 1) : in + (size_t)nyp * 64 + 4 * (4 * (k + 2)), x.yp1);
-    x.xm0 = __ldg(in + (size_t)nxm * 64 + 4 * r0 + 3);
-    x.xp0 = __ldg(in + (size_t)nxp * 64 + 4 * r0);
-    x.xm1 = __ldg(in + (size_t)nxm * 64 + 4 * r1 + 3);
-    x.xp1 = __ldg(in + (size_t)nxp * 64 + 4 * r1);
+    const bool sh_m = grp > 0 && nxm == pkg - 1;
+    const bool sh_p = grp < 3 && next_ok && nxp == pkg + 1;
+    if (valid) {
+        const T* P = in + (size_t)pkg * 64;
+        const int r0 = j + 4 * k, r1 = r0 + 8;
+        ld_row(P + 4 * r0, x.c0);
+        ld_row(P + 4 * r1, x.c1);
+        ld_row(P + 4 * (r0 + 4), x.zmid);
+        ld_row(k == 0 ? in + (size_t)nzm * 64 + 4 * (j + 12) : P + 4 * j, x.zlo);
+        ld_row(k == 0 ? P + 4 * (j + 12) : in + (size_t)nzp * 64 + 4 * j, x.zhi);
+        ld_row(j > 0 ? P + 4 * (r0 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * k), x.ym0);
+        ld_row(j < 3 ? P + 4 * (r0 + 1) : in + (size_t)nyp * 64 + 4 * (4 * k), x.yp0);
+        ld_row(j > 0 ? P + 4 * (r1 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * (k + 2)), x.ym1);
+        ld_row(j < 3 ? P + 4 * (r1 + 1) : in + (size_t)nyp * 64 + 4 * (4 * (k + 2)), x.yp1);
+        if (!sh_m) {
+            x.xm0 = __ldg(in + (size_t)nxm * 64 + 4 * r0 + 3);
+            x.xm1 = __ldg(in + (size_t)nxm * 64 + 4 * r1 + 3);
+        }
+        if (!sh_p) {
+            x.xp0 = __ldg(in + (size_t)nxp * 64 + 4 * r0);
+            x.xp1 = __ldg(in + (size_t)nxp * 64 + 4 * r1);
+        }
+    }
+    // every lane takes part (the caller's trip count is warp-uniform)
+    const T m0 = __shfl_up_sync(0xffffffffu, x.c0[3], 8);
+    const T m1 = __shfl_up_sync(0xffffffffu, x.c1[3], 8);
+    const T p0 = __shfl_down_sync(0xffffffffu, x.c0[0], 8);
+    const T p1 = __shfl_down_sync(0xffffffffu, x.c1[0], 8);
+    if (sh_m) {
+        x.xm0 = m0;
+        x.xm1 = m1;
+    }
+    if (sh_p) {
+        x.xp0 = p0;
+        x.xp1 = p1;
+    }
 }
 
 // Persistent package sweep: an 8-lane group takes packages pkg, pkg + G, ...;
@@ -237,7 +267,7 @@ __device__ __forceinline__ void load_cross2(const T* __restrict__ in, uint32_t p
 // processed, so the face-row gathers do not wait on the face table.
 // Op(x, pkg, r0, r1) consumes the cross of rows r0 = j + 4k and r1 = r0 + 8.
 template <class T, class Op>
-__global__ void __launch_bounds__(256) k_sweep(const T* __restrict__ in,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 2) k_sweep(const T* __restrict__ in,
                                                const uint32_t* __restrict__ face, uint32_t lo,
                                                uint32_t hi, Op op) {
     const uint32_t G = gridDim.x * 32u;  // package groups in flight
@@ -254,7 +284,7 @@ __global__ void __launch_bounds__(256) k_sweep(const T* __restrict__ in,
         if (nxt < hi && g8 < 6) fn = __ldg(face + (size_t)nxt * 8 + g8);
         Cross2<T> x;
         const bool valid = pkg < hi;
-        load_cross2(in, pkg, valid, f, j, k, x);
+        load_cross2(in, pkg, valid, pkg + 1 < hi, f, j, k, x);
         if (valid) op(x, pkg, j + 4 * k, j + 4 * k + 8);
         pkg = nxt;
         f = fn;

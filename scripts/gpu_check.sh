@@ -118,6 +118,25 @@ if [[ $what == sched ]]; then
   timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct,l1tex__t_bytes.sum,smsp__issue_active.avg.pct_of_peak_sustained_active -k regex:"k_sweep" -c 30 --csv --log-file gpurun_out/warm_c2c.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_sched.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 fi
+if [[ $what == xsh ]]; then
+  timeout 900 python -m pytest tests -m gpu -q -x -rf -k "reinit or slab or sign or smoke or refine or c3 or c5 or clean or empty or table1" > gpurun_out/pytest_xsh.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_xsh.log
+  timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_xsh.json 2> gpurun_out/bench_xsh.err
+  timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_xsh.json 2> /dev/null
+  timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct,l1tex__t_bytes.sum,smsp__issue_active.avg.pct_of_peak_sustained_active -k regex:"k_sweep" -c 30 --csv --log-file gpurun_out/warm_c2d.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
+fi
+if [[ $what == l2p ]]; then
+  python -c "
+from cuda.bindings import runtime as rt
+for a in ['cudaDevAttrMaxPersistingL2CacheSize','cudaDevAttrMaxAccessPolicyWindowSize','cudaDevAttrL2CacheSize']:
+    print(a, rt.cudaDeviceGetAttribute(getattr(rt.cudaDeviceAttr, a), 0))
+" > gpurun_out/l2attr.txt 2>&1
+  timeout 900 python -m pytest tests -m gpu -q -x -rf -k "reinit or slab or smoke or c3 or clean" > gpurun_out/pytest_l2p.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_l2p.log
+  for v in 1 0; do
+    SG_L2PERSIST=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_l2p$v.json 2> /dev/null
+    SG_L2PERSIST=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_l2p$v.json 2> /dev/null
+  done
+  timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct -k regex:"k_sweep|k_probe|k_kint|k_gradient" -c 45 --csv --log-file gpurun_out/warm_c2e.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
+fi
 if [[ $what == pdl ]]; then
   timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or smoke or clean" > gpurun_out/pytest_pdl.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pdl.log
   for v in 1 0; do
