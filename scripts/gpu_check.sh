@@ -137,6 +137,14 @@ for a in ['cudaDevAttrMaxPersistingL2CacheSize','cudaDevAttrMaxAccessPolicyWindo
   done
   timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct -k regex:"k_sweep|k_probe|k_kint|k_gradient" -c 45 --csv --log-file gpurun_out/warm_c2e.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
 fi
+if [[ $what == blk ]]; then
+  SG_SWEEP_BLOCKED=1 timeout 900 python -m pytest tests -m gpu -q -x -rf -k "reinit or slab or smoke or c3 or clean or sign" > gpurun_out/pytest_blk.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_blk.log
+  for v in 1 0; do
+    SG_SWEEP_BLOCKED=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_blk$v.json 2> /dev/null
+    SG_SWEEP_BLOCKED=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_blk$v.json 2> /dev/null
+    SG_SWEEP_BLOCKED=$v timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct -k regex:"k_sweep" -c 20 --csv --log-file gpurun_out/warm_blk$v.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+  done
+fi
 if [[ $what == pdl ]]; then
   timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or smoke or clean" > gpurun_out/pytest_pdl.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pdl.log
   for v in 1 0; do
