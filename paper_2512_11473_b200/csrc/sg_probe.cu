@@ -390,15 +390,17 @@ void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void*
     SG_ARG(!is_device_ptr(pos) && !is_device_ptr(phi) && (grad == nullptr || !is_device_ptr(grad)),
            "sg_probe: pos/phi/grad must be all device or all host pointers");
     Staging& S = staging();
-    const int64_t chunk = std::min<int64_t>(n, (int64_t)1 << 22);
+    // ~16 chunks (0.25-2 M particles): short pipeline fill and drain
+    const int64_t chunk = std::min<int64_t>(
+        n, std::max<int64_t>((int64_t)1 << 18, std::min<int64_t>(ceil_div(n, 16), (int64_t)1 << 21)));
     const size_t es = (size_t)g->esz;
     char* buf[2];
     const size_t per = chunk * es * (3 + 1 + (grad ? 3 : 0));
+    // the uploads of the positions do not depend on the grid: only the probe
+    // kernels wait for the caller's stream (the build / reinit / gradient
+    // still running there), so the first chunks' H2D overlap that work
     SG_CUDA(cudaEventRecord(S.ev, s));
-    for (int b = 0; b < 2; ++b) {
-        SG_CUDA(cudaStreamWaitEvent(S.st[b], S.ev, 0));
-        buf[b] = (char*)dalloc(per, S.st[b]);
-    }
+    for (int b = 0; b < 2; ++b) buf[b] = (char*)dalloc(per, S.st[b]);
     const char* hp = (const char*)pos;
     char* ho = (char*)phi;
     char* hg = (char*)grad;
@@ -411,6 +413,7 @@ void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void*
         char* dphi = dp + chunk * es * 3;
         char* dg = dphi + chunk * es;
         SG_CUDA(cudaMemcpyAsync(dp, hp + off * 3 * es, m * 3 * es, cudaMemcpyHostToDevice, st));
+        if (k < 2) SG_CUDA(cudaStreamWaitEvent(st, S.ev, 0));  // grid fields ready
         run(m, dp, dphi, grad ? dg : nullptr, st);
         SG_CUDA(cudaMemcpyAsync(ho + off * es, dphi, m * es, cudaMemcpyDeviceToHost, st));
         if (grad)

@@ -476,7 +476,11 @@ struct KGeo {
     static constexpr int S2MAX = (R + 1) * (R + 1) - 1;  // largest |o|^2 enumerated
 };
 
-template <class T, int R>
+// S2M: the largest |o|^2 enumerated -- (R+1)^2 - 1 in general; 6 for R = 2
+// when the taps at |o|^2 = 8 lie outside the support (h_ratio <= sqrt 2, e.g.
+// the default 1.3: 81 taps), which drops their zero-weight FMAs and the whole
+// (|oy|, |oz|) = (2, 2) row group (same bits: fma(0, h, acc) = acc)
+template <class T, int R, int S2M>
 __global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
                                               const uint32_t* __restrict__ nb, int64_t lo,
                                               int64_t hi, KintC<T> c, T* __restrict__ K,
@@ -611,7 +615,7 @@ __global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
         for (int ga = 0; ga <= R; ++ga) {
 #pragma unroll
             for (int gb = 0; gb <= R; ++gb) {
-                if (ga * ga + gb * gb > Geo::S2MAX) continue;
+                if (ga * ga + gb * gb > S2M) continue;
                 T S[RSX], Dy[RSX], Dz[RSX];
                 if (ga == 0 && gb == 0) {
                     load(0, 0, S);
@@ -645,7 +649,7 @@ __global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
 #pragma unroll
                 for (int ox = -R; ox <= R; ++ox) {
                     const int s2 = ox * ox + ga * ga + gb * gb;
-                    if (s2 > Geo::S2MAX) continue;
+                    if (s2 > S2M) continue;
                     const T w = c.wt[s2];
                     const T wx = ox > 0 ? c.gt[ox][s2] : -c.gt[-ox][s2];
                     const T wy = c.gt[ga][s2];
@@ -829,7 +833,10 @@ static void launch_kint_r(sg_grid* g, const T* phi, const KintC<T>& c, cudaStrea
     const int64_t lo = g->own_lo, hi = g->own_hi;
     if (hi <= lo) return;
     const size_t smem = sizeof(T) * 8 * KGeo<R>::VOL;
-    auto kern = k_kint<T, R>;
+    auto kern = k_kint<T, R, KGeo<R>::S2MAX>;
+    if constexpr (R == 2) {
+        if (c.wt[7] == T(0) && c.wt[8] == T(0)) kern = k_kint<T, 2, 6>;  // |o|^2 = 8 outside
+    }
     if (smem > 48 * 1024)
         SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)ceil_div(hi - lo, 8), 128, smem, s>>>(phi, g->nb, lo, hi, c, (T*)g->kint,

@@ -145,6 +145,22 @@ if [[ $what == blk ]]; then
     SG_SWEEP_BLOCKED=$v timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct -k regex:"k_sweep" -c 20 --csv --log-file gpurun_out/warm_blk$v.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
   done
 fi
+if [[ $what == e2e ]]; then
+  timeout 900 python -m pytest tests -m gpu -q -x -rf -k "probe or smoke or relax" > gpurun_out/pytest_e2e.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_e2e.log
+  timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_e2e.json 2> gpurun_out/bench_e2e.err
+  python - > gpurun_out/pcie.txt 2>&1 <<'PY'
+import torch, time
+for mb in (64, 256):
+    n = mb << 18
+    h = torch.empty(n, dtype=torch.float32).pin_memory(); d = torch.empty(n, device="cuda")
+    for direction in ("h2d", "d2h"):
+        torch.cuda.synchronize(); t = time.perf_counter()
+        for _ in range(5):
+            (d.copy_(h, non_blocking=True) if direction == "h2d" else h.copy_(d, non_blocking=True))
+        torch.cuda.synchronize(); dt = (time.perf_counter() - t) / 5
+        print(direction, mb, "MB", round(n * 4 / dt / 1e9, 1), "GB/s")
+PY
+fi
 if [[ $what == pdl ]]; then
   timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or smoke or clean" > gpurun_out/pytest_pdl.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pdl.log
   for v in 1 0; do

@@ -248,6 +248,28 @@ def test_gradient_normal_kernel(sgm, O, name):
     assert np.max(np.abs(gG - eG) / (np.maximum(1.0, h * np.abs(eG)) / h)) <= tol
 
 
+@pytest.mark.parametrize("h_ratio", [0.5, 1.0, 1.3, 1.45, 1.7])
+def test_kernel_integral_h_ratios(sgm, O, h_ratio):
+    """K7 at every staged radius R = ceil(2 h_ratio) - 1 (0..3), including
+    R = 2 with (1.45) and without (1.3) the |o|^2 = 8 taps in the support."""
+    w = W.config("C1")
+    o = O.Oracle(w)
+    o.build_tables()
+    phi = o.reinit(o.phi_dense(), 3)
+    g = sgm.Grid(w)
+    _upload(g, w, o.to_packages(phi, -o.far, o.far))
+    g.gradient(sgm.SG_KINT, h_ratio=h_ratio)
+    K, G = o.kernel_integrals(phi, h_ratio)
+    S = O.kernel_taps(h_ratio, o.dx)[1].sum()
+    assert abs(g.info["kernel_sum"] - S) < 1e-12
+    gK = g.view("kint").cpu().numpy()
+    gG = g.view("gkint").cpu().numpy()
+    assert np.max(np.abs(gK - o.to_packages(K, S, 0.0))) <= 1e-12
+    h = h_ratio * w.dx
+    eG = _vec_pk(o, G)
+    assert np.max(np.abs(gG - eG) / (np.maximum(1.0, h * np.abs(eG)) / h)) <= 1e-12
+
+
 # ------------------------------------------------------------------- probe --
 
 def _probe_compare(sgm, O, w, pos_np, phi_iters=3):
@@ -288,6 +310,14 @@ def test_probe_c1_lattice_and_random(sgm, O):
     assert np.array_equal(hphi.numpy(), gphi) and np.array_equal(hgrad.numpy(), ggrad)
     pphi, pgrad = g.probe(tpos.cpu())  # pageable
     assert np.array_equal(pphi.numpy(), gphi)
+    # the host path's kernels wait for work still queued on the caller's
+    # stream (its uploads do not): new fields queued right before the call
+    g.reinit(5).gradient(sgm.SG_GRAD)
+    hphi2, hgrad2 = g.probe(hpos)
+    dphi2, dgrad2 = g.probe(tpos)
+    assert not np.array_equal(hphi2.numpy(), hphi.numpy())
+    assert np.array_equal(hphi2.numpy(), dphi2.cpu().numpy())
+    assert np.array_equal(hgrad2.numpy(), dgrad2.cpu().numpy())
 
 
 def test_probe_c4_particles_on_c2(sgm, O):
@@ -299,6 +329,10 @@ def test_probe_c4_particles_on_c2(sgm, O):
     far = np.abs(gphi) == np.float32(o.far)
     frac_band = 1.0 - far.mean()
     assert 0.15 < frac_band < 0.23  # ~18.9 % in active cells
+    # host buffers (the e2e path: 16 pipelined chunks on two staging streams,
+    # uploads overlapping the caller's stream) give the device path's bits
+    hphi, hgrad = g.probe(tpos.cpu().pin_memory())
+    assert np.array_equal(hphi.numpy(), gphi) and np.array_equal(hgrad.numpy(), ggrad)
 
 
 def test_probe_empty_and_zero(sgm, O):
