@@ -161,6 +161,13 @@ for mb in (64, 256):
         print(direction, mb, "MB", round(n * 4 / dt / 1e9, 1), "GB/s")
 PY
 fi
+if [[ $what == bps ]]; then
+  timeout 900 python -m pytest tests -m gpu -q -x -rf -k "kernel or gradient or clean or relax" > gpurun_out/pytest_bps.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_bps.log
+  for v in 0 4 6 8 11; do
+    SG_KINT_BPS=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_bps$v.json 2> /dev/null
+    SG_KINT_BPS=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_bps$v.json 2> /dev/null
+  done
+fi
 if [[ $what == pdl ]]; then
   timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or smoke or clean" > gpurun_out/pytest_pdl.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pdl.log
   for v in 1 0; do
