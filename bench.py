@@ -174,6 +174,72 @@ def run_config(w, n_pkg, n_part, order, world):
             "parallelism": f"zslab{world}" if world > 1 else "1 GPU"}
 
 
+def kernel_rooflines(sg, w, stream, flush, d_pos, n_part, probe_ms, reinit_ms, hbm):
+    """Roofline of each hot-path kernel on its own (SURVEY 8(d) units): the
+    reinit sweep and the probe from the timed steps, the gradient/normal (K6)
+    and kernel-integral (K7) kernels -- concurrent inside a step -- timed
+    apart here on one grid (10 launches each, L2 flushed before each,
+    CUDA events on the launching stream)."""
+    import torch
+    esz = 4 if w.dtype == "f32" else 8
+    g = sg.Grid(w, stream=stream).reinit(REINIT_ITERS, w.cfl, stream=stream)
+    n_act = (g.info["n_pkg"] - 2) * 64
+
+    def timed(fn, reps=10):
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
+    t_grad = timed(lambda: g.gradient(sg.SG_GRAD | sg.SG_NORMAL, w.h_ratio, stream=stream))
+    t_kint = timed(lambda: g.gradient(sg.SG_KINT, w.h_ratio, stream=stream))
+    clock_ghz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"]) \
+        / 1e3 if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1.965
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    fma_peak = sms * 128 * clock_ghz * 1e9  # FP32 FMA lanes x clock (B200_PROFILING.md units)
+
+    def hbm_entry(name, bytes_, ms, note):
+        a = bytes_ / (ms * 1e-3) / 1e9
+        return {"kernel": name, "bound": "hbm", "us": ms * 1e3, "alg_bytes": bytes_,
+                "achieved": a, "unit": "GB/s", "peak": hbm, "frac": a / hbm,
+                "frac_nominal_8tbs": a / 8000.0, "note": note}
+
+    out = [hbm_entry("k_sweep (reinit, per sweep)", (2 * esz + 32 / 64) * n_act, reinit_ms,
+                     "phi in + out + 32 B face row per package")]
+    out.append(hbm_entry("k_gradient (grad + normal)", (esz + 32 / 64 + 7 * esz) * n_act, t_grad,
+                         "phi + face row in; (phi, grad) interleaved + normal out"))
+    fmas = 324.0 * n_act  # 81 taps x (K, Gx, Gy, Gz), direct form (SURVEY 8(d))
+    out.append({"kernel": "k_kint (kernel integrals)", "bound": "alu", "us": t_kint * 1e3,
+                "alg_fma": fmas, "achieved": fmas / (t_kint * 1e-3) / 1e12, "unit": "TFMA/s",
+                "peak": fma_peak / 1e12, "frac": fmas / (t_kint * 1e-3) / fma_peak,
+                "note": "direct-form FMAs (the kernel executes ~1.8x fewer); peak = SMs x "
+                        "128 FP32 lanes x max SM clock"})
+    if probe_ms:
+        # 12 B position in, 16 B (phi, grad) out, 4 B background entry per probe,
+        # plus every touched package's (phi, grad) vectors and neighbour row once
+        with torch.no_grad():
+            inv = torch.tensor(1.0 / w.cell, dtype=d_pos.dtype, device=d_pos.device)
+            c = torch.clamp((d_pos * inv).floor().long(), min=0)
+            c[:, 0].clamp_(max=w.n[0] - 1)
+            c[:, 1].clamp_(max=w.n[1] - 1)
+            c[:, 2].clamp_(max=w.n[2] - 1)
+            bg = g.view("bg").view(torch.int32).long()
+            ids = bg[c[:, 0] + w.n[0] * (c[:, 1] + w.n[1] * c[:, 2])]
+            touched = int(torch.unique(ids[ids >= 2]).numel())
+        pb = 32.0 * n_part + touched * (64 * 4 * esz + 108)
+        out.append(hbm_entry("k_probe", pb, probe_ms,
+                             f"32 B per probe + {touched} touched packages x "
+                             f"({64 * 4 * esz} B + 108 B nb row)"))
+    g.close()
+    return out
+
+
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -300,6 +366,8 @@ def run_ours(args, rank, world, local):
     stages["reinit_plus_gradient_cells_per_s"] = n_act * (REINIT_ITERS + 1) / (
         (st[:, 1].mean() + st[:, 2].mean()) * 1e-3)
     clocks = clk.summary()
+    kernels = kernel_rooflines(sg, w, stream, flush, d_pos, n_part,
+                               float(st[:, 3].mean()) if n_part else None, reinit_ms, hbm)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -322,6 +390,7 @@ def run_ours(args, rank, world, local):
                               "streaming most of it from HBM even below the 126 MB L2 "
                               "(profiles/README.md)")},
         "clocks": clocks,
+        "kernels": kernels,
         "gpu_name": torch.cuda.get_device_name(local),
     }
     if not args.no_cpu_baseline:
