@@ -61,6 +61,9 @@ def parse():
     p.add_argument("--order", default="lattice", choices=["lattice", "shuffled"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-kernel-roofline", action="store_true",
+                   help="skip the per-kernel roofline timings after the timed steps "
+                        "(e.g. under ncu, so the launch list is the steps only)")
     p.add_argument("--slab", action="store_true",
                    help="z-slab path (NCCL) even at one rank (exercises the multi-GPU code)")
     return p.parse_args()
@@ -386,8 +389,9 @@ def run_ours(args, rank, world, local):
     stages["reinit_plus_gradient_cells_per_s"] = n_act * (REINIT_ITERS + 1) / (
         (st[:, 1].mean() + st[:, 2].mean()) * 1e-3)
     clocks = clk.summary()
-    kernels = kernel_rooflines(sg, w, stream, flush, d_pos, n_part,
-                               float(st[:, 3].mean()) if n_part else None, reinit_ms, hbm)
+    kernels = None if args.no_kernel_roofline else kernel_rooflines(
+        sg, w, stream, flush, d_pos, n_part, float(st[:, 3].mean()) if n_part else None,
+        reinit_ms, hbm)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",

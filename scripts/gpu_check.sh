@@ -175,11 +175,20 @@ if [[ $what == final ]]; then
   timeout 900 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
   timeout 900 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > $O/bench_c3.json 2> $O/bench_c3.err
   timeout 900 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_c5.json 2> $O/bench_c5.err
-  B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+  B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-kernel-roofline"
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $B > $O/ncu_launch.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep' -s 25 -c 1 -o $O/prof_reinit $B > $O/ncu_reinit.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gradient|k_kint|k_probe|k_phi_init|k_count|k_tag|k_nb|k_scatter' -s 7 -c 8 -o $O/prof_other $B > $O/ncu_other.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep|k_gradient|k_kint' -s 26 -c 3 -o $O/prof_c3 python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_c3.log 2>&1
+fi
+if [[ $what == wave ]]; then
+  timeout 600 python -m pytest tests -m gpu -q -x -rf -k "wavefront or reinit or c3_full or c5 or smoke or clean or sign" > gpurun_out/pytest_wave.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_wave.log
+  for v in 1 0; do
+    SG_WAVE=$v timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_wave$v.json 2> gpurun_out/bench_wave$v.err
+    SG_WAVE=$v timeout 300 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_wave$v.json 2> /dev/null
+    SG_WAVE=$v timeout 300 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c5_wave$v.json 2> /dev/null
+  done
+  timeout 600 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum -k regex:"k_wave" -c 2 --csv --log-file gpurun_out/warm_wave.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 fi
 if [[ $what == pdl ]]; then
   timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or smoke or clean" > gpurun_out/pytest_pdl.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pdl.log
