@@ -375,27 +375,45 @@ __global__ void __launch_bounds__(kTB) k_scatter(GridC gc, Bits b, int64_t nword
         off = L0 - (int64_t)gc.zs_lo * gc.plane;
         id0 = (uint32_t)(2 + tile_off[blockIdx.x] + ex);
     }
+    // write-out: four rounds of 8 words per warp, lane l takes 8 consecutive
+    // cells (8 (l & 3) ..) of word 8 round + l / 4 -> 32 B per lane, 1 KB per
+    // warp store, two 16 B vector stores when the row start is 16 B aligned
     const int lane = threadIdx.x & 31;
-    const uint32_t m = 1u << lane, below = m - 1u;
-    for (int src = 0; src < 32; ++src) {
+    const int c0 = 8 * (lane & 3);
+#pragma unroll 1
+    for (int round = 0; round < 4; ++round) {
+        const int src = 8 * round + (lane >> 2);
         const int nb_ = __shfl_sync(0xffffffffu, nbits, src);
-        if (nb_ == 0) continue;  // warp-uniform
         const uint32_t a = __shfl_sync(0xffffffffu, act, src);
         const uint32_t cw = __shfl_sync(0xffffffffu, core, src);
         const uint32_t nw = __shfl_sync(0xffffffffu, neg, src);
         const uint32_t i0 = __shfl_sync(0xffffffffu, id0, src);
         const int64_t o = __shfl_sync(0xffffffffu, off, src);
         const int64_t l0 = __shfl_sync(0xffffffffu, L0, src);
-        if (lane < nb_) {
-            uint32_t v;
+        if (c0 >= nb_) continue;
+        uint32_t v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int b = c0 + i;
+            const uint32_t m = 1u << b;
             if (a & m) {
-                v = i0 + __popc(a & below);
-                meta_cell[v] = (uint32_t)(l0 + lane);
-                meta_cat[v] = (cw & m) ? 3 : 2;
+                v[i] = i0 + __popc(a & (m - 1u));
+                if (b < nb_) {
+                    meta_cell[v[i]] = (uint32_t)(l0 + b);
+                    meta_cat[v[i]] = (cw & m) ? 3 : 2;
+                }
             } else {
-                v = (nw & m) ? 0u : 1u;
+                v[i] = (nw & m) ? 0u : 1u;
             }
-            bg[o + lane] = v;
+        }
+        uint32_t* dst = bg + o + c0;
+        if (c0 + 8 <= nb_ && ((uintptr_t)dst & 15u) == 0) {
+            reinterpret_cast<uint4*>(dst)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+            reinterpret_cast<uint4*>(dst)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (c0 + i < nb_) dst[i] = v[i];
         }
     }
 }
@@ -534,10 +552,17 @@ __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
         const double R = 2.598076211353316 * gc.dx;
         const double eps = 1e-9 * (gc.cell + fabs(gc.lower[0]) + fabs(gc.lower[1]) +
                                    fabs(gc.lower[2]) + gc.upper[0] + gc.upper[1] + gc.upper[2]);
+        // the package-centre values: lane i of the package's 16-lane group
+        // evaluates primitive i (n <= SG_MAX_PRIMS = 16), then all share them
+        static_assert(SG_MAX_PRIMS <= 16, "one primitive per lane of a package group");
+        const int lane = threadIdx.x & 31;
+        const unsigned hm = 0xFFFFu << (lane & 16);  // this package's half-warp
+        const double fmine =
+            col < geom.n ? sd_prim(geom.kind[col], geom.p[col], pcx, pcy, pcz) : 0.0;
         double fc[SG_MAX_PRIMS];
         double m = 0.0;
         for (int i = 0; i < geom.n; ++i) {
-            fc[i] = sd_prim(geom.kind[i], geom.p[i], pcx, pcy, pcz);
+            fc[i] = __shfl_sync(hm, fmine, (lane & 16) + i);
             m = i == 0 ? fc[i] : fmin(m, fc[i]);
         }
         uint32_t mask = 0;

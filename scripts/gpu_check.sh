@@ -190,6 +190,13 @@ if [[ $what == wave ]]; then
   done
   timeout 600 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum -k regex:"k_wave" -c 2 --csv --log-file gpurun_out/warm_wave.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 fi
+if [[ $what == init ]]; then
+  timeout 900 python -m pytest tests -m gpu -q -x -rf -k "tables or phi_init or c3 or c5 or smoke or sign or refine or mesh or forced" > gpurun_out/pytest_init.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_init.log
+  timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-kernel-roofline > gpurun_out/bench_init.json 2> /dev/null
+  timeout 300 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-kernel-roofline > gpurun_out/bench_c3_init.json 2> /dev/null
+  timeout 300 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu-baseline --no-kernel-roofline > gpurun_out/bench_c5_init.json 2> /dev/null
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3_init.csv python bench.py --config C3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-kernel-roofline > /dev/null 2>&1
+fi
 if [[ $what == pdl ]]; then
   timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or smoke or clean" > gpurun_out/pytest_pdl.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pdl.log
   for v in 1 0; do
