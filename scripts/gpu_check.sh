@@ -169,7 +169,7 @@ if [[ $what == bps ]]; then
   done
 fi
 if [[ $what == final ]]; then
-  O=gpurun_out/r01g; mkdir -p $O
+  O=gpurun_out/${TAG:-r01h}; mkdir -p $O
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
   timeout 1500 python -m pytest tests -m gpu -q -rf --durations=10 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
   timeout 900 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
@@ -179,7 +179,8 @@ if [[ $what == final ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $B > $O/ncu_launch.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep' -s 25 -c 1 -o $O/prof_reinit $B > $O/ncu_reinit.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gradient|k_kint|k_probe|k_phi_init|k_count|k_tag|k_nb|k_scatter' -s 7 -c 8 -o $O/prof_other $B > $O/ncu_other.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep|k_gradient|k_kint' -s 26 -c 3 -o $O/prof_c3 python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_c3.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep|k_gradient|k_kint' -s 26 -c 3 -o $O/prof_c3 python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-kernel-roofline > $O/ncu_c3.log 2>&1
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c5.csv python bench.py --config C5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-kernel-roofline > $O/ncu_launch_c5.log 2>&1
 fi
 if [[ $what == wave ]]; then
   timeout 600 python -m pytest tests -m gpu -q -x -rf -k "wavefront or reinit or c3_full or c5 or smoke or clean or sign" > gpurun_out/pytest_wave.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_wave.log
