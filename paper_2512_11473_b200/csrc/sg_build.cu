@@ -109,10 +109,28 @@ __global__ void __launch_bounds__(128, 4) k_tag_cull(GridC gc, Geom geom, int32_
     const double eps = 1e-9 * (gc.cell + fabs(gc.lower[0]) + fabs(gc.lower[1]) +
                                fabs(gc.lower[2]) + gc.upper[0] + gc.upper[1] + gc.upper[2]);
     bool skip_mine = false, neg_mine = false;
+    // primitives of a union that provably exceed the minimum at every cell
+    // of the block (1-Lipschitz, radius R from the centre) are not evaluated
+    // there: the minimum over the rest is the same value, bit for bit
+    uint32_t mask_mine = (geom.n >= 32 ? 0xFFFFFFFFu : (1u << geom.n) - 1u);
     if (cull) {
-        const double fc = sd_eval(geom, gc.lower[0] + (double)(32 * q + 16) * gc.cell,
-                                  gc.lower[1] + ((double)(y0 + lane) + 0.5) * gc.cell,
-                                  gc.lower[2] + (double)(z0 + 2) * gc.cell);
+        const double bx = gc.lower[0] + (double)(32 * q + 16) * gc.cell;
+        const double by = gc.lower[1] + ((double)(y0 + lane) + 0.5) * gc.cell;
+        const double bz = gc.lower[2] + (double)(z0 + 2) * gc.cell;
+        double fc;
+        if (geom.n > 1 && !geom.n_leak) {
+            double fi[SG_MAX_PRIMS];
+            fc = 0.0;
+            for (int i = 0; i < geom.n; ++i) {
+                fi[i] = sd_prim(geom.kind[i], geom.p[i], bx, by, bz);
+                fc = i == 0 ? fi[i] : fmin(fc, fi[i]);
+            }
+            mask_mine = 0u;
+            for (int i = 0; i < geom.n; ++i)
+                if (fi[i] - R <= fc + R + eps) mask_mine |= 1u << i;
+        } else {
+            fc = sd_eval(geom, bx, by, bz);
+        }
         skip_mine = fabs(fc) > gc.cell + R + eps;
         neg_mine = fc < 0.0;
     }
@@ -137,7 +155,8 @@ __global__ void __launch_bounds__(128, 4) k_tag_cull(GridC gc, Geom geom, int32_
             double z[4], f[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) z[k] = gc.lower[2] + ((double)(z0 + k) + 0.5) * gc.cell;
-            if (in) sd_eval_col<4>(geom, x, y, z, f);
+            const uint32_t mask = __shfl_sync(0xffffffffu, mask_mine, b);
+            if (in) sd_eval_col_mask<4>(geom, mask, x, y, z, f);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 cw[k] = __ballot_sync(0xffffffffu, in && fabs(f[k]) < gc.cell);
