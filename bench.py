@@ -13,6 +13,11 @@ prism) as the probe batch:
     sg_reinit (20 Godunov sweeps)
     sg_gradient (grad + normal + kernel integrals)
     sg_probe (phi and grad phi at every particle)
+The kernel integrals (sg_gradient(SG_KINT)) need only the final phi and
+nothing later in the step reads them, so they run on a second, low-priority
+stream forked after the reinit and joined before the step ends, overlapping
+the gradient and the probe on the step's high-priority stream
+(--serial-kint: all on one stream).
 value = active data points updated by the reinit + gradient sweeps per second
 of whole step (21 sweeps x 8.58 M active points), i.e. BASELINE's
 "active cells updated/s (reinit+gradient)"; probes/s and per-stage numbers are
@@ -64,6 +69,9 @@ def parse():
     p.add_argument("--no-kernel-roofline", action="store_true",
                    help="skip the per-kernel roofline timings after the timed steps "
                         "(e.g. under ncu, so the launch list is the steps only)")
+    p.add_argument("--serial-kint", action="store_true",
+                   help="kernel integrals inside the gradient stage on the main stream "
+                        "(default: on a second stream, overlapping gradient and probe)")
     p.add_argument("--slab", action="store_true",
                    help="z-slab path (NCCL) even at one rank (exercises the multi-GPU code)")
     return p.parse_args()
@@ -244,6 +252,12 @@ def kernel_rooflines(sg, w, stream, flush, d_pos, n_part, probe_ms, reinit_ms, h
                 "note": "direct-form FMAs (the kernel executes ~1.8x fewer); peak = SMs x "
                         "128 FP32 lanes x max SM clock"})
     if probe_ms:
+        # the probe alone (inside the step it overlaps the kernel integrals)
+        o_phi = torch.empty(n_part, dtype=d_pos.dtype, device=d_pos.device)
+        o_grad = torch.empty((n_part, 3), dtype=d_pos.dtype, device=d_pos.device)
+        probe_ms = timed(lambda: sg.sg_probe(g.handle, n_part, d_pos.data_ptr(), o_phi.data_ptr(),
+                                             o_grad.data_ptr(), None, stream))
+        del o_phi, o_grad
         # 12 B position in, 16 B (phi, grad) out, 4 B background entry per probe,
         # plus every touched package's (phi, grad) vectors and neighbour row once
         with torch.no_grad():
@@ -281,7 +295,9 @@ def run_ours(args, rank, world, local):
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
         return SL.bench_slab(args, w, rank, world, local)
-    stream = torch.cuda.current_stream()
+    # the step's stream: high priority (see the K7 side stream below)
+    stream = torch.cuda.Stream(device=dev, priority=-1)
+    torch.cuda.set_stream(stream)
 
     npdt = np.float32 if w.dtype == "f32" else np.float64
     if w.particles:
@@ -297,13 +313,29 @@ def run_ours(args, rank, world, local):
     flush = L2Flush(dev)
     fields = sg.SG_GRAD | sg.SG_NORMAL | sg.SG_KINT
 
+    # K7 (kernel integrals: FP32-issue bound) only needs the final phi, and
+    # nothing downstream in the step reads K / G: it runs on a second stream
+    # forked after the reinit and joined at the end of the step, concurrently
+    # with K6 (HBM-write bound) and the probe (latency bound) on the main one
+    # (the step runs on a high-priority stream, K7 on a low-priority one: the
+    # block scheduler serves K6 and the probe first and K7 fills the issue
+    # slots they leave while waiting on memory)
+    side = torch.cuda.Stream(device=dev, priority=0)
+    fork, join = torch.cuda.Event(), torch.cuda.Event()
+
     def step(ev, host=None):
         ev[0].record(stream)
         g = sg.Grid(w, stream=stream)
         ev[1].record(stream)
         g.reinit(REINIT_ITERS, w.cfl, stream=stream)
         ev[2].record(stream)
-        g.gradient(fields, w.h_ratio, stream=stream)
+        if args.serial_kint:
+            g.gradient(fields, w.h_ratio, stream=stream)
+        else:
+            fork.record(stream)
+            side.wait_event(fork)
+            g.gradient(sg.SG_KINT, w.h_ratio, stream=side)
+            g.gradient(sg.SG_GRAD | sg.SG_NORMAL, w.h_ratio, stream=stream)
         ev[3].record(stream)
         if n_part == 0:
             pass
@@ -314,6 +346,9 @@ def run_ours(args, rank, world, local):
             hp, hphi, hgrad = host
             sg.sg_probe(g.handle, n_part, hp.data_ptr(), hphi.data_ptr(), hgrad.data_ptr(),
                         d_oob.data_ptr(), stream)
+        if not args.serial_kint:
+            join.record(side)
+            stream.wait_event(join)
         ev[4].record(stream)
         info = g.info
         g.close_async(stream)
@@ -385,7 +420,12 @@ def run_ours(args, rank, world, local):
     stages["reinit"]["ms_per_sweep"] = reinit_ms
     stages["reinit"]["cells_per_s"] = n_act / (reinit_ms * 1e-3)
     stages["probe"]["probes_per_s"] = n_part / max(stages["probe"]["ms"] * 1e-3, 1e-12)
-    stages["gradient"]["note"] = "grad+normal (K6) and kernel integrals (K7)"
+    if args.serial_kint:
+        stages["gradient"]["note"] = "grad+normal (K6) and kernel integrals (K7)"
+    else:
+        stages["gradient"]["note"] = ("grad+normal (K6); the kernel integrals (K7) run on a "
+                                      "second stream from here to the end of the step")
+        stages["probe"]["note"] = "probe (if any), concurrent with K7, then the join of K7"
     stages["reinit_plus_gradient_cells_per_s"] = n_act * (REINIT_ITERS + 1) / (
         (st[:, 1].mean() + st[:, 2].mean()) * 1e-3)
     clocks = clk.summary()
