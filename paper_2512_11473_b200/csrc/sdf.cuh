@@ -228,4 +228,75 @@ __device__ __forceinline__ void sd_eval_col_mask(const Geom& g, uint32_t mask, d
     }
 }
 
+// The same per-point values along a y-column (x, z shared): the torus about
+// the y axis shares sqrt(ex^2 + ez^2) - R between the points, the box its x / z
+// terms, the sphere / shell ex^2 and ez^2; the association of every sum is
+// that of sd_prim, so each f[k] is bit-identical to sd_prim at (x, y[k], z).
+template <int NY>
+__device__ __forceinline__ void sd_prim_coly(int kind, const double* p, double x, double z,
+                                             const double (&y)[NY], double (&f)[NY]) {
+    switch (kind) {
+    case SG_SPHERE:
+    case SG_SHELL: {
+        const double ex = x - p[0], ez = z - p[2];
+        const double ex2 = ex * ex, ez2 = ez * ez;
+        const double rm = 0.5 * (p[3] + p[4]);
+        const double hw = 0.5 * (p[4] - p[3]);
+#pragma unroll
+        for (int k = 0; k < NY; ++k) {
+            const double ey = y[k] - p[1];
+            const double d = sqrt((ex2 + ey * ey) + ez2);
+            f[k] = kind == SG_SPHERE ? d - p[3] : fabs(d - rm) - hw;
+        }
+        return;
+    }
+    case SG_BOX: {
+        const double qx = fabs(x - p[0]) - p[3];
+        const double qz = fabs(z - p[2]) - p[5];
+        const double mx = fmax(qx, 0.0), mz = fmax(qz, 0.0);
+        const double mx2 = mx * mx, mz2 = mz * mz;
+#pragma unroll
+        for (int k = 0; k < NY; ++k) {
+            const double qy = fabs(y[k] - p[1]) - p[4];
+            const double my = fmax(qy, 0.0);
+            f[k] = sqrt((mx2 + my * my) + mz2) + fmin(fmax(qx, fmax(qy, qz)), 0.0);
+        }
+        return;
+    }
+    case SG_TORUS_Y: {
+        const double ex = x - p[0], ez = z - p[2];
+        const double t = sqrt(ex * ex + ez * ez) - p[3];
+        const double t2 = t * t;
+#pragma unroll
+        for (int k = 0; k < NY; ++k) {
+            const double ey = y[k] - p[1];
+            f[k] = sqrt(t2 + ey * ey) - p[4];
+        }
+        return;
+    }
+    default:
+#pragma unroll
+        for (int k = 0; k < NY; ++k) f[k] = sd_prim(kind, p, x, y[k], z);
+        return;
+    }
+}
+
+template <int NY>
+__device__ __forceinline__ void sd_eval_coly_mask(const Geom& g, uint32_t mask, double x, double z,
+                                                  const double (&y)[NY], double (&f)[NY]) {
+    bool first = true;
+    for (int i = 0; i < g.n; ++i) {
+        if (!((mask >> i) & 1u)) continue;
+        double fi[NY];
+        sd_prim_coly<NY>(g.kind[i], g.p[i], x, z, y, fi);
+#pragma unroll
+        for (int k = 0; k < NY; ++k) f[k] = first ? fi[k] : fmin(f[k], fi[k]);
+        first = false;
+    }
+    if (g.n_leak) {
+#pragma unroll
+        for (int k = 0; k < NY; ++k) f[k] = sd_leak(g, x, y[k], z, f[k]);
+    }
+}
+
 }  // namespace sg

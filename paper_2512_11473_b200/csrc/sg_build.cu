@@ -531,7 +531,10 @@ __global__ void __launch_bounds__(256) k_nb(GridC gc, const Geom* __restrict__ g
 // phi = init_scale * f(lower + (I + 0.5) dx) rounded to T (R-11, R-17);
 // singular packages -far / +far in both buffers.  A thread owns one (i, j)
 // column of a package (4 points sharing x and y).
-template <class T>
+// AX = 2: a thread owns the (i, j) column of 4 points along z (x, y shared);
+// AX = 1: the (i, k) column along y (x, z shared) -- chosen for geometries
+// whose expensive terms are shared along y (a torus about the y axis).
+template <class T, int AX>
 __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
                                                   const uint32_t* __restrict__ meta_cell,
                                                   int64_t n_pkg, T* __restrict__ phi0,
@@ -553,15 +556,18 @@ __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
     const uint32_t nx = (uint32_t)gc.n[0], ny = (uint32_t)gc.n[1];
     const uint32_t r = L / nx;
     const int cx = (int)(L - r * nx), cy = (int)(r % ny), cz = (int)(r / ny);
-    const int64_t ix = 4 * (int64_t)cx + (col & 3), iy = 4 * (int64_t)cy + (col >> 2);
+    // column coordinates: (a, b) = (x, y) along z, or (x, z) along y
+    const int64_t ix = 4 * (int64_t)cx + (col & 3);
+    const int64_t ib = 4 * (int64_t)(AX == 2 ? cy : cz) + (col >> 2);
     const double x = gc.lower[0] + ((double)ix + 0.5) * gc.dx;
-    const double y = gc.lower[1] + ((double)iy + 0.5) * gc.dx;
-    double z[4], f[4];
+    const double bb = gc.lower[AX == 2 ? 1 : 2] + ((double)ib + 0.5) * gc.dx;
+    const int cc = AX == 2 ? cz : cy;
+    double w[4], f[4];  // the column's varying coordinate
 #pragma unroll
-    for (int k = 0; k < 4; ++k) z[k] = gc.lower[2] + ((double)(4 * (int64_t)cz + k) + 0.5) * gc.dx;
-    if (geom.n == 1) {
-        sd_eval_col<4>(geom, x, y, z, f);
-    } else {
+    for (int k = 0; k < 4; ++k)
+        w[k] = gc.lower[AX] + ((double)(4 * (int64_t)cc + k) + 0.5) * gc.dx;
+    uint32_t mask = (geom.n >= 32 ? 0xFFFFFFFFu : (1u << geom.n) - 1u);
+    if (geom.n > 1) {
         // unions: primitives that provably exceed the minimum at every data
         // point of the package are dropped (1-Lipschitz bound from the
         // package centre c, data points within R = sqrt(3) 1.5 dx of c)
@@ -584,13 +590,21 @@ __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
             fc[i] = __shfl_sync(hm, fmine, (lane & 16) + i);
             m = i == 0 ? fc[i] : fmin(m, fc[i]);
         }
-        uint32_t mask = 0;
+        mask = 0;
         for (int i = 0; i < geom.n; ++i)
             if (fc[i] - R <= m + R + eps) mask |= 1u << i;
-        sd_eval_col_mask<4>(geom, mask, x, y, z, f);
     }
+    if constexpr (AX == 2) {
+        if (geom.n == 1) sd_eval_col<4>(geom, x, bb, w, f);
+        else sd_eval_col_mask<4>(geom, mask, x, bb, w, f);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) phi0[id * 64 + col + 16 * k] = (T)(gc.init_scale * f[k]);
+        for (int k = 0; k < 4; ++k) phi0[id * 64 + col + 16 * k] = (T)(gc.init_scale * f[k]);
+    } else {
+        sd_eval_coly_mask<4>(geom, mask, x, bb, w, f);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            phi0[id * 64 + (col & 3) + 4 * j + 16 * (col >> 2)] = (T)(gc.init_scale * f[j]);
+    }
 }
 
 // per-plane active counts for slab balancing (planes [zc_lo, zc_lo + nplanes))
@@ -965,12 +979,23 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         if (mesh) {
             launch_phi_init_mesh(gc, g->geom, g->meta_cell, n_pkg, g->dtype, g->phi[0], g->phi[1], s);
         } else {
-            if (g->dtype == SG_F64)
-                k_phi_init<double><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
-                                                      (double*)g->phi[0], (double*)g->phi[1]);
-            else
-                k_phi_init<float><<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg,
-                                                     (float*)g->phi[0], (float*)g->phi[1]);
+            // y-columns when the geometry has a torus about the y axis and
+            // nothing whose shared terms need z-columns
+            bool ycol = false, zcol = false;
+            for (int i = 0; i < g->geom.n; ++i) {
+                ycol = ycol || g->geom.kind[i] == SG_TORUS_Y;
+                zcol = zcol || g->geom.kind[i] == SG_TORUS_Z || g->geom.kind[i] == SG_TRIPRISM_Z;
+            }
+            const bool ax1 = ycol && !zcol && std::getenv("SG_PHI_ZCOL_ONLY") == nullptr;
+            if (g->dtype == SG_F64) {
+                auto kern = ax1 ? k_phi_init<double, 1> : k_phi_init<double, 2>;
+                kern<<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg, (double*)g->phi[0],
+                                        (double*)g->phi[1]);
+            } else {
+                auto kern = ax1 ? k_phi_init<float, 1> : k_phi_init<float, 2>;
+                kern<<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg, (float*)g->phi[0],
+                                        (float*)g->phi[1]);
+            }
             SG_LAUNCHED();
         }
         SG_CUDA(cudaStreamWaitEvent(s, ev_join, 0));

@@ -171,6 +171,26 @@ def test_phi_init(sgm, O, name, scale):
     assert np.array_equal(got, exp.astype(np_dtype(w)))
 
 
+TORUS_Y_BOX = W.Workload("TYB24", (24, 24, 24), 1.0 / 24, dtype="f32",
+                         prims=(W.Prim(W.TORUS_Y, (0.5, 0.5, 0.5, 0.3, 0.08)),
+                                W.Prim(W.BOX, (0.5, 0.5, 0.5, 0.1, 0.1, 0.4))))
+
+
+@pytest.mark.parametrize("seed,n,dtype", [(s, n, d) for s, n in [(0, 13), (1, 16), (2, 20), (3, 24),
+                                                                  (6, 17), (9, 21), (12, 19)]
+                                          for d in ("f64", "f32")] + [(-1, 24, "f32")])
+def test_phi_init_random_scenes(sgm, O, seed, n, dtype):
+    """Initial phi bit-exact on unions of every primitive kind (the y-column
+    evaluation for tori about y, the z-column one otherwise, the per-package
+    primitive mask)."""
+    w = TORUS_Y_BOX if seed < 0 else W.random_scene(seed, n, dtype=dtype)
+    o = O.Oracle(w)
+    o.build_tables()
+    exp = o.to_packages(o.phi_dense(), -o.far, o.far)
+    g = sgm.Grid(w)
+    assert np.array_equal(g.view("phi").cpu().numpy(), exp.astype(np_dtype(w)))
+
+
 def _upload(g, w, pk):
     g.view("phi").copy_(torch.from_numpy(pk.astype(np_dtype(w))))
 
