@@ -1,6 +1,8 @@
 #!/bin/bash
 # One GPU session: build, smoke, GPU tests, bench, ncu launch list + full captures.
-# Usage (from the repo root, under gpurun): bash scripts/gpu_check.sh [tests|bench|ncu|all]
+# Usage (from the repo root, under gpurun): bash scripts/gpu_check.sh MODE
+# MODE: all | tests | bench | c3 | ncu | quick | prof | diag3 | sign | signprof | clean |
+#       probe | kint | mesh | e2e | init | final (TAG=rNN: full capture into gpurun_out/$TAG)
 set -u
 mkdir -p gpurun_out
 what=${1:-all}
@@ -70,81 +72,6 @@ if [[ $what == mesh ]]; then
   timeout 600 python scripts/mesh_bench.py chain 4 5 6 >> gpurun_out/mesh_bench.json 2>> gpurun_out/mesh_bench.err
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_mesh.csv python scripts/mesh_bench.py 5 > /dev/null 2>&1
 fi
-if [[ $what == reinit4 ]]; then
-  timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or c3 or c5 or smoke or clean or sign" > gpurun_out/pytest_r4.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_r4.log
-  timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench.json 2> gpurun_out/bench.err
-  SG_REINIT8=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench8.json 2> /dev/null
-  timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> /dev/null
-  SG_REINIT8=1 timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3_8.json 2> /dev/null
-fi
-if [[ $what == probe2 ]]; then
-  timeout 600 python -m pytest tests -m gpu -q -x -k "probe or smoke or slab or relax" > gpurun_out/pytest_p2.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_p2.log
-  for v in 0 1; do
-    SG_PROBE_V1=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_v$v.json 2> /dev/null
-    SG_PROBE_V1=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e --order shuffled > gpurun_out/bench_s$v.json 2> /dev/null
-  done
-fi
-if [[ $what == fuse ]]; then
-  timeout 600 python -m pytest tests -m gpu -q -x -k "gradient or kernel or fused or probe or relax or clean or smoke" > gpurun_out/pytest_fuse.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_fuse.log
-  for v in 1 0; do
-    SG_FUSE_GRAD=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_fuse$v.json 2> /dev/null
-    SG_FUSE_GRAD=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_fuse$v.json 2> /dev/null
-  done
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python bench.py --config C3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_c3.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_kint" -s 1 -c 1 -o gpurun_out/prof_kint python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_kint.log 2>&1
-fi
-if [[ $what == kint2 ]]; then
-  timeout 600 python -m pytest tests -m gpu -q -x -k "gradient or kernel or relax or clean or smoke" > gpurun_out/pytest_kint2.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_kint2.log
-  for v in 1 0; do
-    SG_KINT_ROWSKIP=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_rs$v.json 2> /dev/null
-    SG_KINT_ROWSKIP=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_rs$v.json 2> /dev/null
-  done
-  # warm-L2 sweeps inside the step: no cache flush/invalidate by ncu
-  timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct,l1tex__t_bytes.sum,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active -k regex:"k_sweep|k_probe|k_kint|k_gradient" --csv --log-file gpurun_out/warm_c2.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
-fi
-if [[ $what == face ]]; then
-  timeout 1500 python -m pytest tests -m gpu -q -x -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-  timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
-  timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
-  timeout 600 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
-  timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct,l1tex__t_bytes.sum,smsp__issue_active.avg.pct_of_peak_sustained_active -k regex:"k_sweep|k_probe|k_gradient" --csv --log-file gpurun_out/warm_c2b.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
-fi
-if [[ $what == sched ]]; then
-  timeout 900 python -m pytest tests -m gpu -q -x -rf -k "tables or reinit or slab or sign or smoke or refine or c3 or c5 or clean or empty" > gpurun_out/pytest_sched.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_sched.log
-  for v in 1 0; do
-    SG_SCHED=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_sc$v.json 2> gpurun_out/bench_sc$v.err
-    SG_SCHED=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_sc$v.json 2> /dev/null
-  done
-  timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct,l1tex__t_bytes.sum,smsp__issue_active.avg.pct_of_peak_sustained_active -k regex:"k_sweep" -c 30 --csv --log-file gpurun_out/warm_c2c.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_sched.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-fi
-if [[ $what == xsh ]]; then
-  timeout 900 python -m pytest tests -m gpu -q -x -rf -k "reinit or slab or sign or smoke or refine or c3 or c5 or clean or empty or table1" > gpurun_out/pytest_xsh.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_xsh.log
-  timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_xsh.json 2> gpurun_out/bench_xsh.err
-  timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_xsh.json 2> /dev/null
-  timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct,l1tex__t_bytes.sum,smsp__issue_active.avg.pct_of_peak_sustained_active -k regex:"k_sweep" -c 30 --csv --log-file gpurun_out/warm_c2d.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
-fi
-if [[ $what == l2p ]]; then
-  python -c "
-from cuda.bindings import runtime as rt
-for a in ['cudaDevAttrMaxPersistingL2CacheSize','cudaDevAttrMaxAccessPolicyWindowSize','cudaDevAttrL2CacheSize']:
-    print(a, rt.cudaDeviceGetAttribute(getattr(rt.cudaDeviceAttr, a), 0))
-" > gpurun_out/l2attr.txt 2>&1
-  timeout 900 python -m pytest tests -m gpu -q -x -rf -k "reinit or slab or smoke or c3 or clean" > gpurun_out/pytest_l2p.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_l2p.log
-  for v in 1 0; do
-    SG_L2PERSIST=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_l2p$v.json 2> /dev/null
-    SG_L2PERSIST=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_l2p$v.json 2> /dev/null
-  done
-  timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct -k regex:"k_sweep|k_probe|k_kint|k_gradient" -c 45 --csv --log-file gpurun_out/warm_c2e.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_warm.log 2>&1
-fi
-if [[ $what == blk ]]; then
-  SG_SWEEP_BLOCKED=1 timeout 900 python -m pytest tests -m gpu -q -x -rf -k "reinit or slab or smoke or c3 or clean or sign" > gpurun_out/pytest_blk.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_blk.log
-  for v in 1 0; do
-    SG_SWEEP_BLOCKED=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_blk$v.json 2> /dev/null
-    SG_SWEEP_BLOCKED=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_blk$v.json 2> /dev/null
-    SG_SWEEP_BLOCKED=$v timeout 900 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,lts__t_sector_hit_rate.pct -k regex:"k_sweep" -c 20 --csv --log-file gpurun_out/warm_blk$v.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-  done
-fi
 if [[ $what == e2e ]]; then
   timeout 900 python -m pytest tests -m gpu -q -x -rf -k "probe or smoke or relax" > gpurun_out/pytest_e2e.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_e2e.log
   timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_e2e.json 2> gpurun_out/bench_e2e.err
@@ -161,13 +88,6 @@ for mb in (64, 256):
         print(direction, mb, "MB", round(n * 4 / dt / 1e9, 1), "GB/s")
 PY
 fi
-if [[ $what == bps ]]; then
-  timeout 900 python -m pytest tests -m gpu -q -x -rf -k "kernel or gradient or clean or relax" > gpurun_out/pytest_bps.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_bps.log
-  for v in 0 4 6 8 11; do
-    SG_KINT_BPS=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_bps$v.json 2> /dev/null
-    SG_KINT_BPS=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_bps$v.json 2> /dev/null
-  done
-fi
 if [[ $what == final ]]; then
   O=gpurun_out/${TAG:-r01h}; mkdir -p $O
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
@@ -182,27 +102,10 @@ if [[ $what == final ]]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep|k_gradient|k_kint' -s 26 -c 3 -o $O/prof_c3 python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-kernel-roofline > $O/ncu_c3.log 2>&1
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c5.csv python bench.py --config C5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-kernel-roofline > $O/ncu_launch_c5.log 2>&1
 fi
-if [[ $what == wave ]]; then
-  timeout 600 python -m pytest tests -m gpu -q -x -rf -k "wavefront or reinit or c3_full or c5 or smoke or clean or sign" > gpurun_out/pytest_wave.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_wave.log
-  for v in 1 0; do
-    SG_WAVE=$v timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_wave$v.json 2> gpurun_out/bench_wave$v.err
-    SG_WAVE=$v timeout 300 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_wave$v.json 2> /dev/null
-    SG_WAVE=$v timeout 300 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c5_wave$v.json 2> /dev/null
-  done
-  timeout 600 ncu --cache-control none --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum -k regex:"k_wave" -c 2 --csv --log-file gpurun_out/warm_wave.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-fi
 if [[ $what == init ]]; then
   timeout 900 python -m pytest tests -m gpu -q -x -rf -k "tables or phi_init or c3 or c5 or smoke or sign or refine or mesh or forced" > gpurun_out/pytest_init.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_init.log
   timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-kernel-roofline > gpurun_out/bench_init.json 2> /dev/null
   timeout 300 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-kernel-roofline > gpurun_out/bench_c3_init.json 2> /dev/null
   timeout 300 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu-baseline --no-kernel-roofline > gpurun_out/bench_c5_init.json 2> /dev/null
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3_init.csv python bench.py --config C3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-kernel-roofline > /dev/null 2>&1
-fi
-if [[ $what == pdl ]]; then
-  timeout 600 python -m pytest tests -m gpu -q -x -k "reinit or slab or smoke or clean" > gpurun_out/pytest_pdl.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pdl.log
-  for v in 1 0; do
-    SG_PDL=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_pdl$v.json 2> /dev/null
-    SG_PDL=$v timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_pdl$v.json 2> /dev/null
-  done
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_probe|k_kint|k_gradient" -s 3 -c 3 -o gpurun_out/prof_pkg python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_pkg.log 2>&1
 fi
