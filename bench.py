@@ -13,11 +13,11 @@ prism) as the probe batch:
     sg_reinit (20 Godunov sweeps)
     sg_gradient (grad + normal + kernel integrals)
     sg_probe (phi and grad phi at every particle)
-The kernel integrals (sg_gradient(SG_KINT)) need only the final phi and
-nothing later in the step reads them, so they run on a second, low-priority
-stream forked after the reinit and joined before the step ends, overlapping
-the gradient and the probe on the step's high-priority stream
-(--serial-kint: all on one stream).
+sg_gradient(SG_GRAD | SG_NORMAL | SG_KINT) runs the gradient / normal (K6)
+and kernel-integral (K7) work in one kernel, K6 warps beside K7 warps.
+(--kint-stream: K7 as a separate call on a second, low-priority stream
+overlapping K6 and the probe on the step's high-priority stream -- the same
+step time on C2.)
 value = active data points updated by the reinit + gradient sweeps per second
 of whole step (21 sweeps x 8.58 M active points), i.e. BASELINE's
 "active cells updated/s (reinit+gradient)"; probes/s and per-stage numbers are
@@ -69,9 +69,10 @@ def parse():
     p.add_argument("--no-kernel-roofline", action="store_true",
                    help="skip the per-kernel roofline timings after the timed steps "
                         "(e.g. under ncu, so the launch list is the steps only)")
-    p.add_argument("--serial-kint", action="store_true",
-                   help="kernel integrals inside the gradient stage on the main stream "
-                        "(default: on a second stream, overlapping gradient and probe)")
+    p.add_argument("--kint-stream", action="store_true",
+                   help="kernel integrals as a separate call on a second, low-priority "
+                        "stream overlapping gradient and probe (default: one sg_gradient "
+                        "call, K6 and K7 in one kernel)")
     p.add_argument("--slab", action="store_true",
                    help="z-slab path (NCCL) even at one rank (exercises the multi-GPU code)")
     return p.parse_args()
@@ -230,6 +231,8 @@ def kernel_rooflines(sg, w, stream, flush, d_pos, n_part, probe_ms, reinit_ms, h
 
     t_grad = timed(lambda: g.gradient(sg.SG_GRAD | sg.SG_NORMAL, w.h_ratio, stream=stream))
     t_kint = timed(lambda: g.gradient(sg.SG_KINT, w.h_ratio, stream=stream))
+    t_both = timed(lambda: g.gradient(sg.SG_GRAD | sg.SG_NORMAL | sg.SG_KINT, w.h_ratio,
+                                      stream=stream))
     clock_ghz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"]) \
         / 1e3 if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1.965
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
@@ -251,6 +254,9 @@ def kernel_rooflines(sg, w, stream, flush, d_pos, n_part, probe_ms, reinit_ms, h
                 "peak": fma_peak / 1e12, "frac": fmas / (t_kint * 1e-3) / fma_peak,
                 "note": "direct-form FMAs (the kernel executes ~1.8x fewer); peak = SMs x "
                         "128 FP32 lanes x max SM clock"})
+    out.append({"kernel": "k_kint<..., K6 fused> (gradient + normal + kernel integrals)",
+                "bound": "alu", "us": t_both * 1e3,
+                "note": "one kernel: K6 warps beside K7 warps; compare with the two above"})
     if probe_ms:
         # the probe alone (inside the step it overlaps the kernel integrals)
         o_phi = torch.empty(n_part, dtype=d_pos.dtype, device=d_pos.device)
@@ -313,13 +319,10 @@ def run_ours(args, rank, world, local):
     flush = L2Flush(dev)
     fields = sg.SG_GRAD | sg.SG_NORMAL | sg.SG_KINT
 
-    # K7 (kernel integrals: FP32-issue bound) only needs the final phi, and
-    # nothing downstream in the step reads K / G: it runs on a second stream
-    # forked after the reinit and joined at the end of the step, concurrently
-    # with K6 (HBM-write bound) and the probe (latency bound) on the main one
-    # (the step runs on a high-priority stream, K7 on a low-priority one: the
-    # block scheduler serves K6 and the probe first and K7 fills the issue
-    # slots they leave while waiting on memory)
+    # --kint-stream: K7 (kernel integrals) only needs the final phi and nothing
+    # downstream in the step reads K / G, so it can run on a second,
+    # low-priority stream forked after the reinit and joined at the end of the
+    # step while K6 and the probe run on the high-priority step stream
     side = torch.cuda.Stream(device=dev, priority=0)
     fork, join = torch.cuda.Event(), torch.cuda.Event()
 
@@ -329,7 +332,7 @@ def run_ours(args, rank, world, local):
         ev[1].record(stream)
         g.reinit(REINIT_ITERS, w.cfl, stream=stream)
         ev[2].record(stream)
-        if args.serial_kint:
+        if not args.kint_stream:
             g.gradient(fields, w.h_ratio, stream=stream)
         else:
             fork.record(stream)
@@ -346,7 +349,7 @@ def run_ours(args, rank, world, local):
             hp, hphi, hgrad = host
             sg.sg_probe(g.handle, n_part, hp.data_ptr(), hphi.data_ptr(), hgrad.data_ptr(),
                         d_oob.data_ptr(), stream)
-        if not args.serial_kint:
+        if args.kint_stream:
             join.record(side)
             stream.wait_event(join)
         ev[4].record(stream)
@@ -420,8 +423,9 @@ def run_ours(args, rank, world, local):
     stages["reinit"]["ms_per_sweep"] = reinit_ms
     stages["reinit"]["cells_per_s"] = n_act / (reinit_ms * 1e-3)
     stages["probe"]["probes_per_s"] = n_part / max(stages["probe"]["ms"] * 1e-3, 1e-12)
-    if args.serial_kint:
-        stages["gradient"]["note"] = "grad+normal (K6) and kernel integrals (K7)"
+    if not args.kint_stream:
+        stages["gradient"]["note"] = ("grad+normal (K6) and kernel integrals (K7): one "
+                                      "sg_gradient call, one kernel (K6 warps beside K7 warps)")
     else:
         stages["gradient"]["note"] = ("grad+normal (K6); the kernel integrals (K7) run on a "
                                       "second stream from here to the end of the step")

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -347,13 +348,28 @@ __device__ __forceinline__ float inv_norm(float m2) { return m2 > 0.f ? rsqrtf(m
 __device__ __forceinline__ double inv_norm(double m2) { return m2 > 0.0 ? 1.0 / sqrt(m2) : 0.0; }
 
 template <class T>
+__device__ __forceinline__ void grad_package(const T* __restrict__ in, T* __restrict__ grad,
+                                             T* __restrict__ normal,
+                                             const uint32_t* __restrict__ face, int64_t pkg,
+                                             bool valid, const StC<T>& c);
+
+template <class T>
 __global__ void __launch_bounds__(256) k_gradient(const T* __restrict__ in, T* __restrict__ grad,
                                                   T* __restrict__ normal,
                                                   const uint32_t* __restrict__ face, int64_t lo,
                                                   int64_t hi, StC<T> c) {
     const int64_t pkg = lo + (((int64_t)blockIdx.x * 256 + threadIdx.x) >> 4);
+    grad_package(in, grad, normal, face, pkg, pkg < hi, c);
+}
+
+// K6 for one x-row (lane r = threadIdx.x & 15 of a 16-lane group) of `pkg`
+template <class T>
+__device__ __forceinline__ void grad_package(const T* __restrict__ in, T* __restrict__ grad,
+                                             T* __restrict__ normal,
+                                             const uint32_t* __restrict__ face, int64_t pkg,
+                                             bool valid, const StC<T>& c) {
     Cross<T> x;
-    if (!load_cross(in, face, pkg, pkg < hi, x)) return;
+    if (!load_cross(in, face, pkg, valid, x)) return;
     T gx[4], gy[4], gz[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -480,11 +496,25 @@ struct KGeo {
 // when the taps at |o|^2 = 8 lie outside the support (h_ratio <= sqrt 2, e.g.
 // the default 1.3: 81 taps), which drops their zero-weight FMAs and the whole
 // (|oy|, |oz|) = (2, 2) row group (same bits: fma(0, h, acc) = acc)
-template <class T, int R, int S2M>
-__global__ void __launch_bounds__(128) k_kint(const T* __restrict__ in,
+// GR: K6 fused in horizontally -- warps 4..7 of a 256-thread block compute the
+// gradient / normal of the block's 8 packages (16 lanes per package, as in
+// k_gradient) while warps 0..3 compute their kernel integrals: the
+// HBM-write-bound K6 warps and the issue-bound K7 warps share every SM.
+template <class T, int R, int S2M, bool GR = false>
+__global__ void __launch_bounds__(GR ? 256 : 128) k_kint(const T* __restrict__ in,
                                               const uint32_t* __restrict__ nb, int64_t lo,
                                               int64_t hi, KintC<T> c, T* __restrict__ K,
-                                              T* __restrict__ G) {
+                                              T* __restrict__ G, T* __restrict__ grad = nullptr,
+                                              T* __restrict__ normal = nullptr,
+                                              const uint32_t* __restrict__ face = nullptr,
+                                              StC<T> cs = StC<T>{}) {
+    if constexpr (GR) {
+        if (threadIdx.x >= 128) {
+            const int64_t pkg = lo + (int64_t)blockIdx.x * 8 + ((threadIdx.x - 128) >> 4);
+            grad_package(in, grad, normal, face, pkg, pkg < hi, cs);
+            return;
+        }
+    }
     using Geo = KGeo<R>;
     constexpr int RS = Geo::RS, RSX = Geo::RSX, SLICE = Geo::SLICE, VOL = Geo::VOL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -828,28 +858,24 @@ static KintC<T> make_kint(double h_ratio, double dx, int R, double* S_out) {
     return c;
 }
 
+// gp / np non-null: K6 fused in (k_kint<..., true>)
 template <class T, int R>
-static void launch_kint_r(sg_grid* g, const T* phi, const KintC<T>& c, cudaStream_t s) {
+static void launch_kint_r(sg_grid* g, const T* phi, const KintC<T>& c, cudaStream_t s,
+                          T* gp = nullptr, T* np = nullptr, StC<T> cs = StC<T>{}) {
     const int64_t lo = g->own_lo, hi = g->own_hi;
     if (hi <= lo) return;
     const size_t smem = sizeof(T) * 8 * KGeo<R>::VOL;
-    auto kern = k_kint<T, R, KGeo<R>::S2MAX>;
+    const bool gr = gp || np;
+    auto kern = gr ? k_kint<T, R, KGeo<R>::S2MAX, true> : k_kint<T, R, KGeo<R>::S2MAX, false>;
     if constexpr (R == 2) {
-        if (c.wt[7] == T(0) && c.wt[8] == T(0)) kern = k_kint<T, 2, 6>;  // |o|^2 = 8 outside
+        if (c.wt[7] == T(0) && c.wt[8] == T(0))  // |o|^2 = 8 outside the support
+            kern = gr ? k_kint<T, 2, 6, true> : k_kint<T, 2, 6, false>;
     }
     if (smem > 48 * 1024)
         SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)ceil_div(hi - lo, 8), 128, smem, s>>>(phi, g->nb, lo, hi, c, (T*)g->kint,
-                                                          (T*)g->gkint);
+    kern<<<(unsigned)ceil_div(hi - lo, 8), gr ? 256 : 128, smem, s>>>(
+        phi, g->nb, lo, hi, c, (T*)g->kint, (T*)g->gkint, gp, np, g->face, cs);
     SG_LAUNCHED();
-}
-
-// library-internal side stream and fork/join events (one per host thread)
-static cudaStream_t grad_side_stream() {
-    static cudaStream_t st = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] { SG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); });
-    return st;
 }
 
 template <class T>
@@ -863,38 +889,37 @@ static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t
     if ((fields & SG_NORMAL) && !g->normal) g->normal = g->alloc(vec_bytes, s);
     if (want_k && !g->kint) g->kint = g->alloc((size_t)g->n_pkg * 64 * sizeof(T), s);
     if (want_k && !g->gkint) g->gkint = g->alloc(vec_bytes, s);
-    // K6 (HBM-write bound) and K7 (FP32 / shared-memory bound) only read phi:
-    // the kernel integrals run on a side stream concurrently with the gradient
-    cudaStream_t sk = s;
-    static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    if (want_g && want_k) {
-        if (!ev_fork) {
-            SG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-            SG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-        }
-        sk = grad_side_stream();
-        SG_CUDA(cudaEventRecord(ev_fork, s));
-        SG_CUDA(cudaStreamWaitEvent(sk, ev_fork, 0));
-    }
+    T* gp = (fields & SG_GRAD) ? (T*)g->grad : nullptr;
+    T* np = (fields & SG_NORMAL) ? (T*)g->normal : nullptr;
+    // K6 (HBM-write bound) and K7 (issue bound) both requested: one kernel,
+    // K6 warps beside K7 warps in every block (k_kint<..., true>), so the two
+    // share the SMs instead of queueing one behind the other
+    // (SG_FUSE_K6K7=0: separate kernels, A/B)
+    static const bool fuse_env = [] {
+        const char* e = std::getenv("SG_FUSE_K6K7");
+        return !(e && e[0] == '0');
+    }();
+    const bool fuse = want_g && want_k && fuse_env;
     if (want_k) {
         // largest |o_k| of a tap: o_k < 2 h_ratio  ->  R = ceil(2 h_ratio) - 1
         const int R = (int)std::ceil(2.0 * h_ratio) - 1;
         double S = 0.0;
         const KintC<T> kc = make_kint<T>(h_ratio, g->gc.dx, R, &S);
+        T* fg = fuse ? gp : nullptr;
+        T* fn = fuse ? np : nullptr;
         switch (R) {
-        case 0: launch_kint_r<T, 0>(g, phi, kc, sk); break;
-        case 1: launch_kint_r<T, 1>(g, phi, kc, sk); break;
-        case 2: launch_kint_r<T, 2>(g, phi, kc, sk); break;
-        default: launch_kint_r<T, 3>(g, phi, kc, sk); break;
+        case 0: launch_kint_r<T, 0>(g, phi, kc, s, fg, fn, c); break;
+        case 1: launch_kint_r<T, 1>(g, phi, kc, s, fg, fn, c); break;
+        case 2: launch_kint_r<T, 2>(g, phi, kc, s, fg, fn, c); break;
+        default: launch_kint_r<T, 3>(g, phi, kc, s, fg, fn, c); break;
         }
-        k_singular<T><<<1, 128, 0, sk>>>((T*)g->kint, (T*)g->gkint, nullptr, nullptr, kc.S, T(0));
+        // singular packages (R-16) of every field written here
+        k_singular<T><<<1, 128, 0, s>>>((T*)g->kint, (T*)g->gkint, fg, fn, kc.S, (T)g->gc.far);
         SG_LAUNCHED();
         g->has_kint = true;
         g->kernel_sum = S;
     }
-    if (want_g) {
-        T* gp = (fields & SG_GRAD) ? (T*)g->grad : nullptr;
-        T* np = (fields & SG_NORMAL) ? (T*)g->normal : nullptr;
+    if (want_g && !fuse) {
         if (hi > lo) {
             // (a persistent 8-lane variant like the reinit sweep measured
             // slower here: the kernel is bound by its 1.8 KB/package of writes)
@@ -904,13 +929,9 @@ static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t
         }
         k_singular<T><<<1, 128, 0, s>>>(nullptr, nullptr, gp, np, T(0), (T)g->gc.far);
         SG_LAUNCHED();
-        if (gp) g->has_grad = true;
-        if (np) g->has_normal = true;
     }
-    if (sk != s) {
-        SG_CUDA(cudaEventRecord(ev_join, sk));
-        SG_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
-    }
+    if (gp) g->has_grad = true;
+    if (np) g->has_normal = true;
 }
 
 void launch_gradient(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t s) {
