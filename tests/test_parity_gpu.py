@@ -290,6 +290,21 @@ def test_kernel_integral_h_ratios(sgm, O, h_ratio):
     assert np.max(np.abs(gG - eG) / (np.maximum(1.0, h * np.abs(eG)) / h)) <= 1e-12
 
 
+@pytest.mark.parametrize("name,h_ratio", [("C1", 1.3), ("C1", 0.5), ("C2", 1.3), ("C2", 1.6),
+                                          ("C2", 0.9)])
+def test_fused_gradient_kernel_equals_separate(sgm, name, h_ratio):
+    """SG_GRAD|SG_NORMAL|SG_KINT in one call runs K6 warps beside K7 warps in
+    one kernel; it must give the bits of the separate K6 and K7 calls."""
+    w = W.config(name)
+    a = sgm.Grid(w).reinit(3)
+    b = sgm.Grid(w).reinit(3)
+    a.gradient(sgm.SG_GRAD | sgm.SG_NORMAL | sgm.SG_KINT, h_ratio=h_ratio)
+    b.gradient(sgm.SG_GRAD | sgm.SG_NORMAL, h_ratio=h_ratio)
+    b.gradient(sgm.SG_KINT, h_ratio=h_ratio)
+    for f in ("grad", "normal", "kint", "gkint"):
+        assert torch.equal(a.view(f), b.view(f)), f
+
+
 # ------------------------------------------------------------------- probe --
 
 def _probe_compare(sgm, O, w, pos_np, phi_iters=3):
