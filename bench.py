@@ -487,11 +487,21 @@ def oracle_sample(w, budget_s: float = 12.0):
             break
     o.gradient(phi)
     dt = time.perf_counter() - t0
-    return {"value": n_act * (sweeps + 1) / dt, "unit": UNIT, "cores": O.get_threads(),
+    cores = O.get_threads()
+    # the same oracle on one thread ("also run with 1 thread"),
+    # one reinit sweep
+    O.set_threads(1)
+    t1 = time.perf_counter()
+    o.reinit_step(phi, w.cfl)
+    dt1 = time.perf_counter() - t1
+    O.set_threads(threads)
+    return {"value": n_act * (sweeps + 1) / dt, "unit": UNIT, "cores": cores,
             "kind": "oracle",
             "sample": f"{sweeps} reinit sweeps + 1 gradient/normal sweep of the dense fp64 oracle "
                       f"on {w.name} ({n_act} active points each); tables and initial phi built "
-                      f"beforehand (untimed); {dt:.1f} s"}
+                      f"beforehand (untimed); {dt:.1f} s",
+            "single_thread": {"value": n_act / dt1, "unit": UNIT, "cores": 1,
+                              "sample": f"1 reinit sweep on one thread, {dt1:.1f} s"}}
 
 
 def cpu_baseline(w, n_act):
