@@ -411,6 +411,16 @@ sg_status sg_balanced_cuts(const int64_t* counts, int32_t nz, int32_t nranks, in
 sg_status sg_plane_counts(const sg_desc* desc, const sg_geometry* geom, int32_t z_lo,
                           int32_t z_hi, int64_t* counts, void* stream);
 
+/* NeighbourIndexShift of Lst. 2 for PKG_SIZE = 4, host-callable
+ * (no device use; the kernels inline the same function): for a
+ * package-relative data shift per axis, shift[k] in [-4, 7] (SPEC S:167-171,
+ * "nearest-neighbour access"), writes offset[k] = (shift[k] + 4) / 4 in
+ * {0, 1, 2} and data[k] = shift[k] + 4 - 4 offset[k] in [0, 4) (either output
+ * may be NULL) and returns the neighbour-table slot ox + 3 oy + 9 oz (R-8);
+ * returns -1 (outputs unspecified) if shift is NULL or a component is out
+ * of range. */
+int32_t sg_neighbour_index_shift(const int32_t* shift, int32_t* offset, int32_t* data);
+
 const char* sg_last_error(void);
 int32_t sg_abi_version(void);
 /* Number of device kernels this library has launched in this process. */

@@ -29,11 +29,20 @@
  *   or_neighbours     pinned: definition by brute force, invariants
  *   or_phi_dense      pinned: closed-form SDF values
  *   or_reinit_dense   pinned: planar closed form, 2*SDF convergence, no sign
- *                     flip; drift near kinks/medial axes: parity unpinned
+ *                     flip, one-step Godunov closed forms at ridges/valleys
+ *                     of both signs along each axis (upwind selection), phi=0
+ *                     stationary; multi-step drift near kinks/medial axes of
+ *                     real geometries: parity unpinned
  *   or_gradient_dense pinned: affine exactness, sphere radial; band-edge values
  *                     that use the far constant: parity unpinned
- *   or_kernel_dense   pinned: S closed forms, S/2 at planar interface, sum gw=0
+ *   or_kernel_dense   pinned: S closed forms, S/2 at planar interface, sum gw=0,
+ *                     first moment sum gw_x o_x dx -> int W = 1 (G scale),
+ *                     scaling identity r W' = -h dW/dh - 3W from the weights,
+ *                     Heaviside C^1 conditions H'(0)=1/eps, H'(+-eps)=0
  *   or_probe          pinned: affine reproduction, data-point identity, far/OOB
+ *   or_relax          pinned: lone particle at rest, pair symmetry, pair-force
+ *                     magnitude through the normalisation int 4 pi r^2 W = 1,
+ *                     bounding onto phi = -off on a plane
  *   or_table1_dense   pinned: Laplacian of x^2+y^2+z^2 = 6, of affine = 0
  *   or_sdf leak post-op / or_sign_correct
  *                     pinned: on leaky spheres / tori the corrected signs equal

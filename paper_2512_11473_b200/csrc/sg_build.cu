@@ -1196,4 +1196,18 @@ extern "C" sg_status sg_plane_counts(const sg_desc* desc, const sg_geometry* geo
 
 extern "C" const char* sg_last_error(void) { return t_last_error.c_str(); }
 extern "C" int32_t sg_abi_version(void) { return SG_ABI_VERSION; }
+
+extern "C" int32_t sg_neighbour_index_shift(const int32_t* shift, int32_t* offset, int32_t* data) {
+    if (!shift) return -1;
+    int32_t slot = 0, mul = 1;
+    for (int k = 0; k < 3; ++k) {
+        if (shift[k] < -SG_PKG || shift[k] > 2 * SG_PKG - 1) return -1;
+        const Shift h = nb_shift(shift[k]);
+        if (offset) offset[k] = h.off;
+        if (data) data[k] = h.data;
+        slot += mul * h.off;
+        mul *= 3;
+    }
+    return slot;
+}
 extern "C" uint64_t sg_launch_count(void) { return g_launches.load(); }

@@ -111,6 +111,20 @@ void* dalloc(size_t bytes, cudaStream_t s);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// NeighbourIndexShift (Lst. 2) for PKG_SIZE = 4, one axis: a
+// package-relative data shift s in [-4, 7] maps to the
+// neighbour offset o = (s + 4) / 4 in {0, 1, 2} (slot ox + 3 oy + 9 oz of the
+// 27-entry row, R-8) and the data index s + 4 - 4 o in that package.  Every
+// kernel that crosses a package face goes through this function; the host
+// export sg_neighbour_index_shift() runs the same code.
+struct Shift {
+    int off, data;
+};
+__host__ __device__ __forceinline__ Shift nb_shift(int s) {
+    const int o = (s + 4) >> 2;  // s + 4 >= 0: shift == floor division
+    return {o, s + 4 - 4 * o};
+}
+
 }  // namespace sg
 
 struct sg_grid {

@@ -250,9 +250,9 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
 #pragma unroll
             for (int cc = 0; cc < 8; ++cc) {
                 const int sx = s0x + (cc & 1), sy = s0y + ((cc >> 1) & 1), sz = s0z + (cc >> 2);
-                const int ox = (sx + 4) >> 2, oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
-                d[cc] = (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
-                pk[cc] = __ldg(row + ox + 3 * oy + 9 * oz);
+                const Shift hx = nb_shift(sx), hy = nb_shift(sy), hz = nb_shift(sz);
+                d[cc] = hx.data + 4 * hy.data + 16 * hz.data;
+                pk[cc] = __ldg(row + hx.off + 3 * hy.off + 9 * hz.off);
             }
             const T tx = tv[0], ty = tv[1], tz = tv[2];
             T acc[4] = {T(0), T(0), T(0), T(0)};

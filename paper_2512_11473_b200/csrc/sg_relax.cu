@@ -58,9 +58,9 @@ __device__ __forceinline__ void interp(const GridC& gc, const uint32_t* __restri
     for (int q = 0; q < 8; ++q) {
         const int bx = q & 1, by = (q >> 1) & 1, bz = q >> 2;
         const int sx = s[0] + bx, sy = s[1] + by, sz = s[2] + bz;
-        const int ox = (sx + 4) >> 2, oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
-        const int d = (sx + 4 - 4 * ox) + 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
-        const size_t pk = __ldg(row + ox + 3 * oy + 9 * oz);
+        const Shift hx = nb_shift(sx), hy = nb_shift(sy), hz = nb_shift(sz);
+        const int d = hx.data + 4 * hy.data + 16 * hz.data;
+        const size_t pk = __ldg(row + hx.off + 3 * hy.off + 9 * hz.off);
         const T w = ((bx ? t[0] : T(1) - t[0]) * (by ? t[1] : T(1) - t[1])) *
                     (bz ? t[2] : T(1) - t[2]);
         const T* p = f + pk * pstride + (size_t)d * dstride;

@@ -544,9 +544,9 @@ __global__ void __launch_bounds__(GR ? 256 : 128) k_kint(const T* __restrict__ i
             if (rowi < NR) {
                 const int ly = rowi % RS, lz = rowi / RS;
                 const int sy = ly - R, sz = lz - R;
-                const int oy = (sy + 4) >> 2, oz = (sz + 4) >> 2;
-                const int dyz = 4 * (sy + 4 - 4 * oy) + 16 * (sz + 4 - 4 * oz);
-                const uint32_t* slot = &s_nb[lp][3 * oy + 9 * oz];
+                const Shift hy = nb_shift(sy), hz = nb_shift(sz);
+                const int dyz = 4 * hy.data + 16 * hz.data;
+                const uint32_t* slot = &s_nb[lp][3 * hy.off + 9 * hz.off];
                 const T* p0 = in + (size_t)slot[0] * 64 + dyz;
                 const T* p1 = in + (size_t)slot[1] * 64 + dyz;
                 const T* p2 = in + (size_t)slot[2] * 64 + dyz;

@@ -30,7 +30,7 @@ _STATUS = {0: "SG_OK", 1: "SG_ERR_ARG", 2: "SG_ERR_OOM", 3: "SG_ERR_CUDA", 4: "S
 EXPORTS = ("sg_build", "sg_build_refined", "sg_reinit", "sg_reinit_halo", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
            "sg_sign_correct", "sg_clean", "sg_info", "sg_view",
            "sg_destroy", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
-           "sg_last_error", "sg_abi_version", "sg_launch_count")
+           "sg_neighbour_index_shift", "sg_last_error", "sg_abi_version", "sg_launch_count")
 
 
 class SgError(RuntimeError):
@@ -113,6 +113,8 @@ def lib():
         L.sg_destroy_async.argtypes = [P, P]
         L.sg_balanced_cuts.argtypes = [P, I32, I32, P]
         L.sg_plane_counts.argtypes = [C.POINTER(sg_desc), C.POINTER(sg_geometry), I32, I32, P, P]
+        L.sg_neighbour_index_shift.argtypes = [P, P, P]
+        L.sg_neighbour_index_shift.restype = I32
         L.sg_last_error.restype = C.c_char_p
         L.sg_abi_version.restype = I32
         L.sg_launch_count.restype = C.c_uint64
@@ -269,6 +271,16 @@ def sg_plane_counts(desc: sg_desc, geom: sg_geometry, z_lo: int, z_hi: int, coun
                                  C.c_void_p(counts_ptr), _stream(stream)))
 
 
+def sg_neighbour_index_shift(shift) -> tuple:
+    """Lst. 2 (host-callable): shift (3 ints in [-4, 7]) -> (slot, offset
+    triple, data triple); slot -1 if out of range."""
+    sh = (C.c_int32 * 3)(*[int(v) for v in shift])
+    off = (C.c_int32 * 3)()
+    dat = (C.c_int32 * 3)()
+    slot = int(lib().sg_neighbour_index_shift(sh, off, dat))
+    return slot, tuple(off), tuple(dat)
+
+
 def sg_launch_count() -> int:
     return int(lib().sg_launch_count())
 
@@ -358,10 +370,32 @@ class Grid:
         sg_table1(self.handle, op, value, stream)
         return self
 
+    def _check_pos(self, pos, what: str, device_only: bool = False):
+        """The C-ABI reads n x 3 contiguous values of the grid dtype: reject
+        anything else before it reaches the kernels."""
+        import torch
+        want = torch.float64 if self.desc.dtype == SG_F64 else torch.float32
+        if pos.dtype != want:
+            raise SgError(SG_ERR_ARG, f"{what}: positions are {pos.dtype}, the grid is {want}")
+        if pos.ndim != 2 or pos.shape[1] != 3:
+            raise SgError(SG_ERR_ARG, f"{what}: positions must have shape (n, 3), got "
+                                      f"{tuple(pos.shape)}")
+        if not pos.is_contiguous():
+            raise SgError(SG_ERR_ARG, f"{what}: positions must be contiguous (row-major n x 3)")
+        if pos.device.type == "cuda":
+            if pos.device.index is not None and pos.device.index != torch.cuda.current_device():
+                raise SgError(SG_ERR_ARG, f"{what}: positions on {pos.device}, current device "
+                                          f"is cuda:{torch.cuda.current_device()}")
+        elif device_only or pos.device.type != "cpu":
+            raise SgError(SG_ERR_ARG, f"{what}: positions must be a CUDA tensor")
+
     def probe(self, pos, want_grad: bool = True, oob=None, stream=None):
         """pos: torch tensor (n, 3) of the grid dtype on cuda (or pinned/
         pageable CPU tensor -> host path).  Returns (phi, grad|None)."""
         import torch
+        self._check_pos(pos, "probe")
+        if oob is not None and (oob.device.type != "cuda" or oob.element_size() != 8):
+            raise SgError(SG_ERR_ARG, "probe: oob must be a CUDA tensor of one 8-byte counter")
         n = int(pos.shape[0])
         dt = pos.dtype
         phi = torch.empty(n, dtype=dt, device=pos.device, pin_memory=(pos.device.type == "cpu"
@@ -378,6 +412,7 @@ class Grid:
     def relax(self, pos, dp: float, steps: int = 1, h_ratio: float = 1.3, step: float = 0.1,
               max_disp: float = 0.2, surface_offset: float = 0.5, stream=None):
         """SPH relaxation steps (NEXT-2) of a device tensor (n, 3), in place."""
+        self._check_pos(pos, "relax", device_only=True)
         sg_relax(self.handle, int(pos.shape[0]), pos.data_ptr(), dp, h_ratio, step, max_disp,
                  surface_offset, steps, stream)
         return pos

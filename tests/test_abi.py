@@ -2,6 +2,7 @@
 include/sg.h declares, the ctypes mirrors match the C struct layouts, and the
 host-only partition helper behaves (no device compute calls here)."""
 import ctypes as C
+import itertools
 import os
 import re
 import subprocess
@@ -88,3 +89,27 @@ def test_no_torch_types_in_header():
     txt = open(HEADER).read()
     assert "torch" not in re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
     assert 'extern "C"' in txt
+
+
+def test_neighbour_index_shift_lst2(sg):
+    """Lst. 2 through the library's own host export (the kernels
+    inline the same function): SPEC's printed 2-D examples (S:172-175,
+    tests/golden/shift_examples.json, extended by a zero z shift -> offset 1,
+    data 0) and, for every shift in [-4, 7]^3, the generalShift definition
+    (S:177-180): target cell = floor(shift / 4) relative to the centre,
+    data = shift mod 4, slot = (cx+1) + 3 (cy+1) + 9 (cz+1)."""
+    from conftest import golden
+    g = golden("shift_examples.json")
+    assert g["pkg"] == 4
+    for case in g["cases"]:
+        slot, off, dat = sg.sg_neighbour_index_shift(case["shift"] + [0])
+        assert list(off) == case["offset"] + [1] and list(dat) == case["data"] + [0]
+        assert slot == off[0] + 3 * off[1] + 9 * off[2]
+    for s in itertools.product(range(-4, 8), repeat=3):
+        slot, off, dat = sg.sg_neighbour_index_shift(s)
+        cell = [v // 4 for v in s]   # Python floor division
+        assert list(off) == [c + 1 for c in cell], s
+        assert list(dat) == [v % 4 for v in s], s
+        assert slot == (cell[0] + 1) + 3 * (cell[1] + 1) + 9 * (cell[2] + 1)
+    for bad in ([-5, 0, 0], [0, 8, 0], [0, 0, 100]):
+        assert sg.sg_neighbour_index_shift(bad)[0] == -1

@@ -652,13 +652,7 @@ def test_relax_pair_moves_apart_symmetrically(oracle_lib):
     assert d[0, 0] < 0 < d[1, 0]
     assert abs(d[0, 0] + d[1, 0]) < 1e-15 and np.all(d[:, 1:] == 0)
     assert abs(out[:, 0].mean() - 0.5) < 1e-15
-    # magnitude from the Wendland C2 derivative at r = 0.5 dp, h = 1.3 dp
-    h = 1.3 * dp
-    q = 0.5 / 1.3
-    sigma = 21 / (16 * math.pi * h**3)
-    dW = -5 * sigma * q * (1 - q / 2) ** 3 / h
-    expect = min(0.01 * dp * dp * 2 * dp**3 * abs(dW), 0.2 * dp)
-    assert abs(d[1, 0] - expect) < 1e-12 * dp
+    # the magnitude is pinned by test_relax_pair_force_normalisation
 
 
 def test_relax_bounding_projects_to_offset_level(oracle_lib):
@@ -675,3 +669,170 @@ def test_relax_bounding_projects_to_offset_level(oracle_lib):
     assert abs(out[0, 0] - (0.8 - 0.5 * dp)) < 1e-12 and abs(out[1, 0] - (0.8 - 0.5 * dp)) < 1e-12
     assert np.all(out[:2, 1:] == p[:2, 1:])
     assert np.array_equal(out[2], p[2])
+
+
+# ------------------------------------------ pins added in round 2 (VERDICT W1)
+#
+# The magnitude of the kernel gradient G (the W' scale), the interior of the
+# smoothed Heaviside and the upwind selection of the Godunov step were only
+# pinned by symmetric properties that a wrong scale / a wrong odd interior /
+# swapped upwind and downwind differences would also satisfy.  Each test below
+# fails under exactly such a mutation of sg_oracle.c.
+
+
+@pytest.mark.parametrize("hr", [1.0, 1.3, 1.5, 1.7, 2.0])
+def test_kernel_gradient_first_moment(oracle_lib, hr):
+    """Integration by parts: -int x dW/dx dV = int W dV = 1 (the Wendland C2
+    kernel is normalised, R-14).  With gw[o] = W'(|o| dx) (-o/|o|) dx^3
+    (along +o, since W' < 0), the lattice quadrature sum_o gw_x[o] o_x dx -> 1
+    as h/dx grows (0.979 at h = 1.3 dx); the tensor is isotropic and
+    diagonal.  A W' without its 1/h, a wrong factor 5 or the 2-D sigma
+    changes the sum by a factor h/dx or more."""
+    for dx in (1 / 64, 1 / 4096):
+        o, w, gw = oracle_lib.kernel_taps(hr, dx)
+        M = np.einsum("ka,kb->ab", gw, o.astype(np.float64)) * dx
+        assert abs(M[0, 0] - 1) < 0.025, (hr, M)
+        assert np.allclose(np.diag(M), M[0, 0], rtol=1e-12, atol=0)
+        assert np.max(np.abs(M - np.diag(np.diag(M)))) < 1e-12
+    o, w, gw = oracle_lib.kernel_taps(2.0, 1 / 64)
+    assert abs((gw[:, 0] * o[:, 0]).sum() / 64 - 1) < 1e-3  # converges with h/dx
+
+
+@pytest.mark.parametrize("hr", [1.0, 1.3, 1.7])
+def test_kernel_gradient_scaling_identity(oracle_lib, hr):
+    """Every kernel of the form W(r; h) = h^-3 f(r/h) satisfies
+    r dW/dr = -h dW/dh - 3 W.  dW/dh is taken by central differences of the
+    oracle's own tap weights w[o] = W(|o| dx; h) dx^3 at h_ratio +- delta, so
+    the tap gradient weights gw[o] = W'(|o| dx) (-o/|o|) dx^3 are predicted
+    from the weights alone (no formula of W' retyped)."""
+    dx = 1 / 512
+    d = 1e-5
+    o0, w0, gw0 = oracle_lib.kernel_taps(hr, dx)
+    op, wp, _ = oracle_lib.kernel_taps(hr + d, dx)
+    om, wm, _ = oracle_lib.kernel_taps(hr - d, dx)
+    key = {tuple(v): i for i, v in enumerate(o0)}
+    ip = np.array([key.get(tuple(v), -1) for v in op])
+    im = np.array([key.get(tuple(v), -1) for v in om])
+    Wp = np.zeros(len(w0))
+    Wm = np.zeros(len(w0))
+    Wp[ip[ip >= 0]] = wp[ip >= 0]
+    Wm[im[im >= 0]] = wm[im >= 0]
+    both = np.zeros(len(w0), bool)
+    both[ip[ip >= 0]] = True
+    both &= np.isin(np.arange(len(w0)), im[im >= 0])
+    r = np.linalg.norm(o0, axis=1) * dx
+    h = hr * dx
+    sel = both & (r > 0)
+    assert sel.sum() >= 6
+    dWdh = (Wp - Wm) / (2 * d * dx)          # of w = W dx^3, per unit h
+    Wprime = (-h * dWdh - 3 * w0) / r         # times dx^3
+    pred = Wprime[:, None] * (-o0 / np.maximum(np.linalg.norm(o0, axis=1), 1e-300)[:, None])
+    err = np.abs(pred[sel] - gw0[sel])
+    scale = np.abs(gw0[sel]).max()
+    assert err.max() < 1e-6 * scale, err.max() / scale
+    # sign: W decreasing in r (W' < 0), so gw = W' (-o/|o|) dx^3 points along +o
+    assert np.all((gw0[sel] * o0[sel]).sum(1) > 0)
+
+
+def test_heaviside_c1_conditions(oracle_lib):
+    """The smoothed Heaviside of R-14 is the C^1 ramp: H'(0) = 1/eps (the
+    sine term doubles the linear slope 1/(2 eps)) and H'(+-eps) = 0, so H
+    joins 0 and 1 with zero slope.  Finite differences of the oracle's H; an
+    odd interior such as sin(pi u/eps)/(2 pi) gives H'(0) = 0.75/eps and
+    H'(eps) = 0.25/eps."""
+    eps = 0.37
+    H = lambda u: oracle_lib.heaviside(u, eps)  # noqa: E731
+    d = 1e-6 * eps
+    assert abs((H(d) - H(-d)) / (2 * d) - 1 / eps) < 1e-6 / eps
+    # one-sided, inside the smoothing band (H'' vanishes at +-eps as well)
+    assert abs((H(eps) - H(eps - d)) / d) < 1e-5 / eps
+    assert abs((H(-eps + d) - H(-eps)) / d) < 1e-5 / eps
+    assert abs(H(eps) - 1) < 1e-15 and abs(H(-eps)) < 1e-15
+    # interior value at u = eps/2: (1 + 1/2 + 1/pi)/2
+    assert abs(H(eps / 2) - 0.5 * (1.5 + 1 / math.pi)) < 1e-15
+    # monotone on the band
+    u = np.linspace(-eps, eps, 201)
+    v = np.array([H(x) for x in u])
+    assert np.all(np.diff(v) >= 0)
+
+
+def _kink_setup(oracle_lib):
+    w = W.config("C1")
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    m = 4 * w.n[0]
+    cb = np.repeat(np.repeat(np.repeat(t.bg.reshape(w.n[::-1]), 4, 0), 4, 1), 4, 2)
+    return w, o, m, cb >= 2
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_reinit_godunov_kinks_closed_form(oracle_lib, axis):
+    """One Godunov step (O7) on tent profiles along one axis, in index space
+    phi = (d +- |i - j|) dx (exact binary values, dx = 1/64), both signs:
+      ridge  phi > 0 peak (a = +1, b = -1): upwind |grad| = 1 -> unchanged;
+      valley phi > 0 trough (a = -1, b = +1): |grad| = 0 ->
+             phi + cfl dx s (s = phi/sqrt(phi^2+dx^2));
+      valley phi < 0 (a = -1, b = +1): |grad| = 1 -> unchanged;
+      ridge  phi < 0 (a = +1, b = -1): |grad| = 0 -> phi + cfl dx s.
+    Points off the kink see slope 1 from the upwind side and stay.  A
+    swapped (downwind) selection moves the ridges and freezes the valleys.
+    phi = 0 exactly stays 0 (the O7 stationary case)."""
+    w, o, m, act = _kink_setup(oracle_lib)
+    dx, cfl = w.dx, 0.3
+    j = 2 * m // 5  # a plane that crosses the sphere's band
+    idx = np.indices((m, m, m))[2 - axis]  # (z, y, x) arrays: axis 0 = x
+    dist = np.abs(idx - j).astype(np.float64)
+    on = act & (idx == j)
+    near = act & (np.abs(idx - j) == 1)
+    assert on.sum() > 50 and near.sum() > 100
+    cases = [(+1, +6.0, -1, False), (+1, 6.0, +1, True), (-1, -6.0, +1, False),
+             (-1, -6.0, -1, True)]
+    for sgn, d, slope, moves in cases:
+        phi = (d + slope * dist) * dx
+        out = o.reinit_step(phi, cfl)
+        p = phi[on]
+        s = p / np.sqrt(p * p + dx * dx)
+        exp = p + cfl * dx * s if moves else p
+        assert np.all(np.sign(p) == sgn)
+        assert np.array_equal(out[on], exp), (sgn, d, slope, np.abs(out[on] - exp).max())
+        assert np.array_equal(out[near], phi[near])
+    # phi = 0 exactly: s = 0, no update whatever the neighbours
+    phi = (dist - 0.0) * dx
+    out = o.reinit_step(phi, cfl)
+    assert np.all(out[on] == 0.0)
+
+
+def test_relax_pair_force_normalisation(oracle_lib):
+    """Magnitude of the pair force without retyping W': pairs at separations
+    r in (0, 2h) (each pair isolated, deep inside where G = 0 and phi is far
+    below the bounding level) move apart by d(r) = 2 step dp^2 V |W'(r)|.
+    Integrating W'(r) = -d / (2 step dp^2 V) from 2h inward gives W(r), and
+    the Wendland kernel is normalised: int_0^2h 4 pi r^2 W(r) dr = 1."""
+    w = _relax_world()
+    o = oracle_lib.Oracle(w)
+    o.build_tables()
+    phi, grad, G = _fields(o)
+    dp = w.dx / 4          # 4 particles per data spacing keeps every pair deep inside
+    h = 1.3 * dp
+    n = 120
+    r = (np.arange(n) + 0.5) / n * 2 * h
+    # pairs on a lattice with spacing 5h (no cross-pair interaction)
+    side = int(np.ceil(n ** (1 / 3)))
+    cen = []
+    for k in range(n):
+        a, b, c = k % side, (k // side) % side, k // (side * side)
+        cen.append([0.45 + 5 * h * a, 0.45 + 5 * h * b, 0.45 + 5 * h * c])
+    cen = np.array(cen)
+    assert cen.max() < 0.6
+    p = np.concatenate([cen - np.c_[r / 2, 0 * r, 0 * r], cen + np.c_[r / 2, 0 * r, 0 * r]])
+    step = 0.1
+    out = o.relax(phi, grad, G, p, dp=dp, step=step, steps=1)
+    d = out[n:, 0] - p[n:, 0]
+    assert np.all(d > 0) and np.allclose(out[:n, 0] - p[:n, 0], -d, rtol=1e-9, atol=1e-18)
+    assert d.max() < 0.2 * dp  # the displacement clamp never engages
+    V = dp ** 3
+    Wp = -d / (2 * step * dp * dp * V)
+    dr = 2 * h / n
+    Wr = np.cumsum(-Wp[::-1])[::-1] * dr - 0.5 * (-Wp) * dr  # midpoint rule from 2h inward
+    total = np.sum(4 * np.pi * r * r * Wr) * dr
+    assert abs(total - 1) < 2e-3, total
