@@ -290,7 +290,9 @@ sg_status sg_probe(const sg_grid* grid, int64_t n, const void* pos, void* phi, v
                    unsigned long long* oob_count, void* stream);
 
 /* Table-1 workloads of the paper, on the current phi:
- *   op 0 "sequential": phi += value at every active data point (in place);
+ *   op 0 "sequential": phi += value at every active data point (in place;
+ *        on a slab grid the ghost packages too, so they stay equal to their
+ *        owner's values); grad / normal / K / G become stale (has_* cleared);
  *   op 1 "stencil": out = 7-point Laplacian of phi at every active data point
  *        ((sum of 6 neighbours - 6 phi) / dx^2), written to the active
  *        packages of the SG_VIEW_PHI_NEXT buffer (phi is unchanged; the

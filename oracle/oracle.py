@@ -20,14 +20,39 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "sg_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
 
-CFLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-          "-std=c11", "-Wall", "-Wno-unknown-pragmas"]
+# -O3 -march=native (the oracle timed as a CPU
+# program); -ffp-contract=off and no -ffast-math keep every double operation
+# a separately rounded IEEE operation in the order written, so the results do
+# not depend on the flags or the host.  The library is built per host CPU
+# (native code of one box may not run on another).
+CFLAGS = ["-O3", "-march=native", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+          "-shared", "-std=c11", "-Wall", "-Wno-unknown-pragmas"]
+
+
+def _cpu_tag() -> str:
+    import hashlib
+    import platform
+    sig = platform.machine()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith(("model name", "flags")):
+                    sig += line
+                if line.strip() == "":
+                    break
+    except OSError:
+        pass
+    return hashlib.sha1(sig.encode()).hexdigest()[:10]
+
+
+LIB = os.path.join(HERE, f"liboracle.{_cpu_tag()}.so")
 
 
 def build(force: bool = False) -> str:
-    """Compile liboracle.so (gcc, no FMA contraction, IEEE double)."""
+    """Compile the oracle library for this host (gcc, no FMA contraction,
+    IEEE double)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        tmp = LIB + ".tmp"
+        tmp = LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, SRC, "-lm"])
         os.replace(tmp, LIB)
     return LIB
@@ -39,7 +64,8 @@ class _Prim(C.Structure):
 
 class _Grid(C.Structure):
     _fields_ = [("lower", C.c_double * 3), ("cell", C.c_double), ("n", C.c_int32 * 3),
-                ("pad", C.c_int32), ("far", C.c_double), ("init_scale", C.c_double)]
+                ("pad", C.c_int32), ("far", C.c_double), ("init_scale", C.c_double),
+                ("win_lo", C.c_int32 * 3), ("win_n", C.c_int32 * 3)]
 
 
 _lib = None
@@ -119,11 +145,26 @@ class Tables:
 
 
 class Oracle:
-    """Dense fp64 oracle bound to one workload (geometry + grid)."""
+    """Dense fp64 oracle bound to one workload (geometry + grid).
 
-    def __init__(self, w):
+    window: None (dense arrays over the whole domain) or a box of background
+    cells ((x0, y0, z0), (x1, y1, z1)), half open: the dense arrays of O6-O10
+    then cover only its fine points (shape (4(z1-z0), 4(y1-y0), 4(x1-x0)));
+    values read outside the box but inside the domain are the initial phi
+    (sg_oracle.c or_grid), exact at depth > (sweeps + stencil radius) from
+    the box faces.  Tables (O3-O5) always cover the whole domain."""
+
+    def __init__(self, w, window=None):
         self.w = w
         self._g = _Grid()
+        self.window = None
+        if window is not None:
+            lo, hi = (tuple(int(v) for v in window[0]), tuple(int(v) for v in window[1]))
+            assert all(0 <= lo[k] < hi[k] <= w.n[k] for k in range(3)), window
+            self.window = (lo, hi)
+            for k in range(3):
+                self._g.win_lo[k] = 4 * lo[k]
+                self._g.win_n[k] = 4 * (hi[k] - lo[k])
         for k in range(3):
             self._g.lower[k] = w.lower[k]
             self._g.n[k] = w.n[k]
@@ -173,7 +214,14 @@ class Oracle:
 
     @property
     def m(self):
-        return tuple(4 * n for n in self.w.n)  # (Mx, My, Mz)
+        """Dense array extents (Mx, My, Mz): the domain, or the window box."""
+        if self.window is not None:
+            lo, hi = self.window
+            return tuple(4 * (hi[k] - lo[k]) for k in range(3))
+        return tuple(4 * n for n in self.w.n)
+
+    def _whole(self, what):
+        assert self.window is None, f"{what}: whole-domain oracle only"
 
     # O1
     def sdf(self, x: np.ndarray) -> np.ndarray:
@@ -288,6 +336,7 @@ class Oracle:
     # NEXT-2 particle relaxation (reading R-21); pos (n, 3) float64, updated copy
     def relax(self, phi, grad, G, pos, dp, h_ratio=1.3, step=0.1, max_disp=0.2,
               surface_offset=0.5, steps=1):
+        self._whole("relax")
         pos = np.ascontiguousarray(np.asarray(pos, dtype=np.float64).reshape(-1, 3)).copy()
         phi = np.ascontiguousarray(phi, dtype=np.float64)
         grad = np.ascontiguousarray(grad, dtype=np.float64)
@@ -304,6 +353,7 @@ class Oracle:
         phi, (coarse_sweeps, refined_sweeps)).  For an fp32 comparison pass
         phi and tau already rounded to float32 (the trust decision is then
         taken in the kernel's precision)."""
+        self._whole("sign_correct")
         t = self.tables if self.tables is not None else self.build_tables()
         bg = t.bg.copy()
         nb = np.ascontiguousarray(t.nb.copy())
@@ -321,6 +371,7 @@ class Oracle:
               cfl: float | None = None):
         """NEXT-3 small-feature cleaning (R-23) of a copy of the dense phi.
         Returns (phi, rounds, modified per round)."""
+        self._whole("clean")
         out = np.ascontiguousarray(np.array(phi, dtype=np.float64, copy=True))
         mods = np.zeros(max(1, max_rounds), np.int64)
         r = self._L().or_clean(self.g, self.prims, self.n_prims, _ptr(self._bg()), _ptr(out),
@@ -330,6 +381,7 @@ class Oracle:
         return out, int(r), [int(v) for v in mods[:max_rounds]]
 
     def to_packages(self, dense: np.ndarray, far_neg: float, far_pos: float) -> np.ndarray:
+        self._whole("to_packages")
         t = self.tables if self.tables is not None else self.build_tables()
         dense = np.ascontiguousarray(dense, dtype=np.float64)
         out = np.empty((t.n_pkg, 64))
@@ -349,3 +401,19 @@ def kernel_taps(h_ratio: float, dx: float):
 
 def heaviside(u: float, eps: float) -> float:
     return float(lib().or_heaviside(u, eps))
+
+
+def box_to_packages(dense_box: np.ndarray) -> np.ndarray:
+    """Layout helper (no arithmetic): a dense box of whole background cells,
+    shape (4 bz, 4 by, 4 bx) x fastest, as per-cell packages
+    [bz, by, bx, 64] in the canonical in-package order d = i + 4 j + 16 k
+    (R-9).  Leading component axes are kept: (c, 4bz, 4by, 4bx) ->
+    (c, bz, by, bx, 64)."""
+    a = np.asarray(dense_box)
+    lead = a.shape[:-3]
+    mz, my, mx = a.shape[-3:]
+    n = len(lead)
+    # (..., bz, k, by, j, bx, i) -> (..., bz, by, bx, k, j, i)
+    order = list(range(n)) + [n, n + 2, n + 4, n + 1, n + 3, n + 5]
+    b = a.reshape(lead + (mz // 4, 4, my // 4, 4, mx // 4, 4)).transpose(order)
+    return np.ascontiguousarray(b).reshape(lead + (mz // 4, my // 4, mx // 4, 64))

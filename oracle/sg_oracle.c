@@ -18,9 +18,15 @@
  * Where PAPER.md is silent the reading taken is the one listed in DESIGN.md
  * "Readings" (R-1 .. R-20, same numbering as SURVEY.md 8(c.3)).
  *
- * Build: gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared (no -ffast-math):
- * every double operation is a separately rounded IEEE operation in the order
- * written, which is what makes the tagging decision |f| < l_c reproducible.
+ * Build: gcc -O3 -march=native -fopenmp -ffp-contract=off -fPIC -shared (no
+ * -ffast-math; one library per host CPU): every double operation is a
+ * separately rounded IEEE operation in the order written, which is what makes
+ * the tagging decision |f| < l_c reproducible.
+ *
+ * Box windows (or_grid.win_lo / win_n): O6-O10 may be evaluated on a box of
+ * the dense grid only (the definition restricted to the box; values outside
+ * it are the initial phi) -- how C3 / C5 are checked and timed, where the
+ * whole dense grid does not fit in memory (69 GB / 550 GB per field).
  *
  * Parity status per function:
  *   or_sdf            pinned: closed forms + brute-force surface sampling
@@ -93,7 +99,23 @@ typedef struct {
     int32_t pad;
     double far;       /* far-field magnitude, reading R-4          */
     double init_scale;
+    /* Box window (0 = the whole domain): the dense arrays of O6-O10 cover
+     * only the fine points [win_lo, win_lo + win_n) per axis (global fine
+     * indices).  A dense value read outside the box but inside the domain is
+     * the initial phi O6 of that point (the window-edge condition): after k
+     * reinit sweeps its error has travelled k points into the box (the
+     * 7-point dependence cone), so the box interior at depth > k plus the
+     * stencil radius of later steps is the whole-domain definition exactly.
+     * This is the definition restricted to a box, for configurations whose
+     * dense grid does not fit in memory (C3, C5).  O7 sign
+     * correction, cleaning and relaxation are whole-domain only. */
+    int32_t win_lo[3];
+    int32_t win_n[3];
 } or_grid;
+
+static inline int full_domain(const or_grid* g) {
+    return g->win_n[0] <= 0 || g->win_n[1] <= 0 || g->win_n[2] <= 0;
+}
 
 #define PKG 4 /* subdivision size, "default by 4"; fixed (R-9) */
 
@@ -519,7 +541,9 @@ typedef struct {
     const or_prim* prims;
     int32_t n_prims;
     const uint32_t* bg;
-    int64_t m[3];
+    int64_t m[3];  /* fine points of the domain per axis            */
+    int64_t o[3];  /* box origin (fine index); 0 for the whole domain */
+    int64_t w[3];  /* box extent; m for the whole domain              */
     double far;
 } dense_ctx;
 
@@ -529,17 +553,36 @@ static void dense_init(dense_ctx* d, const or_grid* g, const or_prim* prims, int
     d->prims = prims;
     d->n_prims = n_prims;
     d->bg = bg;
-    for (int k = 0; k < 3; ++k) d->m[k] = (int64_t)PKG * g->n[k];
+    for (int k = 0; k < 3; ++k) {
+        d->m[k] = (int64_t)PKG * g->n[k];
+        d->o[k] = full_domain(g) ? 0 : g->win_lo[k];
+        d->w[k] = full_domain(g) ? d->m[k] : g->win_n[k];
+    }
     d->far = or_far(g);
 }
+
+/* array index of global fine point I inside the box; in_box tests it */
+static inline int in_box(const dense_ctx* d, int64_t ix, int64_t iy, int64_t iz) {
+    return ix >= d->o[0] && iy >= d->o[1] && iz >= d->o[2] && ix < d->o[0] + d->w[0] &&
+           iy < d->o[1] + d->w[1] && iz < d->o[2] + d->w[2];
+}
+static inline int64_t box_index(const dense_ctx* d, int64_t ix, int64_t iy, int64_t iz) {
+    return (ix - d->o[0]) + d->w[0] * ((iy - d->o[1]) + d->w[1] * (iz - d->o[2]));
+}
+static inline int64_t box_volume(const dense_ctx* d) { return d->w[0] * d->w[1] * d->w[2]; }
 
 static inline int64_t fdiv4(int64_t i) { return i >= 0 ? i / 4 : -((-i + 3) / 4); }
 
 /* value of a scalar dense field at fine index (ix,iy,iz), possibly outside */
+double or_phi_point(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
+                    int64_t ix, int64_t iy, int64_t iz);
+
 static inline double dense_get(const dense_ctx* d, const double* a, int64_t ix, int64_t iy,
                                int64_t iz) {
+    if (in_box(d, ix, iy, iz)) return a[box_index(d, ix, iy, iz)];
     if (ix >= 0 && iy >= 0 && iz >= 0 && ix < d->m[0] && iy < d->m[1] && iz < d->m[2])
-        return a[ix + d->m[0] * (iy + d->m[1] * iz)];
+        /* window edge (box mode only): the initial phi of the point */
+        return or_phi_point(d->g, d->prims, d->n_prims, d->bg, ix, iy, iz);
     uint32_t s = far_pkg_virtual(d->g, d->prims, d->n_prims, fdiv4(ix), fdiv4(iy), fdiv4(iz));
     return s == 0 ? -d->far : d->far;
 }
@@ -559,9 +602,9 @@ void or_phi_dense(const or_grid* g, const or_prim* prims, int32_t n_prims, const
     dense_init(&d, g, prims, n_prims, bg);
     const double s = init_scale(g);
 #pragma omp parallel for collapse(2) schedule(static)
-    for (int64_t iz = 0; iz < d.m[2]; ++iz)
-        for (int64_t iy = 0; iy < d.m[1]; ++iy)
-            for (int64_t ix = 0; ix < d.m[0]; ++ix) {
+    for (int64_t iz = d.o[2]; iz < d.o[2] + d.w[2]; ++iz)
+        for (int64_t iy = d.o[1]; iy < d.o[1] + d.w[1]; ++iy)
+            for (int64_t ix = d.o[0]; ix < d.o[0] + d.w[0]; ++ix) {
                 uint32_t b = bg[lin_cell(g, ix / 4, iy / 4, iz / 4)];
                 double v;
                 if (b >= 2) {
@@ -571,7 +614,7 @@ void or_phi_dense(const or_grid* g, const or_prim* prims, int32_t n_prims, const
                 } else {
                     v = b == 0 ? -d.far : d.far;
                 }
-                phi[ix + d.m[0] * (iy + d.m[1] * iz)] = v;
+                phi[box_index(&d, ix, iy, iz)] = v;
             }
 }
 
@@ -627,10 +670,10 @@ void or_reinit_dense(const or_grid* g, const or_prim* prims, int32_t n_prims, co
     dense_init(&d, g, prims, n_prims, bg);
     const double dx = data_spacing(g);
 #pragma omp parallel for collapse(2) schedule(static)
-    for (int64_t iz = 0; iz < d.m[2]; ++iz)
-        for (int64_t iy = 0; iy < d.m[1]; ++iy)
-            for (int64_t ix = 0; ix < d.m[0]; ++ix) {
-                int64_t I = ix + d.m[0] * (iy + d.m[1] * iz);
+    for (int64_t iz = d.o[2]; iz < d.o[2] + d.w[2]; ++iz)
+        for (int64_t iy = d.o[1]; iy < d.o[1] + d.w[1]; ++iy)
+            for (int64_t ix = d.o[0]; ix < d.o[0] + d.w[0]; ++ix) {
+                int64_t I = box_index(&d, ix, iy, iz);
                 if (!point_active(&d, ix, iy, iz)) {
                     out[I] = phi[I];
                     continue;
@@ -668,12 +711,12 @@ void or_gradient_dense(const or_grid* g, const or_prim* prims, int32_t n_prims,
     dense_ctx d;
     dense_init(&d, g, prims, n_prims, bg);
     const double dx = data_spacing(g);
-    const int64_t plane = d.m[0] * d.m[1] * d.m[2];
+    const int64_t plane = box_volume(&d);
 #pragma omp parallel for collapse(2) schedule(static)
-    for (int64_t iz = 0; iz < d.m[2]; ++iz)
-        for (int64_t iy = 0; iy < d.m[1]; ++iy)
-            for (int64_t ix = 0; ix < d.m[0]; ++ix) {
-                int64_t I = ix + d.m[0] * (iy + d.m[1] * iz);
+    for (int64_t iz = d.o[2]; iz < d.o[2] + d.w[2]; ++iz)
+        for (int64_t iy = d.o[1]; iy < d.o[1] + d.w[1]; ++iy)
+            for (int64_t ix = d.o[0]; ix < d.o[0] + d.w[0]; ++ix) {
+                int64_t I = box_index(&d, ix, iy, iz);
                 double gv[3] = {0.0, 0.0, 0.0};
                 if (point_active(&d, ix, iy, iz)) {
                     gv[0] = (dense_get(&d, phi, ix + 1, iy, iz) - dense_get(&d, phi, ix - 1, iy, iz)) / (2.0 * dx);
@@ -759,16 +802,16 @@ void or_kernel_dense(const or_grid* g, const or_prim* prims, int32_t n_prims, co
     dense_ctx d;
     dense_init(&d, g, prims, n_prims, bg);
     const double dx = data_spacing(g);
-    const int64_t plane = d.m[0] * d.m[1] * d.m[2];
+    const int64_t plane = box_volume(&d);
     taps_t* t = (taps_t*)malloc(sizeof(taps_t));
     make_taps(h_ratio, dx, t);
     double S = 0.0;
     for (int k = 0; k < t->n; ++k) S += t->w[k];
 #pragma omp parallel for collapse(2) schedule(dynamic, 1)
-    for (int64_t iz = 0; iz < d.m[2]; ++iz)
-        for (int64_t iy = 0; iy < d.m[1]; ++iy)
-            for (int64_t ix = 0; ix < d.m[0]; ++ix) {
-                int64_t I = ix + d.m[0] * (iy + d.m[1] * iz);
+    for (int64_t iz = d.o[2]; iz < d.o[2] + d.w[2]; ++iz)
+        for (int64_t iy = d.o[1]; iy < d.o[1] + d.w[1]; ++iy)
+            for (int64_t ix = d.o[0]; ix < d.o[0] + d.w[0]; ++ix) {
+                int64_t I = box_index(&d, ix, iy, iz);
                 double k_acc = 0.0, gacc[3] = {0.0, 0.0, 0.0};
                 uint32_t b = bg[lin_cell(g, ix / 4, iy / 4, iz / 4)];
                 if (b >= 2) {
@@ -800,10 +843,10 @@ void or_table1_dense(const or_grid* g, const or_prim* prims, int32_t n_prims, co
     dense_init(&d, g, prims, n_prims, bg);
     const double dx = data_spacing(g);
 #pragma omp parallel for collapse(2) schedule(static)
-    for (int64_t iz = 0; iz < d.m[2]; ++iz)
-        for (int64_t iy = 0; iy < d.m[1]; ++iy)
-            for (int64_t ix = 0; ix < d.m[0]; ++ix) {
-                int64_t I = ix + d.m[0] * (iy + d.m[1] * iz);
+    for (int64_t iz = d.o[2]; iz < d.o[2] + d.w[2]; ++iz)
+        for (int64_t iy = d.o[1]; iy < d.o[1] + d.w[1]; ++iy)
+            for (int64_t ix = d.o[0]; ix < d.o[0] + d.w[0]; ++ix) {
+                int64_t I = box_index(&d, ix, iy, iz);
                 int act = point_active(&d, ix, iy, iz);
                 if (op == 0) {
                     out[I] = act ? phi[I] + value : phi[I];
@@ -832,7 +875,7 @@ int64_t or_probe(const or_grid* g, const or_prim* prims, int32_t n_prims, const 
     dense_ctx d;
     dense_init(&d, g, prims, n_prims, bg);
     const double dx = data_spacing(g);
-    const int64_t plane = d.m[0] * d.m[1] * d.m[2];
+    const int64_t plane = box_volume(&d);
     int64_t oob = 0;
 #pragma omp parallel for schedule(static) reduction(+ : oob)
     for (int64_t p = 0; p < n; ++p) {
@@ -872,9 +915,8 @@ int64_t or_probe(const or_grid* g, const or_prim* prims, int32_t n_prims, const 
                     int64_t ix = a[0] + b0, iy = a[1] + b1, iz = a[2] + b2;
                     rphi += w * dense_get(&d, phi, ix, iy, iz);
                     if (grad3) {
-                        int in = ix >= 0 && iy >= 0 && iz >= 0 && ix < d.m[0] && iy < d.m[1] && iz < d.m[2];
-                        if (in) {
-                            int64_t I = ix + d.m[0] * (iy + d.m[1] * iz);
+                        if (in_box(&d, ix, iy, iz)) {
+                            int64_t I = box_index(&d, ix, iy, iz);
                             for (int k = 0; k < 3; ++k) rg[k] += w * grad3[k * plane + I];
                         }
                     }
@@ -915,11 +957,11 @@ static void interp_dense(const dense_ctx* d, const double* f3, int ncomp, int64_
         int b0 = b & 1, b1 = (b >> 1) & 1, b2 = (b >> 2) & 1;
         double w = ((b0 ? t[0] : 1.0 - t[0]) * (b1 ? t[1] : 1.0 - t[1])) * (b2 ? t[2] : 1.0 - t[2]);
         int64_t ix = a[0] + b0, iy = a[1] + b1, iz = a[2] + b2;
-        int in = ix >= 0 && iy >= 0 && iz >= 0 && ix < d->m[0] && iy < d->m[1] && iz < d->m[2];
+        int in = in_box(d, ix, iy, iz);
         for (int c = 0; c < ncomp; ++c) {
             double v;
             if (ncomp == 1 && c == 0) v = dense_get(d, f3, ix, iy, iz);
-            else v = in ? f3[c * plane + ix + d->m[0] * (iy + d->m[1] * iz)] : 0.0;
+            else v = in ? f3[c * plane + box_index(d, ix, iy, iz)] : 0.0;
             out[c] += w * v;
         }
     }
@@ -938,9 +980,10 @@ static int in_domain_pos(const or_grid* g, const double x[3], int64_t c[3]) {
 void or_relax(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
               const double* phi, const double* grad3, const double* G3, int64_t n, double* pos,
               double dp, double h_ratio, double step, double max_disp, double off, int32_t steps) {
+    if (!full_domain(g)) return; /* whole-domain operation */
     dense_ctx d;
     dense_init(&d, g, prims, n_prims, bg);
-    const int64_t plane = d.m[0] * d.m[1] * d.m[2];
+    const int64_t plane = box_volume(&d);
     const double PI = 3.14159265358979323846;
     const double h = h_ratio * dp;
     const double sigma = 21.0 / (16.0 * PI * h * h * h);
@@ -1032,6 +1075,7 @@ void or_sign_correct(const or_grid* g, const or_prim* prims, int32_t n_prims, co
                      uint32_t* bg, const uint32_t* meta_cell, int64_t n_pkg, uint32_t* nb,
                      uint8_t* cell_neg, double* phi, double tau, int32_t max_sweeps,
                      int32_t* sweeps) {
+    if (!full_domain(g)) return; /* whole-domain operation */
     const int64_t nx = g->n[0], ny = g->n[1], nz = g->n[2];
     const int64_t ncell = nx * ny * nz;
     static const int off[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
@@ -1192,6 +1236,7 @@ void or_sign_correct(const or_grid* g, const or_prim* prims, int32_t n_prims, co
 int32_t or_clean(const or_grid* g, const or_prim* prims, int32_t n_prims, const uint32_t* bg,
                  double* phi, double h_ratio, double threshold, int32_t reinit_iters, double cfl,
                  int32_t max_rounds, int64_t* modified) {
+    if (!full_domain(g)) return -1; /* whole-domain operation */
     dense_ctx d;
     dense_init(&d, g, prims, n_prims, bg);
     const double dx = data_spacing(g);
@@ -1236,6 +1281,7 @@ int32_t or_clean(const or_grid* g, const or_prim* prims, int32_t n_prims, const 
  * canonical order).  Singular packages take `far_neg` / `far_pos`. */
 void or_gather_packages(const or_grid* g, const double* dense, const uint32_t* meta_cell,
                         int64_t n_pkg, double far_neg, double far_pos, double* out) {
+    if (!full_domain(g)) return; /* whole-domain operation */
     const int64_t nx = g->n[0], ny = g->n[1];
     const int64_t m0 = (int64_t)PKG * g->n[0], m1 = (int64_t)PKG * g->n[1];
     for (int d = 0; d < 64; ++d) {

@@ -47,6 +47,47 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
     throw Error(SG_ERR_CUDA, m);
 }
 
+namespace {
+struct OccKey {
+    const void* k;
+    int dev, threads;
+    size_t smem;
+    bool operator==(const OccKey& o) const {
+        return k == o.k && dev == o.dev && threads == o.threads && smem == o.smem;
+    }
+};
+std::mutex g_occ_mu;
+std::vector<std::pair<OccKey, int>> g_occ;
+std::vector<int> g_sms;
+}  // namespace
+
+int sm_count() {
+    int dev = 0;
+    SG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    if ((int)g_sms.size() <= dev) g_sms.resize(dev + 1, 0);
+    if (!g_sms[dev]) SG_CUDA(cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev));
+    return g_sms[dev];
+}
+
+int resident_blocks(const void* kernel, int threads, size_t smem) {
+    const int sms = sm_count();
+    int dev = 0;
+    SG_CUDA(cudaGetDevice(&dev));
+    const OccKey key{kernel, dev, threads, smem};
+    {
+        std::lock_guard<std::mutex> lk(g_occ_mu);
+        for (auto& e : g_occ)
+            if (e.first == key) return e.second;
+    }
+    int per = 0;
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem));
+    const int r = std::max(1, sms * per);
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    g_occ.push_back({key, r});
+    return r;
+}
+
 static std::once_flag g_pool_once;
 
 void* dalloc(size_t bytes, cudaStream_t s) {
@@ -645,6 +686,13 @@ static GridC make_gridc(const sg_desc* d) {
         gc.idx32 = gc.idx32 && d->lower[k] == 0.0 && (double)gc.upperf[k] == gc.upper[k] &&
                    d->n[k] < (1 << 20);
     }
+    // SG_PROBE_IDX32=0 forces the general fp64 index path (tests compare the
+    // two paths bit for bit)
+    static const bool idx32_off = [] {
+        const char* e = std::getenv("SG_PROBE_IDX32");
+        return e && e[0] == '0';
+    }();
+    if (idx32_off) gc.idx32 = 0;
     gc.inv_cellf = (float)gc.inv_cell;
     gc.inv_dxf = (float)gc.inv_dx;
     return gc;

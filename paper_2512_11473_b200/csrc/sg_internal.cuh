@@ -111,6 +111,13 @@ void* dalloc(size_t bytes, cudaStream_t s);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Resident blocks of `kernel` on the current device (SMs x blocks per SM at
+// `threads` threads and `smem` dynamic shared bytes): the grid of a
+// persistent launch.  Cached per (kernel, device, threads, smem); thread safe.
+int resident_blocks(const void* kernel, int threads, size_t smem = 0);
+// streaming multiprocessors of the current device (cached per device)
+int sm_count();
+
 // NeighbourIndexShift (Lst. 2) for PKG_SIZE = 4, one axis: a
 // package-relative data shift s in [-4, 7] maps to the
 // neighbour offset o = (s + 4) / 4 in {0, 1, 2} (slot ox + 3 oy + 9 oz of the

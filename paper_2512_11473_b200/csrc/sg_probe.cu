@@ -65,13 +65,19 @@ __device__ __forceinline__ bool cell_of<double, false>(const GridC& gc, int k, d
     c = min((int)floor(qdiv(gc, x - gc.lower[k], true)), gc.n[k] - 1);
     return x >= gc.lower[k] && x < gc.upper[k];
 }
+// v = x / dx is exact (power-of-two scaling).  The definition's fraction
+// t = (v - 1/2) - a is computed as v - (a + 1/2): a + 1/2 is exact, and the
+// subtraction is exact for v >= 1/2 (the operands are within a factor 2, or
+// v < 2 and ulp(v) <= 1/2), so t is the fp64 value rounded once -- also for
+// v < 1/2 (a = -1, t = RN(v + 1/2)), where the fp32 u = v - 1/2 itself would
+// be rounded (v < 1/4).  floor(u) is exact in every case.
 template <>
 __device__ __forceinline__ void corner_of<float, true>(const GridC& gc, int k, float x, int& a,
                                                        float& t) {
-    const float u = x * gc.inv_dxf - 0.5f;
-    const float fa = floorf(u);
+    const float v = x * gc.inv_dxf;
+    const float fa = floorf(v - 0.5f);
     a = (int)fa;
-    t = u - fa;
+    t = v - (fa + 0.5f);
 }
 template <>
 __device__ __forceinline__ void corner_of<float, false>(const GridC& gc, int k, float x, int& a,
@@ -323,16 +329,7 @@ static void probe_dev(const sg_grid* g, int64_t n, const void* pos, void* out_ph
     if (n <= 0) return;
     const T* grad = out_grad ? (const T*)g->grad : nullptr;
     constexpr int kWB = ProbeSmem<T>::kWB;
-    static int resident[2] = {0, 0};  // blocks per SM x SMs, per dtype
-    int& rb = resident[sizeof(T) == 8];
-    if (!rb) {
-        int dev = 0, sms = 0, per = 0;
-        SG_CUDA(cudaGetDevice(&dev));
-        SG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_probe<T, false, false>,
-                                                              32 * kWB, 0));
-        rb = std::max(1, sms * per);
-    }
+    const int rb = resident_blocks((const void*)k_probe<T, false, false>, 32 * kWB);
     const int64_t blocks = std::min<int64_t>(ceil_div(n, kPW * kWB), rb);
     const bool vec =
         ((uintptr_t)pos | (uintptr_t)out_phi | (uintptr_t)(out_grad ? out_grad : out_phi)) % 16 == 0;
@@ -362,14 +359,21 @@ struct Staging {
     cudaEvent_t ev = nullptr;
 };
 
+// staging streams and event per host thread and device: concurrent host-
+// buffer probes from two threads never share an event, and the streams
+// belong to the device they stage for (a host-buffer probe returns after its
+// staging streams drained, so one thread's calls never overlap)
 static Staging& staging() {
-    static Staging S;
-    static std::once_flag once;
-    std::call_once(once, [] {
+    static thread_local std::vector<Staging> per_dev;
+    int dev = 0;
+    SG_CUDA(cudaGetDevice(&dev));
+    if ((int)per_dev.size() <= dev) per_dev.resize(dev + 1);
+    Staging& S = per_dev[dev];
+    if (!S.ev) {
         SG_CUDA(cudaStreamCreateWithFlags(&S.st[0], cudaStreamNonBlocking));
         SG_CUDA(cudaStreamCreateWithFlags(&S.st[1], cudaStreamNonBlocking));
         SG_CUDA(cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming));
-    });
+    }
     return S;
 }
 

@@ -158,7 +158,8 @@ __global__ void k_rl_scatter(int64_t n, const T* __restrict__ pos, const int32_t
                              T* __restrict__ spos) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || key[i] < 0) return;
-    const int32_t slot = start[key[i]] + atomicAdd(cursor + key[i], 1);
+    // slots < n < 2^31 (sg_relax checks); the x3 offsets in 64 bit
+    const int64_t slot = start[key[i]] + atomicAdd(cursor + key[i], 1);
     spos[3 * slot] = pos[3 * i];
     spos[3 * slot + 1] = pos[3 * i + 1];
     spos[3 * slot + 2] = pos[3 * i + 2];
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(256) k_rl_force(GridC gc, RelaxC r, int64_t n,
                 if (xx < 0 || xx >= r.nc[0]) continue;
                 const int64_t cc = ((int64_t)z * r.nc[1] + y) * r.nc[0] + xx;
                 const int32_t s0 = start[cc], s1 = s0 + cnt[cc];
-                for (int32_t jj = s0; jj < s1; ++jj) {
+                for (int64_t jj = s0; jj < s1; ++jj) {
                     const T ex = xi - spos[3 * jj], ey = yi - spos[3 * jj + 1],
                             ez = zi - spos[3 * jj + 2];
                     const T d2 = ex * ex + ey * ey + ez * ez;
@@ -340,6 +341,8 @@ extern "C" sg_status sg_relax(sg_grid* g, int64_t n, void* pos, const sg_relax_p
     return guard([&] {
         SG_ARG(g != nullptr && p != nullptr, "sg_relax: null argument");
         SG_ARG(n >= 0 && (n == 0 || pos != nullptr), "sg_relax: bad particle buffer");
+        // cell-list slots and prefix sums are int32
+        SG_ARG(n < (1LL << 31), "sg_relax: at most 2^31 - 1 particles per call");
         SG_ARG(p->dp > 0.0 && p->h_ratio >= 0.5 && p->h_ratio <= 2.0 && p->steps >= 0 &&
                    p->max_disp >= 0.0 && p->surface_offset >= 0.0,
                "sg_relax: bad parameters");

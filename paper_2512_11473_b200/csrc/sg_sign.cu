@@ -85,12 +85,7 @@ __device__ __forceinline__ void raise_flag(bool changed, int* cur) {
 
 // persistent grid: a few resident blocks per SM, grid-stride loops
 static unsigned sweep_blocks(int64_t items) {
-    static int sms = [] {
-        int d = 0, n = 148;
-        if (cudaGetDevice(&d) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-        return n;
-    }();
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), 8LL * sms));
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), 8LL * sm_count()));
 }
 
 // ------------------------------------------------------------- coarse ----

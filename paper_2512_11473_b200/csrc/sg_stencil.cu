@@ -321,12 +321,8 @@ struct ReinitOp {
 // grid size of a persistent sweep: resident blocks, at most the work
 template <class K>
 static unsigned persistent_blocks(K kernel, int64_t packages) {
-    int dev = 0, sms = 0, per = 0;
-    SG_CUDA(cudaGetDevice(&dev));
-    SG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 256, 0));
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(packages * 8, 256),
-                                                            (int64_t)sms * std::max(per, 1)));
+    return (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(packages * 8, 256), resident_blocks((const void*)kernel, 256)));
 }
 
 // K6 -- gradient by Lst. 5 with the arithmetic-mean regulariser, divided by
@@ -737,9 +733,7 @@ static void reinit_launch(sg_grid* g, int cur, const StC<T>& c, int64_t lo, int6
                           cudaStream_t s) {
     if (hi <= lo) return;
     const ReinitOp<T> op{(T*)g->phi[1 - cur], c};
-    static unsigned blocks_max = 0;  // resident blocks (per instantiation)
-    if (!blocks_max) blocks_max = persistent_blocks(k_sweep<T, ReinitOp<T>>, 1 << 30);
-    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div((hi - lo) * 8, 256), blocks_max);
+    const unsigned blocks = persistent_blocks(k_sweep<T, ReinitOp<T>>, hi - lo);
     k_sweep<T, ReinitOp<T>><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], g->face, (uint32_t)lo,
                                                    (uint32_t)hi, op);
 }
@@ -754,17 +748,20 @@ struct GraphKey {
     const void* p1;
     const void* nb;
     int64_t lo, hi;
-    int32_t iters, dt;
-    double cfl;
+    int32_t iters, dt, device;
+    double cfl, dx;  // the captured StC (inv_dx, dx^2, cfl dx) derives from both
     bool operator==(const GraphKey& o) const {
         return p0 == o.p0 && p1 == o.p1 && nb == o.nb && lo == o.lo && hi == o.hi &&
-               iters == o.iters && dt == o.dt && cfl == o.cfl;
+               iters == o.iters && dt == o.dt && device == o.device && cfl == o.cfl &&
+               dx == o.dx;
     }
 };
 
 static std::mutex g_graph_mu;
 static std::vector<std::pair<GraphKey, cudaGraphExec_t>> g_graphs;  // small LRU
-static cudaStream_t g_capture = nullptr;
+// capture streams, one per device (a stream belongs to the device current at
+// its creation)
+static std::vector<cudaStream_t> g_capture;
 
 template <class T>
 static void reinit_t(sg_grid* g, int32_t iters, double cfl, bool halo, cudaStream_t s) {
@@ -781,8 +778,10 @@ static void reinit_t(sg_grid* g, int32_t iters, double cfl, bool halo, cudaStrea
         }
         return;
     }
+    int dev = 0;
+    SG_CUDA(cudaGetDevice(&dev));
     const GraphKey key{g->phi[g->cur], g->phi[1 - g->cur], g->face, lo, hi, iters,
-                       (int32_t)sizeof(T), cfl};
+                       (int32_t)sizeof(T), dev, cfl, g->gc.dx};
     std::lock_guard<std::mutex> lk(g_graph_mu);
     cudaGraphExec_t exec = nullptr;
     for (size_t i = 0; i < g_graphs.size(); ++i)
@@ -792,15 +791,17 @@ static void reinit_t(sg_grid* g, int32_t iters, double cfl, bool halo, cudaStrea
             break;
         }
     if (!exec) {
-        if (!g_capture) SG_CUDA(cudaStreamCreateWithFlags(&g_capture, cudaStreamNonBlocking));
+        if ((int)g_capture.size() <= dev) g_capture.resize(dev + 1, nullptr);
+        cudaStream_t& cap = g_capture[dev];
+        if (!cap) SG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
         cudaGraph_t graph;
-        SG_CUDA(cudaStreamBeginCapture(g_capture, cudaStreamCaptureModeThreadLocal));
+        SG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         int cur = g->cur;
         for (int it = 0; it < iters; ++it) {
-            reinit_launch<T>(g, cur, c, lo, hi, g_capture);
+            reinit_launch<T>(g, cur, c, lo, hi, cap);
             cur = 1 - cur;
         }
-        SG_CUDA(cudaStreamEndCapture(g_capture, &graph));
+        SG_CUDA(cudaStreamEndCapture(cap, &graph));
         SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
         SG_CUDA(cudaGraphDestroy(graph));
         if (g_graphs.size() >= 32) {
@@ -944,12 +945,16 @@ void launch_gradient(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t s
 template <class T>
 static void table1_t(sg_grid* g, int32_t op, double value, cudaStream_t s) {
     const int64_t lo = g->own_lo, hi = g->own_hi;
-    if (hi <= lo) return;
     if (op == 0) {
+        // the add is pointwise: on a slab grid it covers the ghost packages
+        // too, which then hold exactly what their owner computes
+        const int64_t lo = 2, hi = g->n_pkg;
+        if (hi <= lo) return;
         const int64_t n4 = (hi - lo) * 16;
         k_add<T><<<(unsigned)ceil_div(n4, 256), 256, 0, s>>>((T*)g->phi[g->cur], n4, lo * 16,
                                                             (T)value);
     } else {
+        if (hi <= lo) return;
         const unsigned blocks = (unsigned)ceil_div((hi - lo) * 16, 256);
         k_laplace<T><<<blocks, 256, 0, s>>>((const T*)g->phi[g->cur], (T*)g->phi[1 - g->cur],
                                             g->face, lo, hi, (T)(1.0 / (g->gc.dx * g->gc.dx)));
@@ -1007,5 +1012,7 @@ extern "C" sg_status sg_table1(sg_grid* g, int32_t op, double value, void* strea
         SG_ARG(op == 0 || op == 1, "sg_table1: op must be 0 (sequential) or 1 (stencil)");
         SG_CUDA(cudaGetLastError());
         launch_table1(g, op, value, (cudaStream_t)stream);
+        // op 0 changes phi: grad / normal / K / G describe the old field
+        if (op == 0) g->has_grad = g->has_normal = g->has_kint = false;
     });
 }

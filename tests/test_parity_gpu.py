@@ -584,3 +584,103 @@ def test_probe_unaligned_buffers(sgm, O):
     b_grad = torch.empty((pos.shape[0] + 1, 3), dtype=pos.dtype, device="cuda")[1:]
     sgm.sg_probe(g.handle, pos.shape[0], un.data_ptr(), b_phi.data_ptr(), b_grad.data_ptr())
     assert torch.equal(a_phi, b_phi) and torch.equal(a_grad, b_grad)
+
+
+# ------------------------------------------------ edge cases (round 2) ----
+
+LOWFACE = W.Workload("lowface", (16, 16, 16), 1.0 / 16, dtype="f32",
+                     prims=(W.Prim(W.SPHERE, (0.1, 0.45, 0.55, 0.2)),))
+
+
+def _lowface_positions(w, n=40000, seed=4):
+    """Positions with x in [0, dx/4) (the fp32 fast path's u = x/dx - 1/2 is
+    rounded there) inside the band near the lower x face, plus x = 0 exactly
+    and tiny x."""
+    rng = np.random.default_rng(seed)
+    dx = w.cell / 4
+    pos = np.empty((n, 3))
+    pos[:, 0] = rng.uniform(0.0, 0.25 * dx, n)
+    pos[:, 1] = rng.uniform(0.3, 0.6, n)
+    pos[:, 2] = rng.uniform(0.4, 0.7, n)
+    pos[:50, 0] = 0.0
+    pos[50:100, 0] = np.ldexp(1.0, -rng.integers(20, 120, 50))
+    return pos.astype(np.float32)
+
+
+def test_probe_lower_face_fp32(sgm, O):
+    """fp32 dyadic grid whose band touches the lower x face (out-of-domain
+    neighbours by sign, R-6), particles at x < dx/4: against the oracle, and
+    the exact fp32 index path against the fp64 index path bit for bit (the
+    latter in a fresh process with SG_PROBE_IDX32=0)."""
+    w = LOWFACE
+    pos = _lowface_positions(w)
+    g, o, tpos, gphi, ggrad = _probe_compare(sgm, O, w, pos, phi_iters=2)
+    assert (np.abs(gphi) < o.far).mean() > 0.5  # in the band
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tmp = os.path.join(root, "gpurun_out", "lowface_idx64.npz")
+    os.makedirs(os.path.dirname(tmp), exist_ok=True)
+    code = (
+        "import numpy as np, torch, sys\n"
+        "sys.path.insert(0, 'tests')\n"
+        "from test_parity_gpu import LOWFACE, _lowface_positions\n"
+        "from paper_2512_11473_b200 import sg\n"
+        "g = sg.Grid(LOWFACE); g.reinit(2).gradient(sg.SG_GRAD)\n"
+        "p, gr = g.probe(torch.from_numpy(_lowface_positions(LOWFACE)).cuda())\n"
+        f"np.savez({tmp!r}, phi=p.cpu().numpy(), grad=gr.cpu().numpy())\n")
+    env = dict(os.environ, SG_PROBE_IDX32="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    ref = np.load(tmp)
+    g2 = sgm.Grid(w)
+    g2.reinit(2).gradient(sgm.SG_GRAD)
+    a_phi, a_grad = g2.probe(tpos)
+    assert np.array_equal(a_phi.cpu().numpy(), ref["phi"])
+    assert np.array_equal(a_grad.cpu().numpy(), ref["grad"])
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_reinit_phi_exactly_zero(sgm, O, dtype):
+    """O7's stationary case: an active point with phi = 0 exactly stays 0 and
+    its neighbours update as the definition says."""
+    w = W.config("C1").with_(dtype=dtype)
+    o = O.Oracle(w)
+    t = o.build_tables()
+    phi = o.reinit(o.phi_dense(), 3).astype(np_dtype(w)).astype(np.float64)
+    rng = np.random.default_rng(2)
+    band = np.argwhere(np.abs(phi) < 1.5 * w.dx)
+    pick = band[rng.choice(band.shape[0], 200, replace=False)]
+    phi[pick[:, 0], pick[:, 1], pick[:, 2]] = 0.0
+    g = sgm.Grid(w)
+    _upload(g, w, o.to_packages(phi, -o.far, o.far))
+    g.reinit(1)
+    got = g.view("phi").cpu().numpy().astype(np.float64)
+    exp = o.to_packages(o.reinit_step(phi), -o.far, o.far)
+    assert_phi_close(w, got, exp, "phi = 0 step")
+    cells = (pick[:, 2] // 4) + w.n[0] * ((pick[:, 1] // 4) + w.n[1] * (pick[:, 0] // 4))
+    ids = t.bg[cells]
+    ds = (pick[:, 2] % 4) + 4 * (pick[:, 1] % 4) + 16 * (pick[:, 0] % 4)
+    assert np.all(got[ids, ds] == 0.0)
+
+
+def test_table1_add_invalidates_derived_fields(sgm):
+    """sg_table1 op 0 changes phi in place: grad / normal / K / G are stale
+    afterwards (probing grad is a state error until sg_gradient runs again)."""
+    w = W.config("C1")
+    g = sgm.Grid(w)
+    g.reinit(2).gradient(sgm.SG_GRAD | sgm.SG_NORMAL | sgm.SG_KINT)
+    assert g.info["has_grad"] and g.info["has_kint"]
+    g.table1(0, 0.5 * w.dx)
+    info = g.info
+    assert not info["has_grad"] and not info["has_normal"] and not info["has_kint"]
+    pos = torch.tensor([[0.5, 0.5, 0.21]], dtype=torch.float64, device="cuda")
+    with pytest.raises(sgm.SgError) as e:
+        g.probe(pos, want_grad=True)
+    assert e.value.status == sgm.SG_ERR_STATE
+    phi, _ = g.probe(pos, want_grad=False)
+    g.gradient(sgm.SG_GRAD)
+    phi2, _ = g.probe(pos)
+    assert torch.equal(phi, phi2)
