@@ -56,6 +56,26 @@ REINIT_ITERS = 20
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
+def SWEEP_BYTES_SURVEY(esz):
+    """SURVEY 8(d) algorithmic bytes per point of a reinit sweep: phi in +
+    phi out + the package's 108 B neighbour row over its 64 points."""
+    return 2 * esz + 108 / 64
+
+
+def SWEEP_BYTES_FACE(esz):
+    """what k_sweep actually needs: phi in + out + the 32 B face row (the six
+    face slots of the neighbour row)"""
+    return 2 * esz + 32 / 64
+
+
+def profile_json(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -75,6 +95,8 @@ def parse():
                         "call, K6 and K7 in one kernel)")
     p.add_argument("--slab", action="store_true",
                    help="z-slab path (NCCL) even at one rank (exercises the multi-GPU code)")
+    p.add_argument("--no-c3-anchor", action="store_true",
+                   help="skip the C3 sub-record (the HBM-bound reinit anchor)")
     return p.parse_args()
 
 
@@ -238,22 +260,37 @@ def kernel_rooflines(sg, w, stream, flush, d_pos, n_part, probe_ms, reinit_ms, h
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     fma_peak = sms * 128 * clock_ghz * 1e9  # FP32 FMA lanes x clock (B200_PROFILING.md units)
 
-    def hbm_entry(name, bytes_, ms, note):
+    def hbm_entry(name, bytes_, ms, note, layout_bytes=None):
         a = bytes_ / (ms * 1e-3) / 1e9
-        return {"kernel": name, "bound": "hbm", "us": ms * 1e3, "alg_bytes": bytes_,
-                "achieved": a, "unit": "GB/s", "peak": hbm, "frac": a / hbm,
-                "frac_nominal_8tbs": a / 8000.0, "note": note}
+        e = {"kernel": name, "bound": "hbm", "us": ms * 1e3, "alg_bytes": bytes_,
+             "achieved": a, "unit": "GB/s", "peak": hbm, "frac": a / hbm,
+             "frac_nominal_8tbs": a / 8000.0, "note": note}
+        if layout_bytes:
+            al = layout_bytes / (ms * 1e-3) / 1e9
+            e.update({"layout_bytes": layout_bytes, "achieved_layout": al, "frac_layout": al / hbm})
+        return e
 
-    out = [hbm_entry("k_sweep (reinit, per sweep)", (2 * esz + 32 / 64) * n_act, reinit_ms,
-                     "phi in + out + 32 B face row per package")]
-    out.append(hbm_entry("k_gradient (grad + normal)", (esz + 32 / 64 + 7 * esz) * n_act, t_grad,
-                         "phi + face row in; (phi, grad) interleaved + normal out"))
+    out = [hbm_entry("k_sweep (reinit, per sweep)", SWEEP_BYTES_SURVEY(esz) * n_act, reinit_ms,
+                     "SURVEY 8(d): phi in + out + 108 B neighbour row per package; layout: the "
+                     "32 B face row the kernel reads", SWEEP_BYTES_FACE(esz) * n_act)]
+    out.append(hbm_entry("k_gradient (grad + normal)", (4 * esz + 108 / 64 + 3 * esz) * n_act, t_grad,
+                         "SURVEY 8(d): b + 3b + 1.69 + 12 (normals) per point; layout: phi + face "
+                         "row in, (phi, grad) interleaved (16 B) + normal out",
+                         (esz + 32 / 64 + 7 * esz) * n_act))
     fmas = 324.0 * n_act  # 81 taps x (K, Gx, Gy, Gz), direct form
-    out.append({"kernel": "k_kint (kernel integrals)", "bound": "alu", "us": t_kint * 1e3,
-                "alg_fma": fmas, "achieved": fmas / (t_kint * 1e-3) / 1e12, "unit": "TFMA/s",
-                "peak": fma_peak / 1e12, "frac": fmas / (t_kint * 1e-3) / fma_peak,
-                "note": "direct-form FMAs (the kernel executes ~1.8x fewer); peak = SMs x "
-                        "128 FP32 lanes x max SM clock"})
+    ke = {"kernel": "k_kint (kernel integrals)", "bound": "alu", "us": t_kint * 1e3,
+          "alg_fma": fmas, "achieved": fmas / (t_kint * 1e-3) / 1e12, "unit": "TFMA/s",
+          "peak": fma_peak / 1e12, "frac": fmas / (t_kint * 1e-3) / fma_peak,
+          "note": "direct-form FMAs (the kernel executes fewer: sign butterfly, closed form on "
+                  "uniform packages); peak = SMs x 128 FP32 lanes x max SM clock"}
+    fl = (profile_json("ncu_flops.json") or {}).get(w.name, {}).get("k_kint")
+    if fl:
+        # executed FP32 FMA-pipe work counted by ncu (FFMA + FADD + FMUL thread
+        # instructions per launch) over this run's kernel time
+        ex = fl["ffma"] + fl["fadd"] + fl["fmul"]
+        ke.update({"executed_fp32_ops": ex, "executed_frac": ex / (t_kint * 1e-3) / fma_peak,
+                   "executed_source": "profiles/ncu_flops.json"})
+    out.append(ke)
     out.append({"kernel": "k_kint<..., K6 fused> (gradient + normal + kernel integrals)",
                 "bound": "alu", "us": t_both * 1e3,
                 "note": "one kernel: K6 warps beside K7 warps; compare with the two above"})
@@ -280,6 +317,23 @@ def kernel_rooflines(sg, w, stream, flush, d_pos, n_part, probe_ms, reinit_ms, h
                              f"32 B per probe + {touched} touched packages x "
                              f"({64 * 4 * esz} B + 108 B nb row)"))
     g.close()
+    # build kernels: fp64 ALU rooflines from ncu counts of the same launch
+    # (profiles/ncu_flops.json: thread-level DFMA/DADD/DMUL and the kernel's
+    # ncu duration, cold cache and serialised -- a share, not a step time)
+    alu = profile_json("alu_peaks.json") or {}
+    fp64_peak = alu.get("fp64_tflops") or sms * 64 * 2 * clock_ghz / 1e3
+    for name, fl in sorted(((profile_json("ncu_flops.json") or {}).get(w.name) or {}).items()):
+        if not name.startswith(("k_phi_init", "k_tag")):
+            continue
+        dflop = 2 * fl["dfma"] + fl["dadd"] + fl["dmul"]
+        a = dflop / (fl["us"] * 1e-6) / 1e12
+        out.append({"kernel": name, "bound": "alu", "us": fl["us"], "dflop": dflop,
+                    "achieved": a, "unit": "TFLOP/s (fp64)", "peak": fp64_peak,
+                    "frac": a / fp64_peak,
+                    "peak_source": "profiles/alu_peaks.json (measured DFMA chain)" if
+                    alu.get("fp64_tflops") else "SMs x 64 FP64 lanes x 2 x max SM clock",
+                    "note": "executed fp64 flops (2 DFMA + DADD + DMUL) from ncu over the ncu "
+                            "kernel time"})
     return out
 
 
@@ -379,7 +433,7 @@ def run_ours(args, rank, world, local):
     st = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(4)]
                    for k in range(args.steps)])  # ms per stage
     step_ms = st.sum(1)
-    ms = float(step_ms.mean())
+    ms = float(np.median(step_ms))  # median over the timed steps
     n_pkg = info["n_pkg"]
     n_act = (n_pkg - 2) * 64
     updates = n_act * (REINIT_ITERS + 1)
@@ -403,23 +457,25 @@ def run_ours(args, rank, world, local):
             step(ev, (hp, hphi, hgrad))
             torch.cuda.synchronize()
             e_ms.append(ev[0].elapsed_time(ev[4]))
-        e_ms = float(np.mean(e_ms))
+        e_ms = float(np.median(e_ms))
         e2e = {"value": updates / (e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(hp.numel() * hp.element_size()),
                "d2h_bytes_per_step": int((hphi.numel() + hgrad.numel()) * hphi.element_size()),
                "ms_per_step": e_ms, "probes_per_s": n_part / (e_ms * 1e-3)}
 
-    # roofline of the dominant kernel (k_reinit: 20 launches per step)
+    # roofline of the dominant kernel (k_sweep: 20 launches per step)
     esz = 4 if w.dtype == "f32" else 8
-    reinit_ms = float(st[:, 1].mean()) / REINIT_ITERS
-    # read + write phi, the package's 32 B face-table row (SURVEY 8(d) counts the
-    # 108 B neighbour row; the sweep reads the compact face table instead)
-    bytes_per_cell = 2 * esz + 32 / 64
+    reinit_ms = float(np.median(st[:, 1])) / REINIT_ITERS
+    # algorithmic bytes: SURVEY 8(d)'s 2b + 108/64 per point (phi in/out, the
+    # neighbour row); the kernel itself reads the 32 B face row (8.5 B at
+    # fp32), reported beside it
+    bytes_per_cell = SWEEP_BYTES_SURVEY(esz)
     alg_bytes = bytes_per_cell * n_act
     hbm, peak_src = peaks()
     achieved = alg_bytes / (reinit_ms * 1e-3) / 1e9
+    achieved_face = SWEEP_BYTES_FACE(esz) * n_act / (reinit_ms * 1e-3) / 1e9
     stage_names = ["build", "reinit", "gradient", "probe"]
-    stages = {n: {"ms": float(st[:, i].mean())} for i, n in enumerate(stage_names)}
+    stages = {n: {"ms": float(np.median(st[:, i]))} for i, n in enumerate(stage_names)}
     stages["reinit"]["ms_per_sweep"] = reinit_ms
     stages["reinit"]["cells_per_s"] = n_act / (reinit_ms * 1e-3)
     stages["probe"]["probes_per_s"] = n_part / max(stages["probe"]["ms"] * 1e-3, 1e-12)
@@ -431,11 +487,14 @@ def run_ours(args, rank, world, local):
                                       "second stream from here to the end of the step")
         stages["probe"]["note"] = "probe (if any), concurrent with K7, then the join of K7"
     stages["reinit_plus_gradient_cells_per_s"] = n_act * (REINIT_ITERS + 1) / (
-        (st[:, 1].mean() + st[:, 2].mean()) * 1e-3)
+        (np.median(st[:, 1]) + np.median(st[:, 2])) * 1e-3)
     clocks = clk.summary()
     kernels = None if args.no_kernel_roofline else kernel_rooflines(
-        sg, w, stream, flush, d_pos, n_part, float(st[:, 3].mean()) if n_part else None,
+        sg, w, stream, flush, d_pos, n_part, float(np.median(st[:, 3])) if n_part else None,
         reinit_ms, hbm)
+    c3 = None
+    if not args.no_c3_anchor and w.name != "C3":
+        c3 = c3_anchor(sg, stream, flush, hbm)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -451,12 +510,16 @@ def run_ours(args, rank, world, local):
         "roofline": {"kernel": "k_sweep<float, ReinitOp<float>> (reinit sweep)", "bound": "hbm", "achieved": achieved,
                      "peak": hbm, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "bytes_per_cell": bytes_per_cell, "cells_per_launch": n_act,
+                     "bytes_definition": "SURVEY 8(d): 2b + 108/64 per active point",
+                     "achieved_face_bytes": achieved_face, "frac_face_bytes": achieved_face / hbm,
+                     "bytes_per_cell_face": SWEEP_BYTES_FACE(esz),
                      "peak_nominal": 8000.0, "frac_nominal": achieved / 8000.0,
                      "traffic": ncu_traffic("k_sweep", w.name),
-                     "note": (f"working set per sweep {alg_bytes / 1e6:.0f} MB (phi in + out "
-                              "+ face rows); warm-cache ncu shows the double-buffered sweep "
-                              "streaming most of it from HBM even below the 126 MB L2 "
-                              "(profiles/README.md)")},
+                     "note": (f"algorithmic bytes per sweep {alg_bytes / 1e6:.0f} MB; on C2 the "
+                              "double-buffered working set is below the 126 MB L2 and ncu's DRAM "
+                              "bytes per sweep (traffic) are about half of it, so this is not an "
+                              "HBM number -- the HBM anchor is c3_anchor (profiles/README.md)")},
+        "c3_anchor": c3,
         "clocks": clocks,
         "kernels": kernels,
         "gpu_name": torch.cuda.get_device_name(local),
@@ -464,6 +527,45 @@ def run_ours(args, rank, world, local):
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(w, n_act)
     print(json.dumps(out), flush=True)
+
+
+def c3_anchor(sg, stream, flush, hbm, steps=5, warmup=2):
+    """C3 (2048^3 effective, 103.9 M active points, 847 MB of DRAM per sweep
+    in ncu): the configuration whose reinit sweep streams from HBM -- the
+    roofline anchor beside the headline C2 line.  Build + 20 sweeps per step,
+    CUDA events on the step's stream, median over the steps."""
+    import torch
+    w = W.config("C3")
+    esz = 4
+    ts = []
+    for k in range(warmup + steps):
+        flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        g = sg.Grid(w, stream=stream)
+        ev[1].record(stream)
+        g.reinit(REINIT_ITERS, w.cfl, stream=stream)
+        ev[2].record(stream)
+        torch.cuda.synchronize()
+        n_act = (g.info["n_pkg"] - 2) * 64
+        g.close_async(stream)
+        if k >= warmup:
+            ts.append((ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])))
+    ts = np.array(ts)
+    sweep_ms = float(np.median(ts[:, 1])) / REINIT_ITERS
+    a = SWEEP_BYTES_SURVEY(esz) * n_act / (sweep_ms * 1e-3) / 1e9
+    af = SWEEP_BYTES_FACE(esz) * n_act / (sweep_ms * 1e-3) / 1e9
+    tr = ncu_traffic("k_sweep", "C3")
+    return {"workload": "C3: torus+box union 2048^3 effective (512^3 cells x 4^3), f32, "
+                        "build + reinit 20", "active_cells": n_act, "steps": steps,
+            "build_ms": float(np.median(ts[:, 0])), "sweep_us": sweep_ms * 1e3,
+            "cells_per_s": n_act / (sweep_ms * 1e-3),
+            "roofline": {"kernel": "k_sweep<float>", "bound": "hbm", "achieved": a, "peak": hbm,
+                         "unit": "GB/s", "frac": a / hbm, "bytes_per_cell": SWEEP_BYTES_SURVEY(esz),
+                         "achieved_face_bytes": af, "frac_face_bytes": af / hbm,
+                         "frac_nominal": a / 8000.0, "traffic": tr,
+                         "traffic_per_cell": tr / n_act if tr else None,
+                         "dram_achieved": tr / (sweep_ms * 1e-3) / 1e9 if tr else None}}
 
 
 # ------------------------------------------------------ oracle timing ------
@@ -504,12 +606,52 @@ def oracle_sample(w, budget_s: float = 12.0):
                               "sample": f"1 reinit sweep on one thread, {dt1:.1f} s"}}
 
 
+def oracle_window_sample(name="C3", planes=8, budget_s=8.0):
+    """The oracle on a z-window of a configuration whose dense grid does not
+    fit (C3: 69 GB per fp64 field): `planes` background planes around the
+    heaviest plane plus a margin of ceil(20/4) + 1 planes per side, the whole
+    x-y extent; reinit sweeps timed, throughput per active
+    point of the box (every one is updated by each sweep)."""
+    from oracle import oracle as O
+    O.build()
+    threads = len(os.sched_getaffinity(0))
+    O.set_threads(threads)
+    w = W.config(name)
+    full = O.Oracle(w)
+    t = full.build_tables()
+    zc = int(np.argmax(t.plane_count))
+    margin = -(-REINIT_ITERS // 4) + 1
+    z0 = max(0, zc - planes // 2 - margin)
+    z1 = min(w.n[2], z0 + planes + 2 * margin)
+    o = O.Oracle(w, ((0, 0, z0), (w.n[0], w.n[1], z1)))
+    o.tables = t
+    phi = o.phi_dense()
+    n_act = int(t.plane_count[z0:z1].sum()) * 64
+    sweeps, t0 = 0, time.perf_counter()
+    while True:
+        phi = o.reinit_step(phi, w.cfl)
+        sweeps += 1
+        if time.perf_counter() - t0 > budget_s or sweeps >= REINIT_ITERS:
+            break
+    dt = time.perf_counter() - t0
+    return {"config": name, "value": n_act * sweeps / dt, "unit": UNIT, "cores": O.get_threads(),
+            "sample": f"{sweeps} reinit sweeps of the dense fp64 oracle on the z-window "
+                      f"[{z0}, {z1}) of {name} (heaviest plane {zc}, {planes} planes + "
+                      f"{margin}-plane margins, whole x-y extent; {n_act} active points); "
+                      f"tables and initial phi untimed; {dt:.1f} s"}
+
+
 def cpu_baseline(w, n_act):
     try:
-        return oracle_sample(w)
+        out = oracle_sample(w)
     except Exception as e:  # never fail the bench line on the baseline
         return {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
                 "sample": f"failed: {e}"}
+    try:
+        out["windows"] = [oracle_window_sample("C3")]
+    except Exception as e:
+        out["windows"] = [{"config": "C3", "value": None, "sample": f"failed: {e}"}]
+    return out
 
 
 def run_reference(args, rank, world):

@@ -30,8 +30,11 @@
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *     stream).  Calls are stream-ordered and asynchronous unless noted.
  *   - Device pointers are plain CUDA device addresses of the current device.
- *   - The grid handle owns all its device memory (allocated stream-ordered
- *     from the device's default memory pool) and frees it in sg_destroy.
+ *   - The grid handle owns all its device memory and frees it in
+ *     sg_destroy: allocated through the caller's sg_allocator (sg_build_ex),
+ *     else stream-ordered from the library's own memory pool on the device
+ *     (a pool separate from the device's default pool; sg_pool_trim returns
+ *     its free memory).  Call-scoped scratch always comes from that pool.
  *   - Argument errors are reported before any launch (SG_ERR_ARG); CUDA
  *     errors, including asynchronous ones from earlier launches, surface as
  *     SG_ERR_CUDA at the next call that checks.
@@ -48,7 +51,7 @@
 extern "C" {
 #endif
 
-#define SG_ABI_VERSION 2
+#define SG_ABI_VERSION 3
 #define SG_PKG 4        /* package subdivision, "default by 4"        */
 #define SG_MAX_PRIMS 16 /* primitives per geometry                          */
 
@@ -57,7 +60,7 @@ typedef enum {
     SG_ERR_ARG = 1,    /* invalid argument (null pointer, pkg != 4, n <= 0, ...) */
     SG_ERR_OOM = 2,    /* device allocation failed                             */
     SG_ERR_CUDA = 3,   /* CUDA runtime error (incl. no device)                 */
-    SG_ERR_NCCL = 4,   /* reserved for the multi-GPU communicator              */
+    SG_ERR_NCCL = 4,   /* multi-GPU communicator (NCCL missing or a call failed) */
     SG_ERR_STATE = 5,  /* wrong call order, e.g. probing grad before sg_gradient */
     SG_ERR_DOMAIN = 6  /* slab / domain inconsistency                           */
 } sg_status;
@@ -152,6 +155,37 @@ typedef struct {
 
 typedef struct sg_grid sg_grid;
 
+/* ------------------------------------------------- multi-GPU --
+ * The paper runs on one device (SYCL); BASELINE north_star
+ * partitions the packages over the GPUs of one node in z-slabs of the
+ * background grid ("NCCL halo exchange of boundary packages over NVLink each
+ * reinitialization iteration and particles binned to their owning rank").
+ * A communicator joins one process (one GPU) per rank.  A grid built with a
+ * communicator (sg_build_ex) is partitioned: the build all-gathers per-plane
+ * package counts and cuts balanced slabs (sg_slab_plan); sg_reinit,
+ * sg_gradient and sg_probe then exchange what the slab needs themselves.
+ * Every call on such a grid is collective: all ranks call it, in the same
+ * order, with the same scalar arguments.  Results equal the single-GPU grid's
+ * bit for bit (Jacobi sweeps are order independent; ghosts hold the owner's
+ * values). */
+typedef struct sg_comm sg_comm;
+
+#define SG_COMM_ID_BYTES 128 /* an NCCL unique id */
+#define SG_MAX_RANKS 64
+
+enum { SG_COMM_NCCL = 0, SG_COMM_LOCAL = 1 };
+
+/* Allocator of the grid's device memory.  alloc returns `bytes` of device
+ * memory of the current device usable on `stream` (NULL on failure ->
+ * SG_ERR_OOM); free releases it (the library calls it once per allocation,
+ * stream-ordered on the stream of sg_destroy_async, or after a device
+ * synchronisation in sg_destroy).  ctx is passed through. */
+typedef struct {
+    void* (*alloc)(size_t bytes, void* stream, void* ctx);
+    void (*free)(void* ptr, size_t bytes, void* stream, void* ctx);
+    void* ctx;
+} sg_allocator;
+
 /* sg_gradient field selection */
 enum {
     SG_GRAD = 1,   /* grad phi by central difference (Lst. 5)   */
@@ -211,9 +245,82 @@ typedef struct {
     int64_t device_bytes; /* bytes held by the grid                            */
     int64_t own_lo;       /* owned local package ids [own_lo, own_hi); ghost   */
     int64_t own_hi;       /* packages are [2, own_lo) and [own_hi, n_pkg)      */
+    int32_t rank;         /* communicator rank / size (0 / 1 without one)      */
+    int32_t nranks;
 } sg_info_t;
 
+/* The z-slab plan of one rank (host only).  Local ids: 0, 1 singular, then
+ * the stored packages in global id order (global id = local - 2 + id_base).
+ * Halo ranges are local id ranges [a, b) of whole background planes:
+ *   send_lo = first owned plane (-> rank - 1), send_hi = last owned plane
+ *   (-> rank + 1), recv_lo = ghost plane below (<- rank - 1), recv_hi = ghost
+ *   plane above (<- rank + 1); (0, 0) where there is no such neighbour. */
+typedef struct {
+    int32_t z_lo, z_hi;    /* owned planes                                   */
+    int32_t zs_lo, zs_hi;  /* stored planes (owned + one ghost plane per side) */
+    int64_t id_base;       /* global id of local id 2                         */
+    int64_t n_pkg;         /* stored packages + 2                             */
+    int64_t own_lo, own_hi;
+    int64_t send_lo[2], send_hi[2], recv_lo[2], recv_hi[2];
+} sg_plan_t;
+
 /* ---------------------------------------------------------------- calls -- */
+
+/* A fresh communicator id (SG_COMM_ID_BYTES bytes): rank 0 creates it and
+ * sends it to every rank (e.g. torch.distributed.broadcast_object_list).
+ * NCCL is loaded at run time (dlopen "libnccl.so.2"; a copy the process
+ * already loaded -- PyTorch's -- is reused).  SG_ERR_NCCL if unavailable. */
+sg_status sg_comm_unique_id(void* id);
+
+/* Collective over `nranks` processes: rank `rank` joins the NCCL
+ * communicator of `id` on the current device (NVLink / NVSwitch transport
+ * within the node).  0 <= rank < nranks <= SG_MAX_RANKS. */
+sg_status sg_comm_create(const void* id, int32_t rank, int32_t nranks, sg_comm** out);
+
+/* An in-process group of nranks communicators on the current device,
+ * written to comms[0 .. nranks).  Ranks exchange by device-to-device copies
+ * with the NCCL communicator's semantics (stream-ordered grouped send/recv,
+ * all-gather); each rank must be driven by its own host thread, since calls
+ * on partitioned grids are collective and block until the peers arrive.
+ * Emulates P slabs on one GPU (tests); every multi-GPU code path of the
+ * library runs unchanged on it. */
+sg_status sg_comm_create_local(int32_t nranks, sg_comm** comms);
+
+/* rank, size and kind (SG_COMM_NCCL / SG_COMM_LOCAL); outputs may be NULL */
+sg_status sg_comm_info(const sg_comm* comm, int32_t* rank, int32_t* nranks, int32_t* kind);
+
+/* Destroy a communicator (after every grid built on it is destroyed). */
+void sg_comm_destroy(sg_comm* comm);
+
+/* Host-only (no device use): the plan of `rank` among `nranks` from the
+ * per-plane package counts of the whole domain, counts[0 .. nz): cuts as
+ * sg_balanced_cuts (written to cuts[0 .. nranks], may be NULL), stored planes,
+ * global id base, local package count, owned range and halo ranges
+ * (sg_plan_t).  The partitioned build uses exactly this function.
+ * SG_ERR_ARG if nranks < 1, nz < nranks or rank outside [0, nranks). */
+sg_status sg_slab_plan(const int64_t* counts, int32_t nz, int32_t nranks, int32_t rank,
+                       sg_plan_t* plan, int32_t* cuts);
+
+typedef struct {
+    const sg_slab* slab;           /* explicit slab (no comm), NULL = whole domain   */
+    const sg_comm* comm;           /* partition over the communicator's ranks
+                                      (slab must be NULL); NULL = one GPU          */
+    const sg_allocator* allocator; /* grid memory; NULL = the library's pool         */
+} sg_build_opts;
+
+/* sg_build with options (opts may be NULL = sg_build(desc, geom, NULL)).
+ * With a communicator the call is collective: every rank counts the packages
+ * of a uniform range of planes, the counts are all-gathered (one host
+ * synchronisation: it also yields this rank's package count, so the build
+ * itself does not read one back), and the rank builds the slab of
+ * sg_slab_plan with one ghost plane per side.  Mesh geometries are
+ * single-domain only.  Errors as sg_build, SG_ERR_NCCL. */
+sg_status sg_build_ex(const sg_desc* desc, const sg_geometry* geom, const sg_build_opts* opts,
+                      void* stream, sg_grid** out);
+
+/* Return the free memory of the library's pool on the current device to the
+ * system (grid memory in use is kept). */
+sg_status sg_pool_trim(void);
 
 /* Build the sparse grid for `geom` (P:499-526 steps 1-5, single layer):
  *   K1 core tagging at background-cell centres (fp64),
@@ -253,10 +360,17 @@ sg_status sg_build_refined(const sg_grid* parent, const sg_geometry* geom, void*
  * data point (reading R-12; phi' = phi - cfl dx s (|grad phi|_G - 1)),
  * double-buffered; inactive and singular data stay unchanged.  Neighbours
  * across package faces are reached through the neighbour table (Lst. 2).
- * iters >= 0, 0 < cfl <= 0.5.  Asynchronous.  On a slab grid only the owned
- * packages are updated; the caller refreshes the ghost packages of the
- * current buffer (SG_VIEW_PHI, contiguous id ranges, see sg_info) between
- * sweeps, i.e. calls sg_reinit(grid, 1, ...) once per exchange. */
+ * iters >= 0, 0 < cfl <= 0.5.  Asynchronous.  On a slab grid built with an
+ * explicit sg_slab only the owned packages are updated; the caller refreshes
+ * the ghost packages of the current buffer (SG_VIEW_PHI, contiguous id
+ * ranges, see sg_info) between sweeps, i.e. calls sg_reinit(grid, 1, ...)
+ * once per exchange.  On a grid partitioned over a communicator the call is
+ * collective and refreshes the ghosts itself, once per 4 sweeps (the ghost
+ * reuse of sg_reinit_halo): in each group of up to 4 sweeps the first ones
+ * run over owned + ghost packages, the last one updates the two boundary
+ * planes first and sends them (grouped send/recv on an internal stream,
+ * into the neighbours' ghost planes) while it updates the interior
+ * packages. */
 sg_status sg_reinit(sg_grid* grid, int32_t iters, double cfl, void* stream);
 
 /* The same sweeps over every stored package, owned and ghost (a9 with ghost
@@ -271,7 +385,9 @@ sg_status sg_reinit_halo(sg_grid* grid, int32_t iters, double cfl, void* stream)
 
 /* Derived fields from the current phi: any OR of SG_GRAD, SG_NORMAL, SG_KINT.
  * h_ratio = h / dx of the Wendland C2 kernel, in [0.5, 2] (stencil radius
- * <= 3 < 4, so every tap stays in the 27-neighbourhood).  Asynchronous. */
+ * <= 3 < 4, so every tap stays in the 27-neighbourhood).  Asynchronous.
+ * Partitioned grid: collective; the (phi, grad) ghost planes are exchanged
+ * afterwards (probe corners may lie in a ghost plane). */
 sg_status sg_gradient(sg_grid* grid, uint32_t fields, double h_ratio, void* stream);
 
 /* Grid-particle coupling (reading R-15): for each of n positions
@@ -285,7 +401,14 @@ sg_status sg_gradient(sg_grid* grid, uint32_t fields, double h_ratio, void* stre
  * pointers, pinned or pageable (then the call stages them through device
  * buffers in pipelined chunks and returns after the results are in host
  * memory).  grad != NULL requires a prior sg_gradient with SG_GRAD
- * (SG_ERR_STATE otherwise).  n == 0 is a no-op. */
+ * (SG_ERR_STATE otherwise).  n == 0 is a no-op.
+ * Partitioned grid (collective, any n >= 0 per rank): each rank passes its
+ * own particles; K9 bins them to the rank owning their background plane
+ * (stable order; out-of-domain / NaN positions stay and count as OOB), the
+ * per-rank counts are all-gathered (one host synchronisation), positions go
+ * to their owners and results come back with grouped send/recv, and the
+ * results are returned in the caller's order -- bit-identical to a
+ * single-GPU probe. */
 sg_status sg_probe(const sg_grid* grid, int64_t n, const void* pos, void* phi, void* grad,
                    unsigned long long* oob_count, void* stream);
 

@@ -35,6 +35,7 @@ UNITS = {
     "sg_sign.cu": [],
     "sg_clean.cu": [],
     "sg_mesh.cu": ["-fmad=false"],
+    "sg_comm.cu": [],
 }
 
 
@@ -84,7 +85,8 @@ def _build_locked(verbose: bool, ptxas_info: bool) -> str:
         subprocess.check_call(cmd)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"]
+    # NCCL is dlopen'ed at run time (sg_comm.cu): no link-time dependency
+    cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)

@@ -88,21 +88,36 @@ int resident_blocks(const void* kernel, int threads, size_t smem) {
     return r;
 }
 
-static std::once_flag g_pool_once;
+// the library's own stream-ordered pool per device: released memory stays
+// in it (rebuilding a grid every step reuses it) without touching the
+// device's default pool, which other code in the process may use
+static std::mutex g_pool_mu;
+static std::vector<cudaMemPool_t> g_pools;
+
+static cudaMemPool_t lib_pool() {
+    int dev = 0;
+    SG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if ((int)g_pools.size() <= dev) g_pools.resize(dev + 1, nullptr);
+    if (!g_pools[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool;
+        SG_CUDA(cudaMemPoolCreate(&pool, &props));
+        uint64_t thr = UINT64_MAX;
+        SG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        g_pools[dev] = pool;
+    }
+    return g_pools[dev];
+}
 
 void* dalloc(size_t bytes, cudaStream_t s) {
-    std::call_once(g_pool_once, [] {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return;
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    });
     void* p = nullptr;
     if (bytes == 0) bytes = 256;
-    SG_CUDA(cudaMallocAsync(&p, bytes, s));
+    SG_CUDA(cudaMallocFromPoolAsync(&p, bytes, lib_pool(), s));
     return p;
 }
 
@@ -846,13 +861,26 @@ struct BuildGuard {
         for (void* p : tmp) cudaFreeAsync(p, s);
         if (md)
             for (void* p : md->allocs) cudaFreeAsync(p, s);
-        if (g)
-            for (auto& a : g->allocs) cudaFreeAsync(a.first, s);
+        if (g) {
+            for (auto& a : g->allocs) {
+                if (g->has_allocator)
+                    g->allocator.free(a.first, a.second, (void*)s, g->allocator.ctx);
+                else
+                    cudaFreeAsync(a.first, s);
+            }
+            if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
+            if (g->ev_b) cudaEventDestroy(g->ev_b);
+            if (g->ev_x) cudaEventDestroy(g->ev_x);
+        }
     }
 };
 
+static void plane_counts(const sg_desc* desc, const sg_geometry* geom, int32_t z_lo, int32_t z_hi,
+                         int64_t* counts, cudaStream_t s);
+
 static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_slab* slab,
-                       const sg_grid* parent, void* stream, sg_grid** out) {
+                       const sg_grid* parent, void* stream, sg_grid** out,
+                       const sg_comm* comm = nullptr, const sg_allocator* allocator = nullptr) {
     {
         SG_ARG(out != nullptr, "sg_build: null out");
         *out = nullptr;
@@ -860,7 +888,57 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         const int dev = check_device();
         cudaStream_t s = (cudaStream_t)stream;
         auto g = std::make_unique<sg_grid>();
+        if (allocator) {
+            SG_ARG(allocator->alloc && allocator->free, "sg_build: allocator needs alloc and free");
+            g->has_allocator = true;
+            g->allocator = *allocator;
+        }
         BuildGuard guard_mem{g.get(), s};
+        // partition over a communicator: per-plane counts of a uniform plane
+        // range per rank, all-gathered -- the one host synchronisation of a
+        // partitioned build; the plan then fixes this rank's package count
+        sg_slab comm_slab{};
+        int64_t known_npkg = -1;
+        if (comm) {
+            SG_ARG(slab == nullptr && parent == nullptr, "sg_build: comm excludes slab / parent");
+            SG_ARG(geom->n_tris == 0, "sg_build: mesh geometries are single-domain only");
+            const int P = comm_size(comm), r = comm_rank(comm), nz = desc->n[2];
+            SG_ARG(nz >= P, "sg_build: fewer background planes than ranks");
+            g->comm = comm;
+            g->rank = r;
+            g->nranks = P;
+            g->cuts.assign(P + 1, 0);
+            if (P > 1) {
+                const int maxper = (int)ceil_div(nz, P);
+                int64_t* buf = (int64_t*)dalloc(sizeof(int64_t) * maxper * (P + 1), s);
+                guard_mem.tmp.push_back(buf);
+                const int lo = (int)((int64_t)r * nz / P), hi = (int)((int64_t)(r + 1) * nz / P);
+                SG_CUDA(cudaMemsetAsync(buf, 0, sizeof(int64_t) * maxper, s));
+                plane_counts(desc, geom, lo, hi, buf, s);
+                comm_allgather(comm, buf, buf + maxper, sizeof(int64_t) * maxper, s);
+                std::vector<int64_t> all((size_t)P * maxper), counts(nz);
+                SG_CUDA(cudaMemcpyAsync(all.data(), buf + maxper, sizeof(int64_t) * all.size(),
+                                        cudaMemcpyDeviceToHost, s));
+                SG_CUDA(cudaStreamSynchronize(s));
+                SG_CUDA(cudaFreeAsync(buf, s));
+                guard_mem.tmp.pop_back();
+                for (int q = 0; q < P; ++q) {
+                    const int ql = (int)((int64_t)q * nz / P), qh = (int)((int64_t)(q + 1) * nz / P);
+                    for (int z = ql; z < qh; ++z) counts[z] = all[(size_t)q * maxper + (z - ql)];
+                }
+                slab_plan(counts.data(), nz, P, r, &g->plan, g->cuts.data());
+                comm_slab = sg_slab{g->plan.z_lo, g->plan.z_hi, g->plan.id_base};
+                slab = &comm_slab;
+                known_npkg = g->plan.n_pkg;
+                int lo_prio = 0, hi_prio = 0;
+                SG_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+                SG_CUDA(cudaStreamCreateWithPriority(&g->comm_stream, cudaStreamNonBlocking, hi_prio));
+                SG_CUDA(cudaEventCreateWithFlags(&g->ev_b, cudaEventDisableTiming));
+                SG_CUDA(cudaEventCreateWithFlags(&g->ev_x, cudaEventDisableTiming));
+            } else {
+                g->cuts[1] = nz;
+            }
+        }
         g->desc = *desc;
         g->device = dev;
         g->gc = make_gridc(desc);
@@ -952,9 +1030,18 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         SG_LAUNCHED();
 
         // the single host synchronisation: package count, core count and the
-        // domain-boundary flag in one 24 B copy into pinned memory
-        wait_published(pub, gen, s);
-        const int64_t counts[3] = {(int64_t)pub.host[0], (int64_t)pub.host[1], (int64_t)pub.host[2]};
+        // domain-boundary flag in one 24 B copy into pinned memory.  A
+        // partitioned build knows its count from the all-gathered plane
+        // counts: it enqueues everything first and reads the published
+        // values at the end (they are long done by then), taking the
+        // boundary-safe neighbour kernel since the flag is not known yet.
+        int64_t counts[3] = {known_npkg - 2, 0, 1};
+        if (known_npkg < 0) {
+            wait_published(pub, gen, s);
+            counts[0] = (int64_t)pub.host[0];
+            counts[1] = (int64_t)pub.host[1];
+            counts[2] = (int64_t)pub.host[2];
+        }
         const int64_t n_active = counts[0];
         SG_ARG(n_active + 2 < 4294967295LL, "sg_build: more than 2^32-3 packages");
         g->n_pkg = n_active + 2;
@@ -1050,7 +1137,15 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         g->cur = 0;
 
         // owned id range: whole domain -> [2, n_pkg); slab -> plane ranges
-        if (gc.zs_lo == gc.z_lo && gc.zs_hi == gc.z_hi) {
+        if (known_npkg >= 0) {
+            g->own_lo = g->plan.own_lo;
+            g->own_hi = g->plan.own_hi;
+            wait_published(pub, gen, s);
+            if ((int64_t)pub.host[0] != n_active)
+                throw Error(SG_ERR_STATE, "sg_build: partition count differs from the build's");
+            g->n_core = (int64_t)pub.host[1];
+            g->n_inner = n_active - g->n_core;
+        } else if (gc.zs_lo == gc.z_lo && gc.zs_hi == gc.z_hi) {
             g->own_lo = 2;
             g->own_hi = n_pkg;
         } else {
@@ -1079,6 +1174,22 @@ extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, cons
     return guard([&] { build_impl(desc, geom, slab, nullptr, stream, out); });
 }
 
+extern "C" sg_status sg_build_ex(const sg_desc* desc, const sg_geometry* geom,
+                                 const sg_build_opts* opts, void* stream, sg_grid** out) {
+    return guard([&] {
+        const sg_build_opts o = opts ? *opts : sg_build_opts{nullptr, nullptr, nullptr};
+        build_impl(desc, geom, o.slab, nullptr, stream, out, o.comm, o.allocator);
+    });
+}
+
+extern "C" sg_status sg_pool_trim(void) {
+    return guard([&] {
+        cudaMemPool_t pool = lib_pool();
+        SG_CUDA(cudaDeviceSynchronize());
+        SG_CUDA(cudaMemPoolTrimTo(pool, 0));
+    });
+}
+
 extern "C" sg_status sg_build_refined(const sg_grid* parent, const sg_geometry* geom, void* stream,
                                       sg_grid** out) {
     return guard([&] {
@@ -1098,12 +1209,25 @@ extern "C" sg_status sg_build_refined(const sg_grid* parent, const sg_geometry* 
 
 static void free_grid(sg_grid* g, cudaStream_t s, bool async) {
     for (auto& a : g->allocs) {
-        if (async)
+        if (g->has_allocator)
+            g->allocator.free(a.first, a.second, (void*)s, g->allocator.ctx);
+        else if (async)
             cudaFreeAsync(a.first, s);
         else
             cudaFree(a.first);
     }
     g->allocs.clear();
+    if (g->comm_stream) {
+        if (async) {
+            // the comm stream's last exchange must finish before the memory
+            // it touches is reused on s
+            cudaEventRecord(g->ev_x, g->comm_stream);
+            cudaStreamWaitEvent(s, g->ev_x, 0);
+        }
+        cudaStreamDestroy(g->comm_stream);
+    }
+    if (g->ev_b) cudaEventDestroy(g->ev_b);
+    if (g->ev_x) cudaEventDestroy(g->ev_x);
     delete g;
 }
 
@@ -1144,6 +1268,8 @@ extern "C" sg_status sg_info(const sg_grid* g, sg_info_t* info) {
         info->device_bytes = g->bytes();
         info->own_lo = g->own_lo;
         info->own_hi = g->own_hi;
+        info->rank = g->rank;
+        info->nranks = g->nranks;
     });
 }
 
@@ -1215,16 +1341,10 @@ extern "C" sg_status sg_balanced_cuts(const int64_t* counts, int32_t nz, int32_t
     });
 }
 
-extern "C" sg_status sg_plane_counts(const sg_desc* desc, const sg_geometry* geom, int32_t z_lo,
-                                     int32_t z_hi, int64_t* counts, void* stream) {
-    return guard([&] {
-        check_desc(desc, geom);
-        SG_ARG(geom->n_tris == 0, "sg_plane_counts: mesh geometries are single-domain only");
-        SG_ARG(counts != nullptr, "sg_plane_counts: null counts");
-        SG_ARG(z_lo >= 0 && z_lo <= z_hi && z_hi <= desc->n[2], "sg_plane_counts: bad plane range");
-        check_device();
+static void plane_counts(const sg_desc* desc, const sg_geometry* geom, int32_t z_lo, int32_t z_hi,
+                         int64_t* counts, cudaStream_t s) {
+    {
         if (z_hi == z_lo) return;
-        cudaStream_t s = (cudaStream_t)stream;
         GridC gc = make_gridc(desc);
         const Geom ge = make_geom(geom);
         const int32_t zt_lo = std::max(0, z_lo - 1), zt_hi = std::min(desc->n[2], z_hi + 1);
@@ -1239,6 +1359,18 @@ extern "C" sg_status sg_plane_counts(const sg_desc* desc, const sg_geometry* geo
                                                                       (unsigned long long*)counts);
         SG_LAUNCHED();
         SG_CUDA(cudaFreeAsync(core_w, s));
+    }
+}
+
+extern "C" sg_status sg_plane_counts(const sg_desc* desc, const sg_geometry* geom, int32_t z_lo,
+                                     int32_t z_hi, int64_t* counts, void* stream) {
+    return guard([&] {
+        check_desc(desc, geom);
+        SG_ARG(geom->n_tris == 0, "sg_plane_counts: mesh geometries are single-domain only");
+        SG_ARG(counts != nullptr, "sg_plane_counts: null counts");
+        SG_ARG(z_lo >= 0 && z_lo <= z_hi && z_hi <= desc->n[2], "sg_plane_counts: bad plane range");
+        check_device();
+        plane_counts(desc, geom, z_lo, z_hi, counts, (cudaStream_t)stream);
     });
 }
 

@@ -105,9 +105,30 @@ sg_status guard(F&& f) {
     }
 }
 
-// Stream-ordered device allocation from the default pool (memory kept in the
-// pool across grids: release threshold raised on first use).
+// Stream-ordered device allocation from the library's own pool on the
+// current device (memory kept in the pool across grids: its release
+// threshold is raised; the device's default pool is left alone).  Free with
+// cudaFreeAsync.
 void* dalloc(size_t bytes, cudaStream_t s);
+
+// ---- communicator backends (sg_comm.cu) ----
+// all-gather: dst = [nranks][bytes], rank r's `src` at offset r * bytes;
+// stream-ordered on s (device buffers)
+void comm_allgather(const sg_comm* c, const void* src, void* dst, size_t bytes, cudaStream_t s);
+// one group of point-to-point transfers, stream-ordered on s; zero-byte ops
+// must be left out by both sides
+struct P2P {
+    int peer;
+    bool send;
+    void* buf;
+    size_t bytes;
+};
+void comm_group(const sg_comm* c, const P2P* ops, int n, cudaStream_t s);
+int comm_rank(const sg_comm* c);
+int comm_size(const sg_comm* c);
+// the z-slab plan (sg_slab_plan)
+void slab_plan(const int64_t* counts, int32_t nz, int32_t nranks, int32_t rank, sg_plan_t* p,
+               int32_t* cuts);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -171,10 +192,27 @@ struct sg_grid {
     std::vector<std::pair<void*, size_t>> allocs;
     // owned package range [own_lo, own_hi) in local ids
     int64_t own_lo = 2, own_hi = 2;
+    // caller's allocator (sg_build_ex), else the library pool
+    bool has_allocator = false;
+    sg_allocator allocator{};
+    // partition over a communicator (sg_build_ex with comm)
+    const sg_comm* comm = nullptr;
+    int32_t rank = 0, nranks = 1;
+    std::vector<int32_t> cuts;  // [nranks + 1] plane cuts of every rank
+    sg_plan_t plan{};           // this rank's plan (halo ranges)
+    cudaStream_t comm_stream = nullptr;  // exchanges overlapping interior sweeps
+    cudaEvent_t ev_b = nullptr, ev_x = nullptr;
+    bool partitioned() const { return comm != nullptr && nranks > 1; }
 
     void* alloc(size_t bytes, cudaStream_t s) {
-        void* p = sg::dalloc(bytes, s);
-        allocs.emplace_back(p, bytes);
+        void* p = nullptr;
+        if (has_allocator) {
+            p = allocator.alloc(bytes ? bytes : 256, (void*)s, allocator.ctx);
+            if (!p) throw sg::Error(SG_ERR_OOM, "sg_allocator.alloc returned NULL");
+        } else {
+            p = sg::dalloc(bytes, s);
+        }
+        allocs.emplace_back(p, bytes ? bytes : 256);
         return p;
     }
     int64_t bytes() const {
@@ -191,6 +229,9 @@ void launch_gradient(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t s
 void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void* grad,
                   unsigned long long* oob, cudaStream_t s);
 void launch_table1(sg_grid* g, int32_t op, double value, cudaStream_t s);
+// refresh the ghost packages of `field` (per_pkg_bytes per package) from the
+// neighbour ranks of a partitioned grid (grouped send/recv on s)
+void halo_exchange(const sg_grid* g, void* field, size_t per_pkg_bytes, cudaStream_t s);
 
 // NEXT-4 triangle mesh (sg_mesh.cu): device copies, pseudonormals, per-cell
 // triangle bins; fills the mesh fields of `g`

@@ -377,8 +377,283 @@ static Staging& staging() {
     return S;
 }
 
+// ------------------------------------------------- partitioned grids ----
+// K9: particles binned to the rank that owns their
+// background plane, exchanged, probed by the owner, results sent back and
+// restored to the caller's order.  Binning is stable (within a destination
+// the caller's order is kept), so the received batch of every owner is
+// deterministic.
+
+constexpr int kBinT = 4096;  // particles per binning tile (256 threads x 16)
+
+struct BinC {
+    GridC gc;
+    int32_t nranks, self;
+    int32_t cuts[SG_MAX_RANKS + 1];
+};
+
+// owner rank of a position: the containing background plane by the probe's
+// own cell arithmetic (the fp64 definition, R-15); outside the domain or NaN
+// -> this rank (the local probe returns (+far, 0) and counts it)
+template <class T>
+__device__ __forceinline__ int owner_of(const BinC& b, const T* x) {
+    int c[3];
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ok = cell_of<T, false>(b.gc, k, x[k], c[k]) && ok;
+    if (!ok) return b.self;
+    int lo = 0, hi = b.nranks - 1;  // largest r with cuts[r] <= cz
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (b.cuts[mid] <= c[2]) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_bin_count(BinC b, int64_t n, const T* __restrict__ pos,
+                                                   int64_t* __restrict__ hist, int64_t ntiles) {
+    __shared__ int h[SG_MAX_RANKS];
+    for (int d = threadIdx.x; d < b.nranks; d += 256) h[d] = 0;
+    __syncthreads();
+    const int64_t t0 = (int64_t)blockIdx.x * kBinT;
+    for (int q = 0; q < kBinT / 256; ++q) {
+        const int64_t i = t0 + q * 256 + threadIdx.x;
+        if (i < n) atomicAdd(&h[owner_of(b, pos + 3 * i)], 1);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < b.nranks; d += 256) hist[(int64_t)d * ntiles + blockIdx.x] = h[d];
+}
+
+// exclusive scan of the destination-major tile counts (one block; a few
+// hundred thousand entries at most), per-destination totals
+__global__ void __launch_bounds__(1024) k_bin_scan(int64_t* __restrict__ v, int64_t m,
+                                                   int32_t nranks, int64_t ntiles,
+                                                   long long* __restrict__ totals) {
+    __shared__ int64_t part[1024];
+    const int64_t per = (m + 1023) / 1024;
+    const int64_t a = min(m, (int64_t)threadIdx.x * per), e = min(m, a + per);
+    int64_t sum = 0;
+    for (int64_t i = a; i < e; ++i) sum += v[i];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const int64_t add = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+        __syncthreads();
+        part[threadIdx.x] += add;
+        __syncthreads();
+    }
+    int64_t run = part[threadIdx.x] - sum;
+    for (int64_t i = a; i < e; ++i) {
+        const int64_t c = v[i];
+        v[i] = run;
+        run += c;
+    }
+    __syncthreads();
+    if (threadIdx.x < nranks) {
+        const int d = threadIdx.x;
+        const int64_t lo = v[(int64_t)d * ntiles];
+        const int64_t hi = d + 1 < nranks ? v[(int64_t)(d + 1) * ntiles] : part[1023];
+        totals[d] = ntiles ? hi - lo : 0;
+    }
+}
+
+// stable scatter of the positions into destination order; perm[i] = slot
+template <class T>
+__global__ void __launch_bounds__(256) k_bin_scatter(BinC b, int64_t n, const T* __restrict__ pos,
+                                                     const int64_t* __restrict__ off, int64_t ntiles,
+                                                     T* __restrict__ sendpos,
+                                                     uint32_t* __restrict__ perm) {
+    __shared__ int64_t base[SG_MAX_RANKS];
+    __shared__ int wcnt[8][SG_MAX_RANKS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int d = threadIdx.x; d < b.nranks; d += 256) base[d] = off[(int64_t)d * ntiles + blockIdx.x];
+    const int64_t t0 = (int64_t)blockIdx.x * kBinT;
+    for (int q = 0; q < kBinT / 256; ++q) {
+        for (int k = threadIdx.x; k < 8 * SG_MAX_RANKS; k += 256) (&wcnt[0][0])[k] = 0;
+        __syncthreads();
+        const int64_t i = t0 + q * 256 + threadIdx.x;
+        const bool valid = i < n;
+        const int d = valid ? owner_of(b, pos + 3 * i) : -1;
+        const unsigned same = __match_any_sync(0xffffffffu, d);
+        const int rank_w = __popc(same & ((1u << lane) - 1u));
+        if (valid && rank_w == 0) wcnt[warp][d] = __popc(same);
+        __syncthreads();
+        if (valid) {
+            int64_t slot = base[d] + rank_w;
+            for (int w = 0; w < warp; ++w) slot += wcnt[w][d];
+            sendpos[3 * slot] = pos[3 * i];
+            sendpos[3 * slot + 1] = pos[3 * i + 1];
+            sendpos[3 * slot + 2] = pos[3 * i + 2];
+            perm[i] = (uint32_t)slot;
+        }
+        __syncthreads();
+        for (int dd = threadIdx.x; dd < b.nranks; dd += 256) {
+            int64_t t = 0;
+            for (int w = 0; w < 8; ++w) t += wcnt[w][dd];
+            base[dd] += t;
+        }
+        __syncthreads();
+    }
+}
+
+// results back to the caller's order
+template <class T>
+__global__ void k_unbin(int64_t n, const uint32_t* __restrict__ perm, const T* __restrict__ rphi,
+                        const T* __restrict__ rgrad, T* __restrict__ phi, T* __restrict__ grad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t k = perm[i];
+    phi[i] = rphi[k];
+    if (grad) {
+        grad[3 * i] = rgrad[3 * k];
+        grad[3 * i + 1] = rgrad[3 * k + 1];
+        grad[3 * i + 2] = rgrad[3 * k + 2];
+    }
+}
+
+template <class T>
+static void probe_partitioned_dev(const sg_grid* g, int64_t n, const T* pos, T* out_phi, T* out_grad,
+                                  unsigned long long* oob, cudaStream_t s) {
+    const int P = g->nranks, me = g->rank;
+    SG_ARG(n < (1LL << 32), "sg_probe: at most 2^32 - 1 particles per rank on a partitioned grid");
+    BinC b{};
+    b.gc = g->gc;
+    b.nranks = P;
+    b.self = me;
+    for (int r = 0; r <= P; ++r) b.cuts[r] = g->cuts[r];
+    const int64_t ntiles = ceil_div(n, kBinT);
+    const size_t es = sizeof(T);
+    const bool want_grad = out_grad != nullptr;
+    // scratch: hist/offsets | totals | send positions | perm | results
+    auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+    const size_t sz_h = al(sizeof(int64_t) * std::max<int64_t>(1, P * ntiles)),
+                 sz_t = al(sizeof(long long) * (P + 1) * (P + 1)),
+                 sz_p = al(es * 3 * std::max<int64_t>(n, 1)),
+                 sz_m = al(sizeof(uint32_t) * std::max<int64_t>(n, 1)),
+                 sz_r = al(es * 4 * std::max<int64_t>(n, 1));
+    char* buf = (char*)dalloc(sz_h + sz_t + sz_p + sz_m + sz_r, s);
+    int64_t* hist = (int64_t*)buf;
+    // [0, P]: my totals per destination + my grad request; then [P][P + 1]
+    long long* tot = (long long*)(buf + sz_h);
+    T* sendpos = (T*)(buf + sz_h + sz_t);
+    uint32_t* perm = (uint32_t*)(buf + sz_h + sz_t + sz_p);
+    T* res = (T*)(buf + sz_h + sz_t + sz_p + sz_m);  // phi [n] | grad [3n]
+    SG_CUDA(cudaMemsetAsync(tot, 0, sizeof(long long) * P, s));
+    const long long flag = want_grad ? 1 : 0;
+    SG_CUDA(cudaMemcpyAsync(tot + P, &flag, sizeof(flag), cudaMemcpyHostToDevice, s));
+    if (ntiles) {
+        k_bin_count<T><<<(unsigned)ntiles, 256, 0, s>>>(b, n, pos, hist, ntiles);
+        SG_LAUNCHED();
+        k_bin_scan<<<1, 1024, 0, s>>>(hist, P * ntiles, P, ntiles, tot);
+        SG_LAUNCHED();
+        k_bin_scatter<T><<<(unsigned)ntiles, 256, 0, s>>>(b, n, pos, hist, ntiles, sendpos, perm);
+        SG_LAUNCHED();
+    }
+    // count matrix cnt[src][dst] and every rank's grad request (the one host
+    // synchronisation): the owners probe grad for everybody if anybody asks,
+    // so every rank takes the same exchange decisions
+    comm_allgather(g->comm, tot, tot + P + 1, sizeof(long long) * (P + 1), s);
+    std::vector<long long> all((size_t)P * (P + 1)), cnt((size_t)P * P);
+    SG_CUDA(cudaMemcpyAsync(all.data(), tot + P + 1, sizeof(long long) * all.size(),
+                            cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    bool any_grad = false;
+    for (int r = 0; r < P; ++r) {
+        for (int d = 0; d < P; ++d) cnt[(size_t)r * P + d] = all[(size_t)r * (P + 1) + d];
+        any_grad = any_grad || all[(size_t)r * (P + 1) + P] != 0;
+    }
+    if (any_grad && !g->has_grad)  // raised on every rank alike (has_grad is collective)
+        throw Error(SG_ERR_STATE, "sg_probe: grad requested before sg_gradient(SG_GRAD)");
+    const bool want_grad_any = any_grad;
+    std::vector<int64_t> soff(P + 1, 0), roff(P + 1, 0);
+    for (int d = 0; d < P; ++d) soff[d + 1] = soff[d] + cnt[(size_t)me * P + d];
+    for (int r = 0; r < P; ++r) roff[r + 1] = roff[r] + (r == me ? 0 : cnt[(size_t)r * P + me]);
+    const int64_t R = roff[P];
+    T* rphi = res;
+    T* rgrad = res + n;
+    // received batch: positions | phi | grad
+    T* recv = R ? (T*)dalloc(es * 7 * R, s) : nullptr;
+    T* recv_phi = recv + 3 * R;
+    T* recv_grad = recv + 4 * R;
+    std::vector<P2P> ops;
+    for (int d = 0; d < P; ++d) {
+        const int64_t c = cnt[(size_t)me * P + d];
+        if (d != me && c) ops.push_back(P2P{d, true, sendpos + 3 * soff[d], (size_t)c * 3 * es});
+    }
+    for (int r = 0; r < P; ++r) {
+        const int64_t c = r == me ? 0 : cnt[(size_t)r * P + me];
+        if (c) ops.push_back(P2P{r, false, recv + 3 * roff[r], (size_t)c * 3 * es});
+    }
+    comm_group(g->comm, ops.data(), (int)ops.size(), s);
+    // the owner's probes: this rank's own bucket in place, the received batch
+    const int64_t mine = cnt[(size_t)me * P + me];
+    if (mine)
+        probe_dev<T>(g, mine, sendpos + 3 * soff[me], rphi + soff[me],
+                     want_grad_any ? rgrad + 3 * soff[me] : nullptr, oob, s);
+    if (R) probe_dev<T>(g, R, recv, recv_phi, want_grad_any ? recv_grad : nullptr, oob, s);
+    ops.clear();
+    for (int r = 0; r < P; ++r) {
+        const int64_t c = r == me ? 0 : cnt[(size_t)r * P + me];
+        if (!c) continue;
+        ops.push_back(P2P{r, true, recv_phi + roff[r], (size_t)c * es});
+        if (want_grad_any) ops.push_back(P2P{r, true, recv_grad + 3 * roff[r], (size_t)c * 3 * es});
+    }
+    for (int d = 0; d < P; ++d) {
+        const int64_t c = cnt[(size_t)me * P + d];
+        if (d == me || !c) continue;
+        ops.push_back(P2P{d, false, rphi + soff[d], (size_t)c * es});
+        if (want_grad_any) ops.push_back(P2P{d, false, rgrad + 3 * soff[d], (size_t)c * 3 * es});
+    }
+    comm_group(g->comm, ops.data(), (int)ops.size(), s);
+    if (n) {
+        k_unbin<T><<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n, perm, rphi, rgrad, out_phi,
+                                                             want_grad ? out_grad : nullptr);
+        SG_LAUNCHED();
+    }
+    if (recv) SG_CUDA(cudaFreeAsync(recv, s));
+    SG_CUDA(cudaFreeAsync(buf, s));
+}
+
+static void probe_partitioned(const sg_grid* g, int64_t n, const void* pos, void* phi, void* grad,
+                              unsigned long long* oob, cudaStream_t s) {
+    const bool dev = is_device_ptr(pos) && is_device_ptr(phi) && is_device_ptr(grad);
+    const size_t es = (size_t)g->esz;
+    const void* dpos = pos;
+    void* dphi = phi;
+    void* dgrad = grad;
+    char* stage = nullptr;
+    if (!dev) {  // host buffers: whole-array staging
+        SG_ARG(n == 0 || (!is_device_ptr(pos) && !is_device_ptr(phi) &&
+                          (grad == nullptr || !is_device_ptr(grad))),
+               "sg_probe: pos/phi/grad must be all device or all host pointers");
+        stage = (char*)dalloc(std::max<size_t>(1, n * es * 7), s);
+        dpos = stage;
+        dphi = stage + n * es * 3;
+        dgrad = grad ? stage + n * es * 4 : nullptr;
+        if (n) SG_CUDA(cudaMemcpyAsync(stage, pos, n * es * 3, cudaMemcpyHostToDevice, s));
+    }
+    if (g->dtype == SG_F64)
+        probe_partitioned_dev<double>(g, n, (const double*)dpos, (double*)dphi, (double*)dgrad, oob, s);
+    else
+        probe_partitioned_dev<float>(g, n, (const float*)dpos, (float*)dphi, (float*)dgrad, oob, s);
+    if (!dev) {
+        if (n) {
+            SG_CUDA(cudaMemcpyAsync(phi, dphi, n * es, cudaMemcpyDeviceToHost, s));
+            if (grad) SG_CUDA(cudaMemcpyAsync(grad, dgrad, n * es * 3, cudaMemcpyDeviceToHost, s));
+        }
+        SG_CUDA(cudaFreeAsync(stage, s));
+        SG_CUDA(cudaStreamSynchronize(s));
+    }
+}
+
 void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void* grad,
                   unsigned long long* oob, cudaStream_t s) {
+    if (g->partitioned()) {
+        probe_partitioned(g, n, pos, phi, grad, oob, s);
+        return;
+    }
     const bool dev = is_device_ptr(pos) && is_device_ptr(phi) && is_device_ptr(grad);
     auto run = [&](int64_t m, const void* p, void* o, void* og, cudaStream_t st) {
         if (g->dtype == SG_F64)
@@ -438,9 +713,9 @@ extern "C" sg_status sg_probe(const sg_grid* g, int64_t n, const void* pos, void
     return guard([&] {
         SG_ARG(g != nullptr, "sg_probe: null grid");
         SG_ARG(n >= 0, "sg_probe: n must be >= 0");
-        if (n == 0) return;
-        SG_ARG(pos != nullptr && phi != nullptr, "sg_probe: null pos or phi");
-        if (grad != nullptr && !g->has_grad)
+        if (n == 0 && !g->partitioned()) return;  // (collective on a partition)
+        SG_ARG(n == 0 || (pos != nullptr && phi != nullptr), "sg_probe: null pos or phi");
+        if (grad != nullptr && !g->has_grad && !g->partitioned())
             throw Error(SG_ERR_STATE, "sg_probe: grad requested before sg_gradient(SG_GRAD)");
         SG_CUDA(cudaGetLastError());
         launch_probe(g, n, pos, phi, grad, oob_count, (cudaStream_t)stream);

@@ -729,13 +729,50 @@ static StC<T> stencil_consts(const sg_grid* g, double cfl) {
 }
 
 template <class T>
-static void reinit_launch(sg_grid* g, int cur, const StC<T>& c, int64_t lo, int64_t hi,
+static bool reinit_launch(sg_grid* g, int cur, const StC<T>& c, int64_t lo, int64_t hi,
                           cudaStream_t s) {
-    if (hi <= lo) return;
+    if (hi <= lo) return false;
     const ReinitOp<T> op{(T*)g->phi[1 - cur], c};
     const unsigned blocks = persistent_blocks(k_sweep<T, ReinitOp<T>>, hi - lo);
     k_sweep<T, ReinitOp<T>><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], g->face, (uint32_t)lo,
                                                    (uint32_t)hi, op);
+    return true;
+}
+
+// Partitioned grid (a9): groups of up to 4 sweeps per ghost
+// exchange (the ghost plane is 4 data points deep; see sg_reinit_halo).  The
+// first sweeps of a group run over owned + ghost packages; the last one
+// updates the two boundary planes first (the packages the neighbours need),
+// hands them to the internal high-priority comm stream for the grouped
+// send/recv into the neighbours' ghost planes, and updates the interior
+// packages while the transfer runs.  Jacobi sweeps: bit-identical to one GPU.
+template <class T>
+static void reinit_partitioned(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
+    const StC<T> c = stencil_consts<T>(g, cfl);
+    const sg_plan_t& p = g->plan;
+    const bool lower = g->rank > 0, upper = g->rank < g->nranks - 1;
+    // [b0lo, b0hi): first owned plane (if rank - 1 exists); [b1lo, b1hi):
+    // last owned plane (if rank + 1 exists); interior between them
+    const int64_t b0lo = p.own_lo, b0hi = lower ? p.send_lo[1] : p.own_lo;
+    const int64_t b1hi = p.own_hi, b1lo = std::max(b0hi, upper ? p.send_hi[0] : p.own_hi);
+    const size_t per = (size_t)64 * g->esz;
+    for (int done = 0; done < iters;) {
+        const int m = std::min(4, iters - done);
+        for (int i = 0; i + 1 < m; ++i) {
+            if (reinit_launch<T>(g, g->cur, c, 2, g->n_pkg, s)) SG_LAUNCHED();
+            g->cur = 1 - g->cur;
+        }
+        if (reinit_launch<T>(g, g->cur, c, b0lo, b0hi, s)) SG_LAUNCHED();
+        if (reinit_launch<T>(g, g->cur, c, b1lo, b1hi, s)) SG_LAUNCHED();
+        SG_CUDA(cudaEventRecord(g->ev_b, s));
+        SG_CUDA(cudaStreamWaitEvent(g->comm_stream, g->ev_b, 0));
+        halo_exchange(g, g->phi[1 - g->cur], per, g->comm_stream);
+        SG_CUDA(cudaEventRecord(g->ev_x, g->comm_stream));
+        if (reinit_launch<T>(g, g->cur, c, b0hi, b1lo, s)) SG_LAUNCHED();
+        SG_CUDA(cudaStreamWaitEvent(s, g->ev_x, 0));
+        g->cur = 1 - g->cur;
+        done += m;
+    }
 }
 
 // Multi-sweep reinit runs as one CUDA graph of `iters` kernel nodes.  The
@@ -765,6 +802,10 @@ static std::vector<cudaStream_t> g_capture;
 
 template <class T>
 static void reinit_t(sg_grid* g, int32_t iters, double cfl, bool halo, cudaStream_t s) {
+    if (g->partitioned()) {
+        reinit_partitioned<T>(g, iters, cfl, s);
+        return;
+    }
     const StC<T> c = stencil_consts<T>(g, cfl);
     // owned packages, or (halo) every stored package: owned and ghost
     const int64_t lo = halo ? 2 : g->own_lo, hi = halo ? g->n_pkg : g->own_hi;
@@ -931,6 +972,9 @@ static void gradient_t(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t
         k_singular<T><<<1, 128, 0, s>>>(nullptr, nullptr, gp, np, T(0), (T)g->gc.far);
         SG_LAUNCHED();
     }
+    // partitioned grid: the (phi, grad) ghost planes for probes whose
+    // trilinear corners lie in a ghost plane
+    if (gp) halo_exchange(g, gp, (size_t)256 * sizeof(T), s);
     if (gp) g->has_grad = true;
     if (np) g->has_normal = true;
 }

@@ -27,10 +27,15 @@ _STATUS = {0: "SG_OK", 1: "SG_ERR_ARG", 2: "SG_ERR_OOM", 3: "SG_ERR_CUDA", 4: "S
            5: "SG_ERR_STATE", 6: "SG_ERR_DOMAIN"}
 
 # exported symbols declared in include/sg.h (checked by the CPU test suite)
-EXPORTS = ("sg_build", "sg_build_refined", "sg_reinit", "sg_reinit_halo", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
+EXPORTS = ("sg_build", "sg_build_ex", "sg_build_refined", "sg_reinit", "sg_reinit_halo",
+           "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
            "sg_sign_correct", "sg_clean", "sg_info", "sg_view",
            "sg_destroy", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
+           "sg_slab_plan", "sg_comm_unique_id", "sg_comm_create", "sg_comm_create_local",
+           "sg_comm_info", "sg_comm_destroy", "sg_pool_trim",
            "sg_neighbour_index_shift", "sg_last_error", "sg_abi_version", "sg_launch_count")
+SG_COMM_ID_BYTES = 128
+SG_COMM_NCCL, SG_COMM_LOCAL = 0, 1
 
 
 class SgError(RuntimeError):
@@ -77,10 +82,35 @@ class sg_info_t(C.Structure):
                 ("pad", C.c_int32), ("dx", C.c_double), ("far", C.c_double),
                 ("kernel_sum", C.c_double), ("has_grad", C.c_int32), ("has_normal", C.c_int32),
                 ("has_kint", C.c_int32), ("phi_cur", C.c_int32), ("device_bytes", C.c_int64),
-                ("own_lo", C.c_int64), ("own_hi", C.c_int64)]
+                ("own_lo", C.c_int64), ("own_hi", C.c_int64), ("rank", C.c_int32),
+                ("nranks", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
+
+
+class sg_plan_t(C.Structure):
+    _fields_ = [("z_lo", C.c_int32), ("z_hi", C.c_int32), ("zs_lo", C.c_int32),
+                ("zs_hi", C.c_int32), ("id_base", C.c_int64), ("n_pkg", C.c_int64),
+                ("own_lo", C.c_int64), ("own_hi", C.c_int64), ("send_lo", C.c_int64 * 2),
+                ("send_hi", C.c_int64 * 2), ("recv_lo", C.c_int64 * 2), ("recv_hi", C.c_int64 * 2)]
+
+    def as_dict(self):
+        return {k: (tuple(getattr(self, k)) if k.startswith(("send", "recv")) else getattr(self, k))
+                for k, _ in self._fields_}
+
+
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+class sg_allocator(C.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("ctx", C.c_void_p)]
+
+
+class sg_build_opts(C.Structure):
+    _fields_ = [("slab", C.POINTER(sg_slab)), ("comm", C.c_void_p),
+                ("allocator", C.POINTER(sg_allocator))]
 
 
 _lib = None
@@ -113,6 +143,16 @@ def lib():
         L.sg_destroy_async.argtypes = [P, P]
         L.sg_balanced_cuts.argtypes = [P, I32, I32, P]
         L.sg_plane_counts.argtypes = [C.POINTER(sg_desc), C.POINTER(sg_geometry), I32, I32, P, P]
+        L.sg_build_ex.argtypes = [C.POINTER(sg_desc), C.POINTER(sg_geometry),
+                                  C.POINTER(sg_build_opts), P, C.POINTER(P)]
+        L.sg_slab_plan.argtypes = [P, I32, I32, I32, C.POINTER(sg_plan_t), P]
+        L.sg_comm_unique_id.argtypes = [P]
+        L.sg_comm_create.argtypes = [P, I32, I32, C.POINTER(P)]
+        L.sg_comm_create_local.argtypes = [I32, P]
+        L.sg_comm_info.argtypes = [P, P, P, P]
+        L.sg_comm_destroy.argtypes = [P]
+        L.sg_comm_destroy.restype = None
+        L.sg_pool_trim.argtypes = []
         L.sg_neighbour_index_shift.argtypes = [P, P, P]
         L.sg_neighbour_index_shift.restype = I32
         L.sg_last_error.restype = C.c_char_p
@@ -121,7 +161,9 @@ def lib():
         for name in ("sg_build", "sg_build_refined", "sg_reinit", "sg_reinit_halo", "sg_gradient", "sg_probe", "sg_table1", "sg_relax",
                      "sg_sign_correct", "sg_clean",
                      "sg_info",
-                     "sg_view", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts"):
+                     "sg_view", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
+                     "sg_build_ex", "sg_slab_plan", "sg_comm_unique_id", "sg_comm_create",
+                     "sg_comm_create_local", "sg_comm_info", "sg_pool_trim"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -271,6 +313,86 @@ def sg_plane_counts(desc: sg_desc, geom: sg_geometry, z_lo: int, z_hi: int, coun
                                  C.c_void_p(counts_ptr), _stream(stream)))
 
 
+def sg_slab_plan(counts, nranks: int, rank: int) -> tuple:
+    """Host-only z-slab plan (include/sg.h sg_slab_plan): (plan dict, cuts)."""
+    import numpy as np
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.int64))
+    cuts = np.zeros(nranks + 1, dtype=np.int32)
+    p = sg_plan_t()
+    _check(lib().sg_slab_plan(c.ctypes.data_as(C.c_void_p), int(c.size), int(nranks), int(rank),
+                              C.byref(p), cuts.ctypes.data_as(C.c_void_p)))
+    return p.as_dict(), [int(v) for v in cuts]
+
+
+def sg_pool_trim() -> None:
+    _check(lib().sg_pool_trim())
+
+
+class Comm:
+    """Communicator handle (include/sg.h sg_comm_*).
+
+    Comm.nccl(group): one process per GPU, NCCL over NVLink; the unique id is
+    broadcast with torch.distributed (rank 0 creates it).
+    Comm.local(n): n in-process communicators on the current device (each to
+    be driven by its own thread) -- the emulation used by the 1-GPU tests."""
+
+    def __init__(self, handle: int):
+        self.handle = handle
+        r, n, k = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().sg_comm_info(C.c_void_p(handle), C.byref(r), C.byref(n), C.byref(k)))
+        self.rank, self.nranks, self.kind = r.value, n.value, k.value
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_char * SG_COMM_ID_BYTES)()
+        _check(lib().sg_comm_unique_id(buf))
+        return bytes(buf.raw)
+
+    @classmethod
+    def nccl(cls, group=None) -> "Comm":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        uid = (C.c_char * SG_COMM_ID_BYTES).from_buffer_copy(obj[0])
+        out = C.c_void_p()
+        _check(lib().sg_comm_create(uid, rank, world, C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def local(cls, n: int) -> list:
+        arr = (C.c_void_p * n)()
+        _check(lib().sg_comm_create_local(int(n), arr))
+        return [cls(arr[i]) for i in range(n)]
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().sg_comm_destroy(C.c_void_p(self.handle))
+            self.handle = None
+
+
+class TorchAllocator:
+    """sg_allocator backed by PyTorch's caching allocator (grid memory then
+    shows up in torch.cuda.memory_allocated and is shared with torch)."""
+
+    def __init__(self):
+        import torch
+
+        def _alloc(nbytes, stream, ctx):
+            try:
+                return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(),
+                                                          int(stream or 0))
+            except Exception:
+                return None
+
+        def _free(ptr, nbytes, stream, ctx):
+            torch.cuda.caching_allocator_delete(int(ptr))
+
+        self._a, self._f = _ALLOC_FN(_alloc), _FREE_FN(_free)  # keep the thunks alive
+        self.struct = sg_allocator(self._a, self._f, None)
+
+
 def sg_neighbour_index_shift(shift) -> tuple:
     """Lst. 2 (host-callable): shift (3 ints in [-4, 7]) -> (slot, offset
     triple, data triple); slot -1 if out of range."""
@@ -333,9 +455,15 @@ def _cached_desc(w):
 class Grid:
     """Owning handle around sg_build/sg_destroy with torch-friendly calls."""
 
-    def __init__(self, w, slab: tuple | None = None, stream=None, parent=None):
+    def __init__(self, w, slab: tuple | None = None, stream=None, parent=None, comm=None,
+                 allocator=None):
+        """slab: explicit (z_lo, z_hi, id_base); comm: a Comm (partitioned
+        grid, collective calls); allocator: a TorchAllocator (grid memory
+        from PyTorch's caching allocator) or None (the library's pool)."""
         self.w = w
         self.desc, self.geom, self._keep = _cached_desc(w)
+        self.comm = comm
+        self._allocator = allocator  # keep alive while the grid lives
         if parent is not None:  # NEXT-4: layer refined from `parent`
             out = C.c_void_p()
             _check(lib().sg_build_refined(C.c_void_p(parent.handle), C.byref(self.geom),
@@ -345,7 +473,16 @@ class Grid:
         sl = None
         if slab is not None:
             sl = sg_slab(int(slab[0]), int(slab[1]), int(slab[2]))
-        self.handle = sg_build(self.desc, self.geom, sl, stream)
+        if comm is None and allocator is None:
+            self.handle = sg_build(self.desc, self.geom, sl, stream)
+            return
+        opts = sg_build_opts(C.pointer(sl) if sl is not None else None,
+                             C.c_void_p(comm.handle) if comm is not None else None,
+                             C.pointer(allocator.struct) if allocator is not None else None)
+        out = C.c_void_p()
+        _check(lib().sg_build_ex(C.byref(self.desc), C.byref(self.geom), C.byref(opts),
+                                 _stream(stream), C.byref(out)))
+        self.handle = out.value
 
     def refined(self, stream=None) -> "Grid":
         """The next finer layer (cell / 2, 2 n cells per axis) built from this

@@ -43,21 +43,24 @@ def test_exports_every_declared_symbol(sg):
 
 
 def test_abi_version(sg):
-    assert sg.sg_abi_version() == 2
+    assert sg.sg_abi_version() == 3
     assert sg.sg_launch_count() == 0
 
 
 def test_ctypes_layout_matches_header(sg, tmp_path):
     src = tmp_path / "sz.c"
-    src.write_text('#include "sg.h"\n#include <stdio.h>\n#include <stddef.h>\nint main(){printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n",'
+    src.write_text('#include "sg.h"\n#include <stdio.h>\n#include <stddef.h>\nint main(){printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n",'
                    'sizeof(sg_prim),sizeof(sg_geometry),sizeof(sg_desc),sizeof(sg_slab),sizeof(sg_view_t),'
-                   'sizeof(sg_info_t),offsetof(sg_info_t,own_hi),offsetof(sg_desc,init_scale));return 0;}\n')
+                   'sizeof(sg_info_t),offsetof(sg_info_t,own_hi),offsetof(sg_desc,init_scale),'
+                   'sizeof(sg_plan_t),offsetof(sg_plan_t,recv_hi),sizeof(sg_build_opts),sizeof(sg_allocator),'
+                   'offsetof(sg_info_t,nranks));return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I" + os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
     got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
     exp = [C.sizeof(sg.sg_prim), C.sizeof(sg.sg_geometry), C.sizeof(sg.sg_desc), C.sizeof(sg.sg_slab),
            C.sizeof(sg.sg_view_t), C.sizeof(sg.sg_info_t), sg.sg_info_t.own_hi.offset,
-           sg.sg_desc.init_scale.offset]
+           sg.sg_desc.init_scale.offset, C.sizeof(sg.sg_plan_t), sg.sg_plan_t.recv_hi.offset,
+           C.sizeof(sg.sg_build_opts), C.sizeof(sg.sg_allocator), sg.sg_info_t.nranks.offset]
     assert got == exp
 
 
@@ -113,3 +116,47 @@ def test_neighbour_index_shift_lst2(sg):
         assert slot == (cell[0] + 1) + 3 * (cell[1] + 1) + 9 * (cell[2] + 1)
     for bad in ([-5, 0, 0], [0, 8, 0], [0, 0, 100]):
         assert sg.sg_neighbour_index_shift(bad)[0] == -1
+
+
+def test_slab_plan_host_logic(sg):
+    """sg_slab_plan (host only): cuts as sg_balanced_cuts, stored planes one
+    ghost plane per side, contiguous global id ranges that tile the domain,
+    halo ranges = whole stored planes, the send range of rank r the size of
+    the matching receive range of its neighbour."""
+    from oracle.oracle import Oracle
+    import workloads as W
+    for name in ("C1", "C2"):
+        t = Oracle(W.config(name)).build_tables()
+        pc = t.plane_count
+        nz = pc.size
+        for world in (1, 2, 3, 5, 8):
+            plans = [sg.sg_slab_plan(pc, world, r) for r in range(world)]
+            assert all(c == sg.sg_balanced_cuts(pc, world) for _, c in plans)
+            owned = []
+            for r, (p, cuts) in enumerate(plans):
+                assert (p["z_lo"], p["z_hi"]) == (cuts[r], cuts[r + 1])
+                assert p["zs_lo"] == max(0, p["z_lo"] - 1) and p["zs_hi"] == min(nz, p["z_hi"] + 1)
+                assert p["id_base"] == 2 + int(pc[:p["zs_lo"]].sum())
+                assert p["n_pkg"] == 2 + int(pc[p["zs_lo"]:p["zs_hi"]].sum())
+                g = lambda l: l - 2 + p["id_base"]  # noqa: E731
+                owned.append((g(p["own_lo"]), g(p["own_hi"])))
+                first = lambda z: 2 + int(pc[p["zs_lo"]:z].sum())  # noqa: E731
+                if r > 0:
+                    assert p["send_lo"] == (first(p["z_lo"]), first(p["z_lo"] + 1))
+                    assert p["recv_lo"] == (2, first(p["z_lo"]))
+                    q = plans[r - 1][0]
+                    assert p["recv_lo"][1] - p["recv_lo"][0] == q["send_hi"][1] - q["send_hi"][0]
+                    # the same global packages
+                    assert g(p["recv_lo"][0]) == q["send_hi"][0] - 2 + q["id_base"]
+                else:
+                    assert p["send_lo"] == (0, 0) and p["recv_lo"] == (0, 0)
+                if r == world - 1:
+                    assert p["send_hi"] == (0, 0) and p["recv_hi"] == (0, 0)
+                else:
+                    assert p["recv_hi"] == (p["own_hi"], p["n_pkg"])
+            assert owned[0][0] == 2 and owned[-1][1] == t.n_pkg
+            assert all(a[1] == b[0] for a, b in zip(owned, owned[1:]))
+    with pytest.raises(sg.SgError):
+        sg.sg_slab_plan([1, 2, 3], 4, 0)
+    with pytest.raises(sg.SgError):
+        sg.sg_slab_plan([1, 2, 3], 2, 2)

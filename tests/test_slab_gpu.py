@@ -1,6 +1,8 @@
-"""z-slab partition on ONE GPU: P slab grids built with sg_build(slab) in one
-process, halos refreshed by device copies between their views (the same
-ranges the NCCL exchange uses).  The P-slab result must be BITWISE equal to
+"""z-slab partition on ONE GPU through the explicit-slab entry point: P slab
+grids built with sg_build(slab) in one process from the library's plan
+(sg_slab_plan), halos refreshed by device copies between their views over
+the plan's halo ranges (the ranges the library's own exchange uses; the
+partitioned grids with their in-library exchange are tests/test_comm_gpu.py).  The P-slab result must be BITWISE equal to
 the 1-GPU grid (Jacobi sweeps are order independent): tables, phi after 20
 sweeps, grad/normal/kernel integrals and probes."""
 import numpy as np
@@ -20,6 +22,27 @@ def sgm():
     build.build()
     from paper_2512_11473_b200 import sg
     return sg
+
+
+def _owner_mask(pos, w, p):
+    """particles whose containing background plane rank p owns"""
+    cz = torch.floor((pos[:, 2].double() - w.lower[2]) / w.cell)
+    return (cz >= p.z_lo) & (cz < p.z_hi)
+
+
+def _check_plan_ranges(p, g):
+    """the plan's halo ranges are whole stored planes of the built grid"""
+    pf = [int(v) for v in g.view("plane_first").cpu().numpy()]
+
+    def rng(z):
+        return (pf[z - p.zs_lo], pf[z - p.zs_lo + 1])
+    none = (0, 0)
+    assert p.n_pkg == g.info["n_pkg"] == pf[-1]
+    assert (p.own_lo, p.own_hi) == (g.info["own_lo"], g.info["own_hi"])
+    assert p.send_lo == (rng(p.z_lo) if p.rank > 0 else none)
+    assert p.recv_lo == (rng(p.z_lo - 1) if p.rank > 0 else none)
+    assert p.send_hi == (rng(p.z_hi - 1) if p.rank < p.world - 1 else none)
+    assert p.recv_hi == (rng(p.z_hi) if p.rank < p.world - 1 else none)
 
 
 def _exchange_local(grids, halos, name, per):
@@ -53,7 +76,9 @@ def test_slabs_bitwise_equal_one_gpu(sgm, name, P):
     assert np.array_equal(np.diff(pf_full), counts)
     plans = [slab.plan(counts, P, r) for r in range(P)]
     grids = [sgm.Grid(w, slab=(p.z_lo, p.z_hi, p.id_base)) for p in plans]
-    halos = [slab.halo_ranges(p, g.view("plane_first").cpu().numpy()) for p, g in zip(plans, grids)]
+    for p, g in zip(plans, grids):
+        _check_plan_ranges(p, g)
+    halos = plans
     fnb = full.view("nb").cpu().numpy().view(np.uint32)
     fmeta = full.view("meta_cell").cpu().numpy().view(np.uint32)
     for p, g in zip(plans, grids):
@@ -91,7 +116,7 @@ def test_slabs_bitwise_equal_one_gpu(sgm, name, P):
     got_phi = torch.full_like(fphi, float("nan"))
     got_grad = torch.full_like(fgrad, float("nan"))
     for p, g in zip(plans, grids):
-        m = slab.owner_mask(pos, w, p)
+        m = _owner_mask(pos, w, p)
         ph, gr = g.probe(pos[m].contiguous())
         got_phi[m] = ph
         got_grad[m] = gr
@@ -107,8 +132,7 @@ def _slab_setup(sgm, w, P):
     counts = counts.cpu().numpy()
     plans = [slab.plan(counts, P, r) for r in range(P)]
     grids = [sgm.Grid(w, slab=(p.z_lo, p.z_hi, p.id_base)) for p in plans]
-    halos = [slab.halo_ranges(p, g.view("plane_first").cpu().numpy()) for p, g in zip(plans, grids)]
-    return plans, grids, halos
+    return plans, grids, plans
 
 
 def _owned_equal(full, plans, grids, name):
