@@ -283,14 +283,21 @@ def kernel_rooflines(sg, w, stream, flush, d_pos, n_part, probe_ms, reinit_ms, h
           "peak": fma_peak / 1e12, "frac": fmas / (t_kint * 1e-3) / fma_peak,
           "note": "direct-form FMAs (the kernel executes fewer: sign butterfly, closed form on "
                   "uniform packages); peak = SMs x 128 FP32 lanes x max SM clock"}
+    out.append(ke)
     fl = (profile_json("ncu_flops.json") or {}).get(w.name, {}).get("k_kint")
     if fl:
-        # executed FP32 FMA-pipe work counted by ncu (FFMA + FADD + FMUL thread
-        # instructions per launch) over this run's kernel time
+        # the step's fused K6+K7 kernel as ncu counted it: executed FP32
+        # FFMA + FADD + FMUL thread instructions per launch over the ncu
+        # duration of the same launch (cold cache, serialised)
         ex = fl["ffma"] + fl["fadd"] + fl["fmul"]
-        ke.update({"executed_fp32_ops": ex, "executed_frac": ex / (t_kint * 1e-3) / fma_peak,
-                   "executed_source": "profiles/ncu_flops.json"})
-    out.append(ke)
+        ex_peak = (profile_json("alu_peaks.json") or {}).get("fp32_tflops", 2 * fma_peak / 1e12) / 2
+        out.append({"kernel": "k_kint<..., K6 fused> executed FP32 work (ncu)", "bound": "alu",
+                    "us": fl["us"], "executed_fp32_inst": ex,
+                    "achieved": ex / (fl["us"] * 1e-6) / 1e12, "unit": "T inst/s",
+                    "peak": ex_peak, "frac": ex / (fl["us"] * 1e-6) / 1e12 / ex_peak,
+                    "peak_source": "profiles/alu_peaks.json fp32 FMA/s (measured)",
+                    "note": "profiles/ncu_flops.json: FFMA+FADD+FMUL thread instructions; one "
+                            "per FP32 lane-cycle"})
     out.append({"kernel": "k_kint<..., K6 fused> (gradient + normal + kernel integrals)",
                 "bound": "alu", "us": t_both * 1e3,
                 "note": "one kernel: K6 warps beside K7 warps; compare with the two above"})
