@@ -136,6 +136,10 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
     const int64_t stride = (int64_t)gridDim.x * kWB;
     int64_t chunk = (int64_t)blockIdx.x * kWB + w;
     T* io = S.io[w];
+    // far-field constants in the grid dtype (selects, no per-particle fp64)
+    const T far_pos = (T)gc.far, far_neg = -far_pos;
+    // stored background cells < 2^32 (sg_build): 32-bit cell index arithmetic
+    const uint32_t n0 = (uint32_t)gc.n[0], plane = (uint32_t)gc.n[0] * (uint32_t)gc.n[1];
     // persistent warps: the positions of the next chunk are loaded while the
     // current chunk is processed (hides the DRAM latency of the stream)
     T v[12];
@@ -206,8 +210,8 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
 #pragma unroll
         for (int k = 0; k < 3; ++k) ok[j] = cell_of<T, I32>(gc, k, x[j][k], c[j][k]) && ok[j];
         ok[j] = ok[j] && c[j][2] >= gc.z_lo && c[j][2] < gc.z_hi;  // owned planes of a slab
-        b[j] = ok[j] ? __ldg(bg + ((int64_t)(c[j][2] - gc.zs_lo) * gc.n[1] + c[j][1]) * gc.n[0] +
-                             c[j][0])
+        b[j] = ok[j] ? __ldg(bg + ((uint32_t)(c[j][2] - gc.zs_lo) * plane + (uint32_t)c[j][1] * n0 +
+                                   (uint32_t)c[j][0]))
                      : 1u;
     }
     int nband = 0;
@@ -224,7 +228,7 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
             S.pk[w][idx] = b[j];
             S.who[w][idx] = (uint8_t)p;
         } else if (inr) {
-            io[p] = (T)(!ok[j] ? gc.far : (b[j] == 0 ? -gc.far : gc.far));
+            io[p] = (!ok[j] || b[j] != 0) ? far_pos : far_neg;
         }
         nband += __popc(bal);
     }
@@ -246,7 +250,13 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 int ck, a;
-                cell_of<T, I32>(gc, k, xs[3 * p + k], ck);
+                if constexpr (I32) {
+                    // in-domain band particle: the exact x / l_c has no clamp
+                    // to apply (x < upper), as in cell_of<float, true>
+                    ck = __float2int_rd(xs[3 * p + k] * gc.inv_cellf);
+                } else {
+                    cell_of<T, I32>(gc, k, xs[3 * p + k], ck);
+                }
                 corner_of<T, I32>(gc, k, xs[3 * p + k], a, tv[k]);
                 sv[k] = a - 4 * ck;  // in [-1, 3]
             }
