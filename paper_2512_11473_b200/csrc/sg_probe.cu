@@ -207,8 +207,22 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         ok[j] = lane + 32 * j < m;
+        if constexpr (I32) {
+            // exact fp32 path: with lower = 0 and x / l_c exact, x in
+            // [0, upper) <=> floor(x / l_c) in [0, n) -- one unsigned compare
+            // per axis (no clamp can apply); a NaN coordinate (converted to 0
+            // by the floor) is caught by the sum, infinities fall out of range
 #pragma unroll
-        for (int k = 0; k < 3; ++k) ok[j] = cell_of<T, I32>(gc, k, x[j][k], c[j][k]) && ok[j];
+            for (int k = 0; k < 3; ++k) {
+                c[j][k] = __float2int_rd(x[j][k] * gc.inv_cellf);
+                ok[j] = ok[j] && (uint32_t)c[j][k] < (uint32_t)gc.n[k];
+            }
+            const float sum = (x[j][0] + x[j][1]) + x[j][2];
+            ok[j] = ok[j] && sum == sum;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) ok[j] = cell_of<T, I32>(gc, k, x[j][k], c[j][k]) && ok[j];
+        }
         ok[j] = ok[j] && c[j][2] >= gc.z_lo && c[j][2] < gc.z_hi;  // owned planes of a slab
         b[j] = ok[j] ? __ldg(bg + ((uint32_t)(c[j][2] - gc.zs_lo) * plane + (uint32_t)c[j][1] * n0 +
                                    (uint32_t)c[j][0]))
