@@ -70,7 +70,7 @@ def bench_slab(args, w, rank, world, local):
     import torch
     import torch.distributed as dist
 
-    import workloads as W
+    import workloads as W  # noqa: F401
     from . import sg
     from bench import (METRIC, UNIT, REINIT_ITERS, ClockSampler, L2Flush, peaks, workload_name,
                        SWEEP_BYTES_SURVEY)
@@ -79,24 +79,24 @@ def bench_slab(args, w, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     comm = sg.Comm.nccl()
-    npdt = np.float32 if w.dtype == "f32" else np.float64
-    n_all = 0
-    pos_np = np.zeros((0, 3), dtype=npdt)
-    if w.particles:
-        full = W.lattice_particles(w, seed=0, order=args.order, dtype=npdt)
-        n_all = full.shape[0]
-        a, b = share(n_all, world, rank)
-        pos_np = np.ascontiguousarray(full[a:b])
-        del full
+    # every rank generates the workload's particle set on its device and keeps
+    # a contiguous 1/world share (as a loader would hand them out); sg_probe
+    # bins them to their owners
+    full = W.particles(w, seed=0, order=args.order, device="cuda")
+    n_all = int(full.shape[0])
+    a, b = share(n_all, world, rank)
+    d_pos = full[a:b].contiguous()
+    del full
     flush = L2Flush("cuda")
     fields = sg.SG_GRAD | sg.SG_NORMAL | sg.SG_KINT
-    n_local = int(pos_np.shape[0])
-    d_pos = torch.from_numpy(pos_np).cuda()
+    n_local = int(d_pos.shape[0])
+    if w.name == "C5":
+        args.no_e2e = True  # 25 GB of pinned staging per step; the e2e headline is C2's
     d_phi = torch.empty(n_local, dtype=d_pos.dtype, device="cuda")
     d_grad = torch.empty((n_local, 3), dtype=d_pos.dtype, device="cuda")
-    h_pos = torch.from_numpy(pos_np).pin_memory()
-    h_phi = torch.empty(n_local, dtype=d_pos.dtype).pin_memory()
-    h_grad = torch.empty((n_local, 3), dtype=d_pos.dtype).pin_memory()
+    h_pos = d_pos.cpu().pin_memory() if not args.no_e2e else None
+    h_phi = torch.empty(n_local, dtype=d_pos.dtype).pin_memory() if not args.no_e2e else None
+    h_grad = torch.empty((n_local, 3), dtype=d_pos.dtype).pin_memory() if not args.no_e2e else None
 
     def full_step(ev, host=False):
         ev[0].record(stream)

@@ -172,3 +172,30 @@ def test_window_gradient_kernel_probe(sgm, O, name):
     eg3 = egrad
     gg3 = ggrad.cpu().numpy().astype(np.float64)
     assert np.max(np.abs(gg3 - eg3) / np.maximum(1.0, np.abs(eg3))) <= tol
+
+
+@pytest.mark.parametrize("name", ["C5-shell", "C5-small"])
+def test_window_probe_c5_particles(sgm, O, name):
+    """The C5 particle recipe (lattice points inside the shell walls,
+    workloads.shell_lattice_particles) restricted to the window: probe of the
+    uploaded 20-sweep state against the oracle."""
+    win = Win(O, name)
+    w, o, dx = win.w, win.o, win.dx
+    p20 = f32(o.reinit(o.phi_dense(), 20))
+    g = sgm.Grid(w)
+    win.upload(g, p20)
+    g.gradient(sgm.SG_GRAD, h_ratio=w.h_ratio)
+    grad, _ = o.gradient(p20)
+    box = (tuple(4 * v for v in win.lo), tuple(4 * v for v in win.hi))
+    pos = W.shell_lattice_particles(w, box=box, device="cuda")
+    assert pos.shape[0] > 5000
+    gphi, ggrad = g.probe(pos)
+    pos_np = pos.cpu().numpy()
+    ephi, egrad, eoob = o.probe(p20, f32(grad), pos_np)
+    assert eoob == 0
+    # the wall middle (> l_c from both surfaces) is inactive: about half the
+    # wall particles are band particles
+    assert (np.abs(ephi) < o.far).mean() > 0.3
+    assert np.max(np.abs(gphi.cpu().numpy().astype(np.float64) - ephi)) <= 1e-5 * dx
+    gg = ggrad.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(gg - egrad) / np.maximum(1.0, np.abs(egrad))) <= 1e-5

@@ -111,7 +111,10 @@ CONFIGS = {
                    prims=(Prim(TORUS_Y, (0.5, 0.5, 0.5, 0.3, 0.08)),
                           Prim(BOX, (0.5, 0.5, 0.5, 0.1, 0.1, 0.4)))),
     # configs[4]: thin-shell multi-body scene at 4096^3 effective
-    "C5": Workload("C5", (1024, 1024, 1024), 1.0 / 1024, dtype="f32", prims=_multi_shell()),
+    # the particle set: lattice points at dp = dx inside the shell walls
+    # (~8.99e8), shell_lattice_particles below
+    "C5": Workload("C5", (1024, 1024, 1024), 1.0 / 1024, dtype="f32", prims=_multi_shell(),
+                   particles="shell_lattice"),
     # Table 1 shell under reading R-19 (dx = 1/1024)
     "T1": Workload("T1", (256, 256, 256), 1.0 / 256, dtype="f32",
                    prims=(Prim(SHELL, (0.5, 0.5, 0.5, 0.3, 0.31)),)),
@@ -345,3 +348,151 @@ def random_positions(w: Workload, n: int, seed: int = 0, margin: float = 0.0,
     lo = np.array(w.lower) + margin
     hi = np.array(w.lower) + np.array(w.n) * w.cell - margin
     return np.ascontiguousarray(rng.uniform(lo, hi, size=(n, 3)).astype(dtype))
+
+
+# ------------------------------------------------ C5: shell-wall particles --
+_SM_GAMMA = 0x9E3779B97F4A7C15
+_SM_M1 = 0xBF58476D1CE4E5B9
+_SM_M2 = 0x94D049BB133111EB
+
+
+def _i64(c: int) -> int:
+    """a uint64 constant as the int64 with the same bits"""
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+def splitmix64_torch(x):
+    """splitmix64 (same bits as splitmix64 above) on an int64 torch tensor
+    holding uint64 bit patterns: wrapping multiplies, logical shifts."""
+    import torch
+
+    def srl(z, k):
+        return (z >> k) & ((1 << (64 - k)) - 1)
+    z = x + _i64(_SM_GAMMA)
+    z = (z ^ srl(z, 30)) * _i64(_SM_M1)
+    z = (z ^ srl(z, 27)) * _i64(_SM_M2)
+    return z ^ srl(z, 31)
+
+
+def shell_lattice_particles(w: Workload, seed: int = 0, jitter: float = 0.25, z_range=None,
+                            box=None, device="cpu", dtype=None, chunk_planes: int = 256):
+    """C5 particle set: lattice points p_i = (i + 1/2) dp, dp = dx,
+    inside the walls of the scene's shells -- r_in^2 <= |p - c|^2 <= r_out^2
+    for some shell, |p - c|^2 evaluated as ((ex ex + ey ey) + ez ez) in fp64 (a
+    containment predicate, not an SDF) -- in lattice order (z slowest, then y,
+    then x), each coordinate jittered by U(-jitter dp, +jitter dp) from
+    splitmix64(seed ^ (3 L + axis)), L = ix + m (iy + m iz) the LATTICE index
+    (so any sub-range of planes regenerates the same particles).
+    z_range: lattice planes [z0, z1) (default all); box: optional lattice box
+    ((x0, y0, z0), (x1, y1, z1)) restricting the output.  Built row by row:
+    per (shell, lattice row) the wall segments in x are found from the row's
+    distance to the centre, widened by one lattice point each side, and the
+    candidates are tested with the predicate -- no scan of the 4096^3
+    lattice.  Returns an (n, 3) torch tensor on `device`."""
+    import torch
+    dev = torch.device(device)
+    dtype = dtype or (torch.float32 if w.dtype == "f32" else torch.float64)
+    dp = w.dx
+    m = int(round(w.n[0] * w.cell / dp))
+    assert all(int(round(w.n[k] * w.cell / dp)) == m for k in range(3)) and w.lower == (0.0, 0.0, 0.0)
+    shells = [pr.p[:5] for pr in w.prims if pr.kind == SHELL]
+    z0, z1 = (0, m) if z_range is None else (max(0, z_range[0]), min(m, z_range[1]))
+    if box is not None:
+        z0, z1 = max(z0, box[0][2]), min(z1, box[1][2])
+    f64, i64 = torch.float64, torch.int64
+    out = []
+    for za in range(z0, z1, chunk_planes):
+        zb = min(z1, za + chunk_planes)
+        segs = []  # (iz, iy, ia, ib, shell index) rows of int64
+        for si, (cx, cy, cz, ri, ro) in enumerate(shells):
+            iz = torch.arange(za, zb, device=dev, dtype=i64)
+            ez = (iz.to(f64) + 0.5) * dp - cz
+            keep = ez.abs() <= ro
+            iz, ez = iz[keep], ez[keep]
+            if iz.numel() == 0:
+                continue
+            hy = torch.sqrt(torch.clamp(ro * ro - ez * ez, min=0.0))
+            ya = torch.clamp(torch.floor((cy - hy) / dp - 0.5).to(i64) - 1, 0, m - 1)
+            yb = torch.clamp(torch.ceil((cy + hy) / dp - 0.5).to(i64) + 1, 0, m - 1)
+            if box is not None:
+                ya = torch.clamp(ya, min=box[0][1])
+                yb = torch.clamp(yb, max=box[1][1] - 1)
+            cnt = torch.clamp(yb - ya + 1, min=0)
+            rz = torch.repeat_interleave(torch.arange(iz.numel(), device=dev), cnt)
+            if rz.numel() == 0:
+                continue
+            start = torch.cumsum(cnt, 0) - cnt
+            iy = ya[rz] + (torch.arange(rz.numel(), device=dev) - start[rz])
+            ey = (iy.to(f64) + 0.5) * dp - cy
+            d2 = ez[rz] * ez[rz] + ey * ey
+            ho = torch.sqrt(torch.clamp(ro * ro - d2, min=0.0))
+            hin = torch.sqrt(torch.clamp(ri * ri - d2, min=0.0))
+            ok = d2 <= ro * ro
+            izr, iy, ho, hin = iz[rz][ok], iy[ok], ho[ok], hin[ok]
+
+            def lat(v, up):
+                f = v / dp - 0.5
+                return torch.clamp((torch.ceil(f) + 1 if up else torch.floor(f) - 1).to(i64), 0, m - 1)
+            la, lb = lat(cx - ho, False), lat(cx - hin, True)
+            ra, rb = lat(cx + hin, False), lat(cx + ho, True)
+            merged = ra <= lb  # no hole in this row (or margins touch): one segment
+            one = torch.stack([izr, iy, la, torch.where(merged, rb, lb),
+                               torch.full_like(la, si)], 1)
+            two = torch.stack([izr, iy, ra, rb, torch.full_like(la, si)], 1)[~merged]
+            segs += [one, two]
+        if not segs:
+            continue
+        S = torch.cat(segs)
+        if box is not None:
+            S[:, 2] = torch.clamp(S[:, 2], min=box[0][0])
+            S[:, 3] = torch.clamp(S[:, 3], max=box[1][0] - 1)
+            S = S[S[:, 3] >= S[:, 2]]
+        key = (S[:, 0] * m + S[:, 1]) * m + S[:, 2]
+        S = S[torch.argsort(key)]
+        cnt = S[:, 3] - S[:, 2] + 1
+        rs = torch.repeat_interleave(torch.arange(S.shape[0], device=dev), cnt)
+        start = torch.cumsum(cnt, 0) - cnt
+        ix = S[rs, 2] + (torch.arange(rs.numel(), device=dev) - start[rs])
+        iy, iz, sh = S[rs, 1], S[rs, 0], S[rs, 4]
+        del rs, start
+        P = torch.tensor(shells, dtype=f64, device=dev)
+        x = (ix.to(f64) + 0.5) * dp
+        y = (iy.to(f64) + 0.5) * dp
+        z = (iz.to(f64) + 0.5) * dp
+        ex, ey, ez = x - P[sh, 0], y - P[sh, 1], z - P[sh, 2]
+        d2 = (ex * ex + ey * ey) + ez * ez
+        keep = (d2 >= P[sh, 3] * P[sh, 3]) & (d2 <= P[sh, 4] * P[sh, 4])
+        del ex, ey, ez, d2, sh
+        ix, iy, iz, x, y, z = ix[keep], iy[keep], iz[keep], x[keep], y[keep], z[keep]
+        if jitter:
+            L = ix + m * (iy + m * iz)
+            pos = torch.stack([x, y, z], 1)
+            for a in range(3):
+                r = splitmix64_torch(seed ^ (3 * L + a))
+                u = ((r >> 11) & ((1 << 53) - 1)).to(f64) * (1.0 / 9007199254740992.0)
+                pos[:, a] += (u - 0.5) * (2.0 * jitter * dp)
+        else:
+            pos = torch.stack([x, y, z], 1)
+        out.append(pos.to(dtype))
+        del ix, iy, iz, x, y, z, pos
+    if not out:
+        return torch.zeros((0, 3), dtype=dtype, device=dev)
+    return torch.cat(out).contiguous()
+
+
+def particles(w: Workload, seed: int = 0, order: str = "lattice", device="cpu", dtype=None):
+    """The workload's particle set as an (n, 3) torch tensor on `device`
+    (C4: lattice_particles; C5: shell_lattice_particles, generated on the
+    device); empty if the workload has none."""
+    import torch
+    npdt = np.float32 if w.dtype == "f32" else np.float64
+    tdt = dtype or (torch.float32 if w.dtype == "f32" else torch.float64)
+    if not w.particles:
+        return torch.zeros((0, 3), dtype=tdt, device=device)
+    if w.particles == "shell_lattice":
+        p = shell_lattice_particles(w, seed=seed, device=device, dtype=tdt)
+        if order == "shuffled":
+            g = torch.Generator(device="cpu").manual_seed(seed + 1)
+            p = p[torch.randperm(p.shape[0], generator=g).to(p.device)]
+        return p
+    return torch.from_numpy(lattice_particles(w, seed=seed, order=order, dtype=npdt)).to(device)
