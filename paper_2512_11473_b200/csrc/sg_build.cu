@@ -1171,12 +1171,14 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
 
 extern "C" sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, const sg_slab* slab,
                               void* stream, sg_grid** out) {
-    return guard([&] { build_impl(desc, geom, slab, nullptr, stream, out); });
+    return guard([&] {
+        NvtxRange nvtx_("sg_build"); build_impl(desc, geom, slab, nullptr, stream, out); });
 }
 
 extern "C" sg_status sg_build_ex(const sg_desc* desc, const sg_geometry* geom,
                                  const sg_build_opts* opts, void* stream, sg_grid** out) {
     return guard([&] {
+        NvtxRange nvtx_("sg_build_ex");
         const sg_build_opts o = opts ? *opts : sg_build_opts{nullptr, nullptr, nullptr};
         build_impl(desc, geom, o.slab, nullptr, stream, out, o.comm, o.allocator);
     });
@@ -1193,6 +1195,7 @@ extern "C" sg_status sg_pool_trim(void) {
 extern "C" sg_status sg_build_refined(const sg_grid* parent, const sg_geometry* geom, void* stream,
                                       sg_grid** out) {
     return guard([&] {
+        NvtxRange nvtx_("sg_build_refined");
         SG_ARG(parent != nullptr && geom != nullptr, "sg_build_refined: null argument");
         SG_ARG(parent->gc.zs_lo == 0 && parent->gc.zs_hi == parent->gc.n[2] && parent->id_base == 2,
                "sg_build_refined: single-domain parent grids only");
@@ -1239,6 +1242,7 @@ extern "C" void sg_destroy(sg_grid* grid) {
 
 extern "C" sg_status sg_destroy_async(sg_grid* grid, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_("sg_destroy_async");
         if (!grid) return;
         free_grid(grid, (cudaStream_t)stream, true);
         SG_CUDA(cudaGetLastError());
@@ -1365,6 +1369,7 @@ static void plane_counts(const sg_desc* desc, const sg_geometry* geom, int32_t z
 extern "C" sg_status sg_plane_counts(const sg_desc* desc, const sg_geometry* geom, int32_t z_lo,
                                      int32_t z_hi, int64_t* counts, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_("sg_plane_counts");
         check_desc(desc, geom);
         SG_ARG(geom->n_tris == 0, "sg_plane_counts: mesh geometries are single-domain only");
         SG_ARG(counts != nullptr, "sg_plane_counts: null counts");

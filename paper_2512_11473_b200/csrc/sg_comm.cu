@@ -349,6 +349,7 @@ extern "C" sg_status sg_comm_unique_id(void* id) {
 
 extern "C" sg_status sg_comm_create(const void* id, int32_t rank, int32_t nranks, sg_comm** out) {
     return guard([&] {
+        NvtxRange nvtx_("sg_comm_create");
         SG_ARG(id && out, "sg_comm_create: null argument");
         *out = nullptr;
         SG_ARG(nranks >= 1 && nranks <= SG_MAX_RANKS && rank >= 0 && rank < nranks,
@@ -367,6 +368,7 @@ extern "C" sg_status sg_comm_create(const void* id, int32_t rank, int32_t nranks
 
 extern "C" sg_status sg_comm_create_local(int32_t nranks, sg_comm** comms) {
     return guard([&] {
+        NvtxRange nvtx_("sg_comm_create_local");
         SG_ARG(comms != nullptr, "sg_comm_create_local: null comms");
         SG_ARG(nranks >= 1 && nranks <= SG_MAX_RANKS, "sg_comm_create_local: bad nranks");
         auto grp = std::make_shared<LocalGroup>();

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -86,6 +87,13 @@ void clear_last_error();
     do {                                                            \
         if (!(cond)) throw ::sg::Error(SG_ERR_ARG, msg);            \
     } while (0)
+
+// NVTX range over one C-ABI call (header-only NVTX v3: free unless a tool
+// such as nsys / ncu attaches)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 template <class F>
 sg_status guard(F&& f) {

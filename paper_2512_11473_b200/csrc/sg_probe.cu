@@ -735,6 +735,7 @@ using namespace sg;
 extern "C" sg_status sg_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void* grad,
                               unsigned long long* oob_count, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_("sg_probe");
         SG_ARG(g != nullptr, "sg_probe: null grid");
         SG_ARG(n >= 0, "sg_probe: n must be >= 0");
         if (n == 0 && !g->partitioned()) return;  // (collective on a partition)

@@ -339,6 +339,7 @@ using namespace sg;
 extern "C" sg_status sg_relax(sg_grid* g, int64_t n, void* pos, const sg_relax_params* p,
                               void* stream) {
     return guard([&] {
+        NvtxRange nvtx_("sg_relax");
         SG_ARG(g != nullptr && p != nullptr, "sg_relax: null argument");
         SG_ARG(n >= 0 && (n == 0 || pos != nullptr), "sg_relax: bad particle buffer");
         // cell-list slots and prefix sums are int32

@@ -390,6 +390,7 @@ using namespace sg;
 extern "C" sg_status sg_sign_correct(sg_grid* g, double tau, int32_t max_sweeps, int32_t* sweeps,
                                      void* stream) {
     return guard([&] {
+        NvtxRange nvtx_("sg_sign_correct");
         SG_ARG(g != nullptr, "sg_sign_correct: null grid");
         SG_ARG(tau > 0.0 && std::isfinite(tau), "sg_sign_correct: tau must be > 0");
         SG_ARG(g->gc.zs_lo == 0 && g->gc.zs_hi == g->gc.n[2] && g->id_base == 2,

@@ -1019,6 +1019,7 @@ using namespace sg;
 
 extern "C" sg_status sg_reinit(sg_grid* g, int32_t iters, double cfl, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_("sg_reinit");
         SG_ARG(g != nullptr, "sg_reinit: null grid");
         SG_ARG(iters >= 0, "sg_reinit: iters must be >= 0");
         SG_ARG(cfl > 0.0 && cfl <= 0.5, "sg_reinit: cfl must be in (0, 0.5]");
@@ -1030,6 +1031,7 @@ extern "C" sg_status sg_reinit(sg_grid* g, int32_t iters, double cfl, void* stre
 
 extern "C" sg_status sg_reinit_halo(sg_grid* g, int32_t iters, double cfl, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_("sg_reinit_halo");
         SG_ARG(g != nullptr, "sg_reinit_halo: null grid");
         SG_ARG(iters >= 0, "sg_reinit_halo: iters must be >= 0");
         SG_ARG(cfl > 0.0 && cfl <= 0.5, "sg_reinit_halo: cfl must be in (0, 0.5]");
@@ -1041,6 +1043,7 @@ extern "C" sg_status sg_reinit_halo(sg_grid* g, int32_t iters, double cfl, void*
 
 extern "C" sg_status sg_gradient(sg_grid* g, uint32_t fields, double h_ratio, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_("sg_gradient");
         SG_ARG(g != nullptr, "sg_gradient: null grid");
         SG_ARG(fields != 0 && (fields & ~7u) == 0, "sg_gradient: fields must be a non-empty OR of SG_GRAD/SG_NORMAL/SG_KINT");
         if (fields & SG_KINT)
@@ -1052,6 +1055,7 @@ extern "C" sg_status sg_gradient(sg_grid* g, uint32_t fields, double h_ratio, vo
 
 extern "C" sg_status sg_table1(sg_grid* g, int32_t op, double value, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_("sg_table1");
         SG_ARG(g != nullptr, "sg_table1: null grid");
         SG_ARG(op == 0 || op == 1, "sg_table1: op must be 0 (sequential) or 1 (stencil)");
         SG_CUDA(cudaGetLastError());

@@ -1,0 +1,51 @@
+"""compute-sanitizer over every C-ABI entry point (memcheck,
+racecheck, synccheck) on C1-sized inputs, plus a positive control: an
+undersized output buffer must be reported by memcheck."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _sanitizer():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(exe):
+        pytest.skip("compute-sanitizer not installed")
+    from paper_2512_11473_b200 import build
+    build.build()
+    return exe
+
+
+def _run(exe, tool, script, extra=()):
+    r = subprocess.run([exe, "--tool", tool, *extra, "--target-processes", "all",
+                        "--print-limit", "20", sys.executable, script], cwd=ROOT,
+                       capture_output=True, text=True, timeout=900)
+    return r.returncode, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("tool,extra", [("memcheck", ("--leak-check", "no")), ("racecheck", ()),
+                                        ("synccheck", ())])
+def test_sanitizer_clean(tool, extra):
+    exe = _sanitizer()
+    rc, out = _run(exe, tool, "scripts/sanitize_run.py", extra)
+    assert "sanitize_run ok" in out, out[-3000:]
+    if tool == "racecheck":
+        assert "RACECHECK SUMMARY: 0 hazards" in out, out[-3000:]
+    else:
+        assert "ERROR SUMMARY: 0 errors" in out, out[-3000:]
+    assert rc == 0
+
+
+def test_memcheck_catches_undersized_output():
+    exe = _sanitizer()
+    rc, out = _run(exe, "memcheck", "scripts/sanitize_negative.py", ("--leak-check", "no"))
+    assert "Invalid __global__ write" in out or "Invalid __global__ write" in out.replace("  ", " "), \
+        out[-3000:]
