@@ -214,8 +214,9 @@ template <int NZ>
 __device__ __forceinline__ void sd_eval_col_mask(const Geom& g, uint32_t mask, double x, double y,
                                                  const double (&z)[NZ], double (&f)[NZ]) {
     bool first = true;
-    for (int i = 0; i < g.n; ++i) {
-        if (!((mask >> i) & 1u)) continue;
+    // the selected primitives in ascending order (set bits only)
+    for (uint32_t mm = mask; mm; mm &= mm - 1u) {
+        const int i = __ffs(mm) - 1;
         double fi[NZ];
         sd_prim_col<NZ>(g.kind[i], g.p[i], x, y, z, fi);
 #pragma unroll
@@ -285,8 +286,8 @@ template <int NY>
 __device__ __forceinline__ void sd_eval_coly_mask(const Geom& g, uint32_t mask, double x, double z,
                                                   const double (&y)[NY], double (&f)[NY]) {
     bool first = true;
-    for (int i = 0; i < g.n; ++i) {
-        if (!((mask >> i) & 1u)) continue;
+    for (uint32_t mm = mask; mm; mm &= mm - 1u) {
+        const int i = __ffs(mm) - 1;
         double fi[NY];
         sd_prim_coly<NY>(g.kind[i], g.p[i], x, z, y, fi);
 #pragma unroll

@@ -640,15 +640,15 @@ __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
         const unsigned hm = 0xFFFFu << (lane & 16);  // this package's half-warp
         const double fmine =
             col < geom.n ? sd_prim(geom.kind[col], geom.p[col], pcx, pcy, pcz) : 0.0;
-        double fc[SG_MAX_PRIMS];
-        double m = 0.0;
-        for (int i = 0; i < geom.n; ++i) {
-            fc[i] = __shfl_sync(hm, fmine, (lane & 16) + i);
-            m = i == 0 ? fc[i] : fmin(m, fc[i]);
-        }
-        mask = 0;
-        for (int i = 0; i < geom.n; ++i)
-            if (fc[i] - R <= m + R + eps) mask |= 1u << i;
+        // m = min over the primitives by a butterfly over the half-warp (fmin
+        // is exact, so the order does not matter), then each lane decides its
+        // own primitive and one ballot forms the mask -- instead of every lane
+        // walking all primitives
+        double m = col < geom.n ? fmine : INFINITY;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) m = fmin(m, __shfl_xor_sync(hm, m, o));
+        const bool keep = col < geom.n && fmine - R <= m + R + eps;
+        mask = (__ballot_sync(hm, keep) >> (lane & 16)) & 0xFFFFu;
     }
     if constexpr (AX == 2) {
         if (geom.n == 1) sd_eval_col<4>(geom, x, bb, w, f);
