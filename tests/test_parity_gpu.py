@@ -620,8 +620,8 @@ def test_probe_lower_face_fp32(sgm, O):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    tmp = os.path.join(root, "gpurun_out", "lowface_idx64.npz")
-    os.makedirs(os.path.dirname(tmp), exist_ok=True)
+    import tempfile
+    tmp = os.path.join(tempfile.mkdtemp(), "lowface_idx64.npz")
     code = (
         "import numpy as np, torch, sys\n"
         "sys.path.insert(0, 'tests')\n"
@@ -684,3 +684,30 @@ def test_table1_add_invalidates_derived_fields(sgm):
     g.gradient(sgm.SG_GRAD)
     phi2, _ = g.probe(pos)
     assert torch.equal(phi, phi2)
+
+
+def test_probe_chunk_queue_order_bitwise(sgm):
+    """The probe's in-order chunk queue (used for long particle streams such
+    as C5's) gives the static order's results bit for bit (C4 on C2, forced
+    with SG_PROBE_QUEUE=1 in a fresh process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for q in ("0", "1"):
+        import tempfile
+        tmp = os.path.join(tempfile.mkdtemp(), f"probe_queue{q}.npz")
+        code = ("import numpy as np, torch, workloads as W\n"
+                "from paper_2512_11473_b200 import sg\n"
+                "w = W.config('C2'); g = sg.Grid(w); g.reinit(3).gradient(sg.SG_GRAD)\n"
+                "pos = W.particles(w, device='cuda')\n"
+                "oob = torch.zeros(1, dtype=torch.int64, device='cuda')\n"
+                "p, gr = g.probe(pos, oob=oob)\n"
+                f"np.savez({tmp!r}, phi=p.cpu().numpy(), grad=gr.cpu().numpy(), oob=oob.cpu().numpy())\n")
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                           timeout=300, env=dict(os.environ, SG_PROBE_QUEUE=q))
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[q] = np.load(tmp)
+    for k in ("phi", "grad", "oob"):
+        assert np.array_equal(out["0"][k], out["1"][k]), k
