@@ -45,6 +45,15 @@ __device__ __forceinline__ void ld_row(const double* __restrict__ p, double (&r)
     r[2] = b.x;
     r[3] = b.y;
 }
+__device__ __forceinline__ void ld_row_s(const float* p, float (&r)[4]) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
+}
+__device__ __forceinline__ void ld_row_s(const double* p, double (&r)[4]) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0];
+    const double2 b = reinterpret_cast<const double2*>(p)[1];
+    r[0] = a.x; r[1] = a.y; r[2] = b.x; r[3] = b.y;
+}
 __device__ __forceinline__ void st_row(float* p, const float (&r)[4]) {
     *reinterpret_cast<float4*>(p) = make_float4(r[0], r[1], r[2], r[3]);
 }
@@ -90,6 +99,50 @@ __device__ __forceinline__ bool load_cross(const T* __restrict__ in,
     ld_row(j < 3 ? P + 4 * (r + 1) : in + (int64_t)nyp * 64 + 4 * (0 + 4 * k), x.yp);
     ld_row(k > 0 ? P + 4 * (r - 4) : in + (int64_t)nzm * 64 + 4 * (j + 12), x.zm);
     ld_row(k < 3 ? P + 4 * (r + 4) : in + (int64_t)nzp * 64 + 4 * j, x.zp);
+    x.xm = __ldg(in + (int64_t)nxm * 64 + 4 * r + 3);
+    x.xp = __ldg(in + (int64_t)nxp * 64 + 4 * r);
+    return true;
+}
+
+// The same cross with the in-package y / z neighbour rows taken from the
+// lanes that own them (warp shuffles within the package's 16-lane group):
+// only lanes on a package face load a row of the face neighbour.  Every
+// lane loads one own row instead of five -- k_gradient was L1-bound (ncu:
+// L1/TEX throughput 79 %, DRAM 48 %) on the four redundant row loads.
+template <class T>
+__device__ __forceinline__ void shfl_row(const T (&src)[4], int lane, T (&dst)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dst[i] = __shfl_sync(0xffffffffu, src[i], lane);
+}
+
+template <class T>
+__device__ __forceinline__ bool load_cross_s(const T* __restrict__ in,
+                                             const uint32_t* __restrict__ face, int64_t pkg,
+                                             bool valid, Cross<T>& x) {
+    const int r = threadIdx.x & 15;
+    const int j = r & 3, k = r >> 2;
+    uint32_t f = 0;
+    if (valid && r < 6) f = __ldg(face + pkg * 8 + r);
+    const int base = threadIdx.x & 16;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nxm = __shfl_sync(0xffffffffu, f, base + 0);
+    const uint32_t nxp = __shfl_sync(0xffffffffu, f, base + 1);
+    const uint32_t nym = __shfl_sync(0xffffffffu, f, base + 2);
+    const uint32_t nyp = __shfl_sync(0xffffffffu, f, base + 3);
+    const uint32_t nzm = __shfl_sync(0xffffffffu, f, base + 4);
+    const uint32_t nzp = __shfl_sync(0xffffffffu, f, base + 5);
+    const T* P = in + pkg * 64;
+    if (valid) ld_row(P + 4 * r, x.c);
+    // every lane takes part in the shuffles (the caller's groups are whole)
+    shfl_row(x.c, j > 0 ? lane - 1 : lane, x.ym);
+    shfl_row(x.c, j < 3 ? lane + 1 : lane, x.yp);
+    shfl_row(x.c, k > 0 ? lane - 4 : lane, x.zm);
+    shfl_row(x.c, k < 3 ? lane + 4 : lane, x.zp);
+    if (!valid) return false;
+    if (j == 0) ld_row(in + (int64_t)nym * 64 + 4 * (3 + 4 * k), x.ym);
+    if (j == 3) ld_row(in + (int64_t)nyp * 64 + 4 * (0 + 4 * k), x.yp);
+    if (k == 0) ld_row(in + (int64_t)nzm * 64 + 4 * (j + 12), x.zm);
+    if (k == 3) ld_row(in + (int64_t)nzp * 64 + 4 * j, x.zp);
     x.xm = __ldg(in + (int64_t)nxm * 64 + 4 * r + 3);
     x.xp = __ldg(in + (int64_t)nxp * 64 + 4 * r);
     return true;
@@ -347,15 +400,16 @@ template <class T>
 __device__ __forceinline__ void grad_package(const T* __restrict__ in, T* __restrict__ grad,
                                              T* __restrict__ normal,
                                              const uint32_t* __restrict__ face, int64_t pkg,
-                                             bool valid, const StC<T>& c);
+                                             bool valid, const StC<T>& c, T* tile);
 
 template <class T>
 __global__ void __launch_bounds__(256) k_gradient(const T* __restrict__ in, T* __restrict__ grad,
                                                   T* __restrict__ normal,
                                                   const uint32_t* __restrict__ face, int64_t lo,
                                                   int64_t hi, StC<T> c) {
+    __shared__ __align__(16) T s_tile[16][256];
     const int64_t pkg = lo + (((int64_t)blockIdx.x * 256 + threadIdx.x) >> 4);
-    grad_package(in, grad, normal, face, pkg, pkg < hi, c);
+    grad_package(in, grad, normal, face, pkg, pkg < hi, c, s_tile[threadIdx.x >> 4]);
 }
 
 // K6 for one x-row (lane r = threadIdx.x & 15 of a 16-lane group) of `pkg`
@@ -363,9 +417,9 @@ template <class T>
 __device__ __forceinline__ void grad_package(const T* __restrict__ in, T* __restrict__ grad,
                                              T* __restrict__ normal,
                                              const uint32_t* __restrict__ face, int64_t pkg,
-                                             bool valid, const StC<T>& c) {
+                                             bool valid, const StC<T>& c, T* tile) {
     Cross<T> x;
-    if (!load_cross(in, face, pkg, valid, x)) return;
+    if (!load_cross_s(in, face, pkg, valid, x)) return;
     T gx[4], gy[4], gz[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -377,9 +431,22 @@ __device__ __forceinline__ void grad_package(const T* __restrict__ in, T* __rest
     }
     const int r = threadIdx.x & 15;
     if (grad) {
-        T* G = grad + pkg * 256 + 16 * r;
+        // (phi, grad) of the row's 4 points are 64 contiguous bytes per lane;
+        // stored directly, each store instruction would hit a 16 B piece of
+        // 16 lines (ncu: k_gradient L1-bound on store wavefronts).  Through
+        // the package's shared tile the 16 lanes store 256 contiguous bytes
+        // per instruction.
 #pragma unroll
-        for (int i = 0; i < 4; ++i) st_vec4(G + 4 * i, x.c[i], gx[i], gy[i], gz[i]);
+        for (int i = 0; i < 4; ++i) st_vec4(tile + 4 * (4 * r + i), x.c[i], gx[i], gy[i], gz[i]);
+        __syncwarp(0xFFFFu << (threadIdx.x & 16));
+        T* G = grad + pkg * 256;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int d = r + 16 * i;
+            T v[4];
+            ld_row_s(tile + 4 * d, v);
+            st_vec4(G + 4 * d, v[0], v[1], v[2], v[3]);
+        }
     }
     if (normal) {
         T nx[4], ny[4], nz[4];
@@ -404,7 +471,7 @@ __global__ void __launch_bounds__(256) k_laplace(const T* __restrict__ in, T* __
                                                  int64_t hi, T inv_dx2) {
     const int64_t pkg = lo + (((int64_t)blockIdx.x * 256 + threadIdx.x) >> 4);
     Cross<T> x;
-    if (!load_cross(in, face, pkg, pkg < hi, x)) return;
+    if (!load_cross_s(in, face, pkg, pkg < hi, x)) return;
     T o[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -506,8 +573,9 @@ __global__ void __launch_bounds__(GR ? 256 : 128) k_kint(const T* __restrict__ i
                                               StC<T> cs = StC<T>{}) {
     if constexpr (GR) {
         if (threadIdx.x >= 128) {
+            __shared__ __align__(16) T s_gtile[8][256];
             const int64_t pkg = lo + (int64_t)blockIdx.x * 8 + ((threadIdx.x - 128) >> 4);
-            grad_package(in, grad, normal, face, pkg, pkg < hi, cs);
+            grad_package(in, grad, normal, face, pkg, pkg < hi, cs, s_gtile[(threadIdx.x - 128) >> 4]);
             return;
         }
     }
@@ -913,7 +981,9 @@ static void launch_kint_r(sg_grid* g, const T* phi, const KintC<T>& c, cudaStrea
         if (c.wt[7] == T(0) && c.wt[8] == T(0))  // |o|^2 = 8 outside the support
             kern = gr ? k_kint<T, 2, 6, true> : k_kint<T, 2, 6, false>;
     }
-    if (smem > 48 * 1024)
+    // dynamic + static (the fused K6 warps' store tiles) above the 48 KB
+    // default needs the opt-in (fp64 at R >= 2)
+    if (smem + (gr ? 8 * 256 * sizeof(T) : 0) + 8 * 28 * 4 > 48 * 1024)
         SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)ceil_div(hi - lo, 8), gr ? 256 : 128, smem, s>>>(
         phi, g->nb, lo, hi, c, (T*)g->kint, (T*)g->gkint, gp, np, g->face, cs);
