@@ -434,9 +434,15 @@ static bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// host-buffer pipeline: an upload stream, a compute stream and a download
+// stream over a ring of kRing device chunk buffers, so both copy engines
+// stream continuously (a per-chunk upload only waits for its buffer's
+// previous download)
+constexpr int kRing = 4;
 struct Staging {
-    cudaStream_t st[2] = {nullptr, nullptr};
+    cudaStream_t up = nullptr, comp = nullptr, down = nullptr, down2 = nullptr;
     cudaEvent_t ev = nullptr;
+    cudaEvent_t ev_up[kRing], ev_comp[kRing], ev_down[kRing], ev_down2[kRing];
 };
 
 // staging streams and event per host thread and device: concurrent host-
@@ -450,9 +456,17 @@ static Staging& staging() {
     if ((int)per_dev.size() <= dev) per_dev.resize(dev + 1);
     Staging& S = per_dev[dev];
     if (!S.ev) {
-        SG_CUDA(cudaStreamCreateWithFlags(&S.st[0], cudaStreamNonBlocking));
-        SG_CUDA(cudaStreamCreateWithFlags(&S.st[1], cudaStreamNonBlocking));
+        SG_CUDA(cudaStreamCreateWithFlags(&S.up, cudaStreamNonBlocking));
+        SG_CUDA(cudaStreamCreateWithFlags(&S.comp, cudaStreamNonBlocking));
+        SG_CUDA(cudaStreamCreateWithFlags(&S.down, cudaStreamNonBlocking));
+        SG_CUDA(cudaStreamCreateWithFlags(&S.down2, cudaStreamNonBlocking));
         SG_CUDA(cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming));
+        for (int b = 0; b < kRing; ++b) {
+            SG_CUDA(cudaEventCreateWithFlags(&S.ev_up[b], cudaEventDisableTiming));
+            SG_CUDA(cudaEventCreateWithFlags(&S.ev_comp[b], cudaEventDisableTiming));
+            SG_CUDA(cudaEventCreateWithFlags(&S.ev_down[b], cudaEventDisableTiming));
+            SG_CUDA(cudaEventCreateWithFlags(&S.ev_down2[b], cudaEventDisableTiming));
+        }
     }
     return S;
 }
@@ -749,39 +763,54 @@ void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void*
     SG_ARG(!is_device_ptr(pos) && !is_device_ptr(phi) && (grad == nullptr || !is_device_ptr(grad)),
            "sg_probe: pos/phi/grad must be all device or all host pointers");
     Staging& S = staging();
-    // ~16 chunks (0.25-2 M particles): short pipeline fill and drain
+    // ~32 chunks (0.25-2 M particles): short pipeline fill and drain
     const int64_t chunk = std::min<int64_t>(
-        n, std::max<int64_t>((int64_t)1 << 18, std::min<int64_t>(ceil_div(n, 16), (int64_t)1 << 21)));
+        n, std::max<int64_t>((int64_t)1 << 18, std::min<int64_t>(ceil_div(n, 32), (int64_t)1 << 21)));
     const size_t es = (size_t)g->esz;
-    char* buf[2];
     const size_t per = chunk * es * (3 + 1 + (grad ? 3 : 0));
     // the uploads of the positions do not depend on the grid: only the probe
     // kernels wait for the caller's stream (the build / reinit / gradient
     // still running there), so the first chunks' H2D overlap that work
     SG_CUDA(cudaEventRecord(S.ev, s));
-    for (int b = 0; b < 2; ++b) buf[b] = (char*)dalloc(per, S.st[b]);
+    SG_CUDA(cudaStreamWaitEvent(S.comp, S.ev, 0));
+    char* ring = (char*)dalloc(per * kRing, S.up);
+    SG_CUDA(cudaEventRecord(S.ev_up[0], S.up));  // the ring exists on up
+    SG_CUDA(cudaStreamWaitEvent(S.comp, S.ev_up[0], 0));
+    SG_CUDA(cudaStreamWaitEvent(S.down, S.ev_up[0], 0));
+    SG_CUDA(cudaStreamWaitEvent(S.down2, S.ev_up[0], 0));
     const char* hp = (const char*)pos;
     char* ho = (char*)phi;
     char* hg = (char*)grad;
     int64_t k = 0;
     for (int64_t off = 0; off < n; off += chunk, ++k) {
-        const int b = (int)(k & 1);
+        const int b = (int)(k % kRing);
         const int64_t m = std::min(chunk, n - off);
-        cudaStream_t st = S.st[b];
-        char* dp = buf[b];
+        char* dp = ring + per * b;
         char* dphi = dp + chunk * es * 3;
         char* dg = dphi + chunk * es;
-        SG_CUDA(cudaMemcpyAsync(dp, hp + off * 3 * es, m * 3 * es, cudaMemcpyHostToDevice, st));
-        if (k < 2) SG_CUDA(cudaStreamWaitEvent(st, S.ev, 0));  // grid fields ready
-        run(m, dp, dphi, grad ? dg : nullptr, st);
-        SG_CUDA(cudaMemcpyAsync(ho + off * es, dphi, m * es, cudaMemcpyDeviceToHost, st));
+        // buffer b is free once the download of chunk k - kRing is done
+        if (k >= kRing) {
+            SG_CUDA(cudaStreamWaitEvent(S.up, S.ev_down[b], 0));
+            SG_CUDA(cudaStreamWaitEvent(S.up, S.ev_down2[b], 0));
+        }
+        SG_CUDA(cudaMemcpyAsync(dp, hp + off * 3 * es, m * 3 * es, cudaMemcpyHostToDevice, S.up));
+        SG_CUDA(cudaEventRecord(S.ev_up[b], S.up));
+        SG_CUDA(cudaStreamWaitEvent(S.comp, S.ev_up[b], 0));
+        run(m, dp, dphi, grad ? dg : nullptr, S.comp);
+        SG_CUDA(cudaEventRecord(S.ev_comp[b], S.comp));
+        // phi and grad come back on two download streams (two copy engines)
+        SG_CUDA(cudaStreamWaitEvent(S.down, S.ev_comp[b], 0));
+        SG_CUDA(cudaMemcpyAsync(ho + off * es, dphi, m * es, cudaMemcpyDeviceToHost, S.down));
+        SG_CUDA(cudaEventRecord(S.ev_down[b], S.down));
+        SG_CUDA(cudaStreamWaitEvent(S.down2, S.ev_comp[b], 0));
         if (grad)
-            SG_CUDA(cudaMemcpyAsync(hg + off * 3 * es, dg, m * 3 * es, cudaMemcpyDeviceToHost, st));
+            SG_CUDA(cudaMemcpyAsync(hg + off * 3 * es, dg, m * 3 * es, cudaMemcpyDeviceToHost, S.down2));
+        SG_CUDA(cudaEventRecord(S.ev_down2[b], S.down2));
     }
-    for (int b = 0; b < 2; ++b) {
-        SG_CUDA(cudaFreeAsync(buf[b], S.st[b]));
-        SG_CUDA(cudaStreamSynchronize(S.st[b]));
-    }
+    SG_CUDA(cudaEventRecord(S.ev, S.down2));
+    SG_CUDA(cudaStreamWaitEvent(S.down, S.ev, 0));
+    SG_CUDA(cudaFreeAsync(ring, S.down));
+    SG_CUDA(cudaStreamSynchronize(S.down));
 }
 
 }  // namespace sg
