@@ -209,3 +209,43 @@ def test_nccl_communicator_one_rank(sgm):
     assert torch.equal(g.view("phi"), ref.view("phi"))
     g.close()
     comm.close()
+
+
+@pytest.mark.parametrize("seed,n,P,iters", [(1, 24, 2, 6), (3, 20, 3, 9), (5, 31, 5, 4), (7, 17, 4, 13),
+                                            (9, 40, 3, 20)])
+def test_partitioned_random_scenes(sgm, seed, n, P, iters):
+    """Random unions (some bands touching the domain boundary, fp32 / fp64),
+    P ranks with uneven particle shares and out-of-domain positions: every
+    owned field and every probe result equals the 1-GPU grid's bits."""
+    w = W.random_scene(seed, n, dtype="f64" if seed % 4 == 1 else "f32")
+    fields = sgm.SG_GRAD | sgm.SG_NORMAL | sgm.SG_KINT
+    dt = np.float32 if w.dtype == "f32" else np.float64
+    pos_np = W.random_positions(w, 50000, seed=seed, dtype=dt)
+    pos_np[::997] = -1.0  # out of the domain
+    full = sgm.Grid(w)
+    full.reinit(iters, w.cfl).gradient(fields, w.h_ratio)
+    pos = torch.from_numpy(pos_np).cuda()
+    fphi, fgrad = full.probe(pos)
+    rng = np.random.default_rng(seed)
+    cuts = np.sort(rng.integers(0, pos_np.shape[0], P - 1))
+    sh = list(zip([0, *cuts], [*cuts, pos_np.shape[0]]))
+
+    def body(r, comm, st):
+        g = sgm.Grid(w, comm=comm, stream=st)
+        g.reinit(iters, w.cfl, stream=st).gradient(fields, w.h_ratio, stream=st)
+        a, b = sh[r]
+        phi, grad = g.probe(pos[a:b].contiguous(), stream=st)
+        st.synchronize()
+        info = g.info
+        lo, hi = info["own_lo"], info["own_hi"]
+        own = {f: g.view(f)[lo:hi].clone() for f in ("phi", "grad", "normal", "kint", "gkint")}
+        g.close()
+        return info, own, phi.clone(), grad.clone()
+
+    out = run_ranks(P, body)
+    for info, own, _, _ in out:
+        ga, gb = info["own_lo"] - 2 + info["id_base"], info["own_hi"] - 2 + info["id_base"]
+        for f, v in own.items():
+            assert torch.equal(v, full.view(f)[ga:gb]), f
+    assert torch.equal(torch.cat([o[2] for o in out]), fphi)
+    assert torch.equal(torch.cat([o[3] for o in out]), fgrad)
