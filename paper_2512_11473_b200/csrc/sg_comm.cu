@@ -137,6 +137,7 @@ namespace sg {
 
 int comm_rank(const sg_comm* c) { return c ? c->rank : 0; }
 int comm_size(const sg_comm* c) { return c ? c->nranks : 1; }
+int comm_kind(const sg_comm* c) { return c ? c->kind : SG_COMM_LOCAL; }
 
 // SG_COMM_TRACE=1: one stderr line per collective step (debugging hangs)
 static bool trace() {

@@ -134,6 +134,7 @@ struct P2P {
 void comm_group(const sg_comm* c, const P2P* ops, int n, cudaStream_t s);
 int comm_rank(const sg_comm* c);
 int comm_size(const sg_comm* c);
+int comm_kind(const sg_comm* c);  // SG_COMM_NCCL / SG_COMM_LOCAL
 // the z-slab plan (sg_slab_plan)
 void slab_plan(const int64_t* counts, int32_t nz, int32_t nranks, int32_t rank, sg_plan_t* p,
                int32_t* cuts);

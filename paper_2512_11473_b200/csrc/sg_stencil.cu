@@ -814,8 +814,10 @@ static bool reinit_launch(sg_grid* g, int cur, const StC<T>& c, int64_t lo, int6
 // hands them to the internal high-priority comm stream for the grouped
 // send/recv into the neighbours' ghost planes, and updates the interior
 // packages while the transfer runs.  Jacobi sweeps: bit-identical to one GPU.
+// enqueue the schedule on s starting from buffer `cur`; returns the final one
 template <class T>
-static void reinit_partitioned(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
+static int reinit_partitioned_enqueue(sg_grid* g, int cur, int32_t iters, double cfl,
+                                      cudaStream_t s) {
     const StC<T> c = stencil_consts<T>(g, cfl);
     const sg_plan_t& p = g->plan;
     const bool lower = g->rank > 0, upper = g->rank < g->nranks - 1;
@@ -827,20 +829,120 @@ static void reinit_partitioned(sg_grid* g, int32_t iters, double cfl, cudaStream
     for (int done = 0; done < iters;) {
         const int m = std::min(4, iters - done);
         for (int i = 0; i + 1 < m; ++i) {
-            if (reinit_launch<T>(g, g->cur, c, 2, g->n_pkg, s)) SG_LAUNCHED();
-            g->cur = 1 - g->cur;
+            if (reinit_launch<T>(g, cur, c, 2, g->n_pkg, s)) SG_LAUNCHED();
+            cur = 1 - cur;
         }
-        if (reinit_launch<T>(g, g->cur, c, b0lo, b0hi, s)) SG_LAUNCHED();
-        if (reinit_launch<T>(g, g->cur, c, b1lo, b1hi, s)) SG_LAUNCHED();
+        if (reinit_launch<T>(g, cur, c, b0lo, b0hi, s)) SG_LAUNCHED();
+        if (reinit_launch<T>(g, cur, c, b1lo, b1hi, s)) SG_LAUNCHED();
         SG_CUDA(cudaEventRecord(g->ev_b, s));
         SG_CUDA(cudaStreamWaitEvent(g->comm_stream, g->ev_b, 0));
-        halo_exchange(g, g->phi[1 - g->cur], per, g->comm_stream);
+        halo_exchange(g, g->phi[1 - cur], per, g->comm_stream);
         SG_CUDA(cudaEventRecord(g->ev_x, g->comm_stream));
-        if (reinit_launch<T>(g, g->cur, c, b0hi, b1lo, s)) SG_LAUNCHED();
+        if (reinit_launch<T>(g, cur, c, b0hi, b1lo, s)) SG_LAUNCHED();
         SG_CUDA(cudaStreamWaitEvent(s, g->ev_x, 0));
-        g->cur = 1 - g->cur;
+        cur = 1 - cur;
         done += m;
     }
+    return cur;
+}
+
+// Partitioned reinit over NCCL as one CUDA graph (sweeps, the fork to the
+// comm stream, the captured NCCL send/recv groups, the joins): the sweeps of
+// a slab are a few microseconds each at 8 ranks, so host launch latency
+// would dominate.  Cached like the single-GPU graphs (plus the communicator
+// and the halo ranges in the key).  A capture that fails (e.g. an NCCL
+// without graph support) falls back to eager launches for the process;
+// SG_COMM_GRAPHS=0 disables it.  The in-process communicator rendezvous on
+// the host at every exchange, so it always runs eagerly.
+struct PGraphKey {
+    const void* p0;
+    const void* p1;
+    const void* face;
+    const void* comm;
+    int64_t n_pkg, own_lo, own_hi, r[8];
+    int32_t iters, dt, device, cur;
+    double cfl, dx;
+    bool operator==(const PGraphKey& o) const {
+        if (p0 != o.p0 || p1 != o.p1 || face != o.face || comm != o.comm || n_pkg != o.n_pkg ||
+            own_lo != o.own_lo || own_hi != o.own_hi || iters != o.iters || dt != o.dt ||
+            device != o.device || cur != o.cur || cfl != o.cfl || dx != o.dx)
+            return false;
+        for (int i = 0; i < 8; ++i)
+            if (r[i] != o.r[i]) return false;
+        return true;
+    }
+};
+static std::mutex g_pgraph_mu;
+struct PGraph {
+    cudaGraphExec_t exec;
+    uint64_t launches;  // kernel nodes per replay (sg_launch_count)
+};
+static std::vector<std::pair<PGraphKey, PGraph>> g_pgraphs;
+static bool g_pgraph_off = false;
+
+template <class T>
+static void reinit_partitioned(sg_grid* g, int32_t iters, double cfl, cudaStream_t s) {
+    static const bool env_on = [] {
+        const char* e = std::getenv("SG_COMM_GRAPHS");
+        return !(e && e[0] == '0');
+    }();
+    if (!env_on || iters < 2 || comm_kind(g->comm) != SG_COMM_NCCL || g_pgraph_off) {
+        g->cur = reinit_partitioned_enqueue<T>(g, g->cur, iters, cfl, s);
+        return;
+    }
+    int dev = 0;
+    SG_CUDA(cudaGetDevice(&dev));
+    const sg_plan_t& p = g->plan;
+    const PGraphKey key{g->phi[0], g->phi[1], g->face, g->comm, g->n_pkg, g->own_lo, g->own_hi,
+                        {p.send_lo[0], p.send_lo[1], p.send_hi[0], p.send_hi[1], p.recv_lo[0],
+                         p.recv_lo[1], p.recv_hi[0], p.recv_hi[1]},
+                        iters, (int32_t)sizeof(T), dev, g->cur, cfl, g->gc.dx};
+    std::lock_guard<std::mutex> lk(g_pgraph_mu);
+    cudaGraphExec_t exec = nullptr;
+    uint64_t nl = 0;
+    for (auto& e : g_pgraphs)
+        if (e.first == key) {
+            exec = e.second.exec;
+            nl = e.second.launches;
+        }
+    if (!exec) {
+        cudaStream_t cap = nullptr;
+        SG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        cudaGraph_t graph = nullptr;
+        bool ok = true;
+        int cur_end = g->cur;
+        const uint64_t l0 = g_launches.load();
+        try {
+            SG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+            cur_end = reinit_partitioned_enqueue<T>(g, g->cur, iters, cfl, cap);
+            SG_CUDA(cudaStreamEndCapture(cap, &graph));
+            SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        } catch (const Error&) {
+            ok = false;
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(cap, &junk);  // leave capture mode if still in it
+            if (junk) cudaGraphDestroy(junk);
+            cudaGetLastError();
+        }
+        if (graph) cudaGraphDestroy(graph);
+        cudaStreamDestroy(cap);
+        (void)cur_end;
+        nl = g_launches.load() - l0;  // captured, not yet run
+        g_launches.fetch_sub(nl);
+        if (!ok || !exec) {
+            g_pgraph_off = true;  // eager from now on
+            g->cur = reinit_partitioned_enqueue<T>(g, g->cur, iters, cfl, s);
+            return;
+        }
+        if (g_pgraphs.size() >= 16) {
+            cudaGraphExecDestroy(g_pgraphs.front().second.exec);
+            g_pgraphs.erase(g_pgraphs.begin());
+        }
+        g_pgraphs.push_back({key, PGraph{exec, nl}});
+    }
+    SG_CUDA(cudaGraphLaunch(exec, s));
+    g_launches.fetch_add(nl);
+    if (iters & 1) g->cur = 1 - g->cur;
 }
 
 // Multi-sweep reinit runs as one CUDA graph of `iters` kernel nodes.  The
