@@ -27,7 +27,7 @@ namespace sg {
 
 struct RelaxC {
     double lower[3], upper[3];
-    double cs, inv_cs;  // cell-list cell size 2h
+    double cs, inv_cs;  // cell-list cell size h (pairs within 2h: +-2 cells)
     int32_t nc[3];      // cell-list cells per axis
     double h, two_h, sigma, vol;  // Wendland C2, particle volume dp^3
     double step_dp2, max_d, off;  // step dp^2, max_disp dp, surface_offset dp
@@ -193,17 +193,19 @@ __global__ void __launch_bounds__(256) k_rl_force(GridC gc, RelaxC r, int64_t n,
     const T xi = (T)x[0], yi = (T)x[1], zi = (T)x[2];
     const T h = (T)r.h, two_h2 = (T)(r.two_h * r.two_h);
     const T coef = (T)(-5.0 * r.sigma / (r.h * r.h) * r.vol);  // W'(r)/r = coef (1 - q/2)^3
-    for (int dz = -1; dz <= 1; ++dz) {
+    // cells of size h: the partners within 2h lie in the 5 x 5 x 5 cells
+    // around; the 5 cells of one (y, z) row are consecutive in the sorted
+    // array, so each row is one contiguous range
+    const int xa = max(cx - 2, 0), xb = min(cx + 2, r.nc[0] - 1);
+    for (int dz = -2; dz <= 2; ++dz) {
         const int z = cz + dz;
         if (z < 0 || z >= r.nc[2]) continue;
-        for (int dy = -1; dy <= 1; ++dy) {
+        for (int dy = -2; dy <= 2; ++dy) {
             const int y = cy + dy;
             if (y < 0 || y >= r.nc[1]) continue;
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int xx = cx + dx;
-                if (xx < 0 || xx >= r.nc[0]) continue;
-                const int64_t cc = ((int64_t)z * r.nc[1] + y) * r.nc[0] + xx;
-                const int32_t s0 = start[cc], s1 = s0 + cnt[cc];
+            {
+                const int64_t row = ((int64_t)z * r.nc[1] + y) * r.nc[0];
+                const int32_t s0 = start[row + xa], s1 = start[row + xb] + cnt[row + xb];
                 for (int64_t jj = s0; jj < s1; ++jj) {
                     const T ex = xi - spos[3 * jj], ey = yi - spos[3 * jj + 1],
                             ez = zi - spos[3 * jj + 2];
@@ -280,7 +282,7 @@ static void relax_t(sg_grid* g, int64_t n, T* pos, const sg_relax_params* p, cud
     RelaxC r{};
     r.h = p->h_ratio * p->dp;
     r.two_h = 2.0 * r.h;
-    r.cs = r.two_h;
+    r.cs = r.h;
     r.inv_cs = 1.0 / r.cs;
     int64_t C = 1;
     for (int k = 0; k < 3; ++k) {
