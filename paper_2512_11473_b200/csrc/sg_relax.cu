@@ -152,6 +152,16 @@ __global__ void k_rl_scan_add(int32_t* __restrict__ v, int64_t n, const int32_t*
     if (i < n) v[i] += bsum[blockIdx.x];
 }
 
+__device__ __forceinline__ void ld4(const float* p, float (&v)[4]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+__device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
 template <class T>
 __global__ void k_rl_scatter(int64_t n, const T* __restrict__ pos, const int32_t* __restrict__ key,
                              const int32_t* __restrict__ start, int32_t* __restrict__ cursor,
@@ -160,9 +170,11 @@ __global__ void k_rl_scatter(int64_t n, const T* __restrict__ pos, const int32_t
     if (i >= n || key[i] < 0) return;
     // slots < n < 2^31 (sg_relax checks); the x3 offsets in 64 bit
     const int64_t slot = start[key[i]] + atomicAdd(cursor + key[i], 1);
-    spos[3 * slot] = pos[3 * i];
-    spos[3 * slot + 1] = pos[3 * i + 1];
-    spos[3 * slot + 2] = pos[3 * i + 2];
+    // 4 values per particle: one vector load per pair candidate
+    spos[4 * slot] = pos[3 * i];
+    spos[4 * slot + 1] = pos[3 * i + 1];
+    spos[4 * slot + 2] = pos[3 * i + 2];
+    spos[4 * slot + 3] = T(0);
 }
 
 template <class T>
@@ -191,7 +203,7 @@ __global__ void __launch_bounds__(256) k_rl_force(GridC gc, RelaxC r, int64_t n,
     const int cx = k0 % r.nc[0], cy = (k0 / r.nc[0]) % r.nc[1], cz = k0 / (r.nc[0] * r.nc[1]);
     T sx = T(0), sy = T(0), sz = T(0);
     const T xi = (T)x[0], yi = (T)x[1], zi = (T)x[2];
-    const T h = (T)r.h, two_h2 = (T)(r.two_h * r.two_h);
+    const T inv_h = (T)(1.0 / r.h), two_h2 = (T)(r.two_h * r.two_h);
     const T coef = (T)(-5.0 * r.sigma / (r.h * r.h) * r.vol);  // W'(r)/r = coef (1 - q/2)^3
     // cells of size h: the partners within 2h lie in the 5 x 5 x 5 cells
     // around; the 5 cells of one (y, z) row are consecutive in the sorted
@@ -206,12 +218,14 @@ __global__ void __launch_bounds__(256) k_rl_force(GridC gc, RelaxC r, int64_t n,
             {
                 const int64_t row = ((int64_t)z * r.nc[1] + y) * r.nc[0];
                 const int32_t s0 = start[row + xa], s1 = start[row + xb] + cnt[row + xb];
+#pragma unroll 4
                 for (int64_t jj = s0; jj < s1; ++jj) {
-                    const T ex = xi - spos[3 * jj], ey = yi - spos[3 * jj + 1],
-                            ez = zi - spos[3 * jj + 2];
+                    T pj[4];
+                    ld4(spos + 4 * jj, pj);
+                    const T ex = xi - pj[0], ey = yi - pj[1], ez = zi - pj[2];
                     const T d2 = ex * ex + ey * ey + ez * ez;
                     if (d2 > T(0) && d2 < two_h2) {
-                        const T q = sqrt(d2) / h;
+                        const T q = sqrt(d2) * inv_h;
                         const T a = T(1) - T(0.5) * q;
                         const T f = coef * a * a * a;  // W'(|r|) / |r| * V  (q/h factor folded)
                         sx += f * ex;
@@ -304,7 +318,7 @@ static void relax_t(sg_grid* g, int64_t n, T* pos, const sg_relax_params* p, cud
     int32_t* start = (int32_t*)dalloc(sizeof(int32_t) * C, s);
     int32_t* cnt = (int32_t*)dalloc(sizeof(int32_t) * C, s);
     int32_t* bsum = (int32_t*)dalloc(sizeof(int32_t) * nsb, s);
-    T* spos = (T*)dalloc(sizeof(T) * 3 * n, s);
+    T* spos = (T*)dalloc(sizeof(T) * 4 * n, s);
     T* moved = (T*)dalloc(sizeof(T) * 3 * n, s);
     const unsigned pb = (unsigned)ceil_div(n, 256);
     for (int it = 0; it < p->steps; ++it) {
