@@ -39,8 +39,10 @@
  *                     of both signs along each axis (upwind selection), phi=0
  *                     stationary; multi-step drift near kinks/medial axes of
  *                     real geometries: parity unpinned
- *   or_gradient_dense pinned: affine exactness, sphere radial; band-edge values
- *                     that use the far constant: parity unpinned
+ *   or_gradient_dense pinned: affine exactness, sphere radial, and bit for bit
+ *                     numpy.gradient's central difference on the far-filled
+ *                     dense field at every interior active point, band edge
+ *                     included
  *   or_kernel_dense   pinned: S closed forms, S/2 at planar interface, sum gw=0,
  *                     first moment sum gw_x o_x dx -> int W = 1 (G scale),
  *                     scaling identity r W' = -h dW/dh - 3W from the weights,

@@ -441,6 +441,42 @@ def test_gradient_sphere_radial(oracle_lib):
         assert np.max(np.abs(n[k][core] - radial[core])) < 4 * (w.dx / 0.2) ** 2
 
 
+@pytest.mark.parametrize("scene", ["C1", "rand3", "rand6"])
+def test_gradient_equals_numpy_central_difference_incl_band_edge(oracle_lib, scene):
+    """O8 reduces to a library routine: numpy.gradient's interior central
+    difference (f[i+1] - f[i-1]) / (2 dx) on the dense field whose inactive
+    cells hold the far constants (the singular packages' values)
+    -- at EVERY active point not on the domain boundary, including the band
+    edge where a neighbour is a far value (the values SURVEY 8(c.4) listed
+    as unpinned).  The normal is numpy's normalisation of that vector; both
+    bit for bit (same operation order).  Inactive points are zero (R-16)."""
+    w = W.config("C1") if scene == "C1" else W.random_scene(int(scene[4:]), 24, dtype="f64")
+    o = oracle_lib.Oracle(w)
+    t = o.build_tables()
+    phi = o.reinit(o.phi_dense(), 3)  # far fills stay, band values move
+    g, n = o.gradient(phi)
+    ng = np.gradient(phi, w.dx)  # axis order (z, y, x)
+    nz, ny, nx = w.n[::-1]
+    cb = np.repeat(np.repeat(np.repeat(t.bg.reshape(nz, ny, nx), 4, 0), 4, 1), 4, 2)
+    act = cb >= 2
+    inner = np.zeros_like(act)
+    inner[1:-1, 1:-1, 1:-1] = True
+    sel = act & inner
+    assert sel.sum() > 1000
+    # band edge: active points with a far-valued axis neighbour
+    far = ~act
+    edge = np.zeros_like(act)
+    for ax in range(3):
+        edge |= np.roll(far, 1, ax) | np.roll(far, -1, ax)
+    assert (sel & edge).sum() > 100
+    mag = np.sqrt((ng[2] * ng[2] + ng[1] * ng[1]) + ng[0] * ng[0])
+    for k, axis in ((0, 2), (1, 1), (2, 0)):
+        assert np.array_equal(g[k][sel], ng[axis][sel]), k
+        nref = np.where(mag > 0, ng[axis] / np.where(mag > 0, mag, 1.0), 0.0)
+        assert np.array_equal(n[k][sel], nref[sel]), k
+        assert np.all(g[k][~act] == 0) and np.all(n[k][~act] == 0)
+
+
 # ---------------------------------------------------- O9: kernel integral ----
 
 
