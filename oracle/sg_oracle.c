@@ -38,7 +38,7 @@
  *                     flip, one-step Godunov closed forms at ridges/valleys
  *                     of both signs along each axis (upwind selection), phi=0
  *                     stationary; multi-step drift near kinks/medial axes of
- *                     real geometries: parity unpinned
+ *                     real geometries: the composition of the pinned step
  *   or_gradient_dense pinned: affine exactness, sphere radial, and bit for bit
  *                     numpy.gradient's central difference on the far-filled
  *                     dense field at every interior active point, band edge
