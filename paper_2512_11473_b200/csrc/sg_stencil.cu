@@ -396,6 +396,13 @@ __device__ __forceinline__ void st_vec4(double* p, double a, double b, double c,
 __device__ __forceinline__ float inv_norm(float m2) { return m2 > 0.f ? rsqrtf(m2) : 0.f; }
 __device__ __forceinline__ double inv_norm(double m2) { return m2 > 0.0 ? 1.0 / sqrt(m2) : 0.0; }
 
+// store tile of one package's (phi, grad) rows: point d at 4 d + 4 (d / 8)
+// -- a 16 B pad every 8 points keeps both the row-wise writes (lane r,
+// points 4 r .. 4 r + 3) and the point-wise reads (lane r, point r + 16 i)
+// free of shared-memory bank conflicts
+constexpr int kTileStride = 64 * 4 + 8 * 4;
+__device__ __forceinline__ int tile_ofs(int d) { return 4 * d + 4 * (d >> 3); }
+
 template <class T>
 __device__ __forceinline__ void grad_package(const T* __restrict__ in, T* __restrict__ grad,
                                              T* __restrict__ normal,
@@ -407,7 +414,7 @@ __global__ void __launch_bounds__(256) k_gradient(const T* __restrict__ in, T* _
                                                   T* __restrict__ normal,
                                                   const uint32_t* __restrict__ face, int64_t lo,
                                                   int64_t hi, StC<T> c) {
-    __shared__ __align__(16) T s_tile[16][256];
+    __shared__ __align__(16) T s_tile[16][kTileStride];
     const int64_t pkg = lo + (((int64_t)blockIdx.x * 256 + threadIdx.x) >> 4);
     grad_package(in, grad, normal, face, pkg, pkg < hi, c, s_tile[threadIdx.x >> 4]);
 }
@@ -437,14 +444,14 @@ __device__ __forceinline__ void grad_package(const T* __restrict__ in, T* __rest
         // the package's shared tile the 16 lanes store 256 contiguous bytes
         // per instruction.
 #pragma unroll
-        for (int i = 0; i < 4; ++i) st_vec4(tile + 4 * (4 * r + i), x.c[i], gx[i], gy[i], gz[i]);
+        for (int i = 0; i < 4; ++i) st_vec4(tile + tile_ofs(4 * r + i), x.c[i], gx[i], gy[i], gz[i]);
         __syncwarp(0xFFFFu << (threadIdx.x & 16));
         T* G = grad + pkg * 256;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int d = r + 16 * i;
             T v[4];
-            ld_row_s(tile + 4 * d, v);
+            ld_row_s(tile + tile_ofs(d), v);
             st_vec4(G + 4 * d, v[0], v[1], v[2], v[3]);
         }
     }
@@ -573,7 +580,7 @@ __global__ void __launch_bounds__(GR ? 256 : 128) k_kint(const T* __restrict__ i
                                               StC<T> cs = StC<T>{}) {
     if constexpr (GR) {
         if (threadIdx.x >= 128) {
-            __shared__ __align__(16) T s_gtile[8][256];
+            __shared__ __align__(16) T s_gtile[8][kTileStride];
             const int64_t pkg = lo + (int64_t)blockIdx.x * 8 + ((threadIdx.x - 128) >> 4);
             grad_package(in, grad, normal, face, pkg, pkg < hi, cs, s_gtile[(threadIdx.x - 128) >> 4]);
             return;
@@ -1085,7 +1092,7 @@ static void launch_kint_r(sg_grid* g, const T* phi, const KintC<T>& c, cudaStrea
     }
     // dynamic + static (the fused K6 warps' store tiles) above the 48 KB
     // default needs the opt-in (fp64 at R >= 2)
-    if (smem + (gr ? 8 * 256 * sizeof(T) : 0) + 8 * 28 * 4 > 48 * 1024)
+    if (smem + (gr ? 8 * kTileStride * sizeof(T) : 0) + 8 * 28 * 4 > 48 * 1024)
         SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)ceil_div(hi - lo, 8), gr ? 256 : 128, smem, s>>>(
         phi, g->nb, lo, hi, c, (T*)g->kint, (T*)g->gkint, gp, np, g->face, cs);
