@@ -74,7 +74,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
 def _build_locked(verbose: bool, ptxas_info: bool) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
-    objs = []
+    objs, cmds = [], []
     for unit, extra in UNITS.items():
         obj = os.path.join(BUILD, unit.replace(".cu", ".o"))
         cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, unit), "-o", obj]
@@ -82,8 +82,13 @@ def _build_locked(verbose: bool, ptxas_info: bool) -> str:
             cmd.insert(1, "-Xptxas=-v")
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.check_call(cmd)
+        cmds.append(cmd)
         objs.append(obj)
+    # translation units compile in parallel (independent objects)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+            f.result()
     tmp = LIB + ".tmp"
     # NCCL is dlopen'ed at run time (sg_comm.cu): no link-time dependency
     cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-ldl"]
