@@ -104,50 +104,6 @@ __device__ __forceinline__ bool load_cross(const T* __restrict__ in,
     return true;
 }
 
-// The same cross with the in-package y / z neighbour rows taken from the
-// lanes that own them (warp shuffles within the package's 16-lane group):
-// only lanes on a package face load a row of the face neighbour.  Every
-// lane loads one own row instead of five -- k_gradient was L1-bound (ncu:
-// L1/TEX throughput 79 %, DRAM 48 %) on the four redundant row loads.
-template <class T>
-__device__ __forceinline__ void shfl_row(const T (&src)[4], int lane, T (&dst)[4]) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) dst[i] = __shfl_sync(0xffffffffu, src[i], lane);
-}
-
-template <class T>
-__device__ __forceinline__ bool load_cross_s(const T* __restrict__ in,
-                                             const uint32_t* __restrict__ face, int64_t pkg,
-                                             bool valid, Cross<T>& x) {
-    const int r = threadIdx.x & 15;
-    const int j = r & 3, k = r >> 2;
-    uint32_t f = 0;
-    if (valid && r < 6) f = __ldg(face + pkg * 8 + r);
-    const int base = threadIdx.x & 16;
-    const int lane = threadIdx.x & 31;
-    const uint32_t nxm = __shfl_sync(0xffffffffu, f, base + 0);
-    const uint32_t nxp = __shfl_sync(0xffffffffu, f, base + 1);
-    const uint32_t nym = __shfl_sync(0xffffffffu, f, base + 2);
-    const uint32_t nyp = __shfl_sync(0xffffffffu, f, base + 3);
-    const uint32_t nzm = __shfl_sync(0xffffffffu, f, base + 4);
-    const uint32_t nzp = __shfl_sync(0xffffffffu, f, base + 5);
-    const T* P = in + pkg * 64;
-    if (valid) ld_row(P + 4 * r, x.c);
-    // every lane takes part in the shuffles (the caller's groups are whole)
-    shfl_row(x.c, j > 0 ? lane - 1 : lane, x.ym);
-    shfl_row(x.c, j < 3 ? lane + 1 : lane, x.yp);
-    shfl_row(x.c, k > 0 ? lane - 4 : lane, x.zm);
-    shfl_row(x.c, k < 3 ? lane + 4 : lane, x.zp);
-    if (!valid) return false;
-    if (j == 0) ld_row(in + (int64_t)nym * 64 + 4 * (3 + 4 * k), x.ym);
-    if (j == 3) ld_row(in + (int64_t)nyp * 64 + 4 * (0 + 4 * k), x.yp);
-    if (k == 0) ld_row(in + (int64_t)nzm * 64 + 4 * (j + 12), x.zm);
-    if (k == 3) ld_row(in + (int64_t)nzp * 64 + 4 * j, x.zp);
-    x.xm = __ldg(in + (int64_t)nxm * 64 + 4 * r + 3);
-    x.xp = __ldg(in + (int64_t)nxp * 64 + 4 * r);
-    return true;
-}
-
 template <class T>
 struct StC {
     T inv_dx, dx2, cdx, inv_2dx;
@@ -426,7 +382,7 @@ __device__ __forceinline__ void grad_package(const T* __restrict__ in, T* __rest
                                              const uint32_t* __restrict__ face, int64_t pkg,
                                              bool valid, const StC<T>& c, T* tile) {
     Cross<T> x;
-    if (!load_cross_s(in, face, pkg, valid, x)) return;
+    if (!load_cross(in, face, pkg, valid, x)) return;
     T gx[4], gy[4], gz[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -478,7 +434,7 @@ __global__ void __launch_bounds__(256) k_laplace(const T* __restrict__ in, T* __
                                                  int64_t hi, T inv_dx2) {
     const int64_t pkg = lo + (((int64_t)blockIdx.x * 256 + threadIdx.x) >> 4);
     Cross<T> x;
-    if (!load_cross_s(in, face, pkg, pkg < hi, x)) return;
+    if (!load_cross(in, face, pkg, pkg < hi, x)) return;
     T o[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {

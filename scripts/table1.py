@@ -22,9 +22,8 @@ import workloads as W  # noqa: E402
 from paper_2512_11473_b200 import build, sg  # noqa: E402
 
 
-def main():
-    build.build()
-    w = W.config("T1")
+def run(name):
+    w = W.config(name)
     g = sg.Grid(w)
     n_act = (g.info["n_pkg"] - 2) * 64
     res = {}
@@ -42,8 +41,20 @@ def main():
         bytes_ = n_act * (8 if op == 0 else 8 + 108 / 64)
         res[name] = {"ms": ms, "points_per_s": n_act / (ms * 1e-3),
                      "algorithmic_GBps": bytes_ / (ms * 1e-3) / 1e9}
+    g.close()
+    return n_act, res
+
+
+def main():
+    build.build()
+    n_act, res = run("T1")
+    # SURVEY 8(f) NEXT-1 also asks for C5 (the paper shell + 8 small shells,
+    # dx = 1/4096, 970.7 M active points)
+    n5, res5 = run("C5")
     out = {"workload": "Table-1 shelled sphere, dx = 1/1024 (R-19), fp32",
            "active_points": n_act, "gpu": torch.cuda.get_device_name(0), **res,
+           "C5": {"workload": "C5 multi-shell scene, dx = 1/4096, fp32", "active_points": n5,
+                  **res5},
            "paper_table1_cpu_context": {"sequential_1thread": 22.948, "sequential_4threads": 7.429,
                                         "stencil_1thread": 59.972, "stencil_4threads": 21.378,
                                         "source": "PAPER.md P:614-617 (CPU, units not stated)"}}
