@@ -569,7 +569,13 @@ __global__ void __launch_bounds__(GR ? 256 : 128) k_kint(const T* __restrict__ i
         for (int m = 0; m < RPT; ++m) {
             const int rowi = r + 16 * m;
             if (rowi < NR) {
-                const int ly = rowi % RS, lz = rowi / RS;
+                // R = 2: the 8 lanes of a 16 B store phase write rows
+                // ly = 0..3 of two consecutive slices (banks 8 ly and
+                // 8 ly + 4): with 8 consecutive ly of one slice, rows ly and
+                // ly + 4 shared banks (ncu: 2-way conflicts on half the
+                // staging stores)
+                const int ly = RS == 8 ? (rowi & 3) + 4 * ((rowi >> 3) & 1) : rowi % RS;
+                const int lz = RS == 8 ? 2 * (rowi >> 4) + ((rowi >> 2) & 1) : rowi / RS;
                 const int sy = ly - R, sz = lz - R;
                 const Shift hy = nb_shift(sy), hz = nb_shift(sz);
                 const int dyz = 4 * hy.data + 16 * hz.data;
