@@ -289,6 +289,11 @@ sg_status sg_comm_create_local(int32_t nranks, sg_comm** comms);
 /* rank, size and kind (SG_COMM_NCCL / SG_COMM_LOCAL); outputs may be NULL */
 sg_status sg_comm_info(const sg_comm* comm, int32_t* rank, int32_t* nranks, int32_t* kind);
 
+/* Asynchronous communicator errors (ncclCommGetAsyncError: a peer failed or
+ * a transfer broke after its call returned): SG_OK, or SG_ERR_NCCL with the
+ * NCCL message in sg_last_error().  The in-process communicator has none. */
+sg_status sg_comm_check(const sg_comm* comm);
+
 /* Destroy a communicator (after every grid built on it is destroyed). */
 void sg_comm_destroy(sg_comm* comm);
 

@@ -49,6 +49,7 @@ struct Nccl {
     decltype(&ncclRecv) recv = nullptr;
     decltype(&ncclGroupStart) groupStart = nullptr;
     decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclCommGetAsyncError) getAsyncError = nullptr;
     std::string err;
 };
 
@@ -82,6 +83,7 @@ static Nccl& nccl() {
         sym(N.recv, "ncclRecv");
         sym(N.groupStart, "ncclGroupStart");
         sym(N.groupEnd, "ncclGroupEnd");
+        sym(N.getAsyncError, "ncclCommGetAsyncError");
         if (!ok) {
             dlclose(N.h);
             N.h = nullptr;
@@ -396,6 +398,17 @@ extern "C" sg_status sg_comm_info(const sg_comm* c, int32_t* rank, int32_t* nran
         if (rank) *rank = c->rank;
         if (nranks) *nranks = c->nranks;
         if (kind) *kind = c->kind;
+    });
+}
+
+extern "C" sg_status sg_comm_check(const sg_comm* c) {
+    return guard([&] {
+        SG_ARG(c != nullptr, "sg_comm_check: null comm");
+        if (c->kind != SG_COMM_NCCL || !c->nc) return;
+        ncclResult_t r = ncclSuccess;
+        SG_NCCL(nccl().getAsyncError(c->nc, &r));
+        if (r != ncclSuccess && r != ncclInProgress)
+            throw Error(SG_ERR_NCCL, std::string("NCCL async error: ") + nccl().getErrorString(r));
     });
 }
 

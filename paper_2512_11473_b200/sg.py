@@ -32,7 +32,7 @@ EXPORTS = ("sg_build", "sg_build_ex", "sg_build_refined", "sg_reinit", "sg_reini
            "sg_sign_correct", "sg_clean", "sg_info", "sg_view",
            "sg_destroy", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
            "sg_slab_plan", "sg_comm_unique_id", "sg_comm_create", "sg_comm_create_local",
-           "sg_comm_info", "sg_comm_destroy", "sg_pool_trim",
+           "sg_comm_info", "sg_comm_check", "sg_comm_destroy", "sg_pool_trim",
            "sg_neighbour_index_shift", "sg_last_error", "sg_abi_version", "sg_launch_count")
 SG_COMM_ID_BYTES = 128
 SG_COMM_NCCL, SG_COMM_LOCAL = 0, 1
@@ -150,6 +150,7 @@ def lib():
         L.sg_comm_create.argtypes = [P, I32, I32, C.POINTER(P)]
         L.sg_comm_create_local.argtypes = [I32, P]
         L.sg_comm_info.argtypes = [P, P, P, P]
+        L.sg_comm_check.argtypes = [P]
         L.sg_comm_destroy.argtypes = [P]
         L.sg_comm_destroy.restype = None
         L.sg_pool_trim.argtypes = []
@@ -163,7 +164,7 @@ def lib():
                      "sg_info",
                      "sg_view", "sg_destroy_async", "sg_balanced_cuts", "sg_plane_counts",
                      "sg_build_ex", "sg_slab_plan", "sg_comm_unique_id", "sg_comm_create",
-                     "sg_comm_create_local", "sg_comm_info", "sg_pool_trim"):
+                     "sg_comm_create_local", "sg_comm_info", "sg_comm_check", "sg_pool_trim"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -365,6 +366,10 @@ class Comm:
         arr = (C.c_void_p * n)()
         _check(lib().sg_comm_create_local(int(n), arr))
         return [cls(arr[i]) for i in range(n)]
+
+    def check(self):
+        """Raise SgError(SG_ERR_NCCL) on an asynchronous NCCL error."""
+        _check(lib().sg_comm_check(C.c_void_p(self.handle)))
 
     def close(self):
         if getattr(self, "handle", None):

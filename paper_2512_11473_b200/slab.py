@@ -197,5 +197,6 @@ def bench_slab(args, w, rank, world, local):
                                     "ranks incl. the NCCL exchange"},
                "clocks": clk.summary()}
         print(json.dumps(out), flush=True)
+    comm.check()  # surface an asynchronous NCCL error instead of a silent number
     comm.close()
     dist.destroy_process_group()

@@ -203,6 +203,7 @@ def test_nccl_communicator_one_rank(sgm):
     sgm._check(sgm.lib().sg_comm_create(buf, 0, 1, C.byref(out)))
     comm = sgm.Comm(out.value)
     assert (comm.rank, comm.nranks, comm.kind) == (0, 1, sgm.SG_COMM_NCCL)
+    comm.check()  # no asynchronous NCCL error
     w = W.config("C1")
     g = sgm.Grid(w, comm=comm).reinit(5, w.cfl)
     ref = sgm.Grid(w).reinit(5, w.cfl)
