@@ -152,6 +152,7 @@ def bench_slab(args, w, rank, world, local):
     e2e = None
     if not args.no_e2e and w.particles:
         et = timed(True)
+    comm.check()  # an asynchronous NCCL error fails the run instead of printing a number
     tot = torch.tensor([n_pkg_local], dtype=torch.int64, device="cuda")
     dist.all_reduce(tot)
     n_act = int(tot[0].item()) * 64
@@ -197,6 +198,5 @@ def bench_slab(args, w, rank, world, local):
                                     "ranks incl. the NCCL exchange"},
                "clocks": clk.summary()}
         print(json.dumps(out), flush=True)
-    comm.check()  # surface an asynchronous NCCL error instead of a silent number
     comm.close()
     dist.destroy_process_group()
