@@ -614,7 +614,7 @@ def oracle_sample(w, budget_s: float = 12.0):
                               "sample": f"1 reinit sweep on one thread, {dt1:.1f} s"}}
 
 
-def oracle_window_sample(name="C3", planes=8, budget_s=8.0):
+def oracle_window_sample(name="C3", planes=8, budget_s=8.0, xy_box=None):
     """The oracle on a z-window of a configuration whose dense grid does not
     fit (C3: 69 GB per fp64 field): `planes` background planes around the
     heaviest plane plus a margin of ceil(20/4) + 1 planes per side, the whole
@@ -631,10 +631,25 @@ def oracle_window_sample(name="C3", planes=8, budget_s=8.0):
     margin = -(-REINIT_ITERS // 4) + 1
     z0 = max(0, zc - planes // 2 - margin)
     z1 = min(w.n[2], z0 + planes + 2 * margin)
-    o = O.Oracle(w, ((0, 0, z0), (w.n[0], w.n[1], z1)))
+    if xy_box is None:
+        x0, y0, x1, y1 = 0, 0, w.n[0], w.n[1]
+    else:
+        # a box in x-y too (C5: a whole 4096^2 plane is 17 M fine points per
+        # layer): xy_box = (nx, ny) cells around the densest row of the
+        # heaviest plane
+        bx, by = xy_box
+        pl = t.bg.reshape(w.n[2], w.n[1], w.n[0])[zc] >= 2
+        yc = int(np.argmax(pl.sum(axis=1)))
+        xs = np.nonzero(pl[yc])[0]
+        xc = int(np.median(xs)) if xs.size else w.n[0] // 2
+        x0 = max(0, min(w.n[0] - bx, xc - bx // 2))
+        y0 = max(0, min(w.n[1] - by, yc - by // 2))
+        x1, y1 = x0 + bx, y0 + by
+    o = O.Oracle(w, ((x0, y0, z0), (x1, y1, z1)))
     o.tables = t
     phi = o.phi_dense()
-    n_act = int(t.plane_count[z0:z1].sum()) * 64
+    bg3 = t.bg.reshape(w.n[2], w.n[1], w.n[0])[z0:z1, y0:y1, x0:x1]
+    n_act = int(np.count_nonzero(bg3 >= 2)) * 64
     sweeps, t0 = 0, time.perf_counter()
     while True:
         phi = o.reinit_step(phi, w.cfl)
@@ -643,10 +658,10 @@ def oracle_window_sample(name="C3", planes=8, budget_s=8.0):
             break
     dt = time.perf_counter() - t0
     return {"config": name, "value": n_act * sweeps / dt, "unit": UNIT, "cores": O.get_threads(),
-            "sample": f"{sweeps} reinit sweeps of the dense fp64 oracle on the z-window "
-                      f"[{z0}, {z1}) of {name} (heaviest plane {zc}, {planes} planes + "
-                      f"{margin}-plane margins, whole x-y extent; {n_act} active points); "
-                      f"tables and initial phi untimed; {dt:.1f} s"}
+            "sample": f"{sweeps} reinit sweeps of the dense fp64 oracle on the window "
+                      f"z [{z0}, {z1}) x [{x0}, {x1}) y [{y0}, {y1}) of {name} (heaviest plane "
+                      f"{zc}, {planes} planes + {margin}-plane margins; {n_act} active points "
+                      f"in the box); tables and initial phi untimed; {dt:.1f} s"}
 
 
 def cpu_baseline(w, n_act):
@@ -655,10 +670,12 @@ def cpu_baseline(w, n_act):
     except Exception as e:  # never fail the bench line on the baseline
         return {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
                 "sample": f"failed: {e}"}
-    try:
-        out["windows"] = [oracle_window_sample("C3")]
-    except Exception as e:
-        out["windows"] = [{"config": "C3", "value": None, "sample": f"failed: {e}"}]
+    out["windows"] = []
+    for name, kw in (("C3", {}), ("C5", {"xy_box": (128, 48)})):
+        try:
+            out["windows"].append(oracle_window_sample(name, **kw))
+        except Exception as e:
+            out["windows"].append({"config": name, "value": None, "sample": f"failed: {e}"})
     return out
 
 
