@@ -30,6 +30,7 @@ UNITS = {
     # fp32 denormals (< 1.2e-38) never occur in band values / spacings; FTZ
     # removes the denormal paths around MUFU.RSQ
     "sg_stencil.cu": ["-ftz=true"],
+    "sg_tsweep.cu": ["-ftz=true"],  # same flags as sg_stencil.cu: bit-identical sweeps
     "sg_probe.cu": ["-ftz=true"],
     "sg_relax.cu": [],
     "sg_sign.cu": [],

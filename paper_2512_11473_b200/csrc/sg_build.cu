@@ -1211,6 +1211,7 @@ extern "C" sg_status sg_build_refined(const sg_grid* parent, const sg_geometry* 
 }
 
 static void free_grid(sg_grid* g, cudaStream_t s, bool async) {
+    tplan_release(g, s);
     for (auto& a : g->allocs) {
         if (g->has_allocator)
             g->allocator.free(a.first, a.second, (void*)s, g->allocator.ctx);

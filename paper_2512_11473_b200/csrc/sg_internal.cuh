@@ -164,6 +164,10 @@ __host__ __device__ __forceinline__ Shift nb_shift(int s) {
 
 }  // namespace sg
 
+namespace sg {
+struct TPlan;
+}
+
 struct sg_grid {
     sg_desc desc;  // as built (the refined layer derives its own from it)
     sg::GridC gc;
@@ -205,6 +209,8 @@ struct sg_grid {
     bool has_allocator = false;
     sg_allocator allocator{};
     // partition over a communicator (sg_build_ex with comm)
+    sg::TPlan* tplan = nullptr;  // two-sweep reinit tiles (sg_tsweep.cu), lazily built
+
     const sg_comm* comm = nullptr;
     int32_t rank = 0, nranks = 1;
     std::vector<int32_t> cuts;  // [nranks + 1] plane cuts of every rank
@@ -224,6 +230,18 @@ struct sg_grid {
         allocs.emplace_back(p, bytes ? bytes : 256);
         return p;
     }
+    // return one allocation of alloc() before the grid is destroyed
+    void release(void* p, cudaStream_t s) {
+        for (size_t i = 0; i < allocs.size(); ++i)
+            if (allocs[i].first == p) {
+                if (has_allocator)
+                    allocator.free(p, allocs[i].second, (void*)s, allocator.ctx);
+                else
+                    cudaFreeAsync(p, s);
+                allocs.erase(allocs.begin() + i);
+                return;
+            }
+    }
     int64_t bytes() const {
         int64_t b = 0;
         for (auto& a : allocs) b += (int64_t)a.second;
@@ -233,6 +251,30 @@ struct sg_grid {
 
 // kernels / launchers implemented per translation unit
 namespace sg {
+// Two-sweep tile plan of a grid (sg_tsweep.cu): the active packages in Morton
+// order of their background cells, cut into tiles of at most kTI packages; a
+// tile lists its packages, the packages of its face / edge neighbourhood
+// ("halo") with the x-rows of them the two sweeps need, and every slot's six
+// face neighbours as tile-local slots.  Device arrays come from the grid's
+// allocator; the plan is rebuilt after anything rewrites the face table.
+struct TPlan {
+    int state = 0;  // 0: not built, 1: ready, -1: not applicable (single sweeps)
+    int64_t t_cap = 0;
+    uint32_t n_tiles = 0;
+    void* arena = nullptr;
+    int4* cnt = nullptr;        // [t_cap]: (packages, halo packages, first-sweep halo rows, -)
+    uint32_t* ids = nullptr;    // [t_cap][kTCap] global id of each slot
+    uint4* lf = nullptr;        // [t_cap][kTCap] face neighbours as slots (8 x u16)
+    uint16_t* m2 = nullptr;     // [t_cap][kTCap] halo slot: x-rows to load (bit r)
+    uint16_t* comp = nullptr;   // [t_cap][kTComp] first-sweep halo rows (slot << 4 | row)
+    uint32_t* ctr = nullptr;    // [2]: tiles emitted, capacity overflow
+};
+void tplan_invalidate(sg_grid* g, cudaStream_t s);
+void tplan_release(sg_grid* g, cudaStream_t s);
+bool tsweep_ready(sg_grid* g, cudaStream_t s);  // builds the plan on first use
+const void* tsweep_key(const sg_grid* g);
+void tsweep_launch(sg_grid* g, int cur, float inv_dx, float dx2, float cdx, cudaStream_t s);
+
 void launch_reinit(sg_grid* g, int32_t iters, double cfl, cudaStream_t s, bool halo = false);
 void launch_gradient(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t s);
 void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void* grad,

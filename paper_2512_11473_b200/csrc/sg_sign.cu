@@ -433,6 +433,7 @@ extern "C" sg_status sg_sign_correct(sg_grid* g, double tau, int32_t max_sweeps,
             k_nb_fix<<<(unsigned)ceil_div((n_pkg - 2) * 27, 256), 256, 0, s>>>(
                 gc, W, n_pkg, g->meta_cell, g->cell_neg, g->nb, g->face);
             SG_LAUNCHED();
+            tplan_invalidate(g, s);  // the face table changed
         }
 
         // refined: trusted points |phi| < tau, singular packages signed
