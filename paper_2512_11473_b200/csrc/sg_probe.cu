@@ -312,6 +312,7 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
                 sv[k] = a - 4 * ck;  // in [-1, 3]
             }
             const int s0x = sv[0], s0y = sv[1], s0z = sv[2];
+            const uint32_t self = S.pk[w][q];
             uint32_t pk[8];
             int d[8];
 #pragma unroll
@@ -319,7 +320,11 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
                 const int sx = s0x + (cc & 1), sy = s0y + ((cc >> 1) & 1), sz = s0z + (cc >> 2);
                 const Shift hx = nb_shift(sx), hy = nb_shift(sy), hz = nb_shift(sz);
                 d[cc] = hx.data + 4 * hy.data + 16 * hz.data;
-                pk[cc] = __ldg(row + hx.off + 3 * hy.off + 9 * hz.off);
+                // slot 13 (offset (1, 1, 1)) is the package itself (O5): a
+                // corner inside the containing package needs no table load
+                // (all eight for 27/64 of the band particles)
+                const int slot = hx.off + 3 * hy.off + 9 * hz.off;
+                pk[cc] = slot == 13 ? self : __ldg(row + slot);
             }
             const T tx = tv[0], ty = tv[1], tz = tv[2];
             T acc[4] = {T(0), T(0), T(0), T(0)};
@@ -438,11 +443,11 @@ static bool is_device_ptr(const void* p) {
 // stream over a ring of kRing device chunk buffers, so both copy engines
 // stream continuously (a per-chunk upload only waits for its buffer's
 // previous download)
-constexpr int kRing = 4;
+constexpr int kRingMax = 8;
 struct Staging {
     cudaStream_t up = nullptr, comp = nullptr, down = nullptr, down2 = nullptr;
     cudaEvent_t ev = nullptr;
-    cudaEvent_t ev_up[kRing], ev_comp[kRing], ev_down[kRing], ev_down2[kRing];
+    cudaEvent_t ev_up[kRingMax], ev_comp[kRingMax], ev_down[kRingMax], ev_down2[kRingMax];
 };
 
 // staging streams and event per host thread and device: concurrent host-
@@ -461,7 +466,7 @@ static Staging& staging() {
         SG_CUDA(cudaStreamCreateWithFlags(&S.down, cudaStreamNonBlocking));
         SG_CUDA(cudaStreamCreateWithFlags(&S.down2, cudaStreamNonBlocking));
         SG_CUDA(cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming));
-        for (int b = 0; b < kRing; ++b) {
+        for (int b = 0; b < kRingMax; ++b) {
             SG_CUDA(cudaEventCreateWithFlags(&S.ev_up[b], cudaEventDisableTiming));
             SG_CUDA(cudaEventCreateWithFlags(&S.ev_comp[b], cudaEventDisableTiming));
             SG_CUDA(cudaEventCreateWithFlags(&S.ev_down[b], cudaEventDisableTiming));
@@ -763,9 +768,28 @@ void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void*
     SG_ARG(!is_device_ptr(pos) && !is_device_ptr(phi) && (grad == nullptr || !is_device_ptr(grad)),
            "sg_probe: pos/phi/grad must be all device or all host pointers");
     Staging& S = staging();
-    // ~32 chunks (0.25-2 M particles): short pipeline fill and drain
-    const int64_t chunk = std::min<int64_t>(
-        n, std::max<int64_t>((int64_t)1 << 18, std::min<int64_t>(ceil_div(n, 32), (int64_t)1 << 21)));
+    // ~10 chunks of 0.25-2 M particles.  Measured on C4 (19.45 M particles,
+    // 233 MB up + 311 MB down; profiles/r02/e2e_staging.jsonl): 0.6 M-particle
+    // chunks 7.58 ms, 1 M 6.86 ms, 2 M 6.84 ms, 4 M (ring 3) 7.10 ms -- the
+    // copy engines reach their concurrent rate with chunks of >= 1 M, while
+    // the first upload before any kernel (fill) overlaps the caller's build /
+    // reinit / gradient still running on its stream.
+    // (SG_PROBE_CHUNK / SG_PROBE_RING / SG_PROBE_DOWN1: experiment overrides)
+    static const int64_t env_chunk = [] {
+        const char* e = std::getenv("SG_PROBE_CHUNK");
+        return e ? std::atoll(e) : 0LL;
+    }();
+    static const int env_ring = [] {
+        const char* e = std::getenv("SG_PROBE_RING");
+        return e ? std::max(2, std::min(kRingMax, std::atoi(e))) : 4;
+    }();
+    static const bool down1 = [] {
+        const char* e = std::getenv("SG_PROBE_DOWN1");
+        return e && e[0] == '1';
+    }();
+    const int kRing = env_ring;
+    const int64_t chunk = env_chunk > 0 ? std::min<int64_t>(n, env_chunk) : std::min<int64_t>(
+        n, std::max<int64_t>((int64_t)1 << 18, std::min<int64_t>(ceil_div(n, 10), (int64_t)1 << 21)));
     const size_t es = (size_t)g->esz;
     const size_t per = chunk * es * (3 + 1 + (grad ? 3 : 0));
     // the uploads of the positions do not depend on the grid: only the probe
@@ -802,10 +826,11 @@ void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void*
         SG_CUDA(cudaStreamWaitEvent(S.down, S.ev_comp[b], 0));
         SG_CUDA(cudaMemcpyAsync(ho + off * es, dphi, m * es, cudaMemcpyDeviceToHost, S.down));
         SG_CUDA(cudaEventRecord(S.ev_down[b], S.down));
-        SG_CUDA(cudaStreamWaitEvent(S.down2, S.ev_comp[b], 0));
+        cudaStream_t d2 = down1 ? S.down : S.down2;
+        SG_CUDA(cudaStreamWaitEvent(d2, S.ev_comp[b], 0));
         if (grad)
-            SG_CUDA(cudaMemcpyAsync(hg + off * 3 * es, dg, m * 3 * es, cudaMemcpyDeviceToHost, S.down2));
-        SG_CUDA(cudaEventRecord(S.ev_down2[b], S.down2));
+            SG_CUDA(cudaMemcpyAsync(hg + off * 3 * es, dg, m * 3 * es, cudaMemcpyDeviceToHost, d2));
+        SG_CUDA(cudaEventRecord(S.ev_down2[b], d2));
     }
     SG_CUDA(cudaEventRecord(S.ev, S.down2));
     SG_CUDA(cudaStreamWaitEvent(S.down, S.ev, 0));
