@@ -773,7 +773,10 @@ void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void*
     // chunks 7.58 ms, 1 M 6.86 ms, 2 M 6.84 ms, 4 M (ring 3) 7.10 ms -- the
     // copy engines reach their concurrent rate with chunks of >= 1 M, while
     // the first upload before any kernel (fill) overlaps the caller's build /
-    // reinit / gradient still running on its stream.
+    // reinit / gradient still running on its stream.  Chunks are multiples of
+    // 4096 particles: host offsets that are only 16 B aligned (n / 10 =
+    // 1,945,444 particles) cost 7.28 ms against 6.65-6.70 ms for 1.90 M /
+    // 1.97 M / 2 M-particle chunks (profiles/r02/e2e_staging.jsonl).
     // (SG_PROBE_CHUNK / SG_PROBE_RING / SG_PROBE_DOWN1: experiment overrides)
     static const int64_t env_chunk = [] {
         const char* e = std::getenv("SG_PROBE_CHUNK");
@@ -789,7 +792,8 @@ void launch_probe(const sg_grid* g, int64_t n, const void* pos, void* phi, void*
     }();
     const int kRing = env_ring;
     const int64_t chunk = env_chunk > 0 ? std::min<int64_t>(n, env_chunk) : std::min<int64_t>(
-        n, std::max<int64_t>((int64_t)1 << 18, std::min<int64_t>(ceil_div(n, 10), (int64_t)1 << 21)));
+        n, std::max<int64_t>((int64_t)1 << 18,
+                             std::min<int64_t>(ceil_div(ceil_div(n, 10), 4096) * 4096, (int64_t)1 << 21)));
     const size_t es = (size_t)g->esz;
     const size_t per = chunk * es * (3 + 1 + (grad ? 3 : 0));
     // the uploads of the positions do not depend on the grid: only the probe
