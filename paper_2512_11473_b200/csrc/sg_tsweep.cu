@@ -33,13 +33,17 @@
 // list) is built once per grid on the device (one hash set per CTA) and
 // reused by every reinit call; sg_sign_correct's table fix invalidates it.
 //
-// Measured (one B200, profiles/README.md): C2 24.7 us per sweep vs 15.1 us
-// for the single sweep, C3 274 vs 158 us.  The thick band's tiles carry a
+// Measured (one B200, profiles/README.md): C2 24.7-26.9 us per sweep vs 15.1
+// us for the single sweep, C3 274-292 vs 158 us (row-per-lane cp.async
+// staging and this version: TMA bulk staging + two rows per lane; 64-package
+// tiles at 3 CTAs / SM measure the same).  The thick band's tiles carry a
 // large neighbourhood (1.7 halo packages per tile package at 96 packages per
-// tile: 0.9 extra rows loaded and 0.57 extra rows updated in sweep 1 per
-// tile row), one row per lane costs ~51 instructions per point update, and
-// 106 KB of shared memory + 114 registers leave 4 warps per scheduler to
-// hide the staging latency.  Kept as an opt-in path (SG_TSWEEP=1) with its
+// tile: 0.9 extra rows staged and 0.57 extra rows updated in sweep 1 per
+// tile row); ncu (C2): 20 M warp instructions per two-sweep launch, 57 % of
+// them the Godunov arithmetic itself, issue active 45 % (stalls: fixed
+// latency of the arithmetic chains, shared-memory loads and the four
+// barriers per tile), 16 warps per SM.  Kept as an opt-in path (SG_TSWEEP=1)
+// with its
 // bitwise tests (tests/test_tsweep_gpu.py).
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
@@ -56,11 +60,10 @@ constexpr int kTI = 96;        // packages per level-0 chunk
 constexpr int kTCap = 384;     // slots per tile (2 singular + packages + halo)
 constexpr int kTComp = 1280;   // first-sweep halo rows per tile
 constexpr int kTT = 256;       // threads per tile CTA
-constexpr int kTR = (16 * kTI + kTComp + kTT - 1) / kTT;  // first-sweep rows per thread
 constexpr int kHS = 2048;      // plan hash set (>= 19 kTI candidates)
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr uint32_t kInt = 0x80000000u;  // hash value flag: a package of the chunk
-constexpr size_t kTSmem = (size_t)kTCap * (256 + 16 + 4 + 2);
+constexpr size_t kTSmem = (size_t)kTCap * (256 + 16 + 4);
 
 static_assert(2 + kTI + 18 * kTI <= kHS, "plan hash set too small");
 static_assert(kTCap <= 4096, "slots are 12-bit in the row list");
@@ -326,22 +329,85 @@ __device__ __forceinline__ float4 row_step(const float4* D, const uint4* LF, int
     return make_float4(o[0], o[1], o[2], o[3]);
 }
 
+// the two x-rows (j, k), (j, k + 2) of slot s (8 lanes per package, lane
+// (j, k), k in {0, 1}): the cross of load_cross2 (sg_stencil.cu) from the
+// staged slots, then the ReinitOp arithmetic -- bit-identical to k_sweep
+__device__ __forceinline__ void pkg_step(const float4* D, const uint4* LF, int s, int j, int k,
+                                         const StC<float>& c, float4& out0, float4& out1) {
+    const uint4 L = LF[s];
+    const int nxm = L.x & 0xffff, nxp = L.x >> 16, nym = L.y & 0xffff, nyp = L.y >> 16;
+    const int nzm = L.z & 0xffff, nzp = L.z >> 16;
+    const float4* P = D + s * 16;
+    const int r0 = j + 4 * k, r1 = r0 + 8;
+    float c0[4], c1[4], zlo[4], zmid[4], zhi[4], ym0[4], yp0[4], ym1[4], yp1[4], o0[4], o1[4];
+    f4(P[r0], c0);
+    f4(P[r1], c1);
+    f4(P[r0 + 4], zmid);
+    f4(k == 0 ? D[nzm * 16 + j + 12] : P[j], zlo);
+    f4(k == 0 ? P[j + 12] : D[nzp * 16 + j], zhi);
+    f4(j > 0 ? P[r0 - 1] : D[nym * 16 + 3 + 4 * k], ym0);
+    f4(j < 3 ? P[r0 + 1] : D[nyp * 16 + 4 * k], yp0);
+    f4(j > 0 ? P[r1 - 1] : D[nym * 16 + 3 + 4 * (k + 2)], ym1);
+    f4(j < 3 ? P[r1 + 1] : D[nyp * 16 + 4 * (k + 2)], yp1);
+    const float* Xm = reinterpret_cast<const float*>(D + nxm * 16);
+    const float* Xp = reinterpret_cast<const float*>(D + nxp * 16);
+    const float xm0 = Xm[4 * r0 + 3], xm1 = Xm[4 * r1 + 3], xp0 = Xp[4 * r0], xp1 = Xp[4 * r1];
+    godunov_row(c0, xm0, xp0, ym0, yp0, zlo, zmid, c, o0);
+    godunov_row(c1, xm1, xp1, ym1, yp1, zmid, zhi, c, o1);
+    out0 = make_float4(o0[0], o0[1], o0[2], o0[3]);
+    out1 = make_float4(o1[0], o1[1], o1[2], o1[3]);
+}
+
+// TMA bulk copy global -> shared, completing on an mbarrier (1-D, 16 B units)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned tx) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W;\n}\n" ::"r"(b), "r"(parity)
+        : "memory");
+}
+
 // Two Jacobi sweeps phi_in -> phi_out over every active package, one tile per
 // CTA iteration (persistent: tile t = blockIdx.x + i * gridDim.x).  Shared
-// memory: kTCap package slots of 64 floats, their face slots, their ids.
+// memory: kTCap package slots of 64 floats, their face slots, ids, row masks.
+// Staging: TMA bulk copies (one per tile package, one per run of consecutive
+// staged rows of a halo package) completing on one mbarrier phase per tile;
+// the next tile's plan rows are prefetched into registers during sweep 2.
 __global__ void __launch_bounds__(kTT, 2) k_tsweep(const float* __restrict__ in,
                                                    float* __restrict__ out, TPlanDev P,
                                                    StC<float> c) {
-    extern __shared__ __align__(16) unsigned char sm_raw[];
+    extern __shared__ __align__(128) unsigned char sm_raw[];
     float4* D = reinterpret_cast<float4*>(sm_raw);
     uint4* LF = reinterpret_cast<uint4*>(D + kTCap * 16);
     uint32_t* ID = reinterpret_cast<uint32_t*>(LF + kTCap);
-    uint16_t* M2 = reinterpret_cast<uint16_t*>(ID + kTCap);
+    __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
+    const int g8 = tid & 7, j = g8 & 3, k = g8 >> 2, grp = tid >> 3;  // 32 package groups
     const uint32_t nt = (uint32_t)min((long long)*(volatile uint32_t*)P.ctr, (long long)P.t_cap);
-    // the next tile's plan rows travel in registers (slots tid, tid + kTT)
-    // while the current tile is swept
+    if (tid == 0) {
+        mbar_init(&bar, kTT);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
     static_assert(kTCap <= 2 * kTT, "two plan slots per thread");
+    constexpr int kPI = (kTI + 31) / 32;            // tile packages per 8-lane group
+    constexpr int kHR = (kTComp + kTT - 1) / kTT;   // first-sweep halo rows per thread
     int4 cn = make_int4(0, 0, 0, 0);
     uint32_t pid[2] = {0, 0};
     uint4 plf[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
@@ -361,61 +427,103 @@ __global__ void __launch_bounds__(kTT, 2) k_tsweep(const float* __restrict__ in,
         }
     };
     if (blockIdx.x < nt) fetch(blockIdx.x);
+    unsigned phase = 0;
     for (uint32_t t = blockIdx.x; t < nt; t += gridDim.x) {
-        const int nI = cn.x, nH = cn.y, nC = cn.z, nS = 2 + nI + nH;
+        const int nI = cn.x, nC = cn.z, nS = 2 + nI + cn.y;
+        // stage: every thread arrives once with the bytes it issues
+        uint32_t tx = 0;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int s = tid + h * kTT;
             if (s < nS) {
                 ID[s] = pid[h];
                 LF[s] = plf[h];
-                M2[s] = pm2[h];
+                if (s < 2 + nI) {
+                    tx += 256;
+                } else {
+                    for (uint32_t m = pm2[h]; m;) {  // runs of consecutive rows
+                        const int r0 = __ffs(m) - 1;
+                        const uint32_t run = ~(m >> r0);
+                        const int len = run ? __ffs(run) - 1 : 16 - r0;
+                        tx += 16u * len;
+                        m &= ~(((1u << len) - 1u) << r0);
+                    }
+                }
             }
         }
-        __syncthreads();
-        // stage: singular + tile packages whole, halo packages row by row
-        for (int w = tid; w < 16 * (2 + nI); w += kTT)
-            cp16(D + w, in + (size_t)ID[w >> 4] * 64 + 4 * (w & 15));
-        for (int w = tid; w < 16 * nH; w += kTT) {
-            const int s = 2 + nI + (w >> 4), r = w & 15;
-            if ((M2[s] >> r) & 1u) cp16(D + s * 16 + r, in + (size_t)ID[s] * 64 + 4 * r);
+        mbar_arrive_tx(&bar, tx);
+        // the slots were written by threads (generic proxy) in the previous
+        // tile; order those writes before the TMA (async proxy) overwrites
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int s = tid + h * kTT;
+            if (s < nS) {
+                const float* src = in + (size_t)pid[h] * 64;
+                if (s < 2 + nI) {
+                    bulk_g2s(D + s * 16, src, 256, &bar);
+                } else {
+                    for (uint32_t m = pm2[h]; m;) {
+                        const int r0 = __ffs(m) - 1;
+                        const uint32_t run = ~(m >> r0);
+                        const int len = run ? __ffs(run) - 1 : 16 - r0;
+                        bulk_g2s(D + s * 16 + r0, src + 4 * r0, 16u * len, &bar);
+                        m &= ~(((1u << len) - 1u) << r0);
+                    }
+                }
+            }
         }
         // the first-sweep halo row list, read while the stage is in flight
-        const int nint = 16 * nI, n1 = nint + nC;
-        uint32_t ce[kTR];
+        uint32_t ce[kHR];
 #pragma unroll
-        for (int q = 0; q < kTR; ++q) {
+        for (int q = 0; q < kHR; ++q) {
             const int w = tid + kTT * q;
-            ce[q] = (w >= nint && w < n1) ? __ldg(P.comp + (size_t)t * kTComp + (w - nint)) : 0u;
+            ce[q] = w < nC ? __ldg(P.comp + (size_t)t * kTComp + w) : 0u;
         }
-        cp_wait_all();
-        __syncthreads();
-        // sweep 1: the tile's rows and the halo rows at distance 1, kept in
-        // registers until every thread has read its inputs
-        float4 res[kTR];
-        int at[kTR];
+        __syncthreads();  // ID / LF visible
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        // sweep 1: tile packages (two rows per lane) and the halo rows at
+        // distance 1 (one row per lane), kept in registers until every
+        // thread has read its inputs
+        float4 a0[kPI], a1[kPI], hr[kHR];
 #pragma unroll
-        for (int q = 0; q < kTR; ++q) {
+        for (int q = 0; q < kPI; ++q) {
+            const int pi = grp + 32 * q;
+            if (pi < nI) pkg_step(D, LF, 2 + pi, j, k, c, a0[q], a1[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < kHR; ++q) {
             const int w = tid + kTT * q;
-            at[q] = -1;
-            if (w < n1) {
-                const int s = w < nint ? 2 + (w >> 4) : (int)(ce[q] >> 4);
-                const int r = w < nint ? (w & 15) : (int)(ce[q] & 15u);
-                res[q] = row_step(D, LF, s, r, c);
-                at[q] = s * 16 + r;
+            if (w < nC) hr[q] = row_step(D, LF, (int)(ce[q] >> 4), (int)(ce[q] & 15u), c);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kPI; ++q) {
+            const int pi = grp + 32 * q;
+            if (pi < nI) {
+                D[(2 + pi) * 16 + j + 4 * k] = a0[q];
+                D[(2 + pi) * 16 + j + 4 * k + 8] = a1[q];
             }
         }
-        __syncthreads();
 #pragma unroll
-        for (int q = 0; q < kTR; ++q)
-            if (at[q] >= 0) D[at[q]] = res[q];
+        for (int q = 0; q < kHR; ++q) {
+            const int w = tid + kTT * q;
+            if (w < nC) D[(ce[q] >> 4) * 16 + (ce[q] & 15u)] = hr[q];
+        }
         __syncthreads();
         if (t + gridDim.x < nt) fetch(t + gridDim.x);
-        // sweep 2: the tile's rows, straight to HBM
-        for (int w = tid; w < nint; w += kTT) {
-            const int s = 2 + (w >> 4), r = w & 15;
-            const float4 v = row_step(D, LF, s, r, c);
-            *reinterpret_cast<float4*>(out + (size_t)ID[s] * 64 + 4 * r) = v;
+        // sweep 2: the tile packages, straight to HBM
+#pragma unroll
+        for (int q = 0; q < kPI; ++q) {
+            const int pi = grp + 32 * q;
+            if (pi < nI) {
+                float4 v0, v1;
+                pkg_step(D, LF, 2 + pi, j, k, c, v0, v1);
+                float4* O = reinterpret_cast<float4*>(out + (size_t)ID[2 + pi] * 64);
+                O[j + 4 * k] = v0;
+                O[j + 4 * k + 8] = v1;
+            }
         }
         __syncthreads();
     }
