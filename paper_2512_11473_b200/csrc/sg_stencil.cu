@@ -134,10 +134,12 @@ __device__ __forceinline__ void load_cross2(const T* __restrict__ in, uint32_t p
     const int grp = (threadIdx.x >> 3) & 3;
     const uint32_t nxm = __shfl_sync(0xffffffffu, f, base + 0);
     const uint32_t nxp = __shfl_sync(0xffffffffu, f, base + 1);
-    const uint32_t nym = __shfl_sync(0xffffffffu, f, base + 2);
-    const uint32_t nyp = __shfl_sync(0xffffffffu, f, base + 3);
-    const uint32_t nzm = __shfl_sync(0xffffffffu, f, base + 4);
-    const uint32_t nzp = __shfl_sync(0xffffffffu, f, base + 5);
+    // a lane reads the -y face only for j = 0, the +y face only for j = 3,
+    // the -z face only for k = 0 and the +z face only for k = 1: one shuffle
+    // each for "its" y and z neighbour (lanes j = 1, 2 take an unused id)
+    const uint32_t ny = __shfl_sync(0xffffffffu, f, base + (j == 0 ? 2 : 3));
+    const uint32_t nz = __shfl_sync(0xffffffffu, f, base + (k == 0 ? 4 : 5));
+    const uint32_t nym = ny, nyp = ny, nzm = nz, nzp = nz;
     const bool sh_m = grp > 0 && nxm == pkg - 1;
     const bool sh_p = grp < 3 && next_ok && nxp == pkg + 1;
     if (valid) {
