@@ -126,10 +126,14 @@ struct Cross2 {
 // they come by a shuffle of 8 lanes instead of four scalar loads, which cut
 // 16-of-256-byte sector fetches from the L2.  `next_ok`: package pkg + 1 is
 // processed by the next group in this iteration (pkg + 1 < hi).
-template <class T>
+// O32: element offsets fit in 32 bits (n_pkg * 64 < 2^32, every grid up to
+// ~4.5x C5): one 32-bit select + one wide multiply-add per load address
+// instead of a 64-bit pointer select
+template <class T, bool O32 = true>
 __device__ __forceinline__ void load_cross2(const T* __restrict__ in, uint32_t pkg, bool valid,
                                             bool next_ok, uint32_t f, int j, int k,
                                             Cross2<T>& x) {
+    using Off = typename std::conditional<O32, uint32_t, size_t>::type;
     const int base = threadIdx.x & 24;
     const int grp = (threadIdx.x >> 3) & 3;
     const uint32_t nxm = __shfl_sync(0xffffffffu, f, base + 0);
@@ -139,28 +143,27 @@ __device__ __forceinline__ void load_cross2(const T* __restrict__ in, uint32_t p
     // each for "its" y and z neighbour (lanes j = 1, 2 take an unused id)
     const uint32_t ny = __shfl_sync(0xffffffffu, f, base + (j == 0 ? 2 : 3));
     const uint32_t nz = __shfl_sync(0xffffffffu, f, base + (k == 0 ? 4 : 5));
-    const uint32_t nym = ny, nyp = ny, nzm = nz, nzp = nz;
     const bool sh_m = grp > 0 && nxm == pkg - 1;
     const bool sh_p = grp < 3 && next_ok && nxp == pkg + 1;
     if (valid) {
-        const T* P = in + (size_t)pkg * 64;
+        const Off b0 = (Off)pkg * 64, by = (Off)ny * 64, bz = (Off)nz * 64;
         const int r0 = j + 4 * k, r1 = r0 + 8;
-        ld_row(P + 4 * r0, x.c0);
-        ld_row(P + 4 * r1, x.c1);
-        ld_row(P + 4 * (r0 + 4), x.zmid);
-        ld_row(k == 0 ? in + (size_t)nzm * 64 + 4 * (j + 12) : P + 4 * j, x.zlo);
-        ld_row(k == 0 ? P + 4 * (j + 12) : in + (size_t)nzp * 64 + 4 * j, x.zhi);
-        ld_row(j > 0 ? P + 4 * (r0 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * k), x.ym0);
-        ld_row(j < 3 ? P + 4 * (r0 + 1) : in + (size_t)nyp * 64 + 4 * (4 * k), x.yp0);
-        ld_row(j > 0 ? P + 4 * (r1 - 1) : in + (size_t)nym * 64 + 4 * (3 + 4 * (k + 2)), x.ym1);
-        ld_row(j < 3 ? P + 4 * (r1 + 1) : in + (size_t)nyp * 64 + 4 * (4 * (k + 2)), x.yp1);
+        ld_row(in + (b0 + 4 * r0), x.c0);
+        ld_row(in + (b0 + 4 * r1), x.c1);
+        ld_row(in + (b0 + 4 * (r0 + 4)), x.zmid);
+        ld_row(in + (k == 0 ? bz + 4 * (j + 12) : b0 + 4 * j), x.zlo);
+        ld_row(in + (k == 0 ? b0 + 4 * (j + 12) : bz + 4 * j), x.zhi);
+        ld_row(in + (j > 0 ? b0 + 4 * (r0 - 1) : by + 4 * (3 + 4 * k)), x.ym0);
+        ld_row(in + (j < 3 ? b0 + 4 * (r0 + 1) : by + 4 * (4 * k)), x.yp0);
+        ld_row(in + (j > 0 ? b0 + 4 * (r1 - 1) : by + 4 * (3 + 4 * (k + 2))), x.ym1);
+        ld_row(in + (j < 3 ? b0 + 4 * (r1 + 1) : by + 4 * (4 * (k + 2))), x.yp1);
         if (!sh_m) {
-            x.xm0 = __ldg(in + (size_t)nxm * 64 + 4 * r0 + 3);
-            x.xm1 = __ldg(in + (size_t)nxm * 64 + 4 * r1 + 3);
+            x.xm0 = __ldg(in + ((Off)nxm * 64 + 4 * r0 + 3));
+            x.xm1 = __ldg(in + ((Off)nxm * 64 + 4 * r1 + 3));
         }
         if (!sh_p) {
-            x.xp0 = __ldg(in + (size_t)nxp * 64 + 4 * r0);
-            x.xp1 = __ldg(in + (size_t)nxp * 64 + 4 * r1);
+            x.xp0 = __ldg(in + ((Off)nxp * 64 + 4 * r0));
+            x.xp1 = __ldg(in + ((Off)nxp * 64 + 4 * r1));
         }
     }
     // every lane takes part (the caller's trip count is warp-uniform)
@@ -182,7 +185,7 @@ __device__ __forceinline__ void load_cross2(const T* __restrict__ in, uint32_t p
 // the face ids of the next package are loaded while the current one is
 // processed, so the face-row gathers do not wait on the face table.
 // Op(x, pkg, r0, r1) consumes the cross of rows r0 = j + 4k and r1 = r0 + 8.
-template <class T, class Op>
+template <class T, class Op, bool O32 = true>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 2) k_sweep(const T* __restrict__ in,
                                                const uint32_t* __restrict__ face, uint32_t lo,
                                                uint32_t hi, Op op) {
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 2) k_sweep(const T* 
         if (nxt < hi && g8 < 6) fn = __ldg(face + (size_t)nxt * 8 + g8);
         Cross2<T> x;
         const bool valid = pkg < hi;
-        load_cross2(in, pkg, valid, pkg + 1 < hi, f, j, k, x);
+        load_cross2<T, O32>(in, pkg, valid, pkg + 1 < hi, f, j, k, x);
         if (valid) op(x, pkg, j + 4 * k, j + 4 * k + 8);
         pkg = nxt;
         f = fn;
@@ -676,9 +679,11 @@ static bool reinit_launch(sg_grid* g, int cur, const StC<T>& c, int64_t lo, int6
                           cudaStream_t s) {
     if (hi <= lo) return false;
     const ReinitOp<T> op{(T*)g->phi[1 - cur], c};
-    const unsigned blocks = persistent_blocks(k_sweep<T, ReinitOp<T>>, hi - lo);
-    k_sweep<T, ReinitOp<T>><<<blocks, 256, 0, s>>>((const T*)g->phi[cur], g->face, (uint32_t)lo,
-                                                   (uint32_t)hi, op);
+    // 32-bit element offsets below 2^32 data points (the stored packages)
+    auto kern = g->n_pkg * 64 < ((int64_t)1 << 32) ? k_sweep<T, ReinitOp<T>, true>
+                                                   : k_sweep<T, ReinitOp<T>, false>;
+    const unsigned blocks = persistent_blocks(kern, hi - lo);
+    kern<<<blocks, 256, 0, s>>>((const T*)g->phi[cur], g->face, (uint32_t)lo, (uint32_t)hi, op);
     return true;
 }
 
