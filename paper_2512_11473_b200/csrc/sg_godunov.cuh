@@ -79,9 +79,13 @@ __device__ __forceinline__ void godunov_row(const float (&p)[4], float xm, float
                                             const float (&zm)[4], const float (&zp)[4],
                                             const StC<float>& c, float (&o)[4]) {
     float a[4], b[4], wx[4];
+    // a = -sign(p) / dx as one bit operation: the sign bit of p flips
+    // -1/dx.  (p = -0 gets +1/dx where the select gave -1/dx; the step
+    // returns p unchanged for p = +-0 either way: s = 0.)
+    const uint32_t nid = __float_as_uint(-c.inv_dx);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        a[i] = p[i] < 0.f ? c.inv_dx : -c.inv_dx;
+        a[i] = __uint_as_float((__float_as_uint(p[i]) & 0x80000000u) ^ nid);
         b[i] = fabsf(p[i]) * c.inv_dx;
         const float m = i > 0 ? p[i - 1] : xm, q = i < 3 ? p[i + 1] : xp;
         wx[i] = max3f(fmaf(a[i], m, b[i]), fmaf(a[i], q, b[i]), 0.f);
