@@ -121,7 +121,9 @@ struct __align__(16) ProbeSmem {
 
 // I32: the exact fp32 index fast path (gc.idx32); V: 16 B aligned caller
 // buffers (vector staging of full fp32 chunks) -- both resolved at launch
-template <class T, bool I32, bool V, bool Q = false>
+// O32: (package, point, component) offsets of the gradient layout fit in 32
+// bits (n_pkg * 256 < 2^32): 32-bit corner address arithmetic
+template <class T, bool I32, bool V, bool Q = false, bool O32 = false>
 __global__ void __launch_bounds__(32 * ProbeSmem<T>::kWB, 4)
 k_probe(GridC gc, const uint32_t* __restrict__ bg,
                                                const uint32_t* __restrict__ nb,
@@ -331,7 +333,12 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
             if (pg) {
                 T v[8][4];
 #pragma unroll
-                for (int cc = 0; cc < 8; ++cc) ld_vec4(pg + ((size_t)pk[cc] * 64 + d[cc]) * 4, v[cc]);
+                for (int cc = 0; cc < 8; ++cc) {
+                    if constexpr (O32)
+                        ld_vec4(pg + (pk[cc] * 256u + 4u * (uint32_t)d[cc]), v[cc]);
+                    else
+                        ld_vec4(pg + ((size_t)pk[cc] * 64 + d[cc]) * 4, v[cc]);
+                }
 #pragma unroll
                 for (int cc = 0; cc < 8; ++cc) {
                     const T wgt = (((cc & 1) ? tx : T(1) - tx) * ((cc & 2) ? ty : T(1) - ty)) *
@@ -342,7 +349,12 @@ k_probe(GridC gc, const uint32_t* __restrict__ bg,
             } else {
                 T v[8];
 #pragma unroll
-                for (int cc = 0; cc < 8; ++cc) v[cc] = __ldg(phi + (size_t)pk[cc] * 64 + d[cc]);
+                for (int cc = 0; cc < 8; ++cc) {
+                    if constexpr (O32)
+                        v[cc] = __ldg(phi + (pk[cc] * 64u + (uint32_t)d[cc]));
+                    else
+                        v[cc] = __ldg(phi + (size_t)pk[cc] * 64 + d[cc]);
+                }
 #pragma unroll
                 for (int cc = 0; cc < 8; ++cc) {
                     const T wgt = (((cc & 1) ? tx : T(1) - tx) * ((cc & 2) ? ty : T(1) - ty)) *
@@ -410,7 +422,10 @@ static void probe_dev(const sg_grid* g, int64_t n, const void* pos, void* out_ph
     const bool q = force_q == 1 || (force_q != 0 && ceil_div(n, kPW) > 256 * blocks * kWB);
     auto kern = q ? k_probe<T, false, false, true> : k_probe<T, false, false>;
     if constexpr (sizeof(T) == 4) {
-        if (g->gc.idx32)
+        const bool o32 = g->n_pkg * 256 < ((int64_t)1 << 32);
+        if (g->gc.idx32 && vec && o32)
+            kern = q ? k_probe<T, true, true, true, true> : k_probe<T, true, true, false, true>;
+        else if (g->gc.idx32)
             kern = vec ? (q ? k_probe<T, true, true, true> : k_probe<T, true, true>)
                        : (q ? k_probe<T, true, false, true> : k_probe<T, true, false>);
         else if (vec)
