@@ -402,8 +402,10 @@ __device__ __forceinline__ double heav(double u, double eps, double inv_eps) {
 
 // the smoothed Heaviside as selects: both outer branches are exact 0 / 1
 __device__ __forceinline__ float heav_sel(float u, float eps, float inv_eps) {
-    const float q = u * inv_eps;
-    const float sm = 0.5f * (1.f + q + __sinf(3.14159265358979f * q) * 0.318309886183790672f);
+    // 1/2 (1 + q) + sin(pi q) / (2 pi), q = u / eps, as two FMAs around the
+    // MUFU sine (the products of inv_eps are per-launch constants)
+    const float lin = fmaf(u, 0.5f * inv_eps, 0.5f);
+    const float sm = fmaf(__sinf(u * (3.14159265358979f * inv_eps)), 0.159154943091895336f, lin);
     return u < -eps ? 0.f : (u > eps ? 1.f : sm);
 }
 __device__ __forceinline__ double heav_sel(double u, double eps, double inv_eps) {
@@ -513,10 +515,20 @@ __global__ void __launch_bounds__(GR ? 256 : 128) k_kint(const T* __restrict__ i
                 // H(-phi): rows with no value inside the smoothing band
                 // |phi| <= eps take the exact 0 / 1 select only (no sine);
                 // the others the branch-free smooth form
+                // One min / max pass classifies the row: it meets the band
+                // when min |v| <= eps; otherwise H is exactly 1 (0) on all of
+                // it iff max v < 0 (min v > 0).  (A band row is never taken
+                // as uniform, even where its smooth values round to 1 / 0:
+                // the taps then give the same values to rounding.)
                 T h[RSX];
-                bool smooth = false;
+                T vmin = v[0], vmax = v[0], amin = fabs(v[0]);
 #pragma unroll
-                for (int q = 0; q < RS; ++q) smooth = smooth || !(fabs(v[q]) > c.eps);
+                for (int q = 1; q < RS; ++q) {
+                    vmin = fmin(vmin, v[q]);
+                    vmax = fmax(vmax, v[q]);
+                    amin = fmin(amin, fabs(v[q]));
+                }
+                const bool smooth = !(amin > c.eps);
                 if (smooth) {
 #pragma unroll
                     for (int q = 0; q < RSX; ++q) h[q] = heav_sel(-v[q], c.eps, c.inv_eps);
@@ -524,11 +536,8 @@ __global__ void __launch_bounds__(GR ? 256 : 128) k_kint(const T* __restrict__ i
 #pragma unroll
                     for (int q = 0; q < RSX; ++q) h[q] = v[q] < T(0) ? T(1) : T(0);
                 }
-#pragma unroll
-                for (int q = 0; q < RS; ++q) {
-                    all1 = all1 && (h[q] == T(1));
-                    all0 = all0 && (h[q] == T(0));
-                }
+                all1 = all1 && !smooth && vmax < T(0);
+                all0 = all0 && !smooth && vmin > T(0);
                 T* dst = H + lz * SLICE + ly * RSX;
 #pragma unroll
                 for (int q = 0; q < RSX; q += 4) {
