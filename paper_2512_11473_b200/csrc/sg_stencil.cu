@@ -438,8 +438,121 @@ struct KGeo {
 // gradient / normal of the block's 8 packages (16 lanes per package, as in
 // k_gradient) while warps 0..3 compute their kernel integrals: the
 // HBM-write-bound K6 warps and the issue-bound K7 warps share every SM.
+// fp32 tap loop of k_kint on paired-FP32 instructions: the (up to) four
+// rows of a (abs oy, abs oz) group are combined by the sign butterfly with
+// FADD2 / FFMA2 (value pairs (q, q + 1) are aligned register pairs of the
+// staged float4 rows), and every tap whose window offset R + ox is even
+// updates output points (0, 1) and (2, 3) with one FFMA2 each; odd offsets
+// stay scalar.  Per output the operations and their order are those of the
+// generic loop -- bit-identical results.
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
+    return __ffma2_rn(b, make_float2(-1.f, -1.f), a);  // a - b, exact as FADD
+}
+template <int R, int S2M, class Load>
+__device__ __forceinline__ void kint_taps_f2(const KintC<float>& c, Load&& load, float (&acc)[4],
+                                             float (&gx)[4], float (&gy)[4], float (&gz)[4]) {
+    float2 A[2], X[2], Y[2], Z[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) A[u] = X[u] = Y[u] = Z[u] = make_float2(0.f, 0.f);
+    auto pairs = [](const float (&h)[8], float2 (&o)[4]) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) o[u] = make_float2(h[2 * u], h[2 * u + 1]);
+    };
+    auto el = [](const float2 (&v)[4], int q) { return (q & 1) ? v[q >> 1].y : v[q >> 1].x; };
+#pragma unroll
+    for (int ga = 0; ga <= R; ++ga) {
+#pragma unroll
+        for (int gb = 0; gb <= R; ++gb) {
+            if (ga * ga + gb * gb > S2M) continue;
+            float2 S[4], Dy[4], Dz[4];
+            if (ga == 0 && gb == 0) {
+                float h[8];
+                load(0, 0, h);
+                pairs(h, S);
+            } else if (gb == 0 || ga == 0) {
+                float hp[8], hm[8];
+                load(gb == 0 ? ga : 0, gb == 0 ? 0 : gb, hp);
+                load(gb == 0 ? -ga : 0, gb == 0 ? 0 : -gb, hm);
+                float2 p2[4], m2[4];
+                pairs(hp, p2);
+                pairs(hm, m2);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    S[u] = __fadd2_rn(p2[u], m2[u]);
+                    (gb == 0 ? Dy : Dz)[u] = f2sub(p2[u], m2[u]);
+                }
+            } else {
+                float hpp[8], hpm[8], hmp[8], hmm[8];
+                load(ga, gb, hpp);
+                load(ga, -gb, hpm);
+                load(-ga, gb, hmp);
+                load(-ga, -gb, hmm);
+                float2 pp[4], pm[4], mp[4], mm[4];
+                pairs(hpp, pp);
+                pairs(hpm, pm);
+                pairs(hmp, mp);
+                pairs(hmm, mm);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 a1 = __fadd2_rn(pp[u], pm[u]), b1 = __fadd2_rn(mp[u], mm[u]);
+                    const float2 c1 = f2sub(pp[u], pm[u]), d1 = f2sub(mp[u], mm[u]);
+                    S[u] = __fadd2_rn(a1, b1);
+                    Dy[u] = f2sub(a1, b1);
+                    Dz[u] = __fadd2_rn(c1, d1);
+                }
+            }
+#pragma unroll
+            for (int ox = -R; ox <= R; ++ox) {
+                const int s2 = ox * ox + ga * ga + gb * gb;
+                if (s2 > S2M) continue;
+                const float w = c.wt[s2];
+                const float wx = ox > 0 ? c.gt[ox][s2] : -c.gt[-ox][s2];
+                const float wy = c.gt[ga][s2];
+                const float wz = c.gt[gb][s2];
+                const int q0 = R + ox;
+                if ((q0 & 1) == 0) {
+                    const float2 w2 = make_float2(w, w), wx2 = make_float2(wx, wx);
+                    const float2 wy2 = make_float2(wy, wy), wz2 = make_float2(wz, wz);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int p = (q0 >> 1) + u;
+                        A[u] = __ffma2_rn(w2, S[p], A[u]);
+                        if (ox) X[u] = __ffma2_rn(wx2, S[p], X[u]);
+                        if (ga) Y[u] = __ffma2_rn(wy2, Dy[p], Y[u]);
+                        if (gb) Z[u] = __ffma2_rn(wz2, Dz[p], Z[u]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        float& a = (i & 1) ? A[i >> 1].y : A[i >> 1].x;
+                        float& x = (i & 1) ? X[i >> 1].y : X[i >> 1].x;
+                        float& y = (i & 1) ? Y[i >> 1].y : Y[i >> 1].x;
+                        float& z = (i & 1) ? Z[i >> 1].y : Z[i >> 1].x;
+                        const float hv = el(S, q0 + i);
+                        a = fmaf(w, hv, a);
+                        if (ox) x = fmaf(wx, hv, x);
+                        if (ga) y = fmaf(wy, el(Dy, q0 + i), y);
+                        if (gb) z = fmaf(wz, el(Dz, q0 + i), z);
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        acc[2 * u] = A[u].x;
+        acc[2 * u + 1] = A[u].y;
+        gx[2 * u] = X[u].x;
+        gx[2 * u + 1] = X[u].y;
+        gy[2 * u] = Y[u].x;
+        gy[2 * u + 1] = Y[u].y;
+        gz[2 * u] = Z[u].x;
+        gz[2 * u + 1] = Z[u].y;
+    }
+}
+
 template <class T, int R, int S2M, bool GR = false>
-__global__ void __launch_bounds__(GR ? 256 : 128) k_kint(const T* __restrict__ in,
+__global__ void __launch_bounds__(GR ? 256 : 128, (R == 2 && S2M == 6 && sizeof(T) == 4) ? (GR ? 5 : 10) : 1) k_kint(const T* __restrict__ in,
                                               const uint32_t* __restrict__ nb, int64_t lo,
                                               int64_t hi, KintC<T> c, T* __restrict__ K,
                                               T* __restrict__ G, T* __restrict__ grad = nullptr,
@@ -593,56 +706,61 @@ __global__ void __launch_bounds__(GR ? 256 : 128) k_kint(const T* __restrict__ i
                 }
             }
         };
+        if constexpr (sizeof(T) == 4 && RSX == 8) {
+            kint_taps_f2<R, S2M>(c, [&](int oy, int oz, float (&h)[8]) { load(oy, oz, h); }, acc,
+                                 gx, gy, gz);
+        } else {
 #pragma unroll
-        for (int ga = 0; ga <= R; ++ga) {
+            for (int ga = 0; ga <= R; ++ga) {
 #pragma unroll
-            for (int gb = 0; gb <= R; ++gb) {
-                if (ga * ga + gb * gb > S2M) continue;
-                T S[RSX], Dy[RSX], Dz[RSX];
-                if (ga == 0 && gb == 0) {
-                    load(0, 0, S);
-                } else if (gb == 0) {
-                    T p_[RSX], m_[RSX];
-                    load(ga, 0, p_);
-                    load(-ga, 0, m_);
+                for (int gb = 0; gb <= R; ++gb) {
+                    if (ga * ga + gb * gb > S2M) continue;
+                    T S[RSX], Dy[RSX], Dz[RSX];
+                    if (ga == 0 && gb == 0) {
+                        load(0, 0, S);
+                    } else if (gb == 0) {
+                        T p_[RSX], m_[RSX];
+                        load(ga, 0, p_);
+                        load(-ga, 0, m_);
 #pragma unroll
-                    for (int q = 0; q < RSX; ++q) { S[q] = p_[q] + m_[q]; Dy[q] = p_[q] - m_[q]; }
-                } else if (ga == 0) {
-                    T p_[RSX], m_[RSX];
-                    load(0, gb, p_);
-                    load(0, -gb, m_);
+                        for (int q = 0; q < RSX; ++q) { S[q] = p_[q] + m_[q]; Dy[q] = p_[q] - m_[q]; }
+                    } else if (ga == 0) {
+                        T p_[RSX], m_[RSX];
+                        load(0, gb, p_);
+                        load(0, -gb, m_);
 #pragma unroll
-                    for (int q = 0; q < RSX; ++q) { S[q] = p_[q] + m_[q]; Dz[q] = p_[q] - m_[q]; }
-                } else {
-                    T pp[RSX], pm[RSX], mp[RSX], mm[RSX];
-                    load(ga, gb, pp);
-                    load(ga, -gb, pm);
-                    load(-ga, gb, mp);
-                    load(-ga, -gb, mm);
+                        for (int q = 0; q < RSX; ++q) { S[q] = p_[q] + m_[q]; Dz[q] = p_[q] - m_[q]; }
+                    } else {
+                        T pp[RSX], pm[RSX], mp[RSX], mm[RSX];
+                        load(ga, gb, pp);
+                        load(ga, -gb, pm);
+                        load(-ga, gb, mp);
+                        load(-ga, -gb, mm);
 #pragma unroll
-                    for (int q = 0; q < RSX; ++q) {
-                        const T a1 = pp[q] + pm[q], b1 = mp[q] + mm[q];
-                        const T c1 = pp[q] - pm[q], d1 = mp[q] - mm[q];
-                        S[q] = a1 + b1;
-                        Dy[q] = a1 - b1;
-                        Dz[q] = c1 + d1;
+                        for (int q = 0; q < RSX; ++q) {
+                            const T a1 = pp[q] + pm[q], b1 = mp[q] + mm[q];
+                            const T c1 = pp[q] - pm[q], d1 = mp[q] - mm[q];
+                            S[q] = a1 + b1;
+                            Dy[q] = a1 - b1;
+                            Dz[q] = c1 + d1;
+                        }
                     }
-                }
 #pragma unroll
-                for (int ox = -R; ox <= R; ++ox) {
-                    const int s2 = ox * ox + ga * ga + gb * gb;
-                    if (s2 > S2M) continue;
-                    const T w = c.wt[s2];
-                    const T wx = ox > 0 ? c.gt[ox][s2] : -c.gt[-ox][s2];
-                    const T wy = c.gt[ga][s2];
-                    const T wz = c.gt[gb][s2];
+                    for (int ox = -R; ox <= R; ++ox) {
+                        const int s2 = ox * ox + ga * ga + gb * gb;
+                        if (s2 > S2M) continue;
+                        const T w = c.wt[s2];
+                        const T wx = ox > 0 ? c.gt[ox][s2] : -c.gt[-ox][s2];
+                        const T wy = c.gt[ga][s2];
+                        const T wz = c.gt[gb][s2];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const T hv = S[i + R + ox];
-                        acc[i] = fma(w, hv, acc[i]);
-                        if (ox) gx[i] = fma(wx, hv, gx[i]);
-                        if (ga) gy[i] = fma(wy, Dy[i + R + ox], gy[i]);
-                        if (gb) gz[i] = fma(wz, Dz[i + R + ox], gz[i]);
+                        for (int i = 0; i < 4; ++i) {
+                            const T hv = S[i + R + ox];
+                            acc[i] = fma(w, hv, acc[i]);
+                            if (ox) gx[i] = fma(wx, hv, gx[i]);
+                            if (ga) gy[i] = fma(wy, Dy[i + R + ox], gy[i]);
+                            if (gb) gz[i] = fma(wz, Dz[i + R + ox], gz[i]);
+                        }
                     }
                 }
             }
