@@ -1044,6 +1044,10 @@ static void build_impl(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         }
         const int64_t n_active = counts[0];
         SG_ARG(n_active + 2 < 4294967295LL, "sg_build: more than 2^32-3 packages");
+        // the stencil kernels address data points with 32-bit element offsets
+        // (a grid this large would not fit its fields in 180 GB anyway)
+        SG_ARG((n_active + 2) * 64 < ((int64_t)1 << 32),
+               "sg_build: more than 2^32 stored data points on one device");
         g->n_pkg = n_active + 2;
         g->n_core = counts[1];
         g->n_inner = n_active - counts[1];

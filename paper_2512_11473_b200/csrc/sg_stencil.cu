@@ -89,19 +89,20 @@ __device__ __forceinline__ bool load_cross(const T* __restrict__ in,
     const int base = threadIdx.x & 16;
     const uint32_t nxm = __shfl_sync(0xffffffffu, f, base + 0);
     const uint32_t nxp = __shfl_sync(0xffffffffu, f, base + 1);
-    const uint32_t nym = __shfl_sync(0xffffffffu, f, base + 2);
-    const uint32_t nyp = __shfl_sync(0xffffffffu, f, base + 3);
-    const uint32_t nzm = __shfl_sync(0xffffffffu, f, base + 4);
-    const uint32_t nzp = __shfl_sync(0xffffffffu, f, base + 5);
+    // a lane reads the -y face only for j = 0, the +y face only for j = 3 (z:
+    // k = 0 / 3): one shuffle each for its y and z neighbour
+    const uint32_t ny = __shfl_sync(0xffffffffu, f, base + (j == 0 ? 2 : 3));
+    const uint32_t nz = __shfl_sync(0xffffffffu, f, base + (k == 0 ? 4 : 5));
     if (!valid) return false;
-    const T* P = in + pkg * 64;
-    ld_row(P + 4 * r, x.c);
-    ld_row(j > 0 ? P + 4 * (r - 1) : in + (int64_t)nym * 64 + 4 * (3 + 4 * k), x.ym);
-    ld_row(j < 3 ? P + 4 * (r + 1) : in + (int64_t)nyp * 64 + 4 * (0 + 4 * k), x.yp);
-    ld_row(k > 0 ? P + 4 * (r - 4) : in + (int64_t)nzm * 64 + 4 * (j + 12), x.zm);
-    ld_row(k < 3 ? P + 4 * (r + 4) : in + (int64_t)nzp * 64 + 4 * j, x.zp);
-    x.xm = __ldg(in + (int64_t)nxm * 64 + 4 * r + 3);
-    x.xp = __ldg(in + (int64_t)nxp * 64 + 4 * r);
+    // 32-bit element offsets (sg_build rejects grids of >= 2^32 data points)
+    const uint32_t b0 = (uint32_t)pkg * 64u, by = ny * 64u, bz = nz * 64u;
+    ld_row(in + (b0 + 4 * r), x.c);
+    ld_row(in + (j > 0 ? b0 + 4 * (r - 1) : by + 4 * (3 + 4 * k)), x.ym);
+    ld_row(in + (j < 3 ? b0 + 4 * (r + 1) : by + 4 * (0 + 4 * k)), x.yp);
+    ld_row(in + (k > 0 ? b0 + 4 * (r - 4) : bz + 4 * (j + 12)), x.zm);
+    ld_row(in + (k < 3 ? b0 + 4 * (r + 4) : bz + 4 * j), x.zp);
+    x.xm = __ldg(in + (nxm * 64u + 4 * r + 3));
+    x.xp = __ldg(in + (nxp * 64u + 4 * r));
     return true;
 }
 

@@ -286,7 +286,11 @@ __global__ void __launch_bounds__(256) k_tp_plan(const uint32_t* __restrict__ so
                     } else {
                         const int h = h_find(hk, f);
                         l[r] = h < 0 ? 0u : (hv[h] & 0xffffu);  // not staged: never read
+                        // a tile package's face neighbours are all staged
+                        // (6 of the 18 relations); checked, not assumed
+                        if (s < 2 + n && h < 0) atomicOr(P.ctr + 1, 4u);
                     }
+                    if (l[r] >= (uint32_t)nS) atomicOr(P.ctr + 1, 4u);
                 }
             P.lf[t * kTCap + s] =
                 make_uint4(l[0] | (l[1] << 16), l[2] | (l[3] << 16), l[4] | (l[5] << 16), 0u);
@@ -597,6 +601,7 @@ static void tplan_build(sg_grid* g, TPlan* tp, cudaStream_t s) {
         SG_CUDA(cudaMemcpyAsync(h, tp->ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
         SG_CUDA(cudaStreamSynchronize(s));
         if (h[1] & 2u) throw Error(SG_ERR_STATE, "tile plan: a single package overflows a tile");
+        if (h[1] & 4u) throw Error(SG_ERR_STATE, "tile plan: a face slot outside its tile");
         if (!(h[1] & 1u)) {
             tp->n_tiles = h[0];
             tp->state = 1;
