@@ -281,24 +281,29 @@ def kernel_rooflines(sg, w, stream, flush, d_pos, n_part, probe_ms, reinit_ms, h
     fmas = 324.0 * n_act  # 81 taps x (K, Gx, Gy, Gz), direct form
     ke = {"kernel": "k_kint (kernel integrals)", "bound": "alu", "us": t_kint * 1e3,
           "alg_fma": fmas, "achieved": fmas / (t_kint * 1e-3) / 1e12, "unit": "TFMA/s",
-          "peak": fma_peak / 1e12, "frac": fmas / (t_kint * 1e-3) / fma_peak,
-          "note": "direct-form FMAs (the kernel executes fewer: sign butterfly, closed form on "
-                  "uniform packages); peak = SMs x 128 FP32 lanes x max SM clock"}
+          "peak": fma_peak / 1e12, "frac": None,
+          "frac_direct_form": fmas / (t_kint * 1e-3) / fma_peak,
+          "note": "rate of direct-form FMAs (81 taps x 4 per point) against SMs x 128 FP32 lanes x "
+                  "max SM clock; above 1 where the kernel executes fewer FMAs than the direct form "
+                  "(sign butterfly, paired FFMA2, closed form on uniform rows) -- the executed "
+                  "fraction is the ncu entry below"}
     out.append(ke)
     fl = (profile_json("ncu_flops.json") or {}).get(w.name, {}).get("k_kint")
     if fl:
         # the step's fused K6+K7 kernel as ncu counted it: executed FP32
         # FFMA + FADD + FMUL thread instructions per launch over the ncu
         # duration of the same launch (cold cache, serialised)
-        ex = fl["ffma"] + fl["fadd"] + fl["fmul"]
+        ex = fl["ffma"] + fl["fadd"] + fl["fmul"] + 2 * (fl.get("ffma2", 0.0) + fl.get("fadd2", 0.0) +
+                                                         fl.get("fmul2", 0.0))
         ex_peak = (profile_json("alu_peaks.json") or {}).get("fp32_tflops", 2 * fma_peak / 1e12) / 2
         out.append({"kernel": "k_kint<..., K6 fused> executed FP32 work (ncu)", "bound": "alu",
                     "us": fl["us"], "executed_fp32_inst": ex,
                     "achieved": ex / (fl["us"] * 1e-6) / 1e12, "unit": "T inst/s",
                     "peak": ex_peak, "frac": ex / (fl["us"] * 1e-6) / 1e12 / ex_peak,
                     "peak_source": "profiles/alu_peaks.json fp32 FMA/s (measured)",
-                    "note": "profiles/ncu_flops.json: FFMA+FADD+FMUL thread instructions; one "
-                            "per FP32 lane-cycle"})
+                    "note": "profiles/ncu_flops.json: FFMA+FADD+FMUL thread instructions + 2 x the "
+                            "paired FFMA2/FADD2/FMUL2 ones (FP32 lane operations); one per FP32 "
+                            "lane-cycle"})
     out.append({"kernel": "k_kint<..., K6 fused> (gradient + normal + kernel integrals)",
                 "bound": "alu", "us": t_both * 1e3,
                 "note": "one kernel: K6 warps beside K7 warps; compare with the two above"})

@@ -6,7 +6,8 @@ executed-FMA fraction of K7).
     python scripts/ncu_flops.py CONFIG gpurun_out/flops_CONFIG.csv [...more CONFIG CSV pairs]
 
 Per kernel (short name, launches averaged): us (gpu__time_duration), thread-level
-DFMA / DADD / DMUL / FFMA / FADD / FMUL instruction counts, DRAM bytes.
+DFMA / DADD / DMUL / FFMA / FADD / FMUL (and the paired FFMA2 / FADD2 / FMUL2)
+instruction counts, DRAM bytes.
 """
 import csv
 import json
@@ -23,6 +24,10 @@ MET = {
     "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum": "ffma",
     "smsp__sass_thread_inst_executed_op_fadd_pred_on.sum": "fadd",
     "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum": "fmul",
+    # paired FP32 (sm_100): each thread instruction is two lane operations
+    "smsp__sass_thread_inst_executed_op_ffma2_pred_on.sum": "ffma2",
+    "smsp__sass_thread_inst_executed_op_fadd2_pred_on.sum": "fadd2",
+    "smsp__sass_thread_inst_executed_op_fmul2_pred_on.sum": "fmul2",
     "dram__bytes_read.sum": "dram_read",
     "dram__bytes_write.sum": "dram_write",
 }
