@@ -554,8 +554,8 @@ __global__ void __launch_bounds__(256) k_nb(GridC gc, const Geom* __restrict__ g
         const int64_t id = id0 + u;
         v[u] = (uint32_t)id;  // far-field packages neighbour themselves
         if (id < 2 || id >= n_pkg) continue;
-        const uint32_t r = L[u] / nx;
-        const int qx = (int)(L[u] - r * nx) + ox, qy = (int)(r % ny) + oy, qz = (int)(r / ny) + oz;
+        const uint32_t r = gc.fdx.div(L[u]), rz = gc.fdy.div(r);
+        const int qx = (int)(L[u] - r * nx) + ox, qy = (int)(r - rz * ny) + oy, qz = (int)rz + oz;
         if (EDGE &&
             (qx < 0 || qy < 0 || qz < 0 || qx >= gc.n[0] || qy >= gc.n[1] || qz >= gc.n[2])) {
             if (geom->mesh_nt) {  // mesh: sign of the nearest in-domain cell
@@ -610,8 +610,8 @@ __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
     }
     const uint32_t L = __ldg(meta_cell + id);
     const uint32_t nx = (uint32_t)gc.n[0], ny = (uint32_t)gc.n[1];
-    const uint32_t r = L / nx;
-    const int cx = (int)(L - r * nx), cy = (int)(r % ny), cz = (int)(r / ny);
+    const uint32_t r = gc.fdx.div(L), rz = gc.fdy.div(r);
+    const int cx = (int)(L - r * nx), cy = (int)(r - rz * ny), cz = (int)rz;
     // column coordinates: (a, b) = (x, y) along z, or (x, z) along y
     const int64_t ix = 4 * (int64_t)cx + (col & 3);
     const int64_t ib = 4 * (int64_t)(AX == 2 ? cy : cz) + (col >> 2);
@@ -710,6 +710,8 @@ static GridC make_gridc(const sg_desc* d) {
     if (idx32_off) gc.idx32 = 0;
     gc.inv_cellf = (float)gc.inv_cell;
     gc.inv_dxf = (float)gc.inv_dx;
+    gc.fdx = FastDiv((uint32_t)d->n[0]);
+    gc.fdy = FastDiv((uint32_t)d->n[1]);
     return gc;
 }
 

@@ -38,6 +38,29 @@ struct Geom {
 };
 
 // Grid constants passed by value to every kernel.
+// Unsigned division by a grid extent fixed for a launch (Hacker's Delight
+// 10-8, "unsigned division by invariant integers"): q = n / d exactly for all
+// 32-bit n, as one multiply-high, two adds and two shifts instead of the
+// ~20-instruction runtime division (the cell -> (x, y, z) decompositions of
+// the build kernels).
+struct FastDiv {
+    uint32_t d = 1, m = 0, s = 0;
+    FastDiv() = default;
+    explicit FastDiv(uint32_t dd) : d(dd) {
+        if (d > 1) {
+            uint32_t l = 0;
+            while ((uint64_t(1) << l) < d) ++l;  // ceil(log2 d)
+            m = (uint32_t)(((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1);
+            s = l - 1;
+        }
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        if (d == 1) return n;
+        const uint32_t t = __umulhi(m, n);
+        return (t + ((n - t) >> 1)) >> s;
+    }
+};
+
 struct GridC {
     double lower[3];
     double upper[3];  // lower + n * cell
@@ -54,6 +77,7 @@ struct GridC {
     // fp32 index arithmetic is bit-identical to the fp64 definition when l_c
     // is a power of two, lower = 0 and upper is a float (see sg_probe.cu)
     int32_t idx32;
+    FastDiv fdx, fdy;  // division by n[0], n[1] (cell index -> x, y, z)
     float upperf[3];
     float inv_cellf, inv_dxf;
 };
