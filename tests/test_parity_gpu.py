@@ -711,3 +711,20 @@ def test_probe_chunk_queue_order_bitwise(sgm):
         out[q] = np.load(tmp)
     for k in ("phi", "grad", "oob"):
         assert np.array_equal(out["0"][k], out["1"][k]), k
+
+
+def test_repeated_build_with_size_hint(sgm, O):
+    """A second build of the same (desc, geometry) sizes its arena and
+    launches from the first build's counts (no mid-build host wait); its
+    tables and initial phi must equal the first build's and the oracle's."""
+    for name in ("C1", "C2"):
+        w = W.config(name)
+        t = O.Oracle(w).build_tables()
+        a = sgm.Grid(w)
+        b = sgm.Grid(w)  # hinted
+        for g in (a, b):
+            assert np.array_equal(u32(g.view("bg")), t.bg)
+            assert np.array_equal(u32(g.view("nb")), t.nb)
+            assert np.array_equal(u32(g.view("meta_cell")), t.meta_cell)
+        assert a.info["n_core"] == b.info["n_core"] and a.info["n_pkg"] == b.info["n_pkg"]
+        assert torch.equal(a.view("phi"), b.view("phi"))
