@@ -335,11 +335,15 @@ sg_status sg_pool_trim(void);
  *   K4 initial phi = init_scale * f at the 64 data points of each package,
  *      rounded to dtype; singular packages hold -far / +far.
  * One host synchronisation reads back the package count (replaces the
- * paper's USM shared scalar).  slab may be NULL.  On success *out
+ * paper's USM shared scalar).  A repeated build of the same
+ * (desc, geometry) in the process (no slab, mesh or communicator) sizes its
+ * arrays from the previous build's counts and reads the count back only
+ * after all its work is queued (checked; a mismatch rebuilds without the
+ * hint; SG_BUILD_HINT=0 disables this).  slab may be NULL.  On success *out
  * owns the grid.  Errors: SG_ERR_ARG (null pointers, pkg != 4, n < 1,
  * cell <= 0, n_prims outside 1..SG_MAX_PRIMS, unknown kind or dtype, more than
- * 2^32 - 3 stored packages), SG_ERR_DOMAIN (slab outside the domain),
- * SG_ERR_OOM, SG_ERR_CUDA. */
+ * 2^32 - 3 stored packages or 2^32 stored data points), SG_ERR_DOMAIN (slab
+ * outside the domain), SG_ERR_OOM, SG_ERR_CUDA. */
 sg_status sg_build(const sg_desc* desc, const sg_geometry* geom, const sg_slab* slab,
                    void* stream, sg_grid** out);
 
