@@ -297,7 +297,8 @@ void tplan_invalidate(sg_grid* g, cudaStream_t s);
 void tplan_release(sg_grid* g, cudaStream_t s);
 bool tsweep_ready(sg_grid* g, cudaStream_t s);  // builds the plan on first use
 const void* tsweep_key(const sg_grid* g);
-void tsweep_launch(sg_grid* g, int cur, float inv_dx, float dx2, float cdx, cudaStream_t s);
+void tsweep_launch(sg_grid* g, int cur, float inv_dx, float dx2, float cdx, float ncfl,
+                   cudaStream_t s);
 
 void launch_reinit(sg_grid* g, int32_t iters, double cfl, cudaStream_t s, bool halo = false);
 void launch_gradient(sg_grid* g, uint32_t fields, double h_ratio, cudaStream_t s);

@@ -800,6 +800,7 @@ static StC<T> stencil_consts(const sg_grid* g, double cfl) {
     c.dx2 = (T)(g->gc.dx * g->gc.dx);
     c.cdx = (T)(cfl * g->gc.dx);
     c.inv_2dx = (T)(0.5 / g->gc.dx);
+    c.ncfl = (T)(-cfl);
     return c;
 }
 
@@ -1025,7 +1026,7 @@ static void reinit_t(sg_grid* g, int32_t iters, double cfl, bool halo, cudaStrea
         int cur = g->cur;
         if (ts) {
             for (int it = 0; it + 1 < iters; it += 2) {
-                tsweep_launch(g, cur, (float)c.inv_dx, (float)c.dx2, (float)c.cdx, cap);
+                tsweep_launch(g, cur, (float)c.inv_dx, (float)c.dx2, (float)c.cdx, (float)c.ncfl, cap);
                 cur = 1 - cur;
             }
             if (iters & 1) reinit_launch<T>(g, cur, c, lo, hi, cap);

@@ -642,7 +642,8 @@ bool tsweep_ready(sg_grid* g, cudaStream_t s) {
 const void* tsweep_key(const sg_grid* g) { return g->tplan ? g->tplan->arena : nullptr; }
 
 // one launch = two sweeps phi[cur] -> phi[1 - cur]
-void tsweep_launch(sg_grid* g, int cur, float inv_dx, float dx2, float cdx, cudaStream_t s) {
+void tsweep_launch(sg_grid* g, int cur, float inv_dx, float dx2, float cdx, float ncfl,
+                   cudaStream_t s) {
     // per device (the attribute belongs to the current context); cheap, and
     // only called while a graph is captured or for eager launches
     SG_CUDA(cudaFuncSetAttribute(k_tsweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem));
@@ -653,6 +654,7 @@ void tsweep_launch(sg_grid* g, int cur, float inv_dx, float dx2, float cdx, cuda
     c.inv_dx = inv_dx;
     c.dx2 = dx2;
     c.cdx = cdx;
+    c.ncfl = ncfl;
     k_tsweep<<<blocks, kTT, kTSmem, s>>>((const float*)g->phi[cur], (float*)g->phi[1 - cur],
                                          dev_view(tp), c);
     SG_CUDA(cudaGetLastError());  // counted by the caller (one per pass)
