@@ -591,11 +591,48 @@ __global__ void __launch_bounds__(256) k_nb(GridC gc, const Geom* __restrict__ g
 // AX = 2: a thread owns the (i, j) column of 4 points along z (x, y shared);
 // AX = 1: the (i, k) column along y (x, z shared) -- chosen for geometries
 // whose expensive terms are shared along y (a torus about the y axis).
+// The union mask of every package (the primitives that can attain the
+// minimum somewhere in it; see k_phi_init), one thread per package and the
+// primitives in a warp-uniform loop: no divergence between primitive kinds,
+// which the per-lane evaluation inside k_phi_init had (C3: ~28 % of its
+// instructions).
+__global__ void __launch_bounds__(256) k_prim_mask(GridC gc, Geom geom,
+                                                   const uint32_t* __restrict__ meta_cell,
+                                                   int64_t n_pkg, uint32_t* __restrict__ mask) {
+    const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= n_pkg) return;
+    if (id < 2) {
+        mask[id] = 0u;
+        return;
+    }
+    const uint32_t L = __ldg(meta_cell + id);
+    const uint32_t nx = (uint32_t)gc.n[0], ny = (uint32_t)gc.n[1];
+    const uint32_t r = gc.fdx.div(L), rz = gc.fdy.div(r);
+    const int cx = (int)(L - r * nx), cy = (int)(r - rz * ny), cz = (int)rz;
+    const double pcx = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
+    const double pcy = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
+    const double pcz = gc.lower[2] + ((double)cz + 0.5) * gc.cell;
+    const double R = 2.598076211353316 * gc.dx;
+    const double eps = 1e-9 * (gc.cell + fabs(gc.lower[0]) + fabs(gc.lower[1]) +
+                               fabs(gc.lower[2]) + gc.upper[0] + gc.upper[1] + gc.upper[2]);
+    double v[SG_MAX_PRIMS];
+    double m = INFINITY;
+    for (int i = 0; i < geom.n; ++i) {
+        v[i] = sd_prim(geom.kind[i], geom.p[i], pcx, pcy, pcz);
+        m = fmin(m, v[i]);
+    }
+    uint32_t k = 0;
+    for (int i = 0; i < geom.n; ++i)
+        if (v[i] - R <= m + R + eps) k |= 1u << i;
+    mask[id] = k;
+}
+
 template <class T, int AX>
 __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
                                                   const uint32_t* __restrict__ meta_cell,
                                                   int64_t n_pkg, T* __restrict__ phi0,
-                                                  T* __restrict__ phi1) {
+                                                  T* __restrict__ phi1,
+                                                  const uint32_t* __restrict__ pmask) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_pkg * 16) return;
     const int64_t id = t >> 4;
@@ -623,34 +660,8 @@ __global__ void __launch_bounds__(256) k_phi_init(GridC gc, Geom geom,
 #pragma unroll
     for (int k = 0; k < 4; ++k)
         w[k] = gc.lower[AX] + ((double)(4 * (int64_t)cc + k) + 0.5) * gc.dx;
-    uint32_t mask = (geom.n >= 32 ? 0xFFFFFFFFu : (1u << geom.n) - 1u);
-    if (geom.n > 1) {
-        // unions: primitives that provably exceed the minimum at every data
-        // point of the package are dropped (1-Lipschitz bound from the
-        // package centre c, data points within R = sqrt(3) 1.5 dx of c)
-        const double pcx = gc.lower[0] + ((double)cx + 0.5) * gc.cell;
-        const double pcy = gc.lower[1] + ((double)cy + 0.5) * gc.cell;
-        const double pcz = gc.lower[2] + ((double)cz + 0.5) * gc.cell;
-        const double R = 2.598076211353316 * gc.dx;
-        const double eps = 1e-9 * (gc.cell + fabs(gc.lower[0]) + fabs(gc.lower[1]) +
-                                   fabs(gc.lower[2]) + gc.upper[0] + gc.upper[1] + gc.upper[2]);
-        // the package-centre values: lane i of the package's 16-lane group
-        // evaluates primitive i (n <= SG_MAX_PRIMS = 16), then all share them
-        static_assert(SG_MAX_PRIMS <= 16, "one primitive per lane of a package group");
-        const int lane = threadIdx.x & 31;
-        const unsigned hm = 0xFFFFu << (lane & 16);  // this package's half-warp
-        const double fmine =
-            col < geom.n ? sd_prim(geom.kind[col], geom.p[col], pcx, pcy, pcz) : 0.0;
-        // m = min over the primitives by a butterfly over the half-warp (fmin
-        // is exact, so the order does not matter), then each lane decides its
-        // own primitive and one ballot forms the mask -- instead of every lane
-        // walking all primitives
-        double m = col < geom.n ? fmine : INFINITY;
-#pragma unroll
-        for (int o = 1; o < 16; o <<= 1) m = fmin(m, __shfl_xor_sync(hm, m, o));
-        const bool keep = col < geom.n && fmine - R <= m + R + eps;
-        mask = (__ballot_sync(hm, keep) >> (lane & 16)) & 0xFFFFu;
-    }
+    // the package's union mask (k_prim_mask; one primitive needs none)
+    const uint32_t mask = geom.n > 1 ? __ldg(pmask + id) : 1u;
     if constexpr (AX == 2) {
         if (geom.n == 1) sd_eval_col<4>(geom, x, bb, w, f);
         else sd_eval_col_mask<4>(geom, mask, x, bb, w, f);
@@ -1220,16 +1231,28 @@ static void build_once(const sg_desc* desc, const sg_geometry* geom, const sg_sl
                 zcol = zcol || g->geom.kind[i] == SG_TORUS_Z || g->geom.kind[i] == SG_TRIPRISM_Z;
             }
             const bool ax1 = ycol && !zcol && std::getenv("SG_PHI_ZCOL_ONLY") == nullptr;
+            uint32_t* pmask = nullptr;  // union masks (unions only)
+            if (g->geom.n > 1) {
+                pmask = (uint32_t*)dalloc(sizeof(uint32_t) * n_pkg, s);
+                guard_mem.tmp.push_back(pmask);
+                k_prim_mask<<<(unsigned)ceil_div(n_pkg, 256), 256, 0, s>>>(gc, g->geom, g->meta_cell,
+                                                                          n_pkg, pmask);
+                SG_LAUNCHED();
+            }
             if (g->dtype == SG_F64) {
                 auto kern = ax1 ? k_phi_init<double, 1> : k_phi_init<double, 2>;
                 kern<<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg, (double*)g->phi[0],
-                                        (double*)g->phi[1]);
+                                        (double*)g->phi[1], pmask);
             } else {
                 auto kern = ax1 ? k_phi_init<float, 1> : k_phi_init<float, 2>;
                 kern<<<pb, 256, 0, s>>>(gc, g->geom, g->meta_cell, n_pkg, (float*)g->phi[0],
-                                        (float*)g->phi[1]);
+                                        (float*)g->phi[1], pmask);
             }
             SG_LAUNCHED();
+            if (pmask) {
+                SG_CUDA(cudaFreeAsync(pmask, s));
+                guard_mem.tmp.pop_back();
+            }
         }
         SG_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
         g->cur = 0;
