@@ -133,6 +133,7 @@ struct Bits {
     const uint32_t* neg;
     int32_t W;
     int32_t zt_lo;
+    FastDiv fdW;  // division by W (word index -> row, column)
     __device__ __forceinline__ int64_t idx(const GridC& gc, int z, int y, int q) const {
         return ((int64_t)(z - zt_lo) * gc.n[1] + y) * W + q;
     }
@@ -322,6 +323,35 @@ __device__ __forceinline__ uint32_t active_word(const GridC& gc, const Bits& b, 
     return act & valid_bits(gc, q, b.W);
 }
 
+// the same for word t = (row, q) of a warp whose lanes hold consecutive
+// words (every lane of the warp calls it; `in`: t is a word of the planes):
+// the x-neighbour words of a row come from the neighbouring lanes by shuffle
+// where those hold them (one load per row instead of three).  Bit-identical
+// to active_word.
+__device__ __forceinline__ uint32_t active_word_warp(const GridC& gc, const Bits& b, bool in,
+                                                     int z, int y, int q) {
+    const int lane = threadIdx.x & 31;
+    uint32_t act = 0;
+#pragma unroll
+    for (int dz = -1; dz <= 1; ++dz) {
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy) {
+            const int zz = z + dz, yy = y + dy;
+            const bool ok = in && zz >= 0 && zz < gc.n[2] && yy >= 0 && yy < gc.n[1];
+            const int64_t i = ok ? b.idx(gc, zz, yy, q) : 0;
+            const uint32_t w = ok ? __ldg(b.core + i) : 0u;
+            // lane - 1 holds word (row, q - 1) when q > 0 (consecutive words)
+            const uint32_t sl = __shfl_up_sync(0xffffffffu, w, 1);
+            const uint32_t sr = __shfl_down_sync(0xffffffffu, w, 1);
+            uint32_t wl = 0u, wr = 0u;
+            if (ok && q > 0) wl = lane > 0 ? sl : __ldg(b.core + i - 1);
+            if (ok && q < b.W - 1) wr = lane < 31 ? sr : __ldg(b.core + i + 1);
+            act |= w | (w << 1) | (wl >> 31) | (w >> 1) | (wr << 31);
+        }
+    }
+    return in ? act & valid_bits(gc, q, b.W) : 0u;
+}
+
 __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int x = v;
@@ -355,12 +385,16 @@ __global__ void __launch_bounds__(kTB) k_count(GridC gc, Bits b, int64_t nwords,
     __shared__ int s_warp[32];
     const int64_t t = (int64_t)blockIdx.x * kTB + threadIdx.x;
     int cnt = 0, ncore = 0;
-    if (t < nwords) {
-        const int q = (int)(t % b.W);
-        const int64_t row = t / b.W;
-        const int y = (int)(row % gc.n[1]);
-        const int z = gc.zs_lo + (int)(row / gc.n[1]);
-        const uint32_t act = active_word(gc, b, z, y, q);
+    // word t -> (row, q), row -> (y, z): invariant divisors (t < 2^32: the
+    // stored planes' words)
+    const bool in_t = t < nwords;
+    const uint32_t row = b.fdW.div((uint32_t)t), rz = gc.fdy.div(row);
+    const int q = (int)((uint32_t)t - row * (uint32_t)b.W);
+    const int y = (int)(row - rz * (uint32_t)gc.n[1]);
+    const int z = gc.zs_lo + (int)rz;
+    const uint32_t act_all = active_word_warp(gc, b, in_t, z, y, q);
+    if (in_t) {
+        const uint32_t act = act_all;
         act_w[t] = act;
         cnt = __popc(act);
         ncore = __popc(__ldg(b.core + b.idx(gc, z, y, q)) & valid_bits(gc, q, b.W));
@@ -439,10 +473,10 @@ __global__ void __launch_bounds__(kTB) k_scatter(GridC gc, Bits b, int64_t nword
     int nbits = 0;
     int64_t off = 0, L0 = 0;
     if (t < nwords) {
-        const int q = (int)(t % b.W);
-        const int64_t row = t / b.W;
-        const int y = (int)(row % gc.n[1]);
-        const int z = gc.zs_lo + (int)(row / gc.n[1]);
+        const uint32_t row = b.fdW.div((uint32_t)t), rz = gc.fdy.div(row);
+        const int q = (int)((uint32_t)t - row * (uint32_t)b.W);
+        const int y = (int)(row - rz * (uint32_t)gc.n[1]);
+        const int z = gc.zs_lo + (int)rz;
         const int64_t wi = b.idx(gc, z, y, q);
         core = __ldg(b.core + wi);
         neg = __ldg(b.neg + wi);
@@ -1122,7 +1156,7 @@ static void build_once(const sg_desc* desc, const sg_geometry* geom, const sg_sl
         } else {
             launch_tag(gc, g->geom, zt_lo, zt_hi, W, core_w, neg_w, s);
         }
-        const Bits bits{core_w, neg_w, W, zt_lo};
+        const Bits bits{core_w, neg_w, W, zt_lo, FastDiv((uint32_t)W)};
         k_count<<<(unsigned)n_tiles, kTB, 0, s>>>(gc, bits, nwords, act_w, tile_count, d_core);
         SG_LAUNCHED();
         Published& pub = pinned_counts();
@@ -1486,7 +1520,7 @@ static void plane_counts(const sg_desc* desc, const sg_geometry* geom, int32_t z
         const int64_t tag_words = (int64_t)W * gc.n[1] * (zt_hi - zt_lo);
         uint32_t* core_w = (uint32_t*)dalloc(sizeof(uint32_t) * 2 * tag_words, s);
         launch_tag(gc, ge, zt_lo, zt_hi, W, core_w, core_w + tag_words, s);
-        const Bits bits{core_w, core_w + tag_words, W, zt_lo};
+        const Bits bits{core_w, core_w + tag_words, W, zt_lo, FastDiv((uint32_t)W)};
         SG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (z_hi - z_lo), s));
         const int64_t nwords = (int64_t)W * gc.n[1] * (z_hi - z_lo);
         k_plane_count<<<(unsigned)ceil_div(nwords, 256), 256, 0, s>>>(gc, bits, z_lo, nwords,
