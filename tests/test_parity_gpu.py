@@ -728,3 +728,36 @@ def test_repeated_build_with_size_hint(sgm, O):
             assert np.array_equal(u32(g.view("meta_cell")), t.meta_cell)
         assert a.info["n_core"] == b.info["n_core"] and a.info["n_pkg"] == b.info["n_pkg"]
         assert torch.equal(a.view("phi"), b.view("phi"))
+
+
+@pytest.mark.parametrize("skew", ["-7", "5"])
+def test_build_hint_mismatch_rebuilds(skew):
+    """A size hint that is wrong (too small: the compaction's meta writes
+    must stay inside the smaller arena; too large) is detected once the
+    build's work is queued and the grid is rebuilt without it: tables equal
+    the oracle's.  Fresh process with SG_BUILD_HINT_SKEW (the hint of every
+    repeated build is off by that many packages)."""
+    import os
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    code = (
+        "import numpy as np, torch, workloads as W\n"
+        "from oracle.oracle import Oracle\n"
+        "from paper_2512_11473_b200 import sg\n"
+        "for name in ('C1', 'C2'):\n"
+        "    w = W.config(name); t = Oracle(w).build_tables()\n"
+        "    for rep in range(3):\n"
+        "        g = sg.Grid(w)\n"
+        "        assert np.array_equal(g.view('bg').cpu().numpy().view(np.uint32), t.bg), (name, rep)\n"
+        "        assert np.array_equal(g.view('nb').cpu().numpy().view(np.uint32), t.nb), (name, rep)\n"
+        "        assert np.array_equal(g.view('meta_cell').cpu().numpy().view(np.uint32), t.meta_cell)\n"
+        "        assert g.info['n_pkg'] == t.n_pkg\n"
+        "torch.cuda.synchronize()\n"
+        "print('ok')\n")
+    env = dict(os.environ, SG_BUILD_HINT_SKEW=skew)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
