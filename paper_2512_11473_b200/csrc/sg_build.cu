@@ -423,29 +423,49 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ cnt, 
                                                int64_t* __restrict__ out,
                                                volatile long long* __restrict__ host,
                                                long long gen) {
-    __shared__ long long s[1024];
-    const int64_t seg = (n + 1023) / 1024;
-    const int64_t b = (int64_t)threadIdx.x * seg, e = min(n, b + seg);
+    // one block: warp w owns a contiguous range of the counts, read 32 at a
+    // time (coalesced); pass 1 sums the ranges, warp 0 scans the 32 sums,
+    // pass 2 writes the exclusive prefix with warp scans and a running carry
+    __shared__ long long s_tot[32], s_base[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t per = ((n + 31) / 32 + 31) & ~(int64_t)31;
+    const int64_t b = min(n, (int64_t)w * per), e = min(n, b + per);
     long long sum = 0;
-    for (int64_t i = b; i < e; ++i) sum += cnt[i];
-    s[threadIdx.x] = sum;
+    for (int64_t i = b + lane; i < e; i += 32) sum += cnt[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) s_tot[w] = sum;
     __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        long long v = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0;
-        __syncthreads();
-        s[threadIdx.x] += v;
-        __syncthreads();
+    if (w == 0) {
+        const long long v = s_tot[lane];
+        long long x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        s_base[lane] = x - v;
     }
-    long long run = s[threadIdx.x] - sum;
-    for (int64_t i = b; i < e; ++i) {
-        out[i] = run;
-        run += cnt[i];
+    __syncthreads();
+    long long run = s_base[w];
+    for (int64_t i0 = b; i0 < e; i0 += 32) {
+        const int64_t i = i0 + lane;
+        const long long v = i < e ? cnt[i] : 0;
+        long long x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (i < e) out[i] = run + x - v;
+        run += __shfl_sync(0xffffffffu, x, 31);
     }
-    if (threadIdx.x == 1023) {
-        out[n] = s[1023];
+    if (threadIdx.x == 0) {
+        const long long total = s_base[31] + s_tot[31];
+        out[n] = total;
         // publish [active, core, boundary flag] to mapped pinned memory, the
         // generation last: the host polls it instead of a stream sync
-        host[0] = s[1023];
+        host[0] = total;
         host[1] = out[n + 1];
         host[2] = out[n + 2];
         __threadfence_system();
