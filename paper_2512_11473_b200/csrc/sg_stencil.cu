@@ -337,6 +337,74 @@ __device__ __forceinline__ void grad_package(const T* __restrict__ in, T* __rest
     }
 }
 
+// K6 for two x-rows of `pkg` by an 8-lane group (lane (j, k), k in {0, 1}:
+// rows j + 4k and j + 4k + 8), the cross of load_cross2 (warp layout of
+// k_sweep: the four groups of a warp hold consecutive packages).  Same
+// formula per point as grad_package (bit-identical); the (phi, grad) rows go
+// through the package's shared tile so every store instruction writes 128
+// contiguous bytes per group.  Used by the fused K6 + K7 kernel: two K6
+// warps per 8 packages instead of four leave room for more K7 warps.
+template <class T>
+__device__ __forceinline__ void grad_package8(const T* __restrict__ in, T* __restrict__ grad,
+                                              T* __restrict__ normal,
+                                              const uint32_t* __restrict__ face, uint32_t pkg,
+                                              bool valid, bool next_ok, const StC<T>& c, T* tile) {
+    const int g8 = threadIdx.x & 7, j = g8 & 3, k = g8 >> 2;
+    uint32_t f = 0;
+    if (valid && g8 < 6) f = __ldg(face + (size_t)pkg * 8 + g8);
+    Cross2<T> x;
+    load_cross2<T, true>(in, pkg, valid, next_ok, f, j, k, x);
+    if (!valid) return;
+    const int r0 = j + 4 * k, r1 = r0 + 8;
+    T g[2][3][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const T l0 = i > 0 ? x.c0[i - 1] : x.xm0, q0 = i < 3 ? x.c0[i + 1] : x.xp0;
+        const T l1 = i > 0 ? x.c1[i - 1] : x.xm1, q1 = i < 3 ? x.c1[i + 1] : x.xp1;
+        g[0][0][i] = (q0 - l0) * c.inv_2dx;
+        g[0][1][i] = (x.yp0[i] - x.ym0[i]) * c.inv_2dx;
+        g[0][2][i] = (x.zmid[i] - x.zlo[i]) * c.inv_2dx;
+        g[1][0][i] = (q1 - l1) * c.inv_2dx;
+        g[1][1][i] = (x.yp1[i] - x.ym1[i]) * c.inv_2dx;
+        g[1][2][i] = (x.zhi[i] - x.zmid[i]) * c.inv_2dx;
+    }
+    if (grad) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            st_vec4(tile + tile_ofs(4 * r0 + i), x.c0[i], g[0][0][i], g[0][1][i], g[0][2][i]);
+            st_vec4(tile + tile_ofs(4 * r1 + i), x.c1[i], g[1][0][i], g[1][1][i], g[1][2][i]);
+        }
+        __syncwarp(0xFFu << (threadIdx.x & 24));
+        T* G = grad + (size_t)pkg * 256;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int d = g8 + 8 * i;
+            T v[4];
+            ld_row_s(tile + tile_ofs(d), v);
+            st_vec4(G + 4 * d, v[0], v[1], v[2], v[3]);
+        }
+    }
+    if (normal) {
+        T* N = normal + (size_t)pkg * 192;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = h ? r1 : r0;
+            T nx[4], ny[4], nz[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const T inv = inv_norm(g[h][0][i] * g[h][0][i] + g[h][1][i] * g[h][1][i] +
+                                       g[h][2][i] * g[h][2][i]);
+                nx[i] = g[h][0][i] * inv;
+                ny[i] = g[h][1][i] * inv;
+                nz[i] = g[h][2][i] * inv;
+            }
+            st_row(N + 4 * r, nx);
+            st_row(N + 64 + 4 * r, ny);
+            st_row(N + 128 + 4 * r, nz);
+        }
+    }
+}
+
 // Table 1 "stencil": 7-point Laplacian
 template <class T>
 __global__ void __launch_bounds__(256) k_laplace(const T* __restrict__ in, T* __restrict__ out,
@@ -435,9 +503,9 @@ struct KGeo {
 // when the taps at |o|^2 = 8 lie outside the support (h_ratio <= sqrt 2, e.g.
 // the default 1.3: 81 taps), which drops their zero-weight FMAs and the whole
 // (|oy|, |oz|) = (2, 2) row group (same bits: fma(0, h, acc) = acc)
-// GR: K6 fused in horizontally -- warps 4..7 of a 256-thread block compute the
-// gradient / normal of the block's 8 packages (16 lanes per package, as in
-// k_gradient) while warps 0..3 compute their kernel integrals: the
+// GR: K6 fused in horizontally -- warps 4..5 of a 192-thread block compute the
+// gradient / normal of the block's 8 packages (8 lanes per package,
+// grad_package8) while warps 0..3 compute their kernel integrals: the
 // HBM-write-bound K6 warps and the issue-bound K7 warps share every SM.
 // fp32 tap loop of k_kint on paired-FP32 instructions: the (up to) four
 // rows of a (abs oy, abs oz) group are combined by the sign butterfly with
@@ -553,7 +621,7 @@ __device__ __forceinline__ void kint_taps_f2(const KintC<float>& c, Load&& load,
 }
 
 template <class T, int R, int S2M, bool GR = false>
-__global__ void __launch_bounds__(GR ? 256 : 128, (R == 2 && S2M == 6 && sizeof(T) == 4) ? (GR ? 5 : 10) : 1) k_kint(const T* __restrict__ in,
+__global__ void __launch_bounds__(GR ? 192 : 128, (R == 2 && S2M == 6 && sizeof(T) == 4) ? (GR ? 6 : 10) : 1) k_kint(const T* __restrict__ in,
                                               const uint32_t* __restrict__ nb, int64_t lo,
                                               int64_t hi, KintC<T> c, T* __restrict__ K,
                                               T* __restrict__ G, T* __restrict__ grad = nullptr,
@@ -561,10 +629,12 @@ __global__ void __launch_bounds__(GR ? 256 : 128, (R == 2 && S2M == 6 && sizeof(
                                               const uint32_t* __restrict__ face = nullptr,
                                               StC<T> cs = StC<T>{}) {
     if constexpr (GR) {
-        if (threadIdx.x >= 128) {
+        if (threadIdx.x >= 128) {  // K6: warps 4-5, 8 lanes per package
             __shared__ __align__(16) T s_gtile[8][kTileStride];
-            const int64_t pkg = lo + (int64_t)blockIdx.x * 8 + ((threadIdx.x - 128) >> 4);
-            grad_package(in, grad, normal, face, pkg, pkg < hi, cs, s_gtile[(threadIdx.x - 128) >> 4]);
+            const int q = (threadIdx.x - 128) >> 3;
+            const int64_t pkg = lo + (int64_t)blockIdx.x * 8 + q;
+            grad_package8(in, grad, normal, face, (uint32_t)pkg, pkg < hi, pkg + 1 < hi, cs,
+                          s_gtile[q]);
             return;
         }
     }
@@ -1111,7 +1181,7 @@ static void launch_kint_r(sg_grid* g, const T* phi, const KintC<T>& c, cudaStrea
     // default needs the opt-in (fp64 at R >= 2)
     if (smem + (gr ? 8 * kTileStride * sizeof(T) : 0) + 8 * 28 * 4 > 48 * 1024)
         SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)ceil_div(hi - lo, 8), gr ? 256 : 128, smem, s>>>(
+    kern<<<(unsigned)ceil_div(hi - lo, 8), gr ? 192 : 128, smem, s>>>(
         phi, g->nb, lo, hi, c, (T*)g->kint, (T*)g->gkint, gp, np, g->face, cs);
     SG_LAUNCHED();
 }
