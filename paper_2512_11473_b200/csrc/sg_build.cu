@@ -584,7 +584,7 @@ __device__ __noinline__ uint32_t virtual_sign(double lx, double ly, double lz, d
 // Neighbours outside the domain take the sign of f at the virtual cell centre
 // (R-6); cells in the domain but outside the stored planes (beyond a ghost
 // plane) take their sign bit (never dereferenced by owned-point stencils).
-constexpr int kNbPW = 8;  // packages per warp
+constexpr int kNbPW = 16;  // packages per warp
 
 template <bool EDGE>
 __global__ void __launch_bounds__(256) k_nb(GridC gc, const Geom* __restrict__ geom, Bits b,
