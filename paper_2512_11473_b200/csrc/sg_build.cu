@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(kTB) k_scatter(GridC gc, Bits b, int64_t nword
     // warp store, two 16 B vector stores when the row start is 16 B aligned
     const int lane = threadIdx.x & 31;
     const int c0 = 8 * (lane & 3);
-#pragma unroll 1
+#pragma unroll
     for (int round = 0; round < 4; ++round) {
         const int src = 8 * round + (lane >> 2);
         const int nb_ = __shfl_sync(0xffffffffu, nbits, src);
