@@ -332,13 +332,17 @@ __device__ __forceinline__ uint32_t active_word_warp(const GridC& gc, const Bits
                                                      int z, int y, int q) {
     const int lane = threadIdx.x & 31;
     uint32_t act = 0;
+    // word index of (z, y, q) and the row / plane strides (the 3 x 3 rows
+    // differ by constants)
+    const int64_t i0 = in ? b.idx(gc, z, y, q) : 0;
+    const int64_t pw = (int64_t)gc.n[1] * b.W;
 #pragma unroll
     for (int dz = -1; dz <= 1; ++dz) {
 #pragma unroll
         for (int dy = -1; dy <= 1; ++dy) {
             const int zz = z + dz, yy = y + dy;
             const bool ok = in && zz >= 0 && zz < gc.n[2] && yy >= 0 && yy < gc.n[1];
-            const int64_t i = ok ? b.idx(gc, zz, yy, q) : 0;
+            const int64_t i = ok ? i0 + dz * pw + dy * (int64_t)b.W : 0;
             const uint32_t w = ok ? __ldg(b.core + i) : 0u;
             // lane - 1 holds word (row, q - 1) when q > 0 (consecutive words)
             const uint32_t sl = __shfl_up_sync(0xffffffffu, w, 1);
