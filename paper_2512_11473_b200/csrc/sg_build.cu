@@ -410,13 +410,16 @@ __global__ void __launch_bounds__(kTB) k_count(GridC gc, Bits b, int64_t nwords,
                                   (last < 32 && ((act >> last) & 1u)));
         if (edge) atomicOr(reinterpret_cast<unsigned int*>(n_core + 1), 1u);
     }
-    int total;
-    block_excl_scan(cnt, s_warp, total);
+    // the tile's totals only (no prefixes needed here): one packed warp
+    // reduction (each count <= 32 per thread, <= 8192 per tile: 16 bits)
+    const unsigned packed = __reduce_add_sync(0xffffffffu, (unsigned)cnt | ((unsigned)ncore << 16));
+    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = (int)packed;
     __syncthreads();
-    int ctot;
-    block_excl_scan(ncore, s_warp, ctot);
     if (threadIdx.x == 0) {
-        tile_count[blockIdx.x] = total;
+        unsigned sum = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sum += (unsigned)s_warp[w];
+        tile_count[blockIdx.x] = (int)(sum & 0xffffu);
+        const unsigned ctot = sum >> 16;
         if (ctot) atomicAdd(n_core, (unsigned long long)ctot);
     }
 }
